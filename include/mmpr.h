@@ -1,0 +1,239 @@
+/*
+ * mmpr.h -- C-ABI of libmmpr.so, the sm_100a implementation of the
+ * micro-macro (mM) Parareal hot path of arXiv 2310.11365.
+ *
+ * The reference (mcparareal, /root/reference/pkg/src/mcparareal) is pure
+ * Python/numpy with no FFI; each entry point below replaces one of its
+ * callables and is bound from the host mirror paper_2310_11365_b200/_lib.py
+ * through ctypes (INTEGRATION.md shows the binding).  Conventions:
+ *   - every function returns an mmpr_status (0 = launched/ok);
+ *   - all double/int buffers are DEVICE pointers owned by the caller, laid out
+ *     as documented per argument; descriptor structs are HOST pointers passed
+ *     by value into the kernels;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); every call is
+ *     stream-ordered and never synchronises the host, except the explicitly
+ *     named query functions;
+ *   - numerical outcomes the reference reports by exception are returned in
+ *     device status arrays (see each function) so one read at the end of a run
+ *     reproduces the reference's first error.
+ */
+#ifndef MMPR_H
+#define MMPR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MMPR_MAX_REGIONS 4
+#define MMPR_MAX_PARAMS 8
+#define MMPR_MAX_ODE_PARAMS 16
+
+typedef enum {
+  MMPR_OK = 0,
+  MMPR_ERR_ARG = 1,         /* invalid argument (shape, pointer, size) */
+  MMPR_ERR_CUDA = 2,        /* a CUDA runtime call failed */
+  MMPR_ERR_UNSUPPORTED = 3  /* descriptor/geometry not implemented on device */
+} mmpr_status;
+
+/* Drift/diffusion families (MEAN_OF_F statistic, f = identity).  Parameter
+ * layouts follow the reference factories' closures:
+ *  OU          make_perturbed_ou (models.py:265-279): p = {a, a_E, B}
+ *  LINEAR      make_linear, constant coefficients (models.py:360-372):
+ *              p = {A, A_E, A_0, B, B_E, B_0}
+ *  DOUBLE_WELL make_double_well (models.py:339-357):
+ *              p = {4*alpha, 2*gamma, beta, tilt, sigma, 12*alpha}
+ *  CUBIC_MF    builder model for BASELINE config 2, a = cE*s - c1*x - c3*x^3:
+ *              p = {c1, c3, cE, sigma}
+ *  DW_MULT     double-well drift with b = s0*sqrt(1+x^2) (BASELINE config 5):
+ *              p = {4*alpha, 2*gamma, beta, tilt, s0, 12*alpha} */
+enum {
+  MMPR_MODEL_OU = 1,
+  MMPR_MODEL_LINEAR = 2,
+  MMPR_MODEL_DOUBLE_WELL = 3,
+  MMPR_MODEL_CUBIC_MF = 4,
+  MMPR_MODEL_DW_MULT = 5
+};
+
+typedef struct {
+  int32_t kind;
+  int32_t stat_kind; /* 0 = MEAN_OF_F with identity f (only supported kind) */
+  double p[MMPR_MAX_PARAMS];
+} mmpr_model;
+
+/* Half-open regions [s_{i-1}, s_i) (state.py:13-78); a particle on a
+ * separatrix belongs to the right region (searchsorted side="right"). */
+typedef struct {
+  int32_t n_regions;                   /* 1..MMPR_MAX_REGIONS */
+  int32_t pad;
+  double seps[MMPR_MAX_REGIONS - 1];   /* strictly increasing */
+  double centers[MMPR_MAX_REGIONS];    /* RegionPartition.center(i) */
+} mmpr_partition;
+
+/* Moment ODE (coarse propagator) on the packed state [M_1..M_I, S_1..S_I,
+ * a_1..a_I] (moments.py:29-49):
+ *  UNIMODAL        unimodal_rhs(model) (moments.py:52-68), I = 1
+ *  PERTURBED_OU    perturbed_ou_rhs(spec) (moments.py:111-125):
+ *                  p = {mean_rate, var_rate, var_source}, I = 1
+ *  MULTIMODAL      multimodal_rhs(model, ...) (moments.py:145-192):
+ *                  p = {targets[I], rates[I]}
+ *  GAUSSIAN_CUBIC  builder Gaussian closure for CUBIC_MF (BASELINE config 2):
+ *                  p = {c1, c3, cE, sigma}, I = 1 */
+enum {
+  MMPR_ODE_UNIMODAL = 1,
+  MMPR_ODE_PERTURBED_OU = 2,
+  MMPR_ODE_MULTIMODAL = 3,
+  MMPR_ODE_GAUSSIAN_CUBIC = 4
+};
+
+typedef struct {
+  int32_t kind;
+  int32_t n_regions;
+  double p[MMPR_MAX_ODE_PARAMS];
+} mmpr_moment_ode;
+
+/* Coarse integrators: EULER is the fixed-step forward Euler the BASELINE
+ * configs ask for (n = round((t1-t0)/dt) steps); DP54 restates
+ * rk54.integrate (rk54.py:69-129). */
+enum { MMPR_INTEG_EULER = 1, MMPR_INTEG_DP54 = 2 };
+
+typedef struct {
+  int32_t kind;
+  int32_t max_steps;   /* DP54 budget */
+  double dt;           /* EULER step */
+  double rel_tol;      /* DP54 */
+  double abs_tol;      /* DP54 */
+  double first_step;   /* DP54; <= 0 selects the initial-step heuristic */
+} mmpr_integrator;
+
+/* Status codes written to device status arrays. */
+#define MMPR_STAT_OK (-1)
+
+/* ------------------------------------------------------------------ */
+/* Library / device queries (host-synchronous)                         */
+/* ------------------------------------------------------------------ */
+
+/* Version string of the build ("mmpr <git-describe> sm_100a"). */
+const char *mmpr_version(void);
+
+/* Last CUDA error string recorded by a failing call on this thread. */
+const char *mmpr_last_error(void);
+
+/* Max concurrently resident clusters of the fine-sweep kernel for P
+ * particles per slice (cudaOccupancyMaxActiveClusters). */
+int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_out, int32_t *ctas_per_slice_out);
+
+/* ------------------------------------------------------------------ */
+/* Noise: numpy-exact Philox4x64 + SeedSequence + ziggurat streams     */
+/* replaces NoisePlan._generator/normals/init_rng (particles.py:49-65) */
+/* ------------------------------------------------------------------ */
+
+/* Philox keys of SeedSequence(entropy).generate_state(2, uint64) for the
+ * step-noise addresses: FROZEN (seed, 1, n, j) / FRESH (seed, 2, n, j, k),
+ * n in [n_offset, n_offset+n_slices), j in [0, steps).  keys: device
+ * uint64[n_slices][steps][2]. (particles.py:52-61) */
+int mmpr_noise_keys(uint64_t master_seed, int32_t fresh, int32_t iteration,
+                    int32_t n_offset, int32_t n_slices, int32_t steps,
+                    uint64_t *keys, void *stream);
+
+/* Philox key of an arbitrary entropy tuple given as its assembled uint32
+ * words (host array), written to device uint64[2]. */
+int mmpr_entropy_key(const uint32_t *words, int32_t n_words, uint64_t *key_dev, void *stream);
+
+/* Fill n_streams rows of `count` numbers: out[r*pitch + i] = loc + scale*z_i
+ * where z is Generator(Philox(key_r)).standard_normal(count) bit-for-bit
+ * (affine = 0 writes z itself).  keys: device uint64[n_streams][2].
+ * Replaces Generator.standard_normal / Generator.normal
+ * (particles.py:61, models.py:257). */
+int mmpr_normals_fill(const uint64_t *keys, int32_t n_streams, int64_t count,
+                      double *out, int64_t pitch, int32_t affine, double loc,
+                      double scale, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* Fine propagator (particles.py:119-159, engine.py:110-124)           */
+/* ------------------------------------------------------------------ */
+
+/* Euler-Maruyama over `steps` steps for n_slices independent ensembles of
+ * `particles` each, one thread-block cluster per slice, particles resident
+ * in registers, per-step ensemble mean reduced in numpy's pairwise order.
+ *  x_in  : device double, slice s at x_in + s*in_pitch (P values)
+ *  x_out : device double, slice s at x_out + s*out_pitch
+ *  xi    : device double increments, slice s step j at
+ *          xi + s*xi_slice_pitch + j*xi_row_pitch (P values; row pitch even)
+ *  t0    : device double[n_slices] slice start times
+ *  bad_step : device int32[n_slices]; MMPR_STAT_OK or the first step whose
+ *          positions were not all finite (NumericalBlowup(slice, step))
+ *  final_mean : device double[n_slices] (may be NULL): mean of the output. */
+int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_t particles,
+                    int32_t steps, double dt, double sqrt_dt, const double *t0,
+                    const double *x_in, int64_t in_pitch, double *x_out,
+                    int64_t out_pitch, const double *xi, int64_t xi_slice_pitch,
+                    int64_t xi_row_pitch, int32_t *bad_step, double *final_mean,
+                    void *stream);
+
+/* ------------------------------------------------------------------ */
+/* Restriction / matching (particles.py:176-205, coupling.py:26-95)    */
+/* ------------------------------------------------------------------ */
+
+/* Per-region fraction, mean and two-pass population variance of n_ens
+ * ensembles, numpy summation order.  stats: device double[n_ens][3I] packed
+ * [means, variances, fractions]; counts: device int64[n_ens][I]; scratch:
+ * device double, >= n_ens*I*particles values when I > 1 (NULL when I = 1). */
+int mmpr_restrict(const mmpr_partition *part, int32_t n_ens, int64_t particles,
+                  const double *x, int64_t pitch, double *stats, int64_t *counts,
+                  double *scratch, void *stream);
+
+/* Per-region affine match x -> sqrt(var_t/var_c)(x - M_c) + mu_t with the
+ * reference's clamp / degenerate / identity rules.  Ensemble e reads source
+ * x_src + e*src_pitch (src_pitch 0: one shared source, e.g. lift from ens0),
+ * its current moments cur_stats + e*cur_stride (packed 3I) and counts
+ * cur_counts + e*cnt_stride (I), the target targets + e*tgt_stride (packed
+ * 3I, fractions ignored), and writes x_out + e*out_pitch.
+ *  policy: 0 = raise (DegenerateMatch), 1 = collapse
+ *  status: device int32[n_ens]: MMPR_STAT_OK or the first degenerate region
+ *  clamped: device int32[n_ens] (may be NULL): bit i set when region i's
+ *          target variance was negative and clamped to 0 */
+int mmpr_match(const mmpr_partition *part, int32_t n_ens, int64_t particles,
+               const double *targets, int64_t tgt_stride, const double *cur_stats,
+               int64_t cur_stride, const int64_t *cur_counts, int64_t cnt_stride,
+               const double *x_src, int64_t src_pitch, double *x_out, int64_t out_pitch,
+               int32_t policy, int32_t *status, int32_t *clamped, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* Coarse propagator and Parareal correction (moments.py:195-203,      */
+/* engine.py:170-236), one warp, no host round-trip                    */
+/* ------------------------------------------------------------------ */
+
+/* One macro row of the mM iteration for n_slices slices (times: device
+ * double[n_slices+1]).  iteration == 0: pure coarse cascade from rho0.
+ * iteration >= 1: corrected_n = fine_n + (C(macro_n) - cache_in_n), negative
+ * variances clamped, fractions replaced by fine_n's.
+ *  rho0       : device double[3I]
+ *  fine_stats : device double[n][3I] (iteration >= 1)
+ *  cache_in   : device double[n][3I] (iteration >= 1)
+ *  macro_out  : device double[n+1][3I] (row 0 = rho0)
+ *  cache_out  : device double[n][3I] this row's coarse predictions
+ *  raw_out    : device double[n][3I] uncorrected-clamp corrected states (>= 1)
+ *  status     : device int32[n]: MMPR_STAT_OK or 1 = IntegrationFailure
+ *  skip_until : predictions for n < skip_until are copied from cache_in
+ *               (bitwise equal by construction; 0 disables). */
+int mmpr_coarse_row(const mmpr_moment_ode *ode, const mmpr_model *model,
+                    const mmpr_integrator *integ, int32_t n_slices,
+                    const double *times, int32_t iteration, const double *rho0,
+                    const double *fine_stats, const double *cache_in,
+                    double *macro_out, double *cache_out, double *raw_out,
+                    int32_t *status, int32_t skip_until, void *stream);
+
+/* integrate_macro(ode, state, t0, t1, cfg) for n_states independent states
+ * (moments.py:195-203): in/out device double[n_states][3I]. */
+int mmpr_integrate_macro(const mmpr_moment_ode *ode, const mmpr_model *model,
+                         const mmpr_integrator *integ, int32_t n_states,
+                         const double *t0, const double *t1, const double *state_in,
+                         double *state_out, int32_t *status, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MMPR_H */

@@ -1,0 +1,160 @@
+/*
+ * npstream.c -- CPU restatement of the noise stream behind the reference's
+ * NoisePlan (TEST INFRASTRUCTURE: the checker for the GPU stream generator;
+ * never linked into the product).
+ *
+ * Reference call site: mcparareal.particles.NoisePlan._generator/normals
+ *   /root/reference/pkg/src/mcparareal/particles.py:49-61
+ *     np.random.Generator(np.random.Philox(np.random.SeedSequence(entropy)))
+ *         .standard_normal(count)
+ * That algorithm lives in the third-party dependency numpy (not vendored in
+ * /root/reference; pinned here at numpy 2.3.5).  Its published pieces are
+ * restated below:
+ *   1. SeedSequence entropy pool (O'Neill's seed_seq hash mixing, pool of
+ *      four 32-bit words) and generate_state(2, uint64) -> Philox key.
+ *   2. Philox4x64-10 (Salmon et al., SC'11), counter pre-incremented before
+ *      each 4-word block, words served in order from the block.
+ *   3. numpy's 256-layer ziggurat standard normal over one 64-bit word per
+ *      attempt (layer = low 8 bits, sign = bit 8, 52-bit mantissa above),
+ *      wedge test with one extra uniform, Marsaglia tail from layer 0.
+ *      Tables: np_ziggurat_tables.h (recovered by
+ *      oracle/tools/extract_numpy_ziggurat.py).
+ * Pinned against numpy itself in tests/test_oracle_npstream.py.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "np_ziggurat_tables.h"
+
+static const uint64_t NPZ_KI[256] = {NPZ_KI_VALUES};
+static const double NPZ_WI[256] = {NPZ_WI_VALUES};
+static const double NPZ_FI[256] = {NPZ_FI_VALUES};
+
+/* ---- 1. SeedSequence ---------------------------------------------------- */
+#define SS_INIT_A 0x43b0d7e5u
+#define SS_MULT_A 0x931e8875u
+#define SS_INIT_B 0x8b51f9ddu
+#define SS_MULT_B 0x58f38dedu
+#define SS_MIX_L 0xca01f9ddu
+#define SS_MIX_R 0x4973f715u
+
+static uint32_t ss_hashmix(uint32_t v, uint32_t *h) {
+  v ^= *h;
+  *h *= SS_MULT_A;
+  v *= *h;
+  return v ^ (v >> 16);
+}
+
+static uint32_t ss_mix(uint32_t x, uint32_t y) {
+  uint32_t r = SS_MIX_L * x - SS_MIX_R * y;
+  return r ^ (r >> 16);
+}
+
+/* pool[4] from the assembled entropy words (no spawn key). */
+void nps_seedseq_pool(const uint32_t *words, int n_words, uint32_t pool[4]) {
+  uint32_t h = SS_INIT_A;
+  for (int i = 0; i < 4; ++i) pool[i] = ss_hashmix(i < n_words ? words[i] : 0u, &h);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = ss_mix(pool[d], ss_hashmix(pool[s], &h));
+  for (int s = 4; s < n_words; ++s)
+    for (int d = 0; d < 4; ++d) pool[d] = ss_mix(pool[d], ss_hashmix(words[s], &h));
+}
+
+/* generate_state(2, np.uint64): four 32-bit words, little-endian pairs. */
+void nps_seedseq_key(const uint32_t *words, int n_words, uint64_t key[2]) {
+  uint32_t pool[4], out[4], h = SS_INIT_B;
+  nps_seedseq_pool(words, n_words, pool);
+  for (int i = 0; i < 4; ++i) {
+    uint32_t v = pool[i] ^ h;
+    h *= SS_MULT_B;
+    v *= h;
+    out[i] = v ^ (v >> 16);
+  }
+  key[0] = (uint64_t)out[0] | ((uint64_t)out[1] << 32);
+  key[1] = (uint64_t)out[2] | ((uint64_t)out[3] << 32);
+}
+
+/* ---- 2. Philox4x64-10 ---------------------------------------------------- */
+static void mulhilo64(uint64_t a, uint64_t b, uint64_t *hi, uint64_t *lo) {
+  __uint128_t p = (__uint128_t)a * b;
+  *hi = (uint64_t)(p >> 64);
+  *lo = (uint64_t)p;
+}
+
+void nps_philox4x64_10(const uint64_t ctr_in[4], const uint64_t key_in[2], uint64_t out[4]) {
+  uint64_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+  uint64_t k0 = key_in[0], k1 = key_in[1];
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B97F4A7C15ULL; k1 += 0xBB67AE8584CAA73BULL; }
+    uint64_t hi0, lo0, hi1, lo1;
+    mulhilo64(0xD2E7470EE14C6C93ULL, c[0], &hi0, &lo0);
+    mulhilo64(0xCA5A826395121157ULL, c[2], &hi1, &lo1);
+    uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+  }
+  memcpy(out, c, sizeof c);
+}
+
+/* Word i of a fresh stream: block i/4 uses counter (i/4 + 1). */
+uint64_t nps_word(const uint64_t key[2], uint64_t i) {
+  uint64_t ctr[4] = {(i >> 2) + 1, 0, 0, 0}, out[4];
+  if (ctr[0] == 0) ctr[1] = 1; /* carry (never reached in practice) */
+  nps_philox4x64_10(ctr, key, out);
+  return out[i & 3];
+}
+
+typedef struct { uint64_t key[2]; uint64_t pos; uint64_t buf[4]; } nps_stream;
+
+static uint64_t next64(nps_stream *s) {
+  if ((s->pos & 3) == 0) {
+    uint64_t ctr[4] = {(s->pos >> 2) + 1, 0, 0, 0};
+    nps_philox4x64_10(ctr, s->key, s->buf);
+  }
+  return s->buf[s->pos++ & 3];
+}
+
+static double next_unit(nps_stream *s) { return (double)(next64(s) >> 11) * (1.0 / 9007199254740992.0); }
+
+/* ---- 3. ziggurat standard normal ---------------------------------------- */
+static double standard_normal(nps_stream *s) {
+  for (;;) {
+    uint64_t r = next64(s);
+    int layer = (int)(r & 0xff);
+    r >>= 8;
+    int negative = (int)(r & 1);
+    uint64_t mant = (r >> 1) & 0x000fffffffffffffULL;
+    double x = (double)mant * NPZ_WI[layer];
+    if (negative) x = -x;
+    if (mant < NPZ_KI[layer]) return x;
+    if (layer == 0) {
+      for (;;) {
+        double xx = -NPZ_INV_R * log1p(-next_unit(s));
+        double yy = -log1p(-next_unit(s));
+        if (yy + yy > xx * xx) return ((mant >> 8) & 1) ? -(NPZ_R + xx) : NPZ_R + xx;
+      }
+    }
+    if ((NPZ_FI[layer - 1] - NPZ_FI[layer]) * next_unit(s) + NPZ_FI[layer] < exp(-0.5 * x * x)) return x;
+  }
+}
+
+/* Fill out[0..count) from the stream keyed by the SeedSequence entropy words;
+ * returns the number of 64-bit words consumed. */
+uint64_t nps_standard_normal_fill(const uint32_t *words, int n_words, int64_t count, double *out) {
+  nps_stream s;
+  memset(&s, 0, sizeof s);
+  nps_seedseq_key(words, n_words, s.key);
+  for (int64_t i = 0; i < count; ++i) out[i] = standard_normal(&s);
+  return s.pos;
+}
+
+/* Same, from an explicit Philox key (used to cross-check key derivation). */
+uint64_t nps_standard_normal_fill_key(const uint64_t key[2], int64_t count, double *out) {
+  nps_stream s;
+  memset(&s, 0, sizeof s);
+  s.key[0] = key[0];
+  s.key[1] = key[1];
+  for (int64_t i = 0; i < count; ++i) out[i] = standard_normal(&s);
+  return s.pos;
+}

@@ -1,0 +1,133 @@
+"""ctypes binding of libmmpr.so (the C-ABI declared in include/mmpr.h).
+
+The library is built in-tree (``paper_2310_11365_b200/libmmpr.so``) by
+``__graft_entry__.build()`` / ``make -C paper_2310_11365_b200/csrc``.  There is
+no CPU fallback: every device entry point raises ``MmprError`` when the
+library or a CUDA device is unavailable.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmmpr.so")
+
+MAX_REGIONS = 4
+MAX_PARAMS = 8
+MAX_ODE_PARAMS = 16
+
+# model families (include/mmpr.h)
+MODEL_OU = 1
+MODEL_LINEAR = 2
+MODEL_DOUBLE_WELL = 3
+MODEL_CUBIC_MF = 4
+MODEL_DW_MULT = 5
+
+ODE_UNIMODAL = 1
+ODE_PERTURBED_OU = 2
+ODE_MULTIMODAL = 3
+ODE_GAUSSIAN_CUBIC = 4
+
+INTEG_EULER = 1
+INTEG_DP54 = 2
+
+STAT_OK = -1
+
+STATUS_TEXT = {0: "ok", 1: "invalid argument", 2: "CUDA error", 3: "unsupported"}
+
+
+class MmprError(RuntimeError):
+    """A libmmpr call failed (bad argument, CUDA error or unsupported case)."""
+
+
+class Model(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("stat_kind", ctypes.c_int32),
+                ("p", ctypes.c_double * MAX_PARAMS)]
+
+
+class Partition(ctypes.Structure):
+    _fields_ = [("n_regions", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("seps", ctypes.c_double * (MAX_REGIONS - 1)),
+                ("centers", ctypes.c_double * MAX_REGIONS)]
+
+
+class MomentOde(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("n_regions", ctypes.c_int32),
+                ("p", ctypes.c_double * MAX_ODE_PARAMS)]
+
+
+class Integrator(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("max_steps", ctypes.c_int32),
+                ("dt", ctypes.c_double), ("rel_tol", ctypes.c_double),
+                ("abs_tol", ctypes.c_double), ("first_step", ctypes.c_double)]
+
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_U64 = ctypes.c_uint64
+_D = ctypes.c_double
+
+# name -> (restype, argtypes); every symbol include/mmpr.h declares
+SIGNATURES = {
+    "mmpr_version": (ctypes.c_char_p, []),
+    "mmpr_last_error": (ctypes.c_char_p, []),
+    "mmpr_fine_sweep_occupancy": (ctypes.c_int, [_I64, _P, _P]),
+    "mmpr_noise_keys": (ctypes.c_int, [_U64, _I32, _I32, _I32, _I32, _I32, _P, _P]),
+    "mmpr_entropy_key": (ctypes.c_int, [_P, _I32, _P, _P]),
+    "mmpr_normals_fill": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _I32, _D, _D, _P]),
+    "mmpr_fine_sweep": (ctypes.c_int, [_P, _I32, _I64, _I32, _D, _D, _P, _P, _I64, _P, _I64,
+                                        _P, _I64, _I64, _P, _P, _P]),
+    "mmpr_restrict": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _P, _P, _P, _P]),
+    "mmpr_match": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _P,
+                                   _I64, _I32, _P, _P, _P]),
+    "mmpr_coarse_row": (ctypes.c_int, [_P, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
+                                        _I32, _P]),
+    "mmpr_integrate_macro": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libmmpr.so once and bind every declared symbol."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise MmprError(
+                f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke a status-returning entry point; raise MmprError on failure."""
+    lib = load()
+    status = getattr(lib, name)(*args)
+    if status != 0:
+        detail = lib.mmpr_last_error().decode(errors="replace")
+        raise MmprError(f"{name} failed: {STATUS_TEXT.get(status, status)}"
+                        + (f" ({detail})" if detail else ""))
+
+
+def ptr(t) -> int | None:
+    """Raw device pointer of a torch tensor (None passes NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

@@ -1,0 +1,349 @@
+// Coarse propagator (moment ODEs) and the sequential Parareal correction.
+//
+// Replaces, on the device and without host round-trips:
+//   moments.unimodal_rhs / perturbed_ou_rhs / multimodal_rhs / integrate_macro
+//     (/root/reference/pkg/src/mcparareal/moments.py:52-68, 111-125, 145-203)
+//   rk54.integrate (/root/reference/pkg/src/mcparareal/rk54.py:57-129)
+//   the serial loop of engine.run_micro_macro: iteration-0 cascade
+//     (engine.py:170-195) and the correction
+//     corrected = R(F_n) + (C(rho_n^{k+1}) - C(rho_n^k)), negative-variance
+//     clamp, fraction policy (engine.py:210-236).
+// The row is inherently serial in n; one thread walks it with the state in
+// registers (3I <= 12 doubles).  Arithmetic follows the reference's numpy
+// operation order, so forward-Euler rows are bitwise equal to the CPU
+// restatement; DP5(4) matches to rounding (the reference's np.dot goes
+// through BLAS).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "mmpr_device.cuh"
+#include "capi_internal.h"
+
+namespace mmpr {
+
+#define CS_MAXV (3 * MMPR_MAX_REGIONS)
+
+struct State {
+  double y[CS_MAXV];
+};
+
+// numpy pairwise sum for n <= 128 (short vectors: sequential from 0 when
+// n < 8, else 8 accumulators)
+__device__ double small_pairwise(const double *a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = add(r, a[i]);
+    return r;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = add(r[j], a[i + j]);
+  double res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
+  for (; i < n; ++i) res = add(res, a[i]);
+  return res;
+}
+
+__device__ void ode_rhs(const mmpr_moment_ode &ode, const mmpr_model &model, double t, const double *y,
+                        double *dy) {
+  (void)t;
+  const int I = ode.n_regions;
+  switch (ode.kind) {
+    case MMPR_ODE_UNIMODAL: {  // first-order closure with point statistic s = M
+      const double m = y[0], var = y[1];
+      const ModelCoeffs c = coeffs(model, m, m);
+      dy[0] = add(c.drift, mul(0.5, c.diff_dxx));
+      dy[1] = add(mul(add(mul(2.0, c.drift_dx), mul(c.diff_dx, c.diff_dx)), var), mul(c.diff, c.diff));
+      dy[2] = 0.0;
+      break;
+    }
+    case MMPR_ODE_PERTURBED_OU: {
+      const double *p = ode.p;
+      dy[0] = mul(p[0], y[0]);
+      dy[1] = add(mul(p[1], y[1]), p[2]);
+      dy[2] = 0.0;
+      break;
+    }
+    case MMPR_ODE_MULTIMODAL: {  // mixture statistic sum_i a_i M_i (from 0.0)
+      double s = 0.0;
+      for (int i = 0; i < I; ++i) s = add(s, mul(y[2 * I + i], y[i]));
+      for (int i = 0; i < I; ++i) {
+        const ModelCoeffs c = coeffs(model, y[i], s);
+        dy[i] = add(c.drift, mul(0.5, c.diff_dxx));
+        dy[I + i] = add(mul(add(mul(2.0, c.drift_dx), mul(c.diff_dx, c.diff_dx)), y[I + i]), mul(c.diff, c.diff));
+        // -rates * (fractions - targets)
+        dy[2 * I + i] = mul(-ode.p[I + i], sub(y[2 * I + i], ode.p[i]));
+      }
+      break;
+    }
+    case MMPR_ODE_GAUSSIAN_CUBIC: {
+      // dM = cE*M - c1*M - c3*(M*M*M + 3*M*S)
+      // dS = -2*c1*S - 6*c3*S*(M*M + S) + sigma*sigma
+      const double *p = ode.p;
+      const double m = y[0], v = y[1];
+      dy[0] = sub(sub(mul(p[2], m), mul(p[0], m)), mul(p[1], add(mul(mul(m, m), m), mul(mul(3.0, m), v))));
+      dy[1] = add(sub(mul(mul(-2.0, p[0]), v), mul(mul(mul(6.0, p[1]), v), add(mul(m, m), v))),
+                  mul(p[3], p[3]));
+      dy[2] = 0.0;
+      break;
+    }
+    default:
+      for (int i = 0; i < 3 * I; ++i) dy[i] = __longlong_as_double(0x7ff8000000000000ULL);
+  }
+}
+
+__device__ __forceinline__ bool all_finite(const double *v, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!isfinite(v[i])) return false;
+  return true;
+}
+
+// Forward Euler with n = round((t1 - t0)/dt) >= 1 equal steps.
+__device__ int integrate_euler(const mmpr_moment_ode &ode, const mmpr_model &model, double dt, double t0,
+                               double t1, double *y) {
+  const int nv = 3 * ode.n_regions;
+  const double span = sub(t1, t0);
+  if (span == 0.0) return MMPR_STAT_OK;
+  long long n = llrint(div(span, dt));
+  if (n < 1) n = 1;
+  const double h = div(span, (double)n);
+  double k[CS_MAXV];
+  for (long long i = 0; i < n; ++i) {
+    const double t = add(t0, mul((double)i, h));
+    ode_rhs(ode, model, t, y, k);
+    for (int v = 0; v < nv; ++v) y[v] = add(y[v], mul(h, k[v]));
+  }
+  return all_finite(y, nv) ? MMPR_STAT_OK : 1;
+}
+
+// ---- Dormand-Prince 5(4), FSAL, PI step control (rk54.py:16-129) ----------
+__constant__ double c_dp_c[7] = {0.0, 1.0 / 5, 3.0 / 10, 4.0 / 5, 8.0 / 9, 1.0, 1.0};
+__constant__ double c_dp_a[7][6] = {
+    {0, 0, 0, 0, 0, 0},
+    {1.0 / 5, 0, 0, 0, 0, 0},
+    {3.0 / 40, 9.0 / 40, 0, 0, 0, 0},
+    {44.0 / 45, -56.0 / 15, 32.0 / 9, 0, 0, 0},
+    {19372.0 / 6561, -25360.0 / 2187, 64448.0 / 6561, -212.0 / 729, 0, 0},
+    {9017.0 / 3168, -355.0 / 33, 46732.0 / 5247, 49.0 / 176, -5103.0 / 18656, 0},
+    {35.0 / 384, 0.0, 500.0 / 1113, 125.0 / 192, -2187.0 / 6784, 11.0 / 84}};
+__constant__ double c_dp_b5[7] = {35.0 / 384, 0.0, 500.0 / 1113, 125.0 / 192, -2187.0 / 6784, 11.0 / 84, 0.0};
+__constant__ double c_dp_b4[7] = {5179.0 / 57600, 0.0, 7571.0 / 16695, 393.0 / 640, -92097.0 / 339200,
+                                  187.0 / 2100, 1.0 / 40};
+
+__device__ double rms_norm(const double *e, const double *scale, int nv) {
+  double q[CS_MAXV];
+  for (int v = 0; v < nv; ++v) {
+    const double r = div(e[v], scale[v]);
+    q[v] = mul(r, r);
+  }
+  return __dsqrt_rn(div(small_pairwise(q, nv), (double)nv));
+}
+
+__device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &model, const mmpr_integrator &cfg,
+                              double t0, double t1, double *y) {
+  const int nv = 3 * ode.n_regions;
+  const double span = sub(t1, t0);
+  if (span < 0.0) return 1;
+  if (span == 0.0) return MMPR_STAT_OK;
+  double t = t0;
+  double k[7][CS_MAXV];
+  ode_rhs(ode, model, t, y, k[0]);
+  if (!all_finite(k[0], nv)) return 1;
+  double h;
+  if (cfg.first_step > 0.0) {
+    h = cfg.first_step;
+  } else {  // _initial_step
+    double sc[CS_MAXV];
+    for (int v = 0; v < nv; ++v) sc[v] = add(cfg.abs_tol, mul(cfg.rel_tol, fabs(y[v])));
+    const double d0 = rms_norm(y, sc, nv), d1 = rms_norm(k[0], sc, nv);
+    h = (d0 < 1e-5 || d1 < 1e-5) ? 1e-6 : div(mul(0.01, d0), d1);
+  }
+  h = fmin(h, span);
+  double err_prev = 1.0;
+  const double min_step = mul(1e-14, fmax(fmax(fabs(t0), fabs(t1)), 1.0));
+  for (int it = 0; it < cfg.max_steps; ++it) {
+    h = fmin(h, sub(t1, t));
+    double yi[CS_MAXV];
+    for (int i = 1; i < 7; ++i) {
+      for (int v = 0; v < nv; ++v) {
+        double acc;
+        if (i == 1) {
+          acc = mul(c_dp_a[1][0], k[0][v]);
+        } else {
+          acc = mul(c_dp_a[i][0], k[0][v]);
+          for (int l = 1; l < i; ++l) acc = add(acc, mul(c_dp_a[i][l], k[l][v]));
+        }
+        yi[v] = add(y[v], mul(h, acc));
+      }
+      ode_rhs(ode, model, add(t, mul(c_dp_c[i], h)), yi, k[i]);
+    }
+    double y5[CS_MAXV], err[CS_MAXV], sc[CS_MAXV];
+    for (int v = 0; v < nv; ++v) {
+      double b5 = mul(c_dp_b5[0], k[0][v]), e = mul(sub(c_dp_b5[0], c_dp_b4[0]), k[0][v]);
+      for (int l = 1; l < 7; ++l) {
+        b5 = add(b5, mul(c_dp_b5[l], k[l][v]));
+        e = add(e, mul(sub(c_dp_b5[l], c_dp_b4[l]), k[l][v]));
+      }
+      y5[v] = add(y[v], mul(h, b5));
+      err[v] = mul(h, e);
+    }
+    if (!all_finite(y5, nv)) return 1;
+    for (int v = 0; v < nv; ++v) sc[v] = add(cfg.abs_tol, mul(cfg.rel_tol, fmax(fabs(y[v]), fabs(y5[v]))));
+    const double err_norm = rms_norm(err, sc, nv);
+    if (err_norm <= 1.0) {
+      t = add(t, h);
+      for (int v = 0; v < nv; ++v) {
+        y[v] = y5[v];
+        k[0][v] = k[6][v];
+      }
+      if (t >= sub(t1, min_step)) return MMPR_STAT_OK;
+      const double en = fmax(err_norm, 1e-10);
+      const double factor = mul(mul(0.9, pow(en, -(0.7 / 5.0))), pow(err_prev, 0.4 / 5.0));
+      err_prev = en;
+      h = mul(h, fmin(5.0, fmax(0.2, factor)));
+    } else {
+      const double factor = mul(0.9, pow(err_norm, -(0.7 / 5.0)));
+      h = mul(h, fmin(1.0, fmax(0.2, factor)));
+    }
+    if (h < min_step) return 1;
+  }
+  return 1;
+}
+
+__device__ int coarse_step(const mmpr_moment_ode &ode, const mmpr_model &model, const mmpr_integrator &integ,
+                           double t0, double t1, double *y) {
+  if (integ.kind == MMPR_INTEG_EULER) return integrate_euler(ode, model, integ.dt, t0, t1, y);
+  return integrate_dp54(ode, model, integ, t0, t1, y);
+}
+
+struct CoarseParams {
+  mmpr_moment_ode ode;
+  mmpr_model model;
+  mmpr_integrator integ;
+  int n;
+  const double *times;
+  int iteration;
+  const double *rho0;
+  const double *fine;
+  const double *cache_in;
+  double *macro_out;
+  double *cache_out;
+  double *raw_out;
+  int32_t *status;
+  int skip_until;
+};
+
+__global__ void coarse_row_kernel(const CoarseParams p) {
+  if (threadIdx.x != 0) return;
+  const int I = p.ode.n_regions, nv = 3 * I;
+  double cur[CS_MAXV];
+  for (int v = 0; v < nv; ++v) {
+    cur[v] = p.rho0[v];
+    p.macro_out[v] = cur[v];
+  }
+  for (int n = 0; n < p.n; ++n) {
+    double pred[CS_MAXV];
+    int st = MMPR_STAT_OK;
+    if (p.iteration >= 1 && n < p.skip_until) {
+      for (int v = 0; v < nv; ++v) pred[v] = p.cache_in[n * nv + v];
+    } else {
+      for (int v = 0; v < nv; ++v) pred[v] = cur[v];
+      st = coarse_step(p.ode, p.model, p.integ, p.times[n], p.times[n + 1], pred);
+    }
+    p.status[n] = st;
+    for (int v = 0; v < nv; ++v) p.cache_out[n * nv + v] = pred[v];
+    if (p.iteration == 0) {
+      for (int v = 0; v < nv; ++v) cur[v] = pred[v];
+    } else {
+      const double *f = p.fine + n * nv;
+      const double *c = p.cache_in + n * nv;
+      double raw[CS_MAXV];
+      for (int v = 0; v < nv; ++v) raw[v] = add(f[v], sub(pred[v], c[v]));
+      for (int v = 0; v < nv; ++v) p.raw_out[n * nv + v] = raw[v];
+      bool neg = false;
+      for (int i = 0; i < I; ++i) neg |= raw[I + i] < 0.0;
+      for (int i = 0; i < I; ++i) {
+        cur[i] = raw[i];
+        cur[I + i] = (neg && raw[I + i] < 0.0) ? 0.0 : raw[I + i];
+        cur[2 * I + i] = f[2 * I + i];  // fractions from the fine restriction
+      }
+    }
+    for (int v = 0; v < nv; ++v) p.macro_out[(n + 1) * nv + v] = cur[v];
+  }
+}
+
+__global__ void integrate_macro_kernel(const mmpr_moment_ode ode, const mmpr_model model,
+                                       const mmpr_integrator integ, int n_states, const double *t0,
+                                       const double *t1, const double *in, double *out, int32_t *status) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_states) return;
+  const int nv = 3 * ode.n_regions;
+  double y[CS_MAXV];
+  for (int v = 0; v < nv; ++v) y[v] = in[s * nv + v];
+  const int st = coarse_step(ode, model, integ, t0[s], t1[s], y);
+  for (int v = 0; v < nv; ++v) out[s * nv + v] = y[v];
+  status[s] = st;
+}
+
+}  // namespace mmpr
+
+using namespace mmpr;
+
+static int check_ode(const mmpr_moment_ode *ode, const mmpr_integrator *integ) {
+  if (!ode || !integ) return MMPR_ERR_ARG;
+  if (ode->n_regions < 1 || ode->n_regions > MMPR_MAX_REGIONS) return MMPR_ERR_ARG;
+  if (ode->kind < MMPR_ODE_UNIMODAL || ode->kind > MMPR_ODE_GAUSSIAN_CUBIC) return MMPR_ERR_UNSUPPORTED;
+  if (ode->kind != MMPR_ODE_MULTIMODAL && ode->n_regions != 1) return MMPR_ERR_ARG;
+  if (integ->kind == MMPR_INTEG_EULER) {
+    if (!(integ->dt > 0.0)) return MMPR_ERR_ARG;
+  } else if (integ->kind == MMPR_INTEG_DP54) {
+    if (!(integ->rel_tol > 0.0) || !(integ->abs_tol > 0.0) || integ->max_steps < 1) return MMPR_ERR_ARG;
+  } else {
+    return MMPR_ERR_UNSUPPORTED;
+  }
+  return MMPR_OK;
+}
+
+extern "C" int mmpr_coarse_row(const mmpr_moment_ode *ode, const mmpr_model *model, const mmpr_integrator *integ,
+                               int32_t n_slices, const double *times, int32_t iteration, const double *rho0,
+                               const double *fine_stats, const double *cache_in, double *macro_out,
+                               double *cache_out, double *raw_out, int32_t *status, int32_t skip_until,
+                               void *stream) {
+  int st = check_ode(ode, integ);
+  if (st != MMPR_OK) return st;
+  if (!model || n_slices < 0 || !times || !rho0 || !macro_out || !cache_out || !status) return MMPR_ERR_ARG;
+  if (iteration >= 1 && (!fine_stats || !cache_in || !raw_out)) return MMPR_ERR_ARG;
+  CoarseParams p;
+  p.ode = *ode;
+  p.model = *model;
+  p.integ = *integ;
+  p.n = n_slices;
+  p.times = times;
+  p.iteration = iteration;
+  p.rho0 = rho0;
+  p.fine = fine_stats;
+  p.cache_in = cache_in;
+  p.macro_out = macro_out;
+  p.cache_out = cache_out;
+  p.raw_out = raw_out;
+  p.status = status;
+  p.skip_until = skip_until;
+  coarse_row_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  return mmpr_check_launch("coarse_row_kernel");
+}
+
+extern "C" int mmpr_integrate_macro(const mmpr_moment_ode *ode, const mmpr_model *model,
+                                    const mmpr_integrator *integ, int32_t n_states, const double *t0,
+                                    const double *t1, const double *state_in, double *state_out, int32_t *status,
+                                    void *stream) {
+  int st = check_ode(ode, integ);
+  if (st != MMPR_OK) return st;
+  if (!model || n_states < 0 || !t0 || !t1 || !state_in || !state_out || !status) return MMPR_ERR_ARG;
+  if (n_states == 0) return MMPR_OK;
+  const int threads = 64;
+  integrate_macro_kernel<<<(n_states + threads - 1) / threads, threads, 0, (cudaStream_t)stream>>>(
+      *ode, *model, *integ, n_states, t0, t1, state_in, state_out, status);
+  return mmpr_check_launch("integrate_macro_kernel");
+}

@@ -1,0 +1,442 @@
+// Fine propagator: Euler-Maruyama over one Parareal slice for many slices.
+//
+// Replaces particles.propagate_fine + _em_step_raw + ensemble_statistic
+// (/root/reference/pkg/src/mcparareal/particles.py:119-159,
+//  /root/reference/pkg/src/mcparareal/models.py:61-67) and the slice loop of
+// engine._fine_sweep (/root/reference/pkg/src/mcparareal/engine.py:110-124).
+//
+// Layout ("pairwise-leaf layout"): numpy's mean of P values is a fixed
+// binary tree whose leaves are blocks of <= 128 consecutive particles summed
+// by 8 interleaved accumulators.  Each leaf slot of the (padded) tree is
+// owned by 8 lanes; lane j holds particles off+j, off+j+8, ... in registers
+// for the whole slice, so
+//   * the per-step mean is bit-identical to np.mean (lane-sequential sums,
+//     xor-shuffle leaf combine, warp/CTA/cluster levels of the same tree);
+//   * increments are read from a per-CTA contiguous range staged in shared
+//     memory by 1-D bulk async copies (double-buffered, one step ahead);
+//   * a slice larger than one CTA (P > ~12.8k) spans a thread-block cluster
+//     and the tree's top levels are combined through DSMEM, one
+//     barrier.cluster per step.
+// Increments come from HBM: the numpy-exact FROZEN stream is materialised
+// once per run by noise.cu (or injected by the caller).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "mmpr_device.cuh"
+#include "capi_internal.h"
+
+namespace mmpr {
+
+#define FS_MAX_CLUSTER 16
+
+struct FineParams {
+  mmpr_model model;
+  int n_slices;
+  int S;
+  int64_t P;
+  double dt, sqrt_dt, bsd;  // bsd = b*sqrt(dt) for constant-diffusion models
+  const double *t0;
+  const double *x_in;
+  int64_t in_pitch;
+  double *x_out;
+  int64_t out_pitch;
+  const double *xi;
+  int64_t xi_slice_pitch, xi_row_pitch;
+  int32_t *bad_step;
+  double *final_mean;
+  int D;              // tree depth (2^D leaf slots)
+  int slots_per_cta;  // 4 * warps per CTA
+  int ctas;           // CTAs per slice (cluster size)
+  int stage_elems;    // doubles per smem stage (16-B multiple)
+};
+
+struct ClusterSlot {
+  double v;
+  int ok;
+  int bad;
+};
+
+template <int KIND>
+__device__ __forceinline__ double em_update(const FineParams &p, double x, double s, double xi) {
+  // x + a(x,s)*dt + b(x,s)*sqrt(dt)*xi, left to right, each op rounded
+  mmpr_model m = p.model;
+  m.kind = KIND;  // folds the family switch at compile time
+  const double a = drift(m, x, s);
+  const double moved = add(x, mul(a, p.dt));
+  double noise;
+  if (constant_diffusion(KIND)) {
+    noise = mul(p.bsd, xi);
+  } else {
+    noise = mul(mul(diffusion(m, x, s), p.sqrt_dt), xi);
+  }
+  return add(moved, noise);
+}
+
+// PPT: accumulator elements per lane (ceil(max leaf / 8) <= 16)
+template <int KIND, int PPT>
+__global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p) {
+  extern __shared__ __align__(128) double s_stage[];  // [2][stage_elems]
+  __shared__ PwVal s_wp[32];
+  __shared__ PwVal s_cta;
+  __shared__ ClusterSlot s_slot[2][FS_MAX_CLUSTER];
+  __shared__ int s_bad[2];
+  __shared__ __align__(8) uint64_t s_bar[2];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int rank = (p.ctas > 1) ? (int)cluster_ctarank() : 0;
+  const int slice = blockIdx.x / p.ctas;
+  const int64_t nslots = int64_t(1) << p.D;
+
+  // ---- my leaf --------------------------------------------------------------
+  const int64_t slot = (int64_t)rank * p.slots_per_cta + warp * 4 + (lane >> 3);
+  const int j8 = lane & 7;
+  int64_t off = 0, len = 0;
+  if (slot < nslots) pw_leaf(p.P, p.D, slot, &off, &len);
+  const int cnt = (int)(len >> 3);       // elements per lane in the 8-way part
+  const int tail = (int)(len & 7);       // trailing elements added one by one
+  const int64_t tail_off = off + (len & ~int64_t(7));
+  const bool slot_ok = len > 0;
+  const bool warp_has_tail = __any_sync(MMPR_FULL_MASK, tail > 0);
+
+  int64_t lo, hi;
+  {
+    int64_t o2, l2;
+    pw_leaf(p.P, p.D, (int64_t)rank * p.slots_per_cta, &lo, &l2);
+    if (rank == p.ctas - 1) hi = p.P;
+    else pw_leaf(p.P, p.D, (int64_t)(rank + 1) * p.slots_per_cta, &hi, &o2);
+  }
+  const uint32_t stage_bytes = (uint32_t)((((hi - lo) * 8) + 15) & ~int64_t(15));
+
+  // ---- load positions --------------------------------------------------------
+  double x[PPT];
+  double xt = 0.0;
+  const double *xin = p.x_in + (int64_t)slice * p.in_pitch;
+#pragma unroll
+  for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? xin[off + j8 + 8 * m] : 0.0;
+  if (j8 < tail) xt = xin[tail_off + j8];
+
+  // ---- increment pipeline -------------------------------------------------------
+  const double *xi_slice = p.xi + (int64_t)slice * p.xi_slice_pitch;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+    s_bad[0] = 0;
+    s_bad[1] = 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < 2 && j < p.S; ++j) {
+      mbar_arrive_expect_tx(&s_bar[j], stage_bytes);
+      bulk_g2s(s_stage + j * p.stage_elems, xi_slice + j * p.xi_row_pitch + lo, stage_bytes, &s_bar[j]);
+    }
+  }
+  int issued = (p.S < 2) ? p.S : 2;
+
+  // ---- reduction of sum(x) in numpy order + non-finite flag -------------------
+  // Barriers per call: B1 (__syncthreads) and B2 (__syncthreads, or the
+  // cluster barrier).  s_bad is double-buffered by call parity: slot r&1 is
+  // written before B1 of call r and reset (for call r+2) after B1 of r+1.
+  auto reduce = [&](int r, int bad_local, double &mean_out, int &bad_out) {
+    const int par = r & 1;
+    double acc = 0.0;
+    if (cnt > 0) {
+      acc = x[0];
+#pragma unroll
+      for (int m = 1; m < PPT; ++m)
+        if (m < cnt) acc = add(acc, x[m]);
+      acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 1));
+      acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 2));
+      acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 4));
+    }
+    // a leaf shorter than 8 (P < 8) is summed sequentially from 0.0
+    if (warp_has_tail) {
+#pragma unroll
+      for (int i = 0; i < 7; ++i) {
+        const double v = __shfl_sync(MMPR_FULL_MASK, xt, (lane & ~7) | i);
+        if (i < tail) acc = add(acc, v);
+      }
+    }
+    PwVal leaf;
+    leaf.v = acc;
+    leaf.ok = slot_ok ? 1 : 0;
+    const int wbad = __any_sync(MMPR_FULL_MASK, bad_local);
+    leaf = pw_xor_level(leaf, lane, 8);
+    leaf = pw_xor_level(leaf, lane, 16);
+    if (lane == 0) {
+      s_wp[warp] = leaf;
+      if (wbad) s_bad[par] = 1;
+    }
+    __syncthreads();  // B1
+    if (warp == 0) {
+      PwVal v;
+      if (lane < nwarps) v = s_wp[lane];
+      else { v.v = 0.0; v.ok = 0; }
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1)
+        if (m < nwarps) v = pw_xor_level(v, lane, m);
+      if (lane == 0) {
+        s_cta = v;
+        s_bad[par ^ 1] = 0;
+      }
+    }
+    PwVal total;
+    int bad;
+    if (p.ctas == 1) {
+      __syncthreads();  // B2
+      total = s_cta;
+      bad = s_bad[par];
+    } else {
+      if (tid == 0) {
+        const uint32_t local = smem_addr(&s_slot[par][rank]);
+        const uint32_t badv = (uint32_t)s_bad[par];
+        for (int q = 0; q < p.ctas; ++q) {
+          const uint32_t remote = mapa_shared(local, (uint32_t)q);
+          st_cluster_f64(remote, s_cta.v);
+          st_cluster_u32(remote + 8, (uint32_t)s_cta.ok);
+          st_cluster_u32(remote + 12, badv);
+        }
+      }
+      cluster_sync_all();  // B2
+      // every warp combines the per-CTA partials with the same xor tree
+      PwVal v;
+      v.v = 0.0;
+      v.ok = 0;
+      int b = 0;
+      if (lane < p.ctas) {
+        v.v = s_slot[par][lane].v;
+        v.ok = s_slot[par][lane].ok;
+        b = s_slot[par][lane].bad;
+      }
+#pragma unroll
+      for (int m = 1; m < FS_MAX_CLUSTER; m <<= 1)
+        if (m < p.ctas) v = pw_xor_level(v, lane, m);
+      total.v = __shfl_sync(MMPR_FULL_MASK, v.v, 0);
+      total.ok = 1;
+      bad = __any_sync(MMPR_FULL_MASK, b);
+    }
+    mean_out = div(total.v, (double)p.P);
+    bad_out = bad;
+  };
+
+  double s;
+  int bad;
+  reduce(0, 0, s, bad);
+
+  int first_bad = MMPR_STAT_OK;
+  const double t_start = p.t0[slice];
+  (void)t_start;
+  for (int j = 0; j < p.S; ++j) {
+    const int stage = j & 1;
+    mbar_wait_parity(&s_bar[stage], (uint32_t)((j >> 1) & 1));
+    const double *xs = s_stage + stage * p.stage_elems;
+    int bad_local = 0;
+#pragma unroll
+    for (int m = 0; m < PPT; ++m) {
+      if (m < cnt) {
+        x[m] = em_update<KIND>(p, x[m], s, xs[off - lo + j8 + 8 * m]);
+        bad_local |= !finite(x[m]);
+      }
+    }
+    if (j8 < tail) {
+      xt = em_update<KIND>(p, xt, s, xs[tail_off - lo + j8]);
+      bad_local |= !finite(xt);
+    }
+    // The first barrier inside reduce() orders every read of this stage
+    // before the refill issued below.
+    reduce(j + 1, bad_local, s, bad);
+    if (tid == 0 && j + 2 < p.S && !bad) {
+      mbar_arrive_expect_tx(&s_bar[stage], stage_bytes);
+      bulk_g2s(s_stage + stage * p.stage_elems, xi_slice + (int64_t)(j + 2) * p.xi_row_pitch + lo,
+               stage_bytes, &s_bar[stage]);
+      ++issued;
+    }
+    if (bad) {
+      first_bad = j;
+      break;
+    }
+  }
+  // Drain copies still in flight after an early exit.
+  if (tid == 0 && first_bad != MMPR_STAT_OK) {
+    for (int j = first_bad + 1; j < issued; ++j) mbar_wait_parity(&s_bar[j & 1], (uint32_t)((j >> 1) & 1));
+  }
+
+  double *xo = p.x_out + (int64_t)slice * p.out_pitch;
+#pragma unroll
+  for (int m = 0; m < PPT; ++m)
+    if (m < cnt) xo[off + j8 + 8 * m] = x[m];
+  if (j8 < tail) xo[tail_off + j8] = xt;
+  if (tid == 0 && rank == 0) {
+    p.bad_step[slice] = first_bad;
+    if (p.final_mean) p.final_mean[slice] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side geometry
+// ---------------------------------------------------------------------------
+struct FineGeometry {
+  int ppt;  // ceil(max leaf / 8)
+  int D;
+  int slots_per_cta;
+  int ctas;
+  int threads;
+  int stage_elems;
+  size_t smem_bytes;
+};
+
+static int fine_geometry(int64_t P, FineGeometry *g) {
+  if (P < 1) return MMPR_ERR_ARG;
+  g->D = pw_depth(P);
+  const int64_t nslots = int64_t(1) << g->D;
+  int64_t max_leaf = 0;
+  for (int64_t s = 0; s < nslots; ++s) {
+    int64_t o, l;
+    pw_leaf(P, g->D, s, &o, &l);
+    if (l > max_leaf) max_leaf = l;
+  }
+  g->ppt = (int)((max_leaf + 7) / 8);
+  const size_t smem_budget = 200 * 1024;
+  int spc = 128;
+  while (spc > 4 && (size_t)spc * max_leaf * 8 * 2 > smem_budget) spc >>= 1;
+  if (nslots <= spc) {
+    g->slots_per_cta = (int)(nslots < 4 ? 4 : nslots);
+    g->ctas = 1;
+  } else {
+    g->slots_per_cta = spc;
+    g->ctas = (int)(nslots / spc);
+  }
+  if (g->ctas > FS_MAX_CLUSTER) return MMPR_ERR_UNSUPPORTED;
+  g->threads = g->slots_per_cta * 8;
+  // largest per-CTA particle range
+  int64_t max_range = 0;
+  for (int c = 0; c < g->ctas; ++c) {
+    int64_t lo, hi, l;
+    pw_leaf(P, g->D, (int64_t)c * g->slots_per_cta, &lo, &l);
+    if (c == g->ctas - 1) hi = P;
+    else pw_leaf(P, g->D, (int64_t)(c + 1) * g->slots_per_cta, &hi, &l);
+    if (hi - lo > max_range) max_range = hi - lo;
+  }
+  g->stage_elems = (int)((max_range + 1) & ~int64_t(1));
+  g->smem_bytes = (size_t)g->stage_elems * 8 * 2;
+  return MMPR_OK;
+}
+
+template <int KIND, int PPT>
+static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t stream) {
+  auto kern = fine_sweep_kernel<KIND, PPT>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+  if (err != cudaSuccess) return mmpr_check(err, "fine_sweep: smem attribute");
+  if (g.ctas > 8) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err != cudaSuccess) return mmpr_check(err, "fine_sweep: non-portable cluster");
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p.n_slices * g.ctas), 1, 1);
+  cfg.blockDim = dim3((unsigned)g.threads, 1, 1);
+  cfg.dynamicSmemBytes = g.smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)g.ctas;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  err = cudaLaunchKernelEx(&cfg, kern, p);
+  return mmpr_check(err, "fine_sweep_kernel launch");
+}
+
+template <int PPT>
+static int dispatch_kind(const FineParams &p, const FineGeometry &g, cudaStream_t s) {
+  switch (p.model.kind) {
+    case MMPR_MODEL_OU: return launch_fine<MMPR_MODEL_OU, PPT>(p, g, s);
+    case MMPR_MODEL_LINEAR: return launch_fine<MMPR_MODEL_LINEAR, PPT>(p, g, s);
+    case MMPR_MODEL_DOUBLE_WELL: return launch_fine<MMPR_MODEL_DOUBLE_WELL, PPT>(p, g, s);
+    case MMPR_MODEL_CUBIC_MF: return launch_fine<MMPR_MODEL_CUBIC_MF, PPT>(p, g, s);
+    case MMPR_MODEL_DW_MULT: return launch_fine<MMPR_MODEL_DW_MULT, PPT>(p, g, s);
+    default: return MMPR_ERR_UNSUPPORTED;
+  }
+}
+
+}  // namespace mmpr
+
+using namespace mmpr;
+
+extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_t particles, int32_t steps,
+                               double dt, double sqrt_dt, const double *t0, const double *x_in,
+                               int64_t in_pitch, double *x_out, int64_t out_pitch, const double *xi,
+                               int64_t xi_slice_pitch, int64_t xi_row_pitch, int32_t *bad_step,
+                               double *final_mean, void *stream) {
+  if (!model || n_slices < 0 || particles < 1 || steps < 0 || !x_in || !x_out || !bad_step || !t0)
+    return MMPR_ERR_ARG;
+  if (n_slices == 0) return MMPR_OK;
+  if (steps > 0 && (!xi || (xi_row_pitch & 1) || xi_row_pitch < particles ||
+                    (reinterpret_cast<uintptr_t>(xi) & 15) || (steps > 1 && xi_slice_pitch < steps * xi_row_pitch)))
+    return MMPR_ERR_ARG;
+  if (model->stat_kind != 0) return MMPR_ERR_UNSUPPORTED;
+  FineGeometry g;
+  int st = fine_geometry(particles, &g);
+  if (st != MMPR_OK) return st;
+  FineParams p;
+  p.model = *model;
+  p.n_slices = n_slices;
+  p.S = steps;
+  p.P = particles;
+  p.dt = dt;
+  p.sqrt_dt = sqrt_dt;
+  p.bsd = 0.0;
+  switch (model->kind) {
+    case MMPR_MODEL_OU: p.bsd = model->p[2] * sqrt_dt; break;
+    case MMPR_MODEL_DOUBLE_WELL: p.bsd = model->p[4] * sqrt_dt; break;
+    case MMPR_MODEL_CUBIC_MF: p.bsd = model->p[3] * sqrt_dt; break;
+    default: break;
+  }
+  p.t0 = t0;
+  p.x_in = x_in;
+  p.in_pitch = in_pitch;
+  p.x_out = x_out;
+  p.out_pitch = out_pitch;
+  p.xi = xi;
+  p.xi_slice_pitch = xi_slice_pitch;
+  p.xi_row_pitch = xi_row_pitch;
+  p.bad_step = bad_step;
+  p.final_mean = final_mean;
+  p.D = g.D;
+  p.slots_per_cta = g.slots_per_cta;
+  p.ctas = g.ctas;
+  p.stage_elems = g.stage_elems;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (g.ppt <= 8) return dispatch_kind<8>(p, g, s);
+  if (g.ppt <= 13) return dispatch_kind<13>(p, g, s);
+  return dispatch_kind<16>(p, g, s);
+}
+
+extern "C" int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_out, int32_t *ctas_out) {
+  FineGeometry g;
+  int st = fine_geometry(particles, &g);
+  if (st != MMPR_OK) return st;
+  if (ctas_out) *ctas_out = g.ctas;
+  auto kern = fine_sweep_kernel<MMPR_MODEL_OU, 16>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+  if (err != cudaSuccess) return mmpr_check(err, "occupancy: smem attribute");
+  if (g.ctas > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)g.ctas, 1, 1);
+  cfg.blockDim = dim3((unsigned)g.threads, 1, 1);
+  cfg.dynamicSmemBytes = g.smem_bytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)g.ctas;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  err = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+  if (err != cudaSuccess) return mmpr_check(err, "cudaOccupancyMaxActiveClusters");
+  if (clusters_out) *clusters_out = n;
+  return MMPR_OK;
+}

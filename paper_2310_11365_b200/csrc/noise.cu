@@ -1,0 +1,357 @@
+// numpy-exact standard-normal streams on sm_100a.
+//
+// Replaces NoisePlan.normals / init_rng
+// (/root/reference/pkg/src/mcparareal/particles.py:49-65): every (slice,
+// step[, iteration]) address is its own numpy stream
+//   Generator(Philox(SeedSequence((seed, domain, n, j[, k])))).standard_normal(P)
+// and this file reproduces those streams bit-for-bit (libm-ulp caveat on the
+// ~2.6e-4 tail draws: log1p is CUDA's, not glibc's).
+//
+// One CTA materialises one stream.  The stream is a variable-length parse of
+// Philox words (a fast-accept word yields one normal; a wedge word consumes
+// its successor as a uniform; a tail word consumes pairs of successors), so
+// output i is not at word i.  Per chunk of 1024 words:
+//   1. each thread generates one Philox4x64 block (4 consecutive words) and
+//      classifies the words assuming each starts an attempt;
+//   2. each warp parses its 128 words from entry offset 0 by walking only the
+//      non-fast words (warp-uniform loop, ~3 iterations per chunk);
+//   3. warp 0 stitches the 8 speculative parses with the chunk carry (falls
+//      back to an exact sequential re-walk when a speculation is wrong);
+//   4. every produced normal is written at its exact stream position.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mmpr_device.cuh"
+#include "npstream.cuh"
+#include "capi_internal.h"
+
+namespace mmpr {
+
+__constant__ uint64_t c_zig_ki[256] = {NPZ_KI_VALUES};
+__constant__ double c_zig_wi[256] = {NPZ_WI_VALUES};
+__constant__ double c_zig_fi[256] = {NPZ_FI_VALUES};
+
+#define NF_THREADS 256
+#define NF_WARPS (NF_THREADS / 32)
+
+// ---------------------------------------------------------------------------
+// keys
+// ---------------------------------------------------------------------------
+__global__ void noise_keys_kernel(uint64_t seed, int fresh, int iteration, int n_offset, int n_slices,
+                                  int steps, uint64_t *keys) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n_slices * steps) return;
+  const int n = n_offset + (int)(i / steps);
+  const int j = (int)(i % steps);
+  uint32_t w[8];
+  int nw = np::push_int_words(w, 0, seed);
+  nw = np::push_int_words(w, nw, fresh ? 2u : 1u);  // _DOMAIN_STEP_FRESH / _FROZEN
+  nw = np::push_int_words(w, nw, (uint64_t)n);
+  nw = np::push_int_words(w, nw, (uint64_t)j);
+  if (fresh) nw = np::push_int_words(w, nw, (uint64_t)iteration);
+  uint64_t k0, k1;
+  np::seedseq_key(w, nw, k0, k1);
+  keys[2 * i] = k0;
+  keys[2 * i + 1] = k1;
+}
+
+struct EntropyWords {
+  uint32_t w[16];
+};
+
+__global__ void entropy_key_kernel(EntropyWords e, int n, uint64_t *key) {
+  uint64_t k0, k1;
+  np::seedseq_key(e.w, n, k0, k1);
+  key[0] = k0;
+  key[1] = k1;
+}
+
+// ---------------------------------------------------------------------------
+// stream parse helpers
+// ---------------------------------------------------------------------------
+// first set bit at position >= pos in a 128-bit mask, or -1
+__device__ __forceinline__ int next_set128(const uint32_t m[4], int pos) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (pos < 32 * (k + 1)) {
+      uint32_t v = m[k];
+      if (pos > 32 * k) v &= ~((1u << (pos - 32 * k)) - 1u);
+      if (v) return 32 * k + __ffs(v) - 1;
+    }
+  }
+  return -1;
+}
+
+// clear bits [lo, hi) (hi <= 128)
+__device__ __forceinline__ void clear_range128(uint32_t m[4], int lo, int hi) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int a = max(lo, 32 * k), b = min(hi, 32 * (k + 1));
+    if (a < b) {
+      const int n = b - a;
+      const uint32_t bits = (n == 32) ? 0xffffffffu : (((1u << n) - 1u) << (a - 32 * k));
+      m[k] &= ~bits;
+    }
+  }
+}
+
+// bits at positions >= e kept
+__device__ __forceinline__ uint32_t mask_ge(int k, int e) {
+  if (e <= 32 * k) return 0xffffffffu;
+  if (e >= 32 * (k + 1)) return 0u;
+  return ~((1u << (e - 32 * k)) - 1u);
+}
+
+// Exact sequential parse of one warp range from entry `e` (< 128) using the
+// stored non-fast mask and token lengths: returns start mask and exit.
+__device__ int rewalk(const uint32_t na[4], const uint16_t *len, int e, uint32_t S[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) S[k] = mask_ge(k, e);
+  int pos = e;
+  for (;;) {
+    const int b = next_set128(na, pos);
+    if (b < 0) return 0;
+    const int L = len[b];
+    clear_range128(S, b + 1, min(b + L, 128));
+    pos = b + L;
+    if (pos >= 128) return pos - 128;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// stream fill kernel
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NF_THREADS)
+normals_fill_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__restrict__ out,
+                    int64_t pitch, int affine, double loc, double scale) {
+  __shared__ ulonglong2 zig[256];
+  __shared__ uint32_t s_spec[NF_WARPS][4];  // speculative starts (entry 0)
+  __shared__ uint32_t s_prod[NF_WARPS][4];  // words that yield a normal if they start
+  __shared__ uint32_t s_nonfast[NF_WARPS][4];
+  __shared__ uint32_t s_final[NF_WARPS][4];
+  __shared__ __align__(16) uint16_t s_len[NF_THREADS * 4];
+  __shared__ int s_exit[NF_WARPS];
+  __shared__ int s_base[NF_WARPS];
+  __shared__ int s_carry, s_total;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t k0 = keys[2 * blockIdx.x], k1 = keys[2 * blockIdx.x + 1];
+  double *o = out + (int64_t)blockIdx.x * pitch;
+
+  for (int i = tid; i < 256; i += NF_THREADS)
+    zig[i] = make_ulonglong2(c_zig_ki[i], (unsigned long long)__double_as_longlong(c_zig_wi[i]));
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+
+  int64_t produced = 0;
+  for (uint64_t chunk = 0; produced < count; ++chunk) {
+    const uint64_t blk = chunk * NF_THREADS + tid;
+    const uint64_t word0 = blk * 4;
+    uint64_t w[4];
+    np::philox_block(blk, k0, k1, w);
+    const uint64_t succ = __shfl_down_sync(MMPR_FULL_MASK, w[0], 1);
+
+    double val[4];
+    uint32_t nonfast = 0, prod = 0;
+    uint16_t lens[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t r = w[q];
+      const int layer = (int)(r & 0xff);
+      const uint64_t mant = (r >> 9) & 0x000fffffffffffffULL;
+      const ulonglong2 z = zig[layer];
+      const double wi = __longlong_as_double((long long)z.y);
+      // (double)mant * wi, one rounding: (2^52 + mant) * wi - 2^52 * wi
+      double x = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi,
+                          -0x1.0p52 * wi);
+      if ((r >> 8) & 1) x = -x;
+      lens[q] = 1;
+      if (mant >= z.x) {
+        nonfast |= 1u << q;
+        if (layer != 0) {  // wedge: one more uniform
+          uint64_t u64;
+          if (q < 3) u64 = w[q + 1];
+          else if (lane < 31) u64 = succ;
+          else u64 = np::philox_word(word0 + 4, k0, k1);
+          const double u = np::unit_double(u64);
+          const double lhs = add(mul(sub(c_zig_fi[layer - 1], c_zig_fi[layer]), u), c_zig_fi[layer]);
+          if (lhs < exp(mul(mul(-0.5, x), x))) prod |= 1u << q;
+          lens[q] = 2;
+        } else {  // tail
+          uint64_t i = word0 + q + 1;
+          for (;;) {
+            const uint64_t a = ((i >> 2) == blk) ? w[i & 3] : np::philox_word(i, k0, k1);
+            ++i;
+            const uint64_t b = ((i >> 2) == blk) ? w[i & 3] : np::philox_word(i, k0, k1);
+            ++i;
+            const double xx = mul(-NPZ_INV_R, log1p(-np::unit_double(a)));
+            const double yy = -log1p(-np::unit_double(b));
+            if (add(yy, yy) > mul(xx, xx)) {
+              x = ((mant >> 8) & 1) ? -add(NPZ_R, xx) : add(NPZ_R, xx);
+              break;
+            }
+          }
+          prod |= 1u << q;
+          const uint64_t L = i - (word0 + q);
+          lens[q] = (uint16_t)(L < 0xffffu ? L : 0xffffu);
+        }
+      } else {
+        prod |= 1u << q;
+      }
+      val[q] = x;
+    }
+    *reinterpret_cast<ushort4 *>(&s_len[4 * tid]) = make_ushort4(lens[0], lens[1], lens[2], lens[3]);
+
+    // 128-bit masks over this warp's words (bit b = word 4*lane+q)
+    const int sh = 4 * (lane & 7);
+    uint32_t NF[4], PR[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      NF[k] = __reduce_or_sync(MMPR_FULL_MASK, (lane >> 3) == k ? (nonfast << sh) : 0u);
+      PR[k] = __reduce_or_sync(MMPR_FULL_MASK, (lane >> 3) == k ? (prod << sh) : 0u);
+    }
+    const uint64_t lens_packed = (uint64_t)lens[0] | ((uint64_t)lens[1] << 16) |
+                                 ((uint64_t)lens[2] << 32) | ((uint64_t)lens[3] << 48);
+
+    // speculative parse from entry 0 (warp-uniform)
+    uint32_t S[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+    int exit0 = 0;
+    {
+      int pos = 0;
+      for (;;) {
+        const int b = next_set128(NF, pos);
+        if (b < 0) break;
+        const uint64_t lp = __shfl_sync(MMPR_FULL_MASK, lens_packed, b >> 2);
+        const int L = (int)((lp >> (16 * (b & 3))) & 0xffff);
+        clear_range128(S, b + 1, min(b + L, 128));
+        pos = b + L;
+        if (pos >= 128) {
+          exit0 = pos - 128;
+          break;
+        }
+      }
+    }
+    if (lane < 4) {
+      s_spec[warp][lane] = S[lane];
+      s_prod[warp][lane] = PR[lane];
+      s_nonfast[warp][lane] = NF[lane];
+    }
+    if (lane == 0) s_exit[warp] = exit0;
+    __syncthreads();
+
+    // stitch the 8 warp parses (warp 0)
+    if (warp == 0) {
+      const int me = lane < NF_WARPS ? lane : 0;
+      const int e = (me == 0) ? s_carry : s_exit[me - 1];
+      bool ok = true;
+      if (lane < NF_WARPS && e != 0)
+        ok = e < 128 && ((s_spec[me][e >> 5] >> (e & 31)) & 1u);
+      if (__all_sync(MMPR_FULL_MASK, ok)) {
+        int cnt = 0;
+        if (lane < NF_WARPS) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t F = s_spec[me][k] & mask_ge(k, e);
+            s_final[me][k] = F;
+            cnt += __popc(F & s_prod[me][k]);
+          }
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < NF_WARPS; d <<= 1) {
+          const int v = __shfl_up_sync(MMPR_FULL_MASK, incl, d);
+          if (lane >= d) incl += v;
+        }
+        if (lane < NF_WARPS) s_base[lane] = incl - cnt;
+        const int tot = __shfl_sync(MMPR_FULL_MASK, incl, NF_WARPS - 1);
+        __syncwarp();
+        if (lane == 0) {
+          s_total = tot;
+          s_carry = s_exit[NF_WARPS - 1];
+        }
+      } else if (lane == 0) {
+        int ent = s_carry, base = 0;
+        for (int wi = 0; wi < NF_WARPS; ++wi) {
+          uint32_t F[4];
+          int ex;
+          if (ent >= 128) {
+            F[0] = F[1] = F[2] = F[3] = 0u;
+            ex = ent - 128;
+          } else if (ent == 0 || ((s_spec[wi][ent >> 5] >> (ent & 31)) & 1u)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) F[k] = s_spec[wi][k] & mask_ge(k, ent);
+            ex = s_exit[wi];
+          } else {
+            uint32_t na[4] = {s_nonfast[wi][0], s_nonfast[wi][1], s_nonfast[wi][2], s_nonfast[wi][3]};
+            ex = rewalk(na, &s_len[wi * 128], ent, F);
+          }
+          s_base[wi] = base;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            s_final[wi][k] = F[k];
+            base += __popc(F[k] & s_prod[wi][k]);
+          }
+          ent = ex;
+        }
+        s_total = base;
+        s_carry = ent;
+      }
+    }
+    __syncthreads();
+
+    // scatter this thread's normals to their stream positions
+    uint32_t O[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) O[k] = s_final[warp][k] & PR[k];
+    const int64_t base = produced + s_base[warp];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int b = 4 * lane + q;
+      const int k = b >> 5;
+      if ((O[k] >> (b & 31)) & 1u) {
+        int rank = __popc(O[k] & ((1u << (b & 31)) - 1u));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          if (kk < k) rank += __popc(O[kk]);
+        const int64_t idx = base + rank;
+        if (idx < count) o[idx] = affine ? add(loc, mul(scale, val[q])) : val[q];
+      }
+    }
+    produced += s_total;
+    // s_final/s_base/s_total are rewritten only after the next chunk's first
+    // barrier, which every thread reaches after finishing this scatter.
+  }
+}
+
+}  // namespace mmpr
+
+using namespace mmpr;
+
+extern "C" int mmpr_noise_keys(uint64_t master_seed, int32_t fresh, int32_t iteration, int32_t n_offset,
+                               int32_t n_slices, int32_t steps, uint64_t *keys, void *stream) {
+  if (n_slices < 0 || steps < 0 || n_offset < 0 || !keys) return MMPR_ERR_ARG;
+  const int64_t total = (int64_t)n_slices * steps;
+  if (total == 0) return MMPR_OK;
+  const int threads = 128;
+  const int64_t blocks = (total + threads - 1) / threads;
+  noise_keys_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(master_seed, fresh, iteration,
+                                                                           n_offset, n_slices, steps, keys);
+  return mmpr_check_launch("noise_keys_kernel");
+}
+
+extern "C" int mmpr_entropy_key(const uint32_t *words, int32_t n_words, uint64_t *key_dev, void *stream) {
+  if (!words || n_words < 1 || n_words > 16 || !key_dev) return MMPR_ERR_ARG;
+  EntropyWords e;
+  for (int i = 0; i < 16; ++i) e.w[i] = i < n_words ? words[i] : 0u;
+  entropy_key_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(e, n_words, key_dev);
+  return mmpr_check_launch("entropy_key_kernel");
+}
+
+extern "C" int mmpr_normals_fill(const uint64_t *keys, int32_t n_streams, int64_t count, double *out,
+                                 int64_t pitch, int32_t affine, double loc, double scale, void *stream) {
+  if (n_streams < 0 || count < 0 || !keys || !out || (n_streams > 1 && pitch < count)) return MMPR_ERR_ARG;
+  if (n_streams == 0 || count == 0) return MMPR_OK;
+  normals_fill_kernel<<<n_streams, NF_THREADS, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, affine, loc,
+                                                                          scale);
+  return mmpr_check_launch("normals_fill_kernel");
+}
