@@ -1,0 +1,125 @@
+"""Thin, shape-checked wrappers of the libmmpr entry points over torch
+device tensors.  Stream-ordered; nothing here synchronises the host.
+
+All ensembles are float64 rows: a batch of E ensembles of P particles is a
+(E, P) tensor (row pitch = stride(0)); packed macro states are (E, 3I).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+from . import _lib
+from ._device import device, require_cuda, torch
+from .noise import row_pitch
+
+
+def _f64(t, name):
+    if t.dtype != torch.float64 or t.device.type != "cuda":
+        raise ValueError(f"{name} must be a float64 CUDA tensor")
+
+
+def _rows(t, name):
+    _f64(t, name)
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{name} must be a 2-D row-contiguous tensor")
+    return t.stride(0)
+
+
+def fine_sweep(model: _lib.Model, x_in, x_out, t0, steps: int, dt: float, xi, bad_step, final_mean=None,
+               stream=None) -> None:
+    """EM over ``steps`` steps for every row of x_in (E, P) -> x_out (E, P).
+    xi: (E, steps, pitch) increments; t0: (E,) float64; bad_step: (E,) int32."""
+    require_cuda()
+    E, P = x_in.shape
+    in_pitch = _rows(x_in, "x_in")
+    out_pitch = _rows(x_out, "x_out")
+    if x_out.shape != x_in.shape:
+        raise ValueError("x_out must match x_in")
+    _f64(xi, "xi")
+    if xi.dim() != 3 or xi.shape[0] != E or xi.shape[1] < steps or xi.stride(2) != 1:
+        raise ValueError("xi must be (E, >=steps, pitch)")
+    pitch = xi.stride(1)
+    if pitch < P or pitch % 2:
+        raise ValueError("xi row pitch must be even and >= P")
+    if bad_step.dtype != torch.int32 or bad_step.numel() < E:
+        raise ValueError("bad_step must be int32 (E,)")
+    _lib.call("mmpr_fine_sweep", ctypes.byref(model), int(E), int(P), int(steps), float(dt),
+              float(math.sqrt(dt)), t0.data_ptr(), x_in.data_ptr(), int(in_pitch), x_out.data_ptr(),
+              int(out_pitch), xi.data_ptr(), int(xi.stride(0)), int(pitch), bad_step.data_ptr(),
+              _lib.ptr(final_mean), _lib.stream_handle(stream))
+
+
+def restrict(part: _lib.Partition, x, stats, counts, scratch=None, stream=None) -> None:
+    """stats (E, 3I) and counts (E, I) int64 of every row of x (E, P)."""
+    require_cuda()
+    E, P = x.shape
+    pitch = _rows(x, "x")
+    I = part.n_regions
+    _f64(stats, "stats")
+    if stats.shape != (E, 3 * I) or not stats.is_contiguous():
+        raise ValueError("stats must be contiguous (E, 3I)")
+    if counts.dtype != torch.int64 or counts.shape != (E, I) or not counts.is_contiguous():
+        raise ValueError("counts must be contiguous int64 (E, I)")
+    if I > 1:
+        need = E * I * P
+        if scratch is None:
+            scratch = torch.empty(need, dtype=torch.float64, device=device())
+        elif scratch.numel() < need:
+            raise ValueError("scratch too small")
+    _lib.call("mmpr_restrict", ctypes.byref(part), int(E), int(P), x.data_ptr(), int(pitch), stats.data_ptr(),
+              counts.data_ptr(), _lib.ptr(scratch) if I > 1 else None, _lib.stream_handle(stream))
+
+
+def match(part: _lib.Partition, targets, cur_stats, cur_counts, x_src, x_out, policy: int, status, clamped=None,
+          stream=None) -> None:
+    """Affine per-region match of E ensembles.  x_src may have one row (shared
+    source, e.g. lift from ens0), as may cur_stats / cur_counts."""
+    require_cuda()
+    E, P = x_out.shape
+    out_pitch = _rows(x_out, "x_out")
+    src_pitch = _rows(x_src, "x_src") if x_src.shape[0] > 1 else 0
+    if x_src.shape[1] != P or x_src.shape[0] not in (1, E):
+        raise ValueError("x_src must be (1 or E, P)")
+    I = part.n_regions
+    for t, name in ((targets, "targets"), (cur_stats, "cur_stats")):
+        _f64(t, name)
+        if t.dim() != 2 or t.shape[1] != 3 * I or t.stride(1) != 1 or t.shape[0] not in (1, E):
+            raise ValueError(f"{name} must be (1 or E, 3I)")
+    tgt_stride = targets.stride(0) if targets.shape[0] > 1 else 0
+    cur_stride = cur_stats.stride(0) if cur_stats.shape[0] > 1 else 0
+    if cur_counts.dtype != torch.int64 or cur_counts.shape[1] != I or cur_counts.shape[0] not in (1, E):
+        raise ValueError("cur_counts must be int64 (1 or E, I)")
+    cnt_stride = cur_counts.stride(0) if cur_counts.shape[0] > 1 else 0
+    if status.dtype != torch.int32 or status.numel() < E:
+        raise ValueError("status must be int32 (E,)")
+    _lib.call("mmpr_match", ctypes.byref(part), int(E), int(P), targets.data_ptr(), int(tgt_stride),
+              cur_stats.data_ptr(), int(cur_stride), cur_counts.data_ptr(), int(cnt_stride), x_src.data_ptr(),
+              int(src_pitch), x_out.data_ptr(), int(out_pitch), int(policy), status.data_ptr(),
+              _lib.ptr(clamped), _lib.stream_handle(stream))
+
+
+def coarse_row(ode: _lib.MomentOde, model: _lib.Model, integ: _lib.Integrator, times, iteration: int, rho0,
+               fine_stats, cache_in, macro_out, cache_out, raw_out, status, skip_until: int = 0,
+               stream=None) -> None:
+    """One macro row of the mM iteration on the device (one warp)."""
+    require_cuda()
+    n = times.numel() - 1
+    _lib.call("mmpr_coarse_row", ctypes.byref(ode), ctypes.byref(model), ctypes.byref(integ), int(n),
+              times.data_ptr(), int(iteration), rho0.data_ptr(), _lib.ptr(fine_stats), _lib.ptr(cache_in),
+              macro_out.data_ptr(), cache_out.data_ptr(), _lib.ptr(raw_out), status.data_ptr(), int(skip_until),
+              _lib.stream_handle(stream))
+
+
+def integrate_macro(ode: _lib.MomentOde, model: _lib.Model, integ: _lib.Integrator, t0, t1, state_in, state_out,
+                    status, stream=None) -> None:
+    require_cuda()
+    n = state_in.shape[0]
+    _lib.call("mmpr_integrate_macro", ctypes.byref(ode), ctypes.byref(model), ctypes.byref(integ), int(n),
+              t0.data_ptr(), t1.data_ptr(), state_in.data_ptr(), state_out.data_ptr(), status.data_ptr(),
+              _lib.stream_handle(stream))
+
+
+def noise_buffer(n_slices: int, steps: int, P: int):
+    return torch.empty((n_slices, steps, row_pitch(P)), dtype=torch.float64, device=device())
