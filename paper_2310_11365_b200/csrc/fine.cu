@@ -141,17 +141,16 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
   // written before B1 of call r and reset (for call r+2) after B1 of r+1.
   auto reduce = [&](int r, int bad_local, double &mean_out, int &bad_out) {
     const int par = r & 1;
-    double acc = 0.0;
-    if (cnt > 0) {
-      acc = x[0];
+    double acc = x[0];
 #pragma unroll
-      for (int m = 1; m < PPT; ++m)
-        if (m < cnt) acc = add(acc, x[m]);
-      acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 1));
-      acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 2));
-      acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 4));
-    }
+    for (int m = 1; m < PPT; ++m)
+      if (m < cnt) acc = add(acc, x[m]);
+    // all 8 lanes of a slot hold cnt elements; shuffles stay warp-uniform
+    acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 1));
+    acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 2));
+    acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 4));
     // a leaf shorter than 8 (P < 8) is summed sequentially from 0.0
+    if (cnt == 0) acc = 0.0;
     if (warp_has_tail) {
 #pragma unroll
       for (int i = 0; i < 7; ++i) {

@@ -1,0 +1,222 @@
+"""Multi-GPU mM-Parareal: slices sharded across ranks (one process per GPU).
+
+Partition: rank r owns the contiguous slices [r*Ng, (r+1)*Ng).
+Per iteration the only traffic is
+  1. an all-gather of the owned slices' restricted fine moments
+     (Ng * 3I float64 per rank -- the coarse row needs all of them), and
+  2. a ring shift of ONE ensemble: rank r's last matched ensemble u_{b} is
+     the next iteration's input of rank r+1's first slice (engine.py:232-235).
+Every rank integrates the (cheap, serial) coarse row redundantly, so all
+ranks hold bit-identical macro rows; increments are generated per rank for
+its own global slice indices, so the sharded run is bit-identical to the
+single-GPU run of the same N.  Micro statistics and status arrays are
+gathered once, after the last iteration.
+
+The orchestration is written against a small backend interface so the same
+code runs the sm_100a kernels (``GpuBackend``, NCCL) and, in the CPU tests,
+the oracle (gloo).  Production uses ``GpuBackend`` only.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib, kernels
+from .engine import PararealConfig, PararealTrace, _build_trace, _raise_first_error, _StageTimer
+from .models import device_model
+from .moments import device_ode
+from .noise import row_pitch, slice_noise
+from .particles import NoisePlan, ParticleEnsemble, sample_initial
+from .rk54 import integrator_descriptor
+from .state import SINGLE_REGION
+
+
+class GpuBackend:
+    """sm_100a kernels on the rank's current CUDA device."""
+
+    def __init__(self, model, coarse, cfg: PararealConfig):
+        self.model_d = device_model(model)
+        self.ode_d, self.ode_model_d = device_ode(coarse)
+        self.integ_d = integrator_descriptor(cfg.integrator)
+        self.part_d = cfg.partition.descriptor()
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def empty(self, shape, dtype=torch.float64):
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def noise(self, seed, n_offset, n_slices, steps, P, iteration, fresh, out):
+        slice_noise(seed, n_offset, n_slices, steps, P, iteration, fresh, out=out)
+
+    def fine(self, x_in, x_out, t0, steps, dt, xi, bad):
+        kernels.fine_sweep(self.model_d, x_in, x_out, t0, steps, dt, xi, bad)
+
+    def restrict(self, x, stats, counts, scratch):
+        kernels.restrict(self.part_d, x, stats, counts, scratch)
+
+    def coarse_row(self, times, iteration, rho0, fine_stats, cache_in, macro_out, cache_out, raw_out, status,
+                   skip_until):
+        kernels.coarse_row(self.ode_d, self.ode_model_d, self.integ_d, times, iteration, rho0, fine_stats,
+                           cache_in, macro_out, cache_out, raw_out, status, skip_until)
+
+    def match(self, targets, cur, counts, src, out, policy, status):
+        kernels.match(self.part_d, targets, cur, counts, src, out, policy, status)
+
+    def restrict_single(self, x, stats, counts):
+        kernels.restrict(SINGLE_REGION.descriptor(), x, stats, counts)
+
+    def synchronize(self):
+        torch.cuda.synchronize()
+
+
+class TorchComm:
+    """torch.distributed collectives (NCCL on GPU ranks, gloo in CPU tests)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_gather_rows(self, local):
+        out = torch.empty((self.world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
+                          device=local.device)
+        dist.all_gather_into_tensor(out, local.contiguous(), group=self.group)
+        return out
+
+    def shift_right(self, send, recv):
+        """rank r -> r+1; rank 0 receives nothing, the last rank sends nothing."""
+        ops = []
+        if self.rank + 1 < self.world:
+            ops.append(dist.P2POp(dist.isend, send.contiguous(), self.rank + 1, group=self.group))
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.irecv, recv, self.rank - 1, group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def all_max(self, value: float) -> float:
+        t = torch.tensor([value], dtype=torch.float64,
+                         device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+
+def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: NoisePlan, comm=None,
+                            backend=None, reuse_converged_coarse: bool = True) -> PararealTrace:
+    """mM-Parareal over ``comm.world`` ranks; every rank returns the full
+    macro/micro trace, snapshots hold the rank's own slices only
+    (``trace.snapshots[k][m]`` is global slice boundary ``offset + m``)."""
+    comm = comm if comm is not None else TorchComm()
+    be = backend if backend is not None else GpuBackend(model, coarse, cfg)
+    R, G = comm.rank, comm.world
+    N, K, P, S, I = cfg.n_slices, cfg.iterations, cfg.particles, cfg.step.steps_per_slice, cfg.partition.n_regions
+    if N % G:
+        raise ValueError(f"n_slices={N} must be divisible by the world size {G}")
+    Ng = N // G
+    a = R * Ng
+    nv = 3 * I
+    dt = cfg.step.dt
+    times = tuple(cfg.t_start + n * cfg.slice_length for n in range(N + 1))
+    times_d = torch.tensor(times, dtype=torch.float64, device=be.device)
+    retain = cfg.retain_snapshots
+    i32, i64 = torch.int32, torch.int64
+
+    if isinstance(initial, ParticleEnsemble):
+        x0 = initial.device_positions.to(be.device).reshape(1, P)
+    elif hasattr(initial, "kind") and be.device.type == "cuda":
+        x0 = sample_initial(initial, plan, P).device_positions.reshape(1, P)
+    else:
+        x0 = torch.as_tensor(np.asarray(initial.sample(plan.init_rng(), P), dtype=float)).to(be.device).reshape(1, P)
+
+    snap = be.empty((K + 1 if retain else 2, Ng + 1, P))
+    fine = be.empty((Ng, P))
+    xi = be.empty((Ng, S, row_pitch(P)))
+    macro = be.empty((K + 1, N + 1, nv))
+    cache = be.empty((K + 1, N, nv))
+    raw = be.empty((max(K, 1), N, nv))
+    fine_all = be.empty((max(K, 1), N, nv))
+    fine_local = be.empty((Ng, nv))
+    fine_counts = be.empty((Ng, I), i64)
+    micro_local = be.empty((K + 1, Ng + 1, nv))
+    micro_counts_local = be.empty((K + 1, Ng + 1, I), i64)
+    bad_local = torch.full((max(K, 1), Ng), _lib.STAT_OK, dtype=i32, device=be.device)
+    coarse_status = torch.full((K + 1, N), _lib.STAT_OK, dtype=i32, device=be.device)
+    match_local = torch.full((K + 1, Ng), _lib.STAT_OK, dtype=i32, device=be.device)
+    lift_first = torch.full((1,), _lib.STAT_OK, dtype=i32, device=be.device)
+    rho0 = be.empty((1, nv))
+    counts0 = be.empty((1, I), i64)
+    scratch = be.empty(((Ng + 1) * I * P,)) if I > 1 else None
+
+    def sn(k):
+        return snap[k if retain else k % 2]
+
+    # iteration 0: redundant coarse cascade; each rank lifts its own boundaries
+    be.restrict(x0, rho0, counts0, scratch)
+    be.coarse_row(times_d, 0, rho0, None, None, macro[0], cache[0], None, coarse_status[0], 0)
+    be.match(macro[0, a + 1:a + Ng + 1], rho0, counts0, x0, sn(0)[1:], 1, match_local[0])
+    if a == 0:
+        sn(0)[0].copy_(x0[0])
+    else:
+        be.match(macro[0, a:a + 1], rho0, counts0, x0, sn(0)[0:1], 1, lift_first)
+    be.restrict(sn(0), micro_local[0], micro_counts_local[0], scratch)
+    if not plan.fresh:
+        be.noise(plan.master_seed, a, Ng, S, P, 0, False, xi)
+
+    stopped_at = None
+    done = 0
+    for k in range(K):
+        if plan.fresh:
+            be.noise(plan.master_seed, a, Ng, S, P, k, True, xi)
+        cur, nxt = sn(k), sn(k + 1)
+        be.fine(cur[:Ng], fine, times_d[a:a + Ng], S, dt, xi, bad_local[k])
+        be.restrict(fine, fine_local, fine_counts, scratch)
+        fine_all[k].copy_(comm.all_gather_rows(fine_local))
+        be.coarse_row(times_d, k + 1, rho0, fine_all[k], cache[k], macro[k + 1], cache[k + 1], raw[k],
+                      coarse_status[k + 1], (k + 1) if reuse_converged_coarse else 0)
+        be.match(macro[k + 1, a + 1:a + Ng + 1], fine_local, fine_counts, fine, nxt[1:], 0, match_local[k + 1])
+        if a == 0:
+            nxt[0].copy_(x0[0])
+        comm.shift_right(nxt[Ng], nxt[0])
+        be.restrict(nxt, micro_local[k + 1], micro_counts_local[k + 1], scratch)
+        done = k + 1
+        if cfg.stop_wasserstein_tol is not None:
+            diff = (torch.sort(nxt[1:], dim=1).values - torch.sort(cur[1:], dim=1).values).abs_()
+            st = be.empty((Ng, 3))
+            ct = be.empty((Ng, 1), i64)
+            be.restrict_single(diff, st, ct)
+            delta = comm.all_max(float(st[:, 0].max()))
+            if delta <= cfg.stop_wasserstein_tol:
+                stopped_at = k + 1
+                break
+
+    # gather micro statistics and per-slice statuses once
+    Kd = done
+    micro = be.empty((Kd + 1, N + 1, nv))
+    micro_counts = be.empty((Kd + 1, N + 1, I), i64)
+    for k in range(Kd + 1):
+        rows = comm.all_gather_rows(micro_local[k, 1:])
+        micro[k, 1:].copy_(rows)
+        micro[k, 0].copy_(rho0[0])
+        micro_counts[k, 1:].copy_(comm.all_gather_rows(micro_counts_local[k, 1:]))
+        micro_counts[k, 0].copy_(counts0[0])
+    bad = comm.all_gather_rows(bad_local.t().contiguous()).t() if K > 0 else bad_local
+    match_status = comm.all_gather_rows(match_local.t().contiguous()).t()
+    be.synchronize()
+    h = {"macro": macro[:Kd + 1].cpu().numpy(), "micro": micro.cpu().numpy(),
+         "micro_counts": micro_counts.cpu().numpy(), "fine_stats": fine_all[:max(Kd, 1)].cpu().numpy(),
+         "raw": raw[:max(Kd, 1)].cpu().numpy(), "bad": bad.cpu().numpy(),
+         "coarse_status": coarse_status.cpu().numpy(), "match_status": match_status.cpu().numpy(),
+         "rho0": rho0.cpu().numpy(), "counts0": counts0.cpu().numpy()}
+    _raise_first_error(h, N, Kd, I)
+
+    trace = _build_trace(h, None, dataclasses.replace(cfg, retain_snapshots=False), plan, times, Kd, I,
+                         _StageTimer(False), stopped_at)
+    if retain:
+        trace.snapshots = [[ParticleEnsemble._wrap(snap[k, m]) for m in range(Ng + 1)] for k in range(Kd + 1)]
+    trace.timings = {"slice_offset": a, "slices_per_rank": Ng}
+    return trace
+
+

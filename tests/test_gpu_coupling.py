@@ -1,0 +1,137 @@
+"""GPU parity: restriction and matching (coupling.cu) against the reference's
+golden vectors (bit-identical required: both are exact integer bookkeeping
+plus numpy's pairwise reductions and IEEE elementwise arithmetic)."""
+
+import logging
+
+import numpy as np
+import pytest
+
+from oracle import mm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mm():
+    import paper_2310_11365_b200 as mm
+    mm._lib.load()
+    return mm
+
+
+def _parts(mm):
+    return {"single": mm.RegionPartition(),
+            "two": mm.RegionPartition(separatrices=(0.0,), peaks=(-1.5, 1.5)),
+            "three": mm.RegionPartition(separatrices=(0.0, 2.0), peaks=(-1.0, 1.0, 3.0))}
+
+
+def test_restrict_matches_reference_golden(mm, golden):
+    g = golden("coupling")
+    parts = _parts(mm)
+    for en in g["ens_names"]:
+        ens = mm.ParticleEnsemble(g[f"ens_{en}"])
+        for pn, part in parts.items():
+            st = mm.restrict(ens, part)
+            ref = g[f"restrict_{pn}_{en}"]
+            assert np.array_equal(st.packed(), ref), (pn, en)
+            assert st.degenerate == tuple(g[f"restrict_{pn}_{en}_deg"]), (pn, en)
+
+
+def test_match_matches_reference_golden(mm, golden):
+    g = golden("coupling")
+    names = list(g["ens_names"])
+    parts = list(_parts(mm).values())
+    hp = g["hyp_part"]
+    parts.append(mm.RegionPartition(separatrices=(hp[0],), peaks=(hp[1], hp[2])))
+    for c in range(10):
+        pi, ei, collapse, status = (int(v) for v in g[f"match{c}_meta"])
+        part = parts[pi]
+        I = part.n_regions
+        t = g[f"match{c}_target"]
+        target = mm.MacroState(tuple(t[:I]), tuple(t[I:]), (1.0 / I,) * I)
+        ens = mm.ParticleEnsemble(g[f"ens_{names[ei]}"])
+        policy = "collapse" if collapse else "raise"
+        if status >= 0:
+            with pytest.raises(mm.DegenerateMatch) as err:
+                mm.match(target, ens, part, policy)
+            assert err.value.region == status
+        else:
+            out = mm.match(target, ens, part, policy)
+            assert np.array_equal(out.positions, g[f"match{c}_out"]), c
+
+
+def test_known_answers(mm):
+    out = mm.match(mm.MacroState((3.0,), (4.0,), (1.0,)), mm.ParticleEnsemble([-1.0, 1.0]))
+    np.testing.assert_allclose(out.positions, [1.0, 5.0])
+    part = mm.RegionPartition(separatrices=(0.0,), peaks=(-1.0, 1.0))
+    st = mm.region_statistics(mm.ParticleEnsemble([0.0, -1.0]), part)
+    assert st.fractions == (0.5, 0.5) and st.means[1] == 0.0
+    st = mm.region_statistics(mm.ParticleEnsemble([1.0, 2.0, 3.0]), part)
+    assert st.fractions == (0.0, 1.0) and st.means[0] == -1.0 and st.degenerate == (True, False)
+    assert mm.empirical_mean(mm.ParticleEnsemble([1.0, 2.0, 3.0, 4.0])) == 2.5
+    assert mm.empirical_variance(mm.ParticleEnsemble([1.0, 2.0, 3.0, 4.0])) == 1.25
+
+
+def test_negative_target_variance_clamped_with_warning(mm, caplog):
+    with caplog.at_level(logging.WARNING, logger="mcparareal.coupling"):
+        out = mm.match(mm.MacroState((2.0,), (-0.5,), (1.0,)), mm.ParticleEnsemble([-1.0, 0.0, 1.0]))
+    assert "clamping negative target variance" in caplog.text
+    np.testing.assert_array_equal(out.positions, np.full(3, 2.0))
+
+
+def test_degenerate_policies(mm):
+    ens = mm.ParticleEnsemble([2.0, 2.0])
+    target = mm.MacroState((5.0,), (1.0,), (1.0,))
+    with pytest.raises(mm.DegenerateMatch) as err:
+        mm.match(target, ens)
+    assert err.value.region == 0
+    np.testing.assert_array_equal(mm.match(target, ens, degenerate_policy="collapse").positions, [5.0, 5.0])
+    np.testing.assert_array_equal(mm.match(mm.MacroState((5.0,), (0.0,), (1.0,)), ens).positions, [5.0, 5.0])
+    with pytest.raises(ValueError):
+        mm.match(target, ens, degenerate_policy="typo")
+    with pytest.raises(ValueError):
+        mm.match(mm.MacroState((0.0, 1.0), (1.0, 1.0), (0.5, 0.5)), mm.ParticleEnsemble([0.0, 1.0]))
+
+
+@pytest.mark.parametrize("P", [2, 9, 129, 4097, 100_000])
+def test_match_restrict_identity_is_bitwise(mm, P):
+    rng = np.random.default_rng(P)
+    for part in _parts(mm).values():
+        x = rng.normal(0.5, 2.0, P)
+        ens = mm.ParticleEnsemble(x)
+        out = mm.match(mm.restrict(ens, part), ens, part, "collapse")
+        assert np.array_equal(out.positions, x)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_match_against_oracle(mm, seed):
+    rng = np.random.default_rng(1000 + seed)
+    P = int(rng.integers(2, 3000))
+    sep = float(rng.uniform(-1, 1))
+    part_m = mm.RegionPartition(separatrices=(sep,), peaks=(sep - 1.0, sep + 1.0))
+    part_o = O.Partition((sep,), (sep - 1.0, sep + 1.0))
+    x = rng.normal(0.0, float(rng.uniform(0.1, 3.0)), P)
+    if seed % 5 == 0:
+        x = np.round(x, 1)  # ties and repeated values
+    target = np.array([sep - 0.5, sep + 0.5, rng.uniform(1e-4, 2.0), rng.uniform(1e-4, 2.0), 0.5, 0.5])
+    st_ref, _ = O.restrict(x, part_o)
+    st = mm.restrict(mm.ParticleEnsemble(x), part_m)
+    assert np.array_equal(st.packed(), st_ref)
+    try:
+        ref, _ = O.match(target, x, part_o, "raise")
+    except O.OracleDegenerateMatch as e:
+        with pytest.raises(mm.DegenerateMatch) as err:
+            mm.match(mm.MacroState.from_packed(target, 2), mm.ParticleEnsemble(x), part_m)
+        assert err.value.region == e.region
+        return
+    out = mm.match(mm.MacroState.from_packed(target, 2), mm.ParticleEnsemble(x), part_m)
+    assert np.array_equal(out.positions, ref)
+
+
+def test_restrict_large_bimodal_against_oracle(mm):
+    rng = np.random.default_rng(9)
+    P = 1 << 20
+    x = np.where(rng.random(P) < 0.5, -1.0, 1.0) + 0.2 * rng.standard_normal(P)
+    part_m = mm.RegionPartition(separatrices=(0.0,), peaks=(-0.894427, 0.894427))
+    part_o = O.Partition((0.0,), (-0.894427, 0.894427))
+    assert np.array_equal(mm.restrict(mm.ParticleEnsemble(x), part_m).packed(), O.restrict(x, part_o)[0])

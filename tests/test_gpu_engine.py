@@ -1,0 +1,209 @@
+"""GPU parity: the full mM-Parareal run (fine + restrict + coarse + match on
+the device) against the reference's golden traces and the oracle.
+
+Tolerances (north star): trajectories 1e-12 relative (acceptance-1 metric),
+per-iteration moments 1e-10 relative.  Within the GPU implementation the
+k >= n exactness property is required bit for bit.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import mm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TRAJ_TOL = 1e-12
+MOM_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def mm():
+    import paper_2310_11365_b200 as mm
+    mm._lib.load()
+    return mm
+
+
+def _packed(trace, attr):
+    return np.array([[s.packed() for s in row] for row in getattr(trace, attr)])
+
+
+def _snap(trace):
+    return np.array([[e.positions for e in row] for row in trace.snapshots])
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b))) / max(1.0, float(np.max(np.abs(b))))
+
+
+def _check(trace, g, prefix, bitwise_macro=False):
+    macro, micro = _packed(trace, "macro"), _packed(trace, "micro_stats")
+    assert _rel(macro, g[prefix + "macro"]) <= MOM_TOL
+    assert _rel(micro, g[prefix + "micro"]) <= MOM_TOL
+    assert _rel(_snap(trace), g[prefix + "snap"]) <= TRAJ_TOL
+    if bitwise_macro:
+        assert np.array_equal(macro, g[prefix + "macro"])
+        assert np.array_equal(micro, g[prefix + "micro"])
+        assert np.array_equal(_snap(trace), g[prefix + "snap"])
+    assert np.array_equal(np.array(trace.lift_collapses, dtype=float).reshape(-1, 3), g[prefix + "lift"])
+    clamp = np.array(trace.clamp_events, dtype=float).reshape(-1, 4)
+    assert clamp.shape == g[prefix + "clamp"].shape
+    gaps = np.array(trace.fraction_gaps, dtype=float).reshape(-1, 3)
+    assert gaps.shape == g[prefix + "gaps"].shape
+    assert np.allclose(gaps, g[prefix + "gaps"], rtol=0, atol=1e-12)
+
+
+def _c1(mm, P=1000, N=10, K=5):
+    spec = mm.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5)
+    model = mm.make_perturbed_ou(spec)
+    cfg = mm.PararealConfig(n_slices=N, iterations=K, slice_length=0.1, particles=P,
+                            step=mm.StepConfig(dt=1e-3, steps_per_slice=100), integrator=mm.EulerConfig(1e-2))
+    return model, mm.unimodal_rhs(model), mm.InitialDistribution.normal(1.0, 0.01), cfg, mm.NoisePlan(0)
+
+
+def test_config1_shape_matches_reference(mm, golden):
+    g = golden("traces")
+    model, ode, init, cfg, plan = _c1(mm)
+    tr = mm.run_micro_macro(model, ode, init, cfg, plan)
+    _check(tr, g, "c1_", bitwise_macro=True)
+    seq = mm.sequential_fine(model, init, cfg, plan)
+    assert np.array_equal(np.array([e.positions for e in seq]), g["c1_seq"])
+
+
+def test_exactness_k_ge_n_bitwise(mm):
+    model, ode, init, cfg, plan = _c1(mm)
+    tr = mm.run_micro_macro(model, ode, init, cfg, plan)
+    seq = mm.sequential_fine(model, init, cfg, plan)
+    for k in range(1, cfg.iterations + 1):
+        for n in range(k + 1):
+            assert np.array_equal(tr.snapshots[k][n].positions, seq[n].positions), (k, n)
+
+
+def test_reuse_converged_coarse_is_bitwise_neutral(mm):
+    model, ode, init, cfg, plan = _c1(mm, P=3000)
+    a = mm.run_micro_macro(model, ode, init, cfg, plan, reuse_converged_coarse=True)
+    b = mm.run_micro_macro(model, ode, init, cfg, plan, reuse_converged_coarse=False)
+    assert np.array_equal(_packed(a, "macro"), _packed(b, "macro"))
+    assert np.array_equal(_snap(a), _snap(b))
+
+
+def test_retain_snapshots_off_same_moments(mm):
+    model, ode, init, cfg, plan = _c1(mm)
+    a = mm.run_micro_macro(model, ode, init, cfg, plan)
+    import dataclasses
+    cfg2 = dataclasses.replace(cfg, retain_snapshots=False)
+    b = mm.run_micro_macro(model, ode, init, cfg2, plan)
+    assert b.snapshots is None
+    assert np.array_equal(_packed(a, "macro"), _packed(b, "macro"))
+    assert np.array_equal(_packed(a, "micro_stats"), _packed(b, "micro_stats"))
+
+
+@pytest.mark.parametrize("prefix,ode_kind,seed", [("dp_", "perturbed", 77), ("dpu_", "unimodal", 78)])
+def test_reference_default_dp54(mm, golden, prefix, ode_kind, seed):
+    g = golden("traces")
+    spec = mm.PerturbedOUSpec(B=1.0)
+    model = mm.make_perturbed_ou(spec)
+    ode = mm.perturbed_ou_rhs(spec) if ode_kind == "perturbed" else mm.unimodal_rhs(model)
+    cfg = mm.PararealConfig(n_slices=6, iterations=4, slice_length=0.25, particles=500,
+                            step=mm.StepConfig(dt=0.05, steps_per_slice=5))
+    tr = mm.run_micro_macro(model, ode, mm.InitialDistribution.normal(1.0, 0.5), cfg, mm.NoisePlan(seed))
+    _check(tr, g, prefix)
+
+
+def _bimodal_init(mm):
+    return mm.bimodal_initial(-1.0, 1.0, 0.2)
+
+
+def test_config3_shape_matches_reference(mm, golden):
+    g = golden("traces")
+    dw = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.5)
+    model = mm.make_double_well(dw)
+    part = dw.default_partition()
+    ode = mm.multimodal_rhs(model, part, dw.potential, dw.sigma)
+    cfg = mm.PararealConfig(n_slices=8, iterations=4, slice_length=0.0625, particles=1000,
+                            step=mm.StepConfig(dt=2.0 ** -10, steps_per_slice=64), partition=part,
+                            integrator=mm.EulerConfig(2.0 ** -6))
+    tr = mm.run_micro_macro(model, ode, _bimodal_init(mm), cfg, mm.NoisePlan(0))
+    _check(tr, g, "c3_")
+    seq = mm.sequential_fine(model, _bimodal_init(mm), cfg, mm.NoisePlan(0))
+    assert _rel(np.array([e.positions for e in seq]), g["c3_seq"]) <= TRAJ_TOL
+
+
+def test_config2_shape_matches_reference(mm, golden):
+    g = golden("traces")
+    spec = mm.CubicMeanFieldSpec(1.0, 1.0, 1.0, 0.4)
+    model = mm.make_cubic_meanfield(spec)
+    cfg = mm.PararealConfig(n_slices=8, iterations=4, slice_length=0.0625, particles=1000,
+                            step=mm.StepConfig(dt=2.0 ** -10, steps_per_slice=64), integrator=mm.EulerConfig(2.0 ** -6))
+    tr = mm.run_micro_macro(model, mm.gaussian_closure_rhs(spec), mm.InitialDistribution.normal(0.5, 0.04), cfg,
+                            mm.NoisePlan(0))
+    _check(tr, g, "c2_", bitwise_macro=True)
+
+
+def test_config5_shape_matches_reference(mm, golden):
+    g = golden("traces")
+    dw = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.3 * math.sqrt(1.8))
+    model = mm.make_double_well_multiplicative(dw, 0.3)
+    part = dw.default_partition()
+    ode = mm.multimodal_rhs(model, part, dw.potential, dw.sigma)
+    cfg = mm.PararealConfig(n_slices=4, iterations=3, slice_length=0.1, particles=1000,
+                            step=mm.StepConfig(dt=5e-4, steps_per_slice=200), partition=part,
+                            integrator=mm.EulerConfig(1e-2))
+    tr = mm.run_micro_macro(model, ode, _bimodal_init(mm), cfg, mm.NoisePlan(0))
+    _check(tr, g, "c5_")
+
+
+def test_injected_increments_against_oracle(mm):
+    """Injected-increment mode: both sides consume the same seeded array."""
+    P, N, K, S = 2000, 6, 3, 20
+    rng = np.random.default_rng(4)
+    xi = rng.standard_normal((N, S, P))
+    model = mm.make_perturbed_ou(mm.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5))
+    cfg = mm.PararealConfig(n_slices=N, iterations=K, slice_length=S * 1e-3, particles=P,
+                            step=mm.StepConfig(1e-3, S), integrator=mm.EulerConfig(2e-3))
+    ens0 = rng.normal(1.0, 0.1, P)
+    tr = mm.run_micro_macro(model, mm.unimodal_rhs(model), mm.ParticleEnsemble(ens0), cfg, mm.NoisePlan(0),
+                            increments=lambda n, k: xi[n])
+    om = O.model_ou(-1.0, 0.5, 0.5)
+    ref = O.run_micro_macro(om, O.ode_unimodal(om), ens0, N, K, S * 1e-3, 1e-3, S, 0, integ=O.Euler(2e-3),
+                            noise=lambda n, k: xi[n])
+    assert np.array_equal(_packed(tr, "macro"), ref.macro)
+    assert np.array_equal(_snap(tr), np.array([[e for e in row] for row in ref.snapshots]))
+
+
+def test_config4_full_size_properties(mm):
+    """BASELINE config 4 at G=1 (N=64, P=1e5, S=100, K=5): size-independent
+    checks -- k >= n exactness (bitwise vs the GPU's own serial fine
+    solution), macro/micro consistency, and slice 0..1 against the oracle."""
+    N, P, K = 64, 100_000, 5
+    spec = mm.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5)
+    model = mm.make_perturbed_ou(spec)
+    cfg = mm.PararealConfig(n_slices=N, iterations=K, slice_length=0.1, particles=P,
+                            step=mm.StepConfig(dt=1e-3, steps_per_slice=100), integrator=mm.EulerConfig(1e-2))
+    plan = mm.NoisePlan(0)
+    init = mm.InitialDistribution.normal(1.0, 0.01)
+    tr = mm.run_micro_macro(model, mm.unimodal_rhs(model), init, cfg, plan)
+    seq = mm.sequential_fine(model, init, cfg, plan)
+    for k in range(1, K + 1):
+        for n in range(k + 1):
+            assert np.array_equal(tr.snapshots[k][n].positions, seq[n].positions), (k, n)
+    for k in range(K + 1):
+        for n in range(N + 1):
+            mac, mic = tr.macro[k][n], tr.micro_stats[k][n]
+            assert abs(mac.means[0] - mic.means[0]) < 1e-9 * max(1.0, abs(mac.means[0]))
+            assert abs(mac.variances[0] - mic.variances[0]) < 1e-9 * max(1.0, mac.variances[0])
+    ens0 = seq[0].positions
+    om = O.model_ou(-1.0, 0.5, 0.5)
+    x1 = O.propagate_fine(om, ens0, 0, 0.0, 1e-3, 100, O.slice_noise(0, 0, 100, P))
+    assert _rel(seq[1].positions, x1) <= TRAJ_TOL
+
+
+def test_blowup_raises_first_error_in_reference_order(mm):
+    model = mm.make_double_well(mm.DoubleWellSpec(sigma=0.0))
+    cfg = mm.PararealConfig(n_slices=4, iterations=2, slice_length=1.0, particles=16,
+                            step=mm.StepConfig(dt=0.5, steps_per_slice=2), integrator=mm.EulerConfig(0.5))
+    ens = mm.ParticleEnsemble(np.linspace(50.0, 60.0, 16))
+    with pytest.raises((mm.NumericalBlowup, mm.IntegrationFailure)):
+        mm.run_micro_macro(model, mm.unimodal_rhs(model), ens, cfg, mm.NoisePlan(0))
