@@ -1,0 +1,301 @@
+#!/usr/bin/env python
+"""Benchmark of the mM-Parareal hot path (BASELINE.json metric: fine-propagator
+particle-steps/s and Parareal iteration time at 1/2/4/8 B200).
+
+Workload (BASELINE config 4, the weak-scaling sweep the metric is quoted on):
+linear mean-field OU dX = (-X + 0.5 E[X]) dt + 0.5 dW, X0 ~ N(1, 0.1^2),
+P = 1e5 particles per slice, dt = 1e-3 (S = 100 steps per slice, T0 = 0.1),
+N = 64 slices per GPU (N = 64 G), K = 5 iterations, coarse = exact-closure
+mean/variance ODE with forward Euler dt = 1e-2, FROZEN numpy-exact noise,
+seed 0, fp64.  One "step" = one complete run_micro_macro (noise generation,
+iteration 0, K iterations), so value = K*N*P*S / run time (all GPUs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL).  Prints ONE JSON
+line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fine-propagator particle-steps/s (mM-Parareal run, BASELINE config 4)"
+UNIT = "particle-steps/s"
+SLICES_PER_GPU, P, S, DT, K_ITER, SEED = 64, 100_000, 100, 1e-3, 5, 0
+
+
+def workload(G: int) -> dict:
+    return {"workload": "config4: linear mean-field OU weak-scaling sweep (dX=(-X+0.5E[X])dt+0.5dW, "
+                        "X0~N(1,0.1^2)), coarse exact-closure moment ODE, forward Euler dt=1e-2",
+            "slices": SLICES_PER_GPU * G, "slices_per_gpu": SLICES_PER_GPU, "particles_per_slice": P,
+            "steps_per_slice": S, "dt": DT, "iterations": K_ITER, "noise": "frozen, numpy-exact Philox stream",
+            "step": "one full run_micro_macro", "parallelism": f"slices sharded over {G} GPU(s)",
+            "l2": "inputs larger than L2 (5.1 GB of increments per GPU per run)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the fine sweep from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "fine_sweep_ncu.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port: the checker restated from the reference)
+# ---------------------------------------------------------------------------
+def _cpu_slice(args):
+    n, seconds_hint = args
+    import numpy as np
+    from oracle import mm_oracle as O
+    m = O.model_ou(-1.0, 0.5, 0.5)
+    x0 = O.sample_normal_initial(SEED, 1.0, 0.01, P)
+    t = time.perf_counter()
+    xi = O.slice_noise(SEED, n, S, P)
+    O.propagate_fine(m, x0, n, n * S * DT, DT, S, xi)
+    return time.perf_counter() - t
+
+
+def cpu_baseline(seconds: float) -> dict:
+    """Single-core numpy restatement of propagate_fine (noise included) on
+    slices of the workload until ~`seconds` of CPU work."""
+    done, elapsed = 0, 0.0
+    while elapsed < seconds and done < SLICES_PER_GPU:
+        elapsed += _cpu_slice((done, seconds))
+        done += 1
+    value = done * P * S / elapsed
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{done} slice(s) x {S} EM steps x {P} particles of config 4 through the oracle's numpy "
+                      f"restatement of propagate_fine (numpy Philox/ziggurat noise included), {elapsed:.1f} s"}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    G = args.gpus
+    with mp.get_context("fork").Pool(cores) as pool:
+        for _ in range(args.warmup):
+            pool.map(_cpu_slice, [(n, 0) for n in range(cores)])
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_cpu_slice, [(n, 0) for n in range(cores)])
+        elapsed = time.perf_counter() - t
+    value = args.steps * cores * P * S / elapsed
+    sample = (f"per step: {cores} slices of config 4 ({S} steps x {P} particles each) propagated in parallel by "
+              f"{cores} processes running the oracle's numpy restatement of propagate_fine (noise included)")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": G,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload(G),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def our_arm(args):
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    G = world
+    import paper_2310_11365_b200 as mm
+    from paper_2310_11365_b200 import _lib
+    from paper_2310_11365_b200.distributed import run_micro_macro_sharded
+
+    N = SLICES_PER_GPU * G
+    spec = mm.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5)
+    model = mm.make_perturbed_ou(spec)
+    ode = mm.unimodal_rhs(model)
+    cfg = mm.PararealConfig(n_slices=N, iterations=K_ITER, slice_length=S * DT, particles=P,
+                            step=mm.StepConfig(DT, S), integrator=mm.EulerConfig(1e-2), retain_snapshots=False)
+    plan = mm.NoisePlan(SEED)
+    init = mm.InitialDistribution.normal(1.0, 0.01)
+    ens0_dev = mm.sample_initial(init, plan, P)                    # device-resident input
+    ens0_host = ens0_dev.device_positions.cpu().pin_memory()        # pinned host input (e2e)
+
+    def run(ens):
+        if world > 1:
+            return run_micro_macro_sharded(model, ode, ens, cfg, plan)
+        return mm.run_micro_macro(model, ode, ens, cfg, plan)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(max(args.warmup, 0)):
+        run(ens0_dev)
+    barrier()
+
+    # ---- device-resident timing ------------------------------------------------
+    fine_ms = []
+    launches0 = _lib.launch_count["total"]
+    with ClockSampler(local) as clocks:
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            tr = run(ens0_dev)
+            fine_ms.extend(1e3 * v for v in tr.timings.get("fine", []))
+        e1.record()
+        barrier()
+    launches = _lib.launch_count["total"] - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_all = ms
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_all = float(t.item())
+    psteps = K_ITER * N * P * S
+    value = psteps / (ms_all / 1e3)
+
+    # ---- end to end through the public API from pinned host memory ----------
+    e2e_times = []
+    for _ in range(args.steps):
+        barrier()
+        t = time.perf_counter()
+        ens = mm.ParticleEnsemble(ens0_host.to("cuda", non_blocking=True))
+        tr = run(ens)  # returns after the trace arrays reached host memory
+        barrier()
+        e2e_times.append(time.perf_counter() - t)
+    e2e_s = sum(e2e_times) / len(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    d2h = int(getattr(tr, "d2h_bytes", 0))
+    h2d = 8 * P + 8 * (N + 1)  # ens0 from pinned memory + the slice start times
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    peak, peak_src = measured_peak_hbm()
+    Ng = SLICES_PER_GPU
+    fine_bytes = Ng * S * P * 8 + 2 * Ng * P * 8
+    fine_avg_ms = statistics.mean(fine_ms) if fine_ms else float("nan")
+    achieved = fine_bytes / (fine_avg_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_all, "parareal_iteration_ms": ms_all / K_ITER, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload(G),
+        "roofline": {"kernel": "fine_sweep_kernel (mmpr_fine_sweep)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(), "algorithmic_bytes_per_launch": fine_bytes,
+                     "avg_launch_ms": fine_avg_ms,
+                     "bytes_model": "8 B increment read per particle-step + 16 B per particle per slice (x in/out)"},
+        "e2e": {"value": psteps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if G == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return our_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -112,9 +112,17 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         return lib
 
 
+# entry points that launch exactly one kernel each (bench.py counts them)
+LAUNCHING = frozenset({"mmpr_noise_keys", "mmpr_entropy_key", "mmpr_normals_fill", "mmpr_fine_sweep",
+                       "mmpr_restrict", "mmpr_match", "mmpr_coarse_row", "mmpr_integrate_macro"})
+launch_count = {"total": 0}
+
+
 def call(name: str, *args) -> None:
     """Invoke a status-returning entry point; raise MmprError on failure."""
     lib = load()
+    if name in LAUNCHING:
+        launch_count["total"] += 1
     status = getattr(lib, name)(*args)
     if status != 0:
         detail = lib.mmpr_last_error().decode(errors="replace")

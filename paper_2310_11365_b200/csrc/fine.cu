@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "mmpr_device.cuh"
 #include "capi_internal.h"
@@ -297,8 +298,14 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
     if (l > max_leaf) max_leaf = l;
   }
   g->ppt = (int)((max_leaf + 7) / 8);
-  const size_t smem_budget = 200 * 1024;
+  // two increment stages of the CTA's particle range must fit next to the
+  // ~1.5 KB of static shared memory (227 KB opt-in per CTA)
+  const size_t smem_budget = 224 * 1024;
   int spc = 128;
+  if (const char *env = getenv("MMPR_FINE_SLOTS_PER_CTA")) {  // tuning override
+    const int v = atoi(env);
+    if (v >= 4 && v <= 128 && (v & (v - 1)) == 0) spc = v;
+  }
   while (spc > 4 && (size_t)spc * max_leaf * 8 * 2 > smem_budget) spc >>= 1;
   if (nslots <= spc) {
     g->slots_per_cta = (int)(nslots < 4 ? 4 : nslots);

@@ -105,7 +105,8 @@ class TorchComm:
 
 
 def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: NoisePlan, comm=None,
-                            backend=None, reuse_converged_coarse: bool = True) -> PararealTrace:
+                            backend=None, reuse_converged_coarse: bool = True,
+                            record_timings: bool = True) -> PararealTrace:
     """mM-Parareal over ``comm.world`` ranks; every rank returns the full
     macro/micro trace, snapshots hold the rank's own slices only
     (``trace.snapshots[k][m]`` is global slice boundary ``offset + m``)."""
@@ -165,13 +166,16 @@ def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: N
     if not plan.fresh:
         be.noise(plan.master_seed, a, Ng, S, P, 0, False, xi)
 
+    timer = _StageTimer(record_timings and be.device.type == "cuda")
     stopped_at = None
     done = 0
     for k in range(K):
         if plan.fresh:
             be.noise(plan.master_seed, a, Ng, S, P, k, True, xi)
         cur, nxt = sn(k), sn(k + 1)
+        ev = timer.start()
         be.fine(cur[:Ng], fine, times_d[a:a + Ng], S, dt, xi, bad_local[k])
+        timer.stop("fine", ev)
         be.restrict(fine, fine_local, fine_counts, scratch)
         fine_all[k].copy_(comm.all_gather_rows(fine_local))
         be.coarse_row(times_d, k + 1, rho0, fine_all[k], cache[k], macro[k + 1], cache[k + 1], raw[k],
@@ -216,7 +220,10 @@ def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: N
                          _StageTimer(False), stopped_at)
     if retain:
         trace.snapshots = [[ParticleEnsemble._wrap(snap[k, m]) for m in range(Ng + 1)] for k in range(Kd + 1)]
-    trace.timings = {"slice_offset": a, "slices_per_rank": Ng}
+    trace.timings = timer.resolve()
+    trace.timings["slice_offset"] = a
+    trace.timings["slices_per_rank"] = Ng
+    trace.d2h_bytes = int(sum(v.nbytes for v in h.values()))
     return trace
 
 

@@ -92,6 +92,7 @@ class PararealTrace:
     lift_collapses: list = field(default_factory=list)
     timings: dict = field(default_factory=dict)
     stopped_at: int | None = None
+    d2h_bytes: int = 0
 
     @property
     def n_slices(self) -> int:
@@ -274,7 +275,9 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
          ("macro", "micro", "micro_counts", "fine_stats", "raw", "bad", "coarse_status", "match_status",
           "rho0", "counts0")}
     _raise_first_error(h, N, Kd, I)
-    return _build_trace(h, ws, cfg, plan, times, Kd, I, timer, stopped_at)
+    trace = _build_trace(h, ws, cfg, plan, times, Kd, I, timer, stopped_at)
+    trace.d2h_bytes = int(sum(v.nbytes for v in h.values()))
+    return trace
 
 
 def _raise_first_error(h, N: int, K: int, I: int) -> None:
