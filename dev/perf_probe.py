@@ -28,7 +28,10 @@ t0 = torch.zeros(N, dtype=torch.float64, device=dev)
 for spc in ('128', '64', '32'):
     os.environ['MMPR_FINE_SLOTS_PER_CTA'] = spc
     c, k = ctypes.c_int32(0), ctypes.c_int32(0)
-    L.call('mmpr_fine_sweep_occupancy', P, ctypes.byref(c), ctypes.byref(k))
+    try:
+        L.call('mmpr_fine_sweep_occupancy', P, ctypes.byref(c), ctypes.byref(k))
+    except L.MmprError as e:
+        print('spc', spc, e); continue
     ms, all_ = timeit(lambda: kernels.fine_sweep(model, x, out, t0, S, 1e-3, xi, bad))
     byts = N*S*P*8 + 2*N*P*8
     print(f'fine sweep spc={spc} ctas/slice={k.value} clusters={c.value}: {ms:.3f} ms {N*S*P/ms/1e9*1e3:.3e} p-steps/s {byts/ms/1e6:.0f} GB/s  {all_}')
