@@ -165,11 +165,13 @@ def main():
         f"#define NPZ_INV_R {_hex(inv_r)}",
         "#define NPZ_KI_VALUES \\",
     ]
-    lines += ["  " + ", ".join(f"0x{int(v):016x}ULL" for v in ki[i:i + 4]) + ", \\" for i in range(0, 256, 4)]
-    lines += ["", "#define NPZ_WI_VALUES \\"]
-    lines += ["  " + ", ".join(_hex(v) for v in wi[i:i + 4]) + ", \\" for i in range(0, 256, 4)]
-    lines += ["", "#define NPZ_FI_VALUES \\"]
-    lines += ["  " + ", ".join(_hex(v) for v in fi[i:i + 4]) + ", \\" for i in range(0, 256, 4)]
+    def block(values, fmt):
+        rows = [", ".join(fmt(v) for v in values[i:i + 4]) for i in range(0, 256, 4)]
+        return ["  " + r + (", \\" if i < len(rows) - 1 else "") for i, r in enumerate(rows)]
+
+    lines += block(ki, lambda v: f"0x{int(v):016x}ULL")
+    lines += ["", "#define NPZ_WI_VALUES \\"] + block(wi, _hex)
+    lines += ["", "#define NPZ_FI_VALUES \\"] + block(fi, _hex)
     lines += [""]
     with open(OUT, "w") as fh:
         fh.write("\n".join(lines))

@@ -24,10 +24,6 @@ namespace mmpr {
 
 #define CS_MAXV (3 * MMPR_MAX_REGIONS)
 
-struct State {
-  double y[CS_MAXV];
-};
-
 // numpy pairwise sum for n <= 128 (short vectors: sequential from 0 when
 // n < 8, else 8 accumulators)
 __device__ double small_pairwise(const double *a, int n) {
@@ -46,10 +42,11 @@ __device__ double small_pairwise(const double *a, int n) {
   return res;
 }
 
-__device__ void ode_rhs(const mmpr_moment_ode &ode, const mmpr_model &model, double t, const double *y,
-                        double *dy) {
+template <int NV>
+__device__ __forceinline__ void ode_rhs(const mmpr_moment_ode &ode, const mmpr_model &model, double t,
+                                        const double *y, double *dy) {
   (void)t;
-  const int I = ode.n_regions;
+  constexpr int I = NV / 3;
   switch (ode.kind) {
     case MMPR_ODE_UNIMODAL: {  // first-order closure with point statistic s = M
       const double m = y[0], var = y[1];
@@ -68,7 +65,9 @@ __device__ void ode_rhs(const mmpr_moment_ode &ode, const mmpr_model &model, dou
     }
     case MMPR_ODE_MULTIMODAL: {  // mixture statistic sum_i a_i M_i (from 0.0)
       double s = 0.0;
+#pragma unroll
       for (int i = 0; i < I; ++i) s = add(s, mul(y[2 * I + i], y[i]));
+#pragma unroll
       for (int i = 0; i < I; ++i) {
         const ModelCoeffs c = coeffs(model, y[i], s);
         dy[i] = add(c.drift, mul(0.5, c.diff_dxx));
@@ -90,32 +89,36 @@ __device__ void ode_rhs(const mmpr_moment_ode &ode, const mmpr_model &model, dou
       break;
     }
     default:
-      for (int i = 0; i < 3 * I; ++i) dy[i] = __longlong_as_double(0x7ff8000000000000ULL);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) dy[i] = __longlong_as_double(0x7ff8000000000000ULL);
   }
 }
 
-__device__ __forceinline__ bool all_finite(const double *v, int n) {
-  for (int i = 0; i < n; ++i)
-    if (!isfinite(v[i])) return false;
-  return true;
+template <int NV>
+__device__ __forceinline__ bool all_finite(const double *v) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) ok &= (bool)isfinite(v[i]);
+  return ok;
 }
 
 // Forward Euler with n = round((t1 - t0)/dt) >= 1 equal steps.
+template <int NV>
 __device__ int integrate_euler(const mmpr_moment_ode &ode, const mmpr_model &model, double dt, double t0,
                                double t1, double *y) {
-  const int nv = 3 * ode.n_regions;
   const double span = sub(t1, t0);
   if (span == 0.0) return MMPR_STAT_OK;
   long long n = llrint(div(span, dt));
   if (n < 1) n = 1;
   const double h = div(span, (double)n);
-  double k[CS_MAXV];
+  double k[NV];
   for (long long i = 0; i < n; ++i) {
     const double t = add(t0, mul((double)i, h));
-    ode_rhs(ode, model, t, y, k);
-    for (int v = 0; v < nv; ++v) y[v] = add(y[v], mul(h, k[v]));
+    ode_rhs<NV>(ode, model, t, y, k);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) y[v] = add(y[v], mul(h, k[v]));
   }
-  return all_finite(y, nv) ? MMPR_STAT_OK : 1;
+  return all_finite<NV>(y) ? MMPR_STAT_OK : 1;
 }
 
 // ---- Dormand-Prince 5(4), FSAL, PI step control (rk54.py:16-129) ----------
@@ -132,32 +135,36 @@ __constant__ double c_dp_b5[7] = {35.0 / 384, 0.0, 500.0 / 1113, 125.0 / 192, -2
 __constant__ double c_dp_b4[7] = {5179.0 / 57600, 0.0, 7571.0 / 16695, 393.0 / 640, -92097.0 / 339200,
                                   187.0 / 2100, 1.0 / 40};
 
-__device__ double rms_norm(const double *e, const double *scale, int nv) {
-  double q[CS_MAXV];
-  for (int v = 0; v < nv; ++v) {
+template <int NV>
+__device__ __forceinline__ double rms_norm(const double *e, const double *scale) {
+  double q[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
     const double r = div(e[v], scale[v]);
     q[v] = mul(r, r);
   }
-  return __dsqrt_rn(div(small_pairwise(q, nv), (double)nv));
+  return __dsqrt_rn(div(small_pairwise(q, NV), (double)NV));
 }
 
+template <int NV>
 __device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &model, const mmpr_integrator &cfg,
                               double t0, double t1, double *y) {
-  const int nv = 3 * ode.n_regions;
+  constexpr int nv = NV;
   const double span = sub(t1, t0);
   if (span < 0.0) return 1;
   if (span == 0.0) return MMPR_STAT_OK;
   double t = t0;
-  double k[7][CS_MAXV];
-  ode_rhs(ode, model, t, y, k[0]);
-  if (!all_finite(k[0], nv)) return 1;
+  double k[7][NV];
+  ode_rhs<NV>(ode, model, t, y, k[0]);
+  if (!all_finite<NV>(k[0])) return 1;
   double h;
   if (cfg.first_step > 0.0) {
     h = cfg.first_step;
   } else {  // _initial_step
-    double sc[CS_MAXV];
+    double sc[NV];
+#pragma unroll
     for (int v = 0; v < nv; ++v) sc[v] = add(cfg.abs_tol, mul(cfg.rel_tol, fabs(y[v])));
-    const double d0 = rms_norm(y, sc, nv), d1 = rms_norm(k[0], sc, nv);
+    const double d0 = rms_norm<NV>(y, sc), d1 = rms_norm<NV>(k[0], sc);
     h = (d0 < 1e-5 || d1 < 1e-5) ? 1e-6 : div(mul(0.01, d0), d1);
   }
   h = fmin(h, span);
@@ -165,23 +172,28 @@ __device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &mode
   const double min_step = mul(1e-14, fmax(fmax(fabs(t0), fabs(t1)), 1.0));
   for (int it = 0; it < cfg.max_steps; ++it) {
     h = fmin(h, sub(t1, t));
-    double yi[CS_MAXV];
+    double yi[NV];
+#pragma unroll
     for (int i = 1; i < 7; ++i) {
+#pragma unroll
       for (int v = 0; v < nv; ++v) {
         double acc;
         if (i == 1) {
           acc = mul(c_dp_a[1][0], k[0][v]);
         } else {
           acc = mul(c_dp_a[i][0], k[0][v]);
+#pragma unroll
           for (int l = 1; l < i; ++l) acc = add(acc, mul(c_dp_a[i][l], k[l][v]));
         }
         yi[v] = add(y[v], mul(h, acc));
       }
-      ode_rhs(ode, model, add(t, mul(c_dp_c[i], h)), yi, k[i]);
+      ode_rhs<NV>(ode, model, add(t, mul(c_dp_c[i], h)), yi, k[i]);
     }
-    double y5[CS_MAXV], err[CS_MAXV], sc[CS_MAXV];
+    double y5[NV], err[NV], sc[NV];
+#pragma unroll
     for (int v = 0; v < nv; ++v) {
       double b5 = mul(c_dp_b5[0], k[0][v]), e = mul(sub(c_dp_b5[0], c_dp_b4[0]), k[0][v]);
+#pragma unroll
       for (int l = 1; l < 7; ++l) {
         b5 = add(b5, mul(c_dp_b5[l], k[l][v]));
         e = add(e, mul(sub(c_dp_b5[l], c_dp_b4[l]), k[l][v]));
@@ -189,11 +201,13 @@ __device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &mode
       y5[v] = add(y[v], mul(h, b5));
       err[v] = mul(h, e);
     }
-    if (!all_finite(y5, nv)) return 1;
+    if (!all_finite<NV>(y5)) return 1;
+#pragma unroll
     for (int v = 0; v < nv; ++v) sc[v] = add(cfg.abs_tol, mul(cfg.rel_tol, fmax(fabs(y[v]), fabs(y5[v]))));
-    const double err_norm = rms_norm(err, sc, nv);
+    const double err_norm = rms_norm<NV>(err, sc);
     if (err_norm <= 1.0) {
       t = add(t, h);
+#pragma unroll
       for (int v = 0; v < nv; ++v) {
         y[v] = y5[v];
         k[0][v] = k[6][v];
@@ -212,10 +226,11 @@ __device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &mode
   return 1;
 }
 
-__device__ int coarse_step(const mmpr_moment_ode &ode, const mmpr_model &model, const mmpr_integrator &integ,
-                           double t0, double t1, double *y) {
-  if (integ.kind == MMPR_INTEG_EULER) return integrate_euler(ode, model, integ.dt, t0, t1, y);
-  return integrate_dp54(ode, model, integ, t0, t1, y);
+template <int NV>
+__device__ __forceinline__ int coarse_step(const mmpr_moment_ode &ode, const mmpr_model &model,
+                                           const mmpr_integrator &integ, double t0, double t1, double *y) {
+  if (integ.kind == MMPR_INTEG_EULER) return integrate_euler<NV>(ode, model, integ.dt, t0, t1, y);
+  return integrate_dp54<NV>(ode, model, integ, t0, t1, y);
 }
 
 struct CoarseParams {
@@ -235,55 +250,68 @@ struct CoarseParams {
   int skip_until;
 };
 
+template <int NV>
 __global__ void coarse_row_kernel(const CoarseParams p) {
   if (threadIdx.x != 0) return;
-  const int I = p.ode.n_regions, nv = 3 * I;
-  double cur[CS_MAXV];
-  for (int v = 0; v < nv; ++v) {
+  constexpr int I = NV / 3;
+  double cur[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
     cur[v] = p.rho0[v];
     p.macro_out[v] = cur[v];
   }
   for (int n = 0; n < p.n; ++n) {
-    double pred[CS_MAXV];
+    double pred[NV];
     int st = MMPR_STAT_OK;
     if (p.iteration >= 1 && n < p.skip_until) {
-      for (int v = 0; v < nv; ++v) pred[v] = p.cache_in[n * nv + v];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) pred[v] = p.cache_in[n * NV + v];
     } else {
-      for (int v = 0; v < nv; ++v) pred[v] = cur[v];
-      st = coarse_step(p.ode, p.model, p.integ, p.times[n], p.times[n + 1], pred);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) pred[v] = cur[v];
+      st = coarse_step<NV>(p.ode, p.model, p.integ, p.times[n], p.times[n + 1], pred);
     }
     p.status[n] = st;
-    for (int v = 0; v < nv; ++v) p.cache_out[n * nv + v] = pred[v];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) p.cache_out[n * NV + v] = pred[v];
     if (p.iteration == 0) {
-      for (int v = 0; v < nv; ++v) cur[v] = pred[v];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) cur[v] = pred[v];
     } else {
-      const double *f = p.fine + n * nv;
-      const double *c = p.cache_in + n * nv;
-      double raw[CS_MAXV];
-      for (int v = 0; v < nv; ++v) raw[v] = add(f[v], sub(pred[v], c[v]));
-      for (int v = 0; v < nv; ++v) p.raw_out[n * nv + v] = raw[v];
+      const double *f = p.fine + n * NV;
+      const double *c = p.cache_in + n * NV;
+      double raw[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) raw[v] = add(f[v], sub(pred[v], c[v]));
+#pragma unroll
+      for (int v = 0; v < NV; ++v) p.raw_out[n * NV + v] = raw[v];
       bool neg = false;
+#pragma unroll
       for (int i = 0; i < I; ++i) neg |= raw[I + i] < 0.0;
+#pragma unroll
       for (int i = 0; i < I; ++i) {
         cur[i] = raw[i];
         cur[I + i] = (neg && raw[I + i] < 0.0) ? 0.0 : raw[I + i];
         cur[2 * I + i] = f[2 * I + i];  // fractions from the fine restriction
       }
     }
-    for (int v = 0; v < nv; ++v) p.macro_out[(n + 1) * nv + v] = cur[v];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) p.macro_out[(n + 1) * NV + v] = cur[v];
   }
 }
 
+template <int NV>
 __global__ void integrate_macro_kernel(const mmpr_moment_ode ode, const mmpr_model model,
                                        const mmpr_integrator integ, int n_states, const double *t0,
                                        const double *t1, const double *in, double *out, int32_t *status) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_states) return;
-  const int nv = 3 * ode.n_regions;
-  double y[CS_MAXV];
-  for (int v = 0; v < nv; ++v) y[v] = in[s * nv + v];
-  const int st = coarse_step(ode, model, integ, t0[s], t1[s], y);
-  for (int v = 0; v < nv; ++v) out[s * nv + v] = y[v];
+  double y[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) y[v] = in[s * NV + v];
+  const int st = coarse_step<NV>(ode, model, integ, t0[s], t1[s], y);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) out[s * NV + v] = y[v];
   status[s] = st;
 }
 
@@ -330,7 +358,13 @@ extern "C" int mmpr_coarse_row(const mmpr_moment_ode *ode, const mmpr_model *mod
   p.raw_out = raw_out;
   p.status = status;
   p.skip_until = skip_until;
-  coarse_row_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  cudaStream_t st_ = (cudaStream_t)stream;
+  switch (ode->n_regions) {
+    case 1: coarse_row_kernel<3><<<1, 32, 0, st_>>>(p); break;
+    case 2: coarse_row_kernel<6><<<1, 32, 0, st_>>>(p); break;
+    case 3: coarse_row_kernel<9><<<1, 32, 0, st_>>>(p); break;
+    default: coarse_row_kernel<12><<<1, 32, 0, st_>>>(p); break;
+  }
   return mmpr_check_launch("coarse_row_kernel");
 }
 
@@ -343,7 +377,13 @@ extern "C" int mmpr_integrate_macro(const mmpr_moment_ode *ode, const mmpr_model
   if (!model || n_states < 0 || !t0 || !t1 || !state_in || !state_out || !status) return MMPR_ERR_ARG;
   if (n_states == 0) return MMPR_OK;
   const int threads = 64;
-  integrate_macro_kernel<<<(n_states + threads - 1) / threads, threads, 0, (cudaStream_t)stream>>>(
-      *ode, *model, *integ, n_states, t0, t1, state_in, state_out, status);
+  const int blocks = (n_states + threads - 1) / threads;
+  cudaStream_t st_ = (cudaStream_t)stream;
+  switch (ode->n_regions) {
+    case 1: integrate_macro_kernel<3><<<blocks, threads, 0, st_>>>(*ode, *model, *integ, n_states, t0, t1, state_in, state_out, status); break;
+    case 2: integrate_macro_kernel<6><<<blocks, threads, 0, st_>>>(*ode, *model, *integ, n_states, t0, t1, state_in, state_out, status); break;
+    case 3: integrate_macro_kernel<9><<<blocks, threads, 0, st_>>>(*ode, *model, *integ, n_states, t0, t1, state_in, state_out, status); break;
+    default: integrate_macro_kernel<12><<<blocks, threads, 0, st_>>>(*ode, *model, *integ, n_states, t0, t1, state_in, state_out, status); break;
+  }
   return mmpr_check_launch("integrate_macro_kernel");
 }

@@ -30,6 +30,7 @@
 namespace mmpr {
 
 #define FS_MAX_CLUSTER 16
+#define FS_L2_AHEAD 3  // steps of increments kept in flight towards L2 beyond the smem stages
 
 struct FineParams {
   mmpr_model model;
@@ -133,6 +134,8 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
       mbar_arrive_expect_tx(&s_bar[j], stage_bytes);
       bulk_g2s(s_stage + j * p.stage_elems, xi_slice + j * p.xi_row_pitch + lo, stage_bytes, &s_bar[j]);
     }
+    for (int j = 2; j < 2 + FS_L2_AHEAD && j < p.S; ++j)
+      prefetch_l2(xi_slice + (int64_t)j * p.xi_row_pitch + lo, stage_bytes);
   }
   int issued = (p.S < 2) ? p.S : 2;
 
@@ -140,7 +143,9 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
   // Barriers per call: B1 (__syncthreads) and B2 (__syncthreads, or the
   // cluster barrier).  s_bad is double-buffered by call parity: slot r&1 is
   // written before B1 of call r and reset (for call r+2) after B1 of r+1.
-  auto reduce = [&](int r, int bad_local, double &mean_out, int &bad_out) {
+  // `refill` (>= 0): step whose increments go into the stage this step just
+  // consumed -- issued right after B1, when every thread has read it.
+  auto reduce = [&](int r, int bad_local, int refill, double &mean_out, int &bad_out) {
     const int par = r & 1;
     double acc = x[0];
 #pragma unroll
@@ -170,6 +175,17 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
       if (wbad) s_bad[par] = 1;
     }
     __syncthreads();  // B1
+    if (tid == 0 && refill >= 0) {
+      const int st = refill & 1;
+      mbar_arrive_expect_tx(&s_bar[st], stage_bytes);
+      bulk_g2s(s_stage + st * p.stage_elems, xi_slice + (int64_t)refill * p.xi_row_pitch + lo, stage_bytes,
+               &s_bar[st]);
+      ++issued;
+      const int pf = refill + FS_L2_AHEAD;  // pull a later step towards L2
+      if (pf < p.S) prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
+    }
+    PwVal total;
+    int bad;
     if (warp == 0) {
       PwVal v;
       if (lane < nwarps) v = s_wp[lane];
@@ -177,28 +193,24 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
 #pragma unroll
       for (int m = 1; m < 32; m <<= 1)
         if (m < nwarps) v = pw_xor_level(v, lane, m);
-      if (lane == 0) {
-        s_cta = v;
-        s_bad[par ^ 1] = 0;
+      if (p.ctas == 1) {
+        if (lane == 0) {
+          s_cta = v;
+          s_bad[par ^ 1] = 0;
+        }
+      } else if (lane < p.ctas) {  // one lane per destination CTA
+        const uint32_t remote = mapa_shared(smem_addr(&s_slot[par][rank]), (uint32_t)lane);
+        st_cluster_v2(remote, __double_as_longlong(v.v),
+                      (unsigned long long)(uint32_t)v.ok | ((unsigned long long)(uint32_t)s_bad[par] << 32));
+        __syncwarp(__activemask());
+        if (lane == 0) s_bad[par ^ 1] = 0;
       }
     }
-    PwVal total;
-    int bad;
     if (p.ctas == 1) {
       __syncthreads();  // B2
       total = s_cta;
       bad = s_bad[par];
     } else {
-      if (tid == 0) {
-        const uint32_t local = smem_addr(&s_slot[par][rank]);
-        const uint32_t badv = (uint32_t)s_bad[par];
-        for (int q = 0; q < p.ctas; ++q) {
-          const uint32_t remote = mapa_shared(local, (uint32_t)q);
-          st_cluster_f64(remote, s_cta.v);
-          st_cluster_u32(remote + 8, (uint32_t)s_cta.ok);
-          st_cluster_u32(remote + 12, badv);
-        }
-      }
       cluster_sync_all();  // B2
       // every warp combines the per-CTA partials with the same xor tree
       PwVal v;
@@ -223,7 +235,7 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
 
   double s;
   int bad;
-  reduce(0, 0, s, bad);
+  reduce(0, 0, -1, s, bad);
 
   int first_bad = MMPR_STAT_OK;
   const double t_start = p.t0[slice];
@@ -244,15 +256,8 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
       xt = em_update<KIND>(p, xt, s, xs[tail_off - lo + j8]);
       bad_local |= !finite(xt);
     }
-    // The first barrier inside reduce() orders every read of this stage
-    // before the refill issued below.
-    reduce(j + 1, bad_local, s, bad);
-    if (tid == 0 && j + 2 < p.S && !bad) {
-      mbar_arrive_expect_tx(&s_bar[stage], stage_bytes);
-      bulk_g2s(s_stage + stage * p.stage_elems, xi_slice + (int64_t)(j + 2) * p.xi_row_pitch + lo,
-               stage_bytes, &s_bar[stage]);
-      ++issued;
-    }
+    // B1 inside reduce() orders every read of this stage before its refill
+    reduce(j + 1, bad_local, (j + 2 < p.S) ? j + 2 : -1, s, bad);
     if (bad) {
       first_bad = j;
       break;

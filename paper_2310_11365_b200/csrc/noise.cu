@@ -102,8 +102,8 @@ __device__ __forceinline__ uint32_t mask_ge(int k, int e) {
   return ~((1u << (e - 32 * k)) - 1u);
 }
 
-// Exact sequential parse of one warp range from entry `e` (< 128) using the
-// stored non-fast mask and token lengths: returns start mask and exit.
+// Exact sequential parse of one 128-word range from entry `e` (< 128) with
+// token lengths `len`: start mask and exit (words consumed past the range).
 __device__ int rewalk(const uint32_t na[4], const uint16_t *len, int e, uint32_t S[4]) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) S[k] = mask_ge(k, e);
@@ -118,20 +118,74 @@ __device__ int rewalk(const uint32_t na[4], const uint16_t *len, int e, uint32_t
   }
 }
 
+// Parse from entry 0 when every non-fast word is a wedge (length 2): in a
+// maximal run of wedge words starting at a, the words at odd offsets
+// a+1, a+3, ... (up to one past the run) are consumed uniforms, the rest
+// start attempts.  Runs are separated by parity of their start with one
+// carry-propagating add (the simdjson odd-backslash trick).
+__device__ __forceinline__ void wedge_parse(const uint32_t nf[4], uint32_t S[4], int &exit) {
+  const uint64_t EVEN = 0x5555555555555555ULL, ODD = 0xAAAAAAAAAAAAAAAAULL;
+  const uint64_t wl = (uint64_t)nf[0] | ((uint64_t)nf[1] << 32);
+  const uint64_t wh = (uint64_t)nf[2] | ((uint64_t)nf[3] << 32);
+  const uint64_t pl = wl << 1, ph = (wh << 1) | (wl >> 63);        // W << 1
+  const uint64_t sl = wl & ~pl, sh = wh & ~ph;                      // run starts
+  const uint64_t el = sl & EVEN, eh = sh & EVEN;                    // even-start runs
+  const uint64_t al = wl + el;                                      // carry through runs
+  const uint64_t ah = wh + eh + (al < wl ? 1ULL : 0ULL);
+  const uint64_t rel = wl & ~al, reh = wh & ~ah;                    // even-start run bits
+  const uint64_t rol = wl & ~rel, roh = wh & ~reh;                  // odd-start run bits
+  const uint64_t cl = ((rel << 1) & ODD) | ((rol << 1) & EVEN);
+  const uint64_t ch = ((((reh << 1) | (rel >> 63)) & ODD)) | ((((roh << 1) | (rol >> 63)) & EVEN));
+  S[0] = ~(uint32_t)cl;
+  S[1] = ~(uint32_t)(cl >> 32);
+  S[2] = ~(uint32_t)ch;
+  S[3] = ~(uint32_t)(ch >> 32);
+  // a wedge starting at word 127 consumes word 0 of the next range
+  exit = ((wh >> 63) & 1ULL) && ((S[3] >> 31) & 1u) ? 1 : 0;
+}
+
+// Tail attempt starting at stream word `wi` (layer 0, mantissa >= ki[0]):
+// Marsaglia's tail over successive pairs of uniforms.  Rare (~2.6e-4 of the
+// draws), so the successor words are recomputed from the counter.
+__device__ __noinline__ double tail_token(uint64_t wi, uint64_t mant, uint64_t k0, uint64_t k1, int *len) {
+  uint64_t i = wi + 1;
+  for (;;) {
+    const uint64_t a = np::philox_word(i++, k0, k1);
+    const uint64_t b = np::philox_word(i++, k0, k1);
+    const double xx = mul(-NPZ_INV_R, log1p(-np::unit_double(a)));
+    const double yy = -log1p(-np::unit_double(b));
+    if (add(yy, yy) > mul(xx, xx)) {
+      const uint64_t L = i - wi;
+      *len = (int)(L < 0xffffu ? L : 0xffffu);
+      return ((mant >> 8) & 1) ? -add(NPZ_R, xx) : add(NPZ_R, xx);
+    }
+  }
+}
+
+// Wedge test of layer `layer` at x with the next word's uniform.
+__device__ __noinline__ bool wedge_accepts(int layer, double x, uint64_t next_word) {
+  const double u = np::unit_double(next_word);
+  const double lhs = add(mul(sub(c_zig_fi[layer - 1], c_zig_fi[layer]), u), c_zig_fi[layer]);
+  return lhs < exp(mul(mul(-0.5, x), x));
+}
+
 // ---------------------------------------------------------------------------
 // stream fill kernel
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NF_THREADS)
+#define NF_BPT 2                          // Philox blocks (rows) per thread per chunk
+#define NF_RANGES (NF_WARPS * NF_BPT)     // 128-word ranges per chunk (<= 32)
+
+__global__ void __launch_bounds__(NF_THREADS, 3)
 normals_fill_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__restrict__ out,
                     int64_t pitch, int affine, double loc, double scale) {
   __shared__ ulonglong2 zig[256];
-  __shared__ uint32_t s_spec[NF_WARPS][4];  // speculative starts (entry 0)
-  __shared__ uint32_t s_prod[NF_WARPS][4];  // words that yield a normal if they start
-  __shared__ uint32_t s_nonfast[NF_WARPS][4];
-  __shared__ uint32_t s_final[NF_WARPS][4];
-  __shared__ __align__(16) uint16_t s_len[NF_THREADS * 4];
-  __shared__ int s_exit[NF_WARPS];
-  __shared__ int s_base[NF_WARPS];
+  __shared__ __align__(16) uint32_t s_spec[NF_RANGES][4];  // speculative starts (entry 0)
+  __shared__ __align__(16) uint32_t s_prod[NF_RANGES][4];  // words that yield a normal if they start
+  __shared__ __align__(16) uint32_t s_nonfast[NF_RANGES][4];
+  __shared__ __align__(16) uint32_t s_final[NF_RANGES][4];
+  __shared__ __align__(16) uint16_t s_len[NF_RANGES * 128];
+  __shared__ int s_exit[NF_RANGES];
+  __shared__ int s_base[NF_RANGES];
   __shared__ int s_carry, s_total;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -143,112 +197,99 @@ normals_fill_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__
   if (tid == 0) s_carry = 0;
   __syncthreads();
 
+  const int sh = 4 * (lane & 7);
   int64_t produced = 0;
   for (uint64_t chunk = 0; produced < count; ++chunk) {
-    const uint64_t blk = chunk * NF_THREADS + tid;
-    const uint64_t word0 = blk * 4;
-    uint64_t w[4];
-    np::philox_block(blk, k0, k1, w);
-    const uint64_t succ = __shfl_down_sync(MMPR_FULL_MASK, w[0], 1);
-
-    double val[4];
-    uint32_t nonfast = 0, prod = 0;
-    uint16_t lens[4];
+    double val[NF_BPT][4];
+    uint32_t prod_nib[NF_BPT], tail_nib[NF_BPT];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t r = w[q];
-      const int layer = (int)(r & 0xff);
-      const uint64_t mant = (r >> 9) & 0x000fffffffffffffULL;
-      const ulonglong2 z = zig[layer];
-      const double wi = __longlong_as_double((long long)z.y);
-      // (double)mant * wi, one rounding: (2^52 + mant) * wi - 2^52 * wi
-      double x = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi,
-                          -0x1.0p52 * wi);
-      if ((r >> 8) & 1) x = -x;
-      lens[q] = 1;
-      if (mant >= z.x) {
-        nonfast |= 1u << q;
-        if (layer != 0) {  // wedge: one more uniform
-          uint64_t u64;
-          if (q < 3) u64 = w[q + 1];
-          else if (lane < 31) u64 = succ;
-          else u64 = np::philox_word(word0 + 4, k0, k1);
-          const double u = np::unit_double(u64);
-          const double lhs = add(mul(sub(c_zig_fi[layer - 1], c_zig_fi[layer]), u), c_zig_fi[layer]);
-          if (lhs < exp(mul(mul(-0.5, x), x))) prod |= 1u << q;
-          lens[q] = 2;
-        } else {  // tail
-          uint64_t i = word0 + q + 1;
-          for (;;) {
-            const uint64_t a = ((i >> 2) == blk) ? w[i & 3] : np::philox_word(i, k0, k1);
-            ++i;
-            const uint64_t b = ((i >> 2) == blk) ? w[i & 3] : np::philox_word(i, k0, k1);
-            ++i;
-            const double xx = mul(-NPZ_INV_R, log1p(-np::unit_double(a)));
-            const double yy = -log1p(-np::unit_double(b));
-            if (add(yy, yy) > mul(xx, xx)) {
-              x = ((mant >> 8) & 1) ? -add(NPZ_R, xx) : add(NPZ_R, xx);
-              break;
-            }
+    for (int r = 0; r < NF_BPT; ++r) {
+      const uint64_t blk = (chunk * NF_BPT + r) * NF_THREADS + tid;
+      const uint64_t word0 = blk * 4;
+      uint64_t w[4];
+      np::philox_block(blk, k0, k1, w);
+      const uint64_t succ = __shfl_down_sync(MMPR_FULL_MASK, w[0], 1);
+      uint32_t nonfast = 0, prod = 0, tails = 0;
+      uint16_t lens[4] = {1, 1, 1, 1};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t rw = w[q];
+        const int layer = (int)(rw & 0xff);
+        const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
+        const ulonglong2 z = zig[layer];
+        const double wi = __longlong_as_double((long long)z.y);
+        // (double)mant * wi rounded once: (2^52 + mant) * wi - 2^52 * wi
+        double x = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
+        if ((rw >> 8) & 1) x = -x;
+        val[r][q] = x;
+        if (mant >= z.x) {
+          nonfast |= 1u << q;
+          if (layer != 0) {
+            const uint64_t nx = (q < 3) ? w[q + 1] : (lane < 31 ? succ : np::philox_word(word0 + 4, k0, k1));
+            if (wedge_accepts(layer, x, nx)) prod |= 1u << q;
+            lens[q] = 2;
+          } else {
+            int L;
+            tail_token(word0 + q, mant, k0, k1, &L);
+            lens[q] = (uint16_t)L;
+            tails |= 1u << q;
+            prod |= 1u << q;
           }
+        } else {
           prod |= 1u << q;
-          const uint64_t L = i - (word0 + q);
-          lens[q] = (uint16_t)(L < 0xffffu ? L : 0xffffu);
         }
-      } else {
-        prod |= 1u << q;
       }
-      val[q] = x;
-    }
-    *reinterpret_cast<ushort4 *>(&s_len[4 * tid]) = make_ushort4(lens[0], lens[1], lens[2], lens[3]);
-
-    // 128-bit masks over this warp's words (bit b = word 4*lane+q)
-    const int sh = 4 * (lane & 7);
-    uint32_t NF[4], PR[4];
+      prod_nib[r] = prod;
+      tail_nib[r] = tails;
+      const int range = r * NF_WARPS + warp;
+      *reinterpret_cast<ushort4 *>(&s_len[range * 128 + 4 * lane]) = make_ushort4(lens[0], lens[1], lens[2], lens[3]);
+      uint32_t NF[4], PR[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      NF[k] = __reduce_or_sync(MMPR_FULL_MASK, (lane >> 3) == k ? (nonfast << sh) : 0u);
-      PR[k] = __reduce_or_sync(MMPR_FULL_MASK, (lane >> 3) == k ? (prod << sh) : 0u);
-    }
-    const uint64_t lens_packed = (uint64_t)lens[0] | ((uint64_t)lens[1] << 16) |
-                                 ((uint64_t)lens[2] << 32) | ((uint64_t)lens[3] << 48);
-
-    // speculative parse from entry 0 (warp-uniform)
-    uint32_t S[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-    int exit0 = 0;
-    {
-      int pos = 0;
-      for (;;) {
-        const int b = next_set128(NF, pos);
-        if (b < 0) break;
-        const uint64_t lp = __shfl_sync(MMPR_FULL_MASK, lens_packed, b >> 2);
-        const int L = (int)((lp >> (16 * (b & 3))) & 0xffff);
-        clear_range128(S, b + 1, min(b + L, 128));
-        pos = b + L;
-        if (pos >= 128) {
-          exit0 = pos - 128;
-          break;
+      for (int k = 0; k < 4; ++k) {
+        NF[k] = __reduce_or_sync(MMPR_FULL_MASK, (lane >> 3) == k ? (nonfast << sh) : 0u);
+        PR[k] = __reduce_or_sync(MMPR_FULL_MASK, (lane >> 3) == k ? (prod << sh) : 0u);
+      }
+      uint32_t S[4];
+      int exit0 = 0;
+      if (!__any_sync(MMPR_FULL_MASK, tails != 0)) {
+        wedge_parse(NF, S, exit0);
+      } else {  // a tail token in this range: general walk (warp-uniform)
+        const uint64_t lp = (uint64_t)lens[0] | ((uint64_t)lens[1] << 16) | ((uint64_t)lens[2] << 32) |
+                            ((uint64_t)lens[3] << 48);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) S[k] = 0xffffffffu;
+        int pos = 0;
+        for (;;) {
+          const int b = next_set128(NF, pos);
+          if (b < 0) break;
+          const uint64_t l = __shfl_sync(MMPR_FULL_MASK, lp, b >> 2);
+          const int L = (int)((l >> (16 * (b & 3))) & 0xffff);
+          clear_range128(S, b + 1, min(b + L, 128));
+          pos = b + L;
+          if (pos >= 128) {
+            exit0 = pos - 128;
+            break;
+          }
         }
       }
+      if (lane < 4) {
+        s_spec[range][lane] = S[lane];
+        s_prod[range][lane] = PR[lane];
+        s_nonfast[range][lane] = NF[lane];
+      }
+      if (lane == 0) s_exit[range] = exit0;
     }
-    if (lane < 4) {
-      s_spec[warp][lane] = S[lane];
-      s_prod[warp][lane] = PR[lane];
-      s_nonfast[warp][lane] = NF[lane];
-    }
-    if (lane == 0) s_exit[warp] = exit0;
     __syncthreads();
 
-    // stitch the 8 warp parses (warp 0)
+    // stitch the NF_RANGES speculative parses in stream order (warp 0)
     if (warp == 0) {
-      const int me = lane < NF_WARPS ? lane : 0;
+      const int me = lane < NF_RANGES ? lane : 0;
       const int e = (me == 0) ? s_carry : s_exit[me - 1];
       bool ok = true;
-      if (lane < NF_WARPS && e != 0)
-        ok = e < 128 && ((s_spec[me][e >> 5] >> (e & 31)) & 1u);
+      if (lane < NF_RANGES && e != 0) ok = e < 128 && ((s_spec[me][e >> 5] >> (e & 31)) & 1u);
       if (__all_sync(MMPR_FULL_MASK, ok)) {
         int cnt = 0;
-        if (lane < NF_WARPS) {
+        if (lane < NF_RANGES) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t F = s_spec[me][k] & mask_ge(k, e);
@@ -258,38 +299,38 @@ normals_fill_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__
         }
         int incl = cnt;
 #pragma unroll
-        for (int d = 1; d < NF_WARPS; d <<= 1) {
+        for (int d = 1; d < 32; d <<= 1) {
           const int v = __shfl_up_sync(MMPR_FULL_MASK, incl, d);
           if (lane >= d) incl += v;
         }
-        if (lane < NF_WARPS) s_base[lane] = incl - cnt;
-        const int tot = __shfl_sync(MMPR_FULL_MASK, incl, NF_WARPS - 1);
+        if (lane < NF_RANGES) s_base[lane] = incl - cnt;
+        const int tot = __shfl_sync(MMPR_FULL_MASK, incl, NF_RANGES - 1);
         __syncwarp();
         if (lane == 0) {
           s_total = tot;
-          s_carry = s_exit[NF_WARPS - 1];
+          s_carry = s_exit[NF_RANGES - 1];
         }
       } else if (lane == 0) {
         int ent = s_carry, base = 0;
-        for (int wi = 0; wi < NF_WARPS; ++wi) {
+        for (int ri = 0; ri < NF_RANGES; ++ri) {
           uint32_t F[4];
           int ex;
           if (ent >= 128) {
             F[0] = F[1] = F[2] = F[3] = 0u;
             ex = ent - 128;
-          } else if (ent == 0 || ((s_spec[wi][ent >> 5] >> (ent & 31)) & 1u)) {
+          } else if (ent == 0 || ((s_spec[ri][ent >> 5] >> (ent & 31)) & 1u)) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) F[k] = s_spec[wi][k] & mask_ge(k, ent);
-            ex = s_exit[wi];
+            for (int k = 0; k < 4; ++k) F[k] = s_spec[ri][k] & mask_ge(k, ent);
+            ex = s_exit[ri];
           } else {
-            uint32_t na[4] = {s_nonfast[wi][0], s_nonfast[wi][1], s_nonfast[wi][2], s_nonfast[wi][3]};
-            ex = rewalk(na, &s_len[wi * 128], ent, F);
+            const uint32_t na[4] = {s_nonfast[ri][0], s_nonfast[ri][1], s_nonfast[ri][2], s_nonfast[ri][3]};
+            ex = rewalk(na, &s_len[ri * 128], ent, F);
           }
-          s_base[wi] = base;
+          s_base[ri] = base;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            s_final[wi][k] = F[k];
-            base += __popc(F[k] & s_prod[wi][k]);
+            s_final[ri][k] = F[k];
+            base += __popc(F[k] & s_prod[ri][k]);
           }
           ent = ex;
         }
@@ -300,22 +341,37 @@ normals_fill_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__
     __syncthreads();
 
     // scatter this thread's normals to their stream positions
-    uint32_t O[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) O[k] = s_final[warp][k] & PR[k];
-    const int64_t base = produced + s_base[warp];
+    for (int r = 0; r < NF_BPT; ++r) {
+      const int range = r * NF_WARPS + warp;
+      const uint4 F = *reinterpret_cast<const uint4 *>(s_final[range]);
+      const uint32_t Fk[4] = {F.x, F.y, F.z, F.w};
+      const int k = lane >> 3;
+      int pre = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int b = 4 * lane + q;
-      const int k = b >> 5;
-      if ((O[k] >> (b & 31)) & 1u) {
-        int rank = __popc(O[k] & ((1u << (b & 31)) - 1u));
+      for (int kk = 0; kk < 4; ++kk)
+        if (kk < k) pre += __popc(Fk[kk] & s_prod[range][kk]);
+      const uint32_t Ok = Fk[k] & s_prod[range][k];
+      pre += __popc(Ok & ((1u << sh) - 1u));
+      const uint32_t nib = (Ok >> sh) & 0xfu;
+      const int64_t base = produced + s_base[range] + pre;
+      const uint64_t word0 = ((chunk * NF_BPT + r) * NF_THREADS + tid) * 4;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          if (kk < k) rank += __popc(O[kk]);
-        const int64_t idx = base + rank;
-        if (idx < count) o[idx] = affine ? add(loc, mul(scale, val[q])) : val[q];
+      for (int q = 0; q < 4; ++q) {
+        if ((nib >> q) & 1u) {
+          const int64_t idx = base + __popc(nib & ((1u << q) - 1u));
+          if (idx < count) {
+            double v = val[r][q];
+            if ((tail_nib[r] >> q) & 1u) {  // rare: recompute the tail value
+              const uint64_t rw = np::philox_word(word0 + q, k0, k1);
+              int L;
+              v = tail_token(word0 + q, (rw >> 9) & 0x000fffffffffffffULL, k0, k1, &L);
+            }
+            o[idx] = affine ? add(loc, mul(scale, v)) : v;
+          }
+        }
       }
+      (void)prod_nib;
     }
     produced += s_total;
     // s_final/s_base/s_total are rewritten only after the next chunk's first
