@@ -53,7 +53,7 @@ struct FineParams {
   int stage_elems;    // doubles per smem stage (16-B multiple)
 };
 
-struct ClusterSlot {
+struct __align__(16) ClusterSlot {
   double v;
   int ok;
   int bad;
