@@ -93,9 +93,11 @@ _lib = None
 _lock = threading.Lock()
 
 
-def load(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load libmmpr.so once and bind every declared symbol."""
+def load(path: str | None = None) -> ctypes.CDLL:
+    """Load libmmpr.so once and bind every declared symbol (MMPR_LIB
+    overrides the in-tree path, for A/B kernel experiments)."""
     global _lib
+    path = path or os.environ.get("MMPR_LIB") or LIB_PATH
     with _lock:
         if _lib is not None:
             return _lib

@@ -32,6 +32,8 @@ __constant__ double c_zig_wi[256] = {NPZ_WI_VALUES};
 __constant__ double c_zig_fi[256] = {NPZ_FI_VALUES};
 
 #define NF_THREADS 256
+// streams at or above which one warp (not one CTA) materialises a stream
+#define MMPR_WARP_STREAMS_MIN 256
 #define NF_WARPS (NF_THREADS / 32)
 
 // ---------------------------------------------------------------------------
@@ -163,7 +165,7 @@ __device__ __noinline__ double tail_token(uint64_t wi, uint64_t mant, uint64_t k
 }
 
 // Wedge test of layer `layer` at x with the next word's uniform.
-__device__ __noinline__ bool wedge_accepts(int layer, double x, uint64_t next_word) {
+__device__ __forceinline__ bool wedge_accepts(int layer, double x, uint64_t next_word) {
   const double u = np::unit_double(next_word);
   const double lhs = add(mul(sub(c_zig_fi[layer - 1], c_zig_fi[layer]), u), c_zig_fi[layer]);
   return lhs < exp(mul(mul(-0.5, x), x));
@@ -379,6 +381,153 @@ normals_fill_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__
   }
 }
 
+// ---------------------------------------------------------------------------
+// warp-per-stream fill (many streams): no block barriers at all
+// ---------------------------------------------------------------------------
+// Each warp owns one stream and walks it in sub-chunks of 32 lanes x 8
+// consecutive words.  A lane parses its 8 words from an assumed entry with
+// the wedge bit trick (or a short exact loop when a tail token is present);
+// entries are then stitched lane to lane with shuffles until stable (an
+// entry of 1 usually just truncates the speculative parse), the produced
+// normals are counted with a warp scan and written at their exact positions.
+#define NW_WORDS 8
+#define NW_THREADS 256
+
+// Lane parse of 8 words from entry e (< 8) when all non-fast words are wedges.
+__device__ __forceinline__ void wedge_parse8(uint32_t nf, int e, uint32_t &S, int &exit) {
+  const uint32_t w = nf >> e;
+  const int width = NW_WORDS - e;
+  const uint32_t starts = w & ~(w << 1);
+  const uint32_t re = w & ~(w + (starts & 0x55555555u));   // runs starting at even offsets
+  const uint32_t ro = w & ~re;
+  const uint32_t cov = ((re << 1) & 0xAAAAAAAAu) | ((ro << 1) & 0x55555555u);
+  const uint32_t s_rel = ~cov & ((1u << width) - 1u);
+  S = s_rel << e;
+  exit = (((w & s_rel) >> (width - 1)) & 1u) ? 1 : 0;
+}
+
+// Exact lane parse from entry e with tail tokens present (rare path).
+__device__ __noinline__ void general_parse8(uint32_t nf, uint32_t tt, int e, uint64_t word0, uint64_t k0,
+                                            uint64_t k1, uint32_t *S_out, int *exit_out) {
+  uint32_t S = 0;
+  int pos = e;
+  while (pos < NW_WORDS) {
+    S |= 1u << pos;
+    int L = 1;
+    if ((nf >> pos) & 1u) {
+      if ((tt >> pos) & 1u) {
+        tail_token(word0 + pos, 0, k0, k1, &L);  // length only
+      } else {
+        L = 2;
+      }
+    }
+    pos += L;
+  }
+  *S_out = S;
+  *exit_out = pos - NW_WORDS;
+}
+
+__global__ void __launch_bounds__(NW_THREADS, 3)
+normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int n_streams, int64_t count, double *__restrict__ out,
+                         int64_t pitch, int affine, double loc, double scale) {
+  __shared__ ulonglong2 zig[256];
+  for (int i = threadIdx.x; i < 256; i += NW_THREADS)
+    zig[i] = make_ulonglong2(c_zig_ki[i], (unsigned long long)__double_as_longlong(c_zig_wi[i]));
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int stream = blockIdx.x * (NW_THREADS / 32) + (threadIdx.x >> 5);
+  if (stream >= n_streams) return;
+  const uint64_t k0 = keys[2 * stream], k1 = keys[2 * stream + 1];
+  double *o = out + (int64_t)stream * pitch;
+
+  int carry = 0;
+  int64_t produced = 0;
+  for (uint64_t sub = 0; produced < count; ++sub) {
+    const uint64_t word0 = (sub * 32 + lane) * NW_WORDS;
+    uint64_t w[NW_WORDS];
+    np::philox_block(word0 / 4, k0, k1, w);
+    np::philox_block(word0 / 4 + 1, k0, k1, w + 4);
+    const uint64_t succ = __shfl_down_sync(MMPR_FULL_MASK, w[0], 1);
+    double x[NW_WORDS];
+    uint32_t nf = 0, pr = 0, tt = 0;
+#pragma unroll
+    for (int i = 0; i < NW_WORDS; ++i) {
+      const uint64_t rw = w[i];
+      const int layer = (int)(rw & 0xff);
+      const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
+      const ulonglong2 z = zig[layer];
+      const double wi = __longlong_as_double((long long)z.y);
+      double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
+      if ((rw >> 8) & 1) v = -v;
+      x[i] = v;
+      if (mant >= z.x) {
+        nf |= 1u << i;
+        if (layer != 0) {
+          const uint64_t nx = (i < NW_WORDS - 1) ? w[i + 1]
+                              : (lane < 31 ? succ : np::philox_word(word0 + NW_WORDS, k0, k1));
+          if (wedge_accepts(layer, v, nx)) pr |= 1u << i;
+        } else {
+          tt |= 1u << i;
+          pr |= 1u << i;
+        }
+      } else {
+        pr |= 1u << i;
+      }
+    }
+    // speculative lane parse from entry 0, then stitch entries lane to lane
+    uint32_t S;
+    int ex, ecur = 0;
+    if (tt == 0) wedge_parse8(nf, 0, S, ex);
+    else general_parse8(nf, tt, 0, word0, k0, k1, &S, &ex);
+    for (;;) {
+      int e = __shfl_up_sync(MMPR_FULL_MASK, ex, 1);
+      if (lane == 0) e = carry;
+      bool changed = false;
+      if (e != ecur) {
+        changed = true;
+        if (e >= NW_WORDS) {
+          S = 0;
+          ex = e - NW_WORDS;
+        } else if (ecur == 0 && ((S >> e) & 1u)) {
+          S &= ~((1u << e) - 1u);  // same attempt boundaries from e on: same exit
+        } else if (tt == 0) {
+          wedge_parse8(nf, e, S, ex);
+        } else {
+          general_parse8(nf, tt, e, word0, k0, k1, &S, &ex);
+        }
+        ecur = e;
+      }
+      if (!__any_sync(MMPR_FULL_MASK, changed)) break;
+    }
+    const uint32_t O = S & pr;
+    const int cnt = __popc(O);
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(MMPR_FULL_MASK, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int total = __shfl_sync(MMPR_FULL_MASK, incl, 31);
+    carry = __shfl_sync(MMPR_FULL_MASK, ex, 31);
+    const int64_t base = produced + incl - cnt;
+#pragma unroll
+    for (int i = 0; i < NW_WORDS; ++i) {
+      if ((O >> i) & 1u) {
+        const int64_t idx = base + __popc(O & ((1u << i) - 1u));
+        if (idx < count) {
+          double v = x[i];
+          if ((tt >> i) & 1u) {  // rare: tail value
+            int L;
+            v = tail_token(word0 + i, (w[i] >> 9) & 0x000fffffffffffffULL, k0, k1, &L);
+          }
+          o[idx] = affine ? add(loc, mul(scale, v)) : v;
+        }
+      }
+    }
+    produced += total;
+  }
+}
+
 }  // namespace mmpr
 
 using namespace mmpr;
@@ -407,6 +556,12 @@ extern "C" int mmpr_normals_fill(const uint64_t *keys, int32_t n_streams, int64_
                                  int64_t pitch, int32_t affine, double loc, double scale, void *stream) {
   if (n_streams < 0 || count < 0 || !keys || !out || (n_streams > 1 && pitch < count)) return MMPR_ERR_ARG;
   if (n_streams == 0 || count == 0) return MMPR_OK;
+  if (n_streams >= MMPR_WARP_STREAMS_MIN) {  // one warp per stream
+    const int per_cta = NW_THREADS / 32;
+    normals_fill_warp_kernel<<<(n_streams + per_cta - 1) / per_cta, NW_THREADS, 0, (cudaStream_t)stream>>>(
+        keys, n_streams, count, out, pitch, affine, loc, scale);
+    return mmpr_check_launch("normals_fill_warp_kernel");
+  }
   normals_fill_kernel<<<n_streams, NF_THREADS, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, affine, loc,
                                                                           scale);
   return mmpr_check_launch("normals_fill_kernel");
