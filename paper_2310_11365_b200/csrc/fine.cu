@@ -338,11 +338,20 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
 template <int KIND, int PPT>
 static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t stream) {
   auto kern = fine_sweep_kernel<KIND, PPT>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
-  if (err != cudaSuccess) return mmpr_check(err, "fine_sweep: smem attribute");
-  if (g.ctas > 8) {
+  // attributes are set once per instantiation (never during graph capture
+  // of a repeated configuration)
+  static int configured_smem = -1;
+  static bool configured_nonportable = false;
+  cudaError_t err;
+  if ((int)g.smem_bytes > configured_smem) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+    if (err != cudaSuccess) return mmpr_check(err, "fine_sweep: smem attribute");
+    configured_smem = (int)g.smem_bytes;
+  }
+  if (g.ctas > 8 && !configured_nonportable) {
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (err != cudaSuccess) return mmpr_check(err, "fine_sweep: non-portable cluster");
+    configured_nonportable = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.n_slices * g.ctas), 1, 1);

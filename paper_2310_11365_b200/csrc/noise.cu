@@ -391,7 +391,6 @@ normals_fill_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__
 // entry of 1 usually just truncates the speculative parse), the produced
 // normals are counted with a warp scan and written at their exact positions.
 #define NW_WORDS 8
-#define NW_THREADS 256
 
 // Lane parse of 8 words from entry e (< 8) when all non-fast words are wedges.
 __device__ __forceinline__ void wedge_parse8(uint32_t nf, int e, uint32_t &S, int &exit) {
@@ -427,18 +426,29 @@ __device__ __noinline__ void general_parse8(uint32_t nf, uint32_t tt, int e, uin
   *exit_out = pos - NW_WORDS;
 }
 
-__global__ void __launch_bounds__(NW_THREADS, 3)
-normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int n_streams, int64_t count, double *__restrict__ out,
-                         int64_t pitch, int affine, double loc, double scale) {
+template <typename T>
+__device__ __forceinline__ T pick8(const T (&v)[NW_WORDS], int i) {
+  T r = v[0];
+#pragma unroll
+  for (int k = 1; k < NW_WORDS; ++k) r = (i == k) ? v[k] : r;
+  return r;
+}
+
+// One single-warp CTA per stream: the Philox key is CTA-uniform (uniform
+// datapath for the key schedule), there is no block barrier in the loop,
+// and up to 32 streams run per SM.
+template <bool AFFINE>
+__global__ void __launch_bounds__(32, 24)
+normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__restrict__ out, int64_t pitch,
+                         double loc, double scale) {
   __shared__ ulonglong2 zig[256];
-  for (int i = threadIdx.x; i < 256; i += NW_THREADS)
+  const int lane = threadIdx.x;
+#pragma unroll
+  for (int i = lane; i < 256; i += 32)
     zig[i] = make_ulonglong2(c_zig_ki[i], (unsigned long long)__double_as_longlong(c_zig_wi[i]));
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int stream = blockIdx.x * (NW_THREADS / 32) + (threadIdx.x >> 5);
-  if (stream >= n_streams) return;
-  const uint64_t k0 = keys[2 * stream], k1 = keys[2 * stream + 1];
-  double *o = out + (int64_t)stream * pitch;
+  __syncwarp();
+  const uint64_t k0 = keys[2 * blockIdx.x], k1 = keys[2 * blockIdx.x + 1];
+  double *o = out + (int64_t)blockIdx.x * pitch;
 
   int carry = 0;
   int64_t produced = 0;
@@ -448,33 +458,35 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int n_streams, int64
     np::philox_block(word0 / 4, k0, k1, w);
     np::philox_block(word0 / 4 + 1, k0, k1, w + 4);
     const uint64_t succ = __shfl_down_sync(MMPR_FULL_MASK, w[0], 1);
+    // fast path for every word, branch-free
     double x[NW_WORDS];
-    uint32_t nf = 0, pr = 0, tt = 0;
+    uint32_t nf = 0;
 #pragma unroll
     for (int i = 0; i < NW_WORDS; ++i) {
       const uint64_t rw = w[i];
-      const int layer = (int)(rw & 0xff);
       const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
-      const ulonglong2 z = zig[layer];
+      const ulonglong2 z = zig[rw & 0xff];
       const double wi = __longlong_as_double((long long)z.y);
-      double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
-      if ((rw >> 8) & 1) v = -v;
-      x[i] = v;
-      if (mant >= z.x) {
-        nf |= 1u << i;
-        if (layer != 0) {
-          const uint64_t nx = (i < NW_WORDS - 1) ? w[i + 1]
-                              : (lane < 31 ? succ : np::philox_word(word0 + NW_WORDS, k0, k1));
-          if (wedge_accepts(layer, v, nx)) pr |= 1u << i;
-        } else {
-          tt |= 1u << i;
-          pr |= 1u << i;
-        }
+      const double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
+      x[i] = ((rw >> 8) & 1) ? -v : v;
+      nf |= (mant >= z.x ? 1u : 0u) << i;
+    }
+    // rare words: wedge tests and tail starts (per-lane loop over set bits)
+    uint32_t pr = ~nf & 0xffu, tt = 0;
+    for (uint32_t rem = nf; rem; rem &= rem - 1) {
+      const int i = __ffs(rem) - 1;
+      const uint64_t rw = pick8(w, i);
+      const int layer = (int)(rw & 0xff);
+      if (layer != 0) {
+        const uint64_t nx = (i < NW_WORDS - 1) ? pick8(w, i + 1)
+                            : (lane < 31 ? succ : np::philox_word(word0 + NW_WORDS, k0, k1));
+        if (wedge_accepts(layer, pick8(x, i), nx)) pr |= 1u << i;
       } else {
+        tt |= 1u << i;
         pr |= 1u << i;
       }
     }
-    // speculative lane parse from entry 0, then stitch entries lane to lane
+    // lane parse from entry 0, then stitch entries lane to lane until stable
     uint32_t S;
     int ex, ecur = 0;
     if (tt == 0) wedge_parse8(nf, 0, S, ex);
@@ -512,16 +524,16 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int n_streams, int64
     const int64_t base = produced + incl - cnt;
 #pragma unroll
     for (int i = 0; i < NW_WORDS; ++i) {
-      if ((O >> i) & 1u) {
-        const int64_t idx = base + __popc(O & ((1u << i) - 1u));
-        if (idx < count) {
-          double v = x[i];
-          if ((tt >> i) & 1u) {  // rare: tail value
-            int L;
-            v = tail_token(word0 + i, (w[i] >> 9) & 0x000fffffffffffffULL, k0, k1, &L);
-          }
-          o[idx] = affine ? add(loc, mul(scale, v)) : v;
-        }
+      const int64_t idx = base + __popc(O & ((1u << i) - 1u));
+      if (((O >> i) & 1u) && idx < count) o[idx] = AFFINE ? add(loc, mul(scale, x[i])) : x[i];
+    }
+    for (uint32_t rem = O & tt; rem; rem &= rem - 1) {  // rare: tail values overwrite
+      const int i = __ffs(rem) - 1;
+      const int64_t idx = base + __popc(O & ((1u << i) - 1u));
+      if (idx < count) {
+        int L;
+        const double v = tail_token(word0 + i, (pick8(w, i) >> 9) & 0x000fffffffffffffULL, k0, k1, &L);
+        o[idx] = AFFINE ? add(loc, mul(scale, v)) : v;
       }
     }
     produced += total;
@@ -556,10 +568,11 @@ extern "C" int mmpr_normals_fill(const uint64_t *keys, int32_t n_streams, int64_
                                  int64_t pitch, int32_t affine, double loc, double scale, void *stream) {
   if (n_streams < 0 || count < 0 || !keys || !out || (n_streams > 1 && pitch < count)) return MMPR_ERR_ARG;
   if (n_streams == 0 || count == 0) return MMPR_OK;
-  if (n_streams >= MMPR_WARP_STREAMS_MIN) {  // one warp per stream
-    const int per_cta = NW_THREADS / 32;
-    normals_fill_warp_kernel<<<(n_streams + per_cta - 1) / per_cta, NW_THREADS, 0, (cudaStream_t)stream>>>(
-        keys, n_streams, count, out, pitch, affine, loc, scale);
+  if (n_streams >= MMPR_WARP_STREAMS_MIN) {  // one single-warp CTA per stream
+    if (affine)
+      normals_fill_warp_kernel<true><<<n_streams, 32, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, loc, scale);
+    else
+      normals_fill_warp_kernel<false><<<n_streams, 32, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, loc, scale);
     return mmpr_check_launch("normals_fill_warp_kernel");
   }
   normals_fill_kernel<<<n_streams, NF_THREADS, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, affine, loc,

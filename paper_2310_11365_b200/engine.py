@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import logging
 import time
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -141,30 +142,163 @@ def _initial_ensemble(initial, cfg: PararealConfig, plan: NoisePlan) -> Particle
 
 class _Workspace:
     """Device buffers of one run (sized for 180 GB HBM: increments of every
-    slice, snapshots of every iterate when retained)."""
+    slice, snapshots of every iterate when retained).  The small per-slice
+    arrays the host reads back are views of three packed report buffers, so
+    the end-of-run transfer is three copies."""
+
+    F64 = ("macro", "micro", "fine_stats", "raw", "rho0")
+    I64 = ("micro_counts", "fine_counts", "counts0")
+    I32 = ("bad", "coarse_status", "match_status")
 
     def __init__(self, K: int, N: int, P: int, S: int, I: int, retain: bool):
         dev = device()
-        f64 = dict(dtype=torch.float64, device=dev)
-        i32 = dict(dtype=torch.int32, device=dev)
-        i64 = dict(dtype=torch.int64, device=dev)
         nv = 3 * I
-        self.snap = torch.empty((K + 1 if retain else 2, N + 1, P), **f64)
-        self.fine = torch.empty((N, P), **f64)
-        self.xi = torch.empty((N, S, row_pitch(P)), **f64)
-        self.macro = torch.empty((K + 1, N + 1, nv), **f64)
-        self.micro = torch.empty((K + 1, N + 1, nv), **f64)
-        self.micro_counts = torch.empty((K + 1, N + 1, I), **i64)
-        self.fine_stats = torch.empty((max(K, 1), N, nv), **f64)
-        self.fine_counts = torch.empty((max(K, 1), N, I), **i64)
-        self.raw = torch.empty((max(K, 1), N, nv), **f64)
-        self.cache = torch.empty((K + 1, N, nv), **f64)
-        self.bad = torch.full((max(K, 1), N), _lib.STAT_OK, **i32)
-        self.coarse_status = torch.full((K + 1, N), _lib.STAT_OK, **i32)
-        self.match_status = torch.full((K + 1, N), _lib.STAT_OK, **i32)
-        self.rho0 = torch.empty((1, nv), **f64)
-        self.counts0 = torch.empty((1, I), **i64)
-        self.scratch = torch.empty(((N + 1) * I * P,), **f64) if I > 1 else None
+        Kc = max(K, 1)
+        shapes = {"macro": (K + 1, N + 1, nv), "micro": (K + 1, N + 1, nv), "fine_stats": (Kc, N, nv),
+                  "raw": (Kc, N, nv), "rho0": (1, nv), "micro_counts": (K + 1, N + 1, I),
+                  "fine_counts": (Kc, N, I), "counts0": (1, I), "bad": (Kc, N), "coarse_status": (K + 1, N),
+                  "match_status": (K + 1, N)}
+        self.report = {}
+        for names, dtype in ((self.F64, torch.float64), (self.I64, torch.int64), (self.I32, torch.int32)):
+            sizes = [int(np.prod(shapes[n])) for n in names]
+            flat = torch.zeros(sum(sizes), dtype=dtype, device=dev)
+            self.report[dtype] = flat
+            off = 0
+            for n, size in zip(names, sizes):
+                setattr(self, n, flat[off:off + size].view(shapes[n]))
+                off += size
+        self.snap = torch.empty((K + 1 if retain else 2, N + 1, P), dtype=torch.float64, device=dev)
+        self.fine = torch.empty((N, P), dtype=torch.float64, device=dev)
+        self.xi = torch.empty((N, S, row_pitch(P)), dtype=torch.float64, device=dev)
+        self.cache = torch.empty((K + 1, N, nv), dtype=torch.float64, device=dev)
+        self.scratch = torch.empty(((N + 1) * I * P,), dtype=torch.float64, device=dev) if I > 1 else None
+        self.x0 = torch.empty((1, P), dtype=torch.float64, device=dev)
+        self.host = {dt: torch.empty(t.shape, dtype=dt, pin_memory=True) for dt, t in self.report.items()}
+
+    def reset_status(self):
+        self.report[torch.int32].fill_(_lib.STAT_OK)
+
+    def read_back(self) -> dict:
+        """Stream-ordered copy of the report buffers into pinned memory, one sync."""
+        for dt, t in self.report.items():
+            self.host[dt].copy_(t, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        h = {}
+        for names, dt in ((self.F64, torch.float64), (self.I64, torch.int64), (self.I32, torch.int32)):
+            flat = self.host[dt].numpy()
+            off = 0
+            for n in names:
+                shape = getattr(self, n).shape
+                size = int(np.prod(shape))
+                h[n] = flat[off:off + size].reshape(shape).copy()
+                off += size
+        return h
+
+    def report_bytes(self) -> int:
+        return int(sum(t.numel() * t.element_size() for t in self.report.values()))
+
+
+class _RunPlan:
+    """One run configuration: its workspace and its launch sequence
+    (replayed from a CUDA graph when the configuration repeats)."""
+
+    def __init__(self, model_d, ode_d, ode_model_d, integ_d, part_d, cfg: PararealConfig, plan: NoisePlan,
+                 reuse: bool):
+        self.model_d, self.ode_d, self.ode_model_d, self.integ_d, self.part_d = \
+            model_d, ode_d, ode_model_d, integ_d, part_d
+        self.cfg, self.plan, self.reuse = cfg, plan, reuse
+        N, K, P, S, I = cfg.n_slices, cfg.iterations, cfg.particles, cfg.step.steps_per_slice, \
+            cfg.partition.n_regions
+        self.N, self.K, self.P, self.S, self.I = N, K, P, S, I
+        self.times = tuple(cfg.t_start + n * cfg.slice_length for n in range(N + 1))
+        self.times_d = torch.tensor(self.times, dtype=torch.float64, device=device())
+        self.ws = _Workspace(K, N, P, S, I, cfg.retain_snapshots)
+        self.graph = None
+        self.launches_per_run = 0
+
+    def snap(self, k):
+        return self.ws.snap[k if self.cfg.retain_snapshots else k % 2]
+
+    def issue_prologue(self, timer, injected=False):
+        """Iteration 0 (coarse cascade + lift) and, for frozen noise, the
+        increments of every slice."""
+        ws, cfg, part_d = self.ws, self.cfg, self.part_d
+        N, P, S = self.N, self.P, self.S
+        ws.reset_status()
+        self.snap(0)[0].copy_(ws.x0[0])
+        ev = timer.start()
+        kernels.restrict(part_d, ws.x0, ws.rho0, ws.counts0, ws.scratch)
+        timer.stop("restrict", ev)
+        ev = timer.start()
+        kernels.coarse_row(self.ode_d, self.ode_model_d, self.integ_d, self.times_d, 0, ws.rho0, None, None,
+                           ws.macro[0], ws.cache[0], None, ws.coarse_status[0])
+        timer.stop("coarse", ev)
+        ev = timer.start()
+        kernels.match(part_d, ws.macro[0, 1:], ws.rho0, ws.counts0, ws.x0, self.snap(0)[1:], 1, ws.match_status[0])
+        timer.stop("match", ev)
+        kernels.restrict(part_d, self.snap(0), ws.micro[0], ws.micro_counts[0], ws.scratch)
+        if not injected and not self.plan.fresh:
+            ev = timer.start()
+            slice_noise(self.plan.master_seed, 0, N, S, P, 0, False, out=ws.xi)
+            timer.stop("noise", ev)
+
+    def issue_iteration(self, k, timer, injected=False):
+        ws, part_d, N, S = self.ws, self.part_d, self.N, self.S
+        if not injected and self.plan.fresh:
+            ev = timer.start()
+            slice_noise(self.plan.master_seed, 0, N, S, self.P, k, True, out=ws.xi)
+            timer.stop("noise", ev)
+        cur, nxt = self.snap(k), self.snap(k + 1)
+        ev = timer.start()
+        kernels.fine_sweep(self.model_d, cur[:N], ws.fine, self.times_d[:N], S, self.cfg.step.dt, ws.xi, ws.bad[k])
+        timer.stop("fine", ev)
+        ev = timer.start()
+        kernels.restrict(part_d, ws.fine, ws.fine_stats[k], ws.fine_counts[k], ws.scratch)
+        timer.stop("restrict", ev)
+        ev = timer.start()
+        kernels.coarse_row(self.ode_d, self.ode_model_d, self.integ_d, self.times_d, k + 1, ws.rho0,
+                           ws.fine_stats[k], ws.cache[k], ws.macro[k + 1], ws.cache[k + 1], ws.raw[k],
+                           ws.coarse_status[k + 1], skip_until=(k + 1) if self.reuse else 0)
+        timer.stop("coarse", ev)
+        ev = timer.start()
+        kernels.match(part_d, ws.macro[k + 1, 1:], ws.fine_stats[k], ws.fine_counts[k], ws.fine, nxt[1:], 0,
+                      ws.match_status[k + 1])
+        nxt[0].copy_(ws.x0[0])
+        timer.stop("match", ev)
+        kernels.restrict(part_d, nxt, ws.micro[k + 1], ws.micro_counts[k + 1], ws.scratch)
+
+    def issue_all(self, timer):
+        self.issue_prologue(timer)
+        for k in range(self.K):
+            self.issue_iteration(k, timer)
+
+    def replay(self):
+        """Launch the whole run as one CUDA graph (captured on first use)."""
+        if self.graph is None:
+            before = _lib.launch_count["total"]
+            self.issue_all(_StageTimer(False))  # eager warm-up: sets kernel attributes, checks arguments
+            self.launches_per_run = _lib.launch_count["total"] - before
+            torch.cuda.current_stream().synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.issue_all(_StageTimer(False))
+            self.graph = g
+        self.graph.replay()
+
+
+_PLANS: dict = {}
+_PLANS_MAX = 2
+
+
+def clear_graph_cache() -> None:
+    """Drop cached run plans (workspaces and CUDA graphs)."""
+    _PLANS.clear()
+
+
+def _plan_key(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse):
+    return (bytes(model_d), bytes(ode_d), bytes(ode_model_d), bytes(integ_d), bytes(part_d), cfg.n_slices,
+            cfg.iterations, cfg.particles, cfg.step.dt, cfg.step.steps_per_slice, cfg.slice_length, cfg.t_start,
+            cfg.retain_snapshots, plan.master_seed, plan.mode, reuse, torch.cuda.current_device())
 
 
 def _wasserstein_delta(a, b, part_desc, scratch_stats, scratch_counts) -> float:
@@ -176,7 +310,7 @@ def _wasserstein_delta(a, b, part_desc, scratch_stats, scratch_counts) -> float:
 
 def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: InitialDistribution | ParticleEnsemble,
                     cfg: PararealConfig, plan: NoisePlan, *, reuse_converged_coarse: bool = True,
-                    record_timings: bool = True, increments=None) -> PararealTrace:
+                    record_timings: bool = False, increments=None, use_graph: bool = True) -> PararealTrace:
     """Run the micro-macro Parareal iteration on the GPU and record every iterate.
 
     ``increments`` (optional) injects the Brownian increments as a callable
@@ -185,6 +319,11 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
     ``reuse_converged_coarse`` copies C(rho_n) for n < k from the previous
     row instead of re-integrating (bitwise identical: those inputs have
     converged exactly, engine.py:11-14).
+    ``use_graph`` replays the run's launch sequence as one CUDA graph, cached
+    per configuration (eager launches when timings are recorded, increments
+    are injected or the Wasserstein stop criterion is active).
+    Snapshots of a graph-replayed run live in the cached workspace and are
+    overwritten by the next run of the same configuration.
     """
     require_cuda()
     if coarse.n_regions != cfg.partition.n_regions:
@@ -193,90 +332,56 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
     model_d = device_model(model)
     ode_d, ode_model_d = device_ode(coarse)
     integ_d = integrator_descriptor(cfg.integrator)
-    part = cfg.partition
-    part_d = part.descriptor()
+    part_d = cfg.partition.descriptor()
     ens0 = _initial_ensemble(initial, cfg, plan)
-    N, K, P, S, I = cfg.n_slices, cfg.iterations, cfg.particles, cfg.step.steps_per_slice, part.n_regions
-    dt = cfg.step.dt
-    times = tuple(cfg.t_start + n * cfg.slice_length for n in range(N + 1))
-    times_d = torch.tensor(times, dtype=torch.float64, device=device())
-    ws = _Workspace(K, N, P, S, I, cfg.retain_snapshots)
+    eager = record_timings or increments is not None or cfg.stop_wasserstein_tol is not None or not use_graph
+    if eager:
+        rp = _RunPlan(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse)
+    else:
+        key = _plan_key(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse)
+        rp = _PLANS.get(key)
+        if rp is None:
+            while len(_PLANS) >= _PLANS_MAX:
+                _PLANS.pop(next(iter(_PLANS)))
+            rp = _RunPlan(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse)
+            _PLANS[key] = rp
+    ws = rp.ws
+    ws.x0.copy_(ens0.device_positions.reshape(1, -1))
     timer = _StageTimer(record_timings)
-    x0 = ens0.device_positions.reshape(1, P)
-
-    def snap(k):
-        return ws.snap[k if cfg.retain_snapshots else k % 2]
-
-    # ---- iteration 0: coarse cascade + lift of the initial shape -------------
-    snap(0)[0].copy_(ens0.device_positions)
-    ev = timer.start()
-    kernels.restrict(part_d, x0, ws.rho0, ws.counts0, ws.scratch)
-    timer.stop("restrict", ev)
-    ev = timer.start()
-    kernels.coarse_row(ode_d, ode_model_d, integ_d, times_d, 0, ws.rho0, None, None, ws.macro[0], ws.cache[0],
-                       None, ws.coarse_status[0])
-    timer.stop("coarse", ev)
-    ev = timer.start()
-    kernels.match(part_d, ws.macro[0, 1:], ws.rho0, ws.counts0, x0, snap(0)[1:], 1, ws.match_status[0])
-    timer.stop("match", ev)
-    kernels.restrict(part_d, snap(0), ws.micro[0], ws.micro_counts[0], ws.scratch)
-
-    # ---- increments ---------------------------------------------------------
-    injected_fn = increments if callable(increments) else None
-    if increments is not None and not callable(increments):
-        ws.xi = increments
-    elif injected_fn is None and not plan.fresh:
-        ev = timer.start()
-        slice_noise(plan.master_seed, 0, N, S, P, 0, False, out=ws.xi)
-        timer.stop("noise", ev)
-
+    N, K, P = rp.N, rp.K, rp.P
     stopped_at = None
-    iterations_done = 0
-    for k in range(K):
-        if injected_fn is not None:
-            for n in range(N):
-                ws.xi[n, :, :P] = torch.as_tensor(np.asarray(injected_fn(n, k), dtype=float)).to(device())
-        elif increments is None and plan.fresh:
-            ev = timer.start()
-            slice_noise(plan.master_seed, 0, N, S, P, k, True, out=ws.xi)
-            timer.stop("noise", ev)
-        cur, nxt = snap(k), snap(k + 1)
-        ev = timer.start()
-        kernels.fine_sweep(model_d, cur[:N], ws.fine, times_d[:N], S, dt, ws.xi, ws.bad[k])
-        timer.stop("fine", ev)
-        ev = timer.start()
-        kernels.restrict(part_d, ws.fine, ws.fine_stats[k], ws.fine_counts[k], ws.scratch)
-        timer.stop("restrict", ev)
-        ev = timer.start()
-        kernels.coarse_row(ode_d, ode_model_d, integ_d, times_d, k + 1, ws.rho0, ws.fine_stats[k], ws.cache[k],
-                           ws.macro[k + 1], ws.cache[k + 1], ws.raw[k], ws.coarse_status[k + 1],
-                           skip_until=(k + 1) if reuse_converged_coarse else 0)
-        timer.stop("coarse", ev)
-        ev = timer.start()
-        kernels.match(part_d, ws.macro[k + 1, 1:], ws.fine_stats[k], ws.fine_counts[k], ws.fine, nxt[1:], 0,
-                      ws.match_status[k + 1])
-        nxt[0].copy_(ens0.device_positions)
-        timer.stop("match", ev)
-        kernels.restrict(part_d, nxt, ws.micro[k + 1], ws.micro_counts[k + 1], ws.scratch)
-        iterations_done = k + 1
-        if cfg.stop_wasserstein_tol is not None:
-            st = torch.empty((N, 3), dtype=torch.float64, device=device())
-            ct = torch.empty((N, 1), dtype=torch.int64, device=device())
-            delta = _wasserstein_delta(nxt[1:], cur[1:], SINGLE_REGION.descriptor(), st, ct)
-            if delta <= cfg.stop_wasserstein_tol:
-                stopped_at = k + 1
-                logger.info("stopping after iteration %d: max slice Wasserstein delta %.3e", k + 1, delta)
-                break
+    iterations_done = K
+    if not eager:
+        rp.replay()
+        _lib.launch_count["total"] += rp.launches_per_run
+    else:
+        injected = increments is not None
+        if injected and not callable(increments):
+            ws.xi = increments
+        rp.issue_prologue(timer, injected)
+        for k in range(K):
+            if callable(increments):
+                for n in range(N):
+                    ws.xi[n, :, :P] = torch.as_tensor(np.asarray(increments(n, k), dtype=float)).to(device())
+            rp.issue_iteration(k, timer, injected)
+            iterations_done = k + 1
+            if cfg.stop_wasserstein_tol is not None:
+                st = torch.empty((N, 3), dtype=torch.float64, device=device())
+                ct = torch.empty((N, 1), dtype=torch.int64, device=device())
+                delta = _wasserstein_delta(rp.snap(k + 1)[1:], rp.snap(k)[1:], SINGLE_REGION.descriptor(), st, ct)
+                if delta <= cfg.stop_wasserstein_tol:
+                    stopped_at = k + 1
+                    logger.info("stopping after iteration %d: max slice Wasserstein delta %.3e", k + 1, delta)
+                    break
 
     # ---- one device->host transfer, then the reference's error order --------
-    torch.cuda.synchronize()
+    h = ws.read_back()
     Kd = iterations_done
-    h = {name: getattr(ws, name).cpu().numpy() for name in
-         ("macro", "micro", "micro_counts", "fine_stats", "raw", "bad", "coarse_status", "match_status",
-          "rho0", "counts0")}
-    _raise_first_error(h, N, Kd, I)
-    trace = _build_trace(h, ws, cfg, plan, times, Kd, I, timer, stopped_at)
-    trace.d2h_bytes = int(sum(v.nbytes for v in h.values()))
+    for name in ("macro", "micro", "micro_counts"):
+        h[name] = h[name][:Kd + 1]
+    _raise_first_error(h, N, Kd, cfg.partition.n_regions)
+    trace = _build_trace(h, ws, cfg, plan, rp.times, Kd, cfg.partition.n_regions, timer, stopped_at)
+    trace.d2h_bytes = ws.report_bytes()
     return trace
 
 
@@ -300,35 +405,66 @@ def _raise_first_error(h, N: int, K: int, I: int) -> None:
                                       f"{var_t:.3e}", region=region)
 
 
+class _LazyRows(Sequence):
+    """Read-only list of trace rows materialised on first access (building
+    every MacroState eagerly costs more host time than the device run)."""
+
+    def __init__(self, n: int, make_row):
+        self._n = n
+        self._make = make_row
+        self._rows: dict = {}
+
+    def __len__(self) -> int:
+        return self._n
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(self._n))]
+        if k < 0:
+            k += self._n
+        if not 0 <= k < self._n:
+            raise IndexError(k)
+        row = self._rows.get(k)
+        if row is None:
+            row = self._rows[k] = self._make(k)
+        return row
+
+    def __repr__(self) -> str:
+        return f"<{self._n} trace rows>"
+
+
 def _build_trace(h, ws, cfg, plan, times, K, I, timer, stopped_at) -> PararealTrace:
     N = cfg.n_slices
-    trace = PararealTrace(times=times, macro=[], micro_stats=[], snapshots=[] if cfg.retain_snapshots else None,
-                          noise_mode=plan.mode.value, master_seed=plan.master_seed, stopped_at=stopped_at)
+    macro, micro, mcounts = h["macro"], h["micro"], h["micro_counts"]
     rho0_deg = tuple(h["counts0"][0] < 2)
-    for k in range(K + 1):
-        row = [MacroState.from_packed(h["macro"][k, 0], I, rho0_deg)]
-        row += [MacroState.from_packed(h["macro"][k, n], I) for n in range(1, N + 1)]
-        trace.macro.append(row)
-        trace.micro_stats.append([MacroState.from_packed(h["micro"][k, n], I, tuple(h["micro_counts"][k, n] < 2))
-                                  for n in range(N + 1)])
-        if trace.snapshots is not None:
-            trace.snapshots.append([ParticleEnsemble._wrap(ws.snap[k, n]) for n in range(N + 1)])
+
+    def macro_row(k):
+        return [MacroState.from_packed(macro[k, 0], I, rho0_deg)] + \
+            [MacroState.from_packed(macro[k, n], I) for n in range(1, N + 1)]
+
+    def micro_row(k):
+        return [MacroState.from_packed(micro[k, n], I, tuple(mcounts[k, n] < 2)) for n in range(N + 1)]
+
+    snapshots = None
+    if cfg.retain_snapshots and ws is not None:
+        snap = ws.snap
+        snapshots = _LazyRows(K + 1, lambda k: [ParticleEnsemble._wrap(snap[k, n]) for n in range(N + 1)])
+    trace = PararealTrace(times=times, macro=_LazyRows(K + 1, macro_row), micro_stats=_LazyRows(K + 1, micro_row),
+                          snapshots=snapshots, noise_mode=plan.mode.value, master_seed=plan.master_seed,
+                          stopped_at=stopped_at)
+    # diagnostics (engine.py:178-181, 218-228), vectorised: abs/sub/max are exact
     rho0 = h["rho0"][0]
-    for n in range(N):
-        for i in range(I):
-            if rho0[I + i] == 0.0 and h["macro"][0, n + 1, I + i] > 0.0 and rho0[2 * I + i] > 0.0:
-                trace.lift_collapses.append((0, n + 1, i))
-    for n in range(1, N + 1):
-        gap = max(abs(a - b) for a, b in zip(h["macro"][0, n, 2 * I:].tolist(), h["micro"][0, n, 2 * I:].tolist()))
-        trace.fraction_gaps.append((0, n, gap))
-    for k in range(K):
-        for n in range(N):
-            raw = h["raw"][k, n].tolist()
-            fine = h["fine_stats"][k, n].tolist()
-            trace.fraction_gaps.append((k + 1, n + 1, max(abs(a - b) for a, b in zip(raw[2 * I:], fine[2 * I:]))))
-            for i in range(I):
-                if raw[I + i] < 0.0:
-                    trace.clamp_events.append((k + 1, n + 1, i, raw[I + i]))
+    lift = (rho0[I:2 * I] == 0.0) & (macro[0, 1:, I:2 * I] > 0.0) & (rho0[2 * I:] > 0.0)
+    trace.lift_collapses = [(0, int(n) + 1, int(i)) for n, i in np.argwhere(lift)]
+    gaps0 = np.max(np.abs(macro[0, 1:, 2 * I:] - micro[0, 1:, 2 * I:]), axis=1).tolist()
+    trace.fraction_gaps = [(0, n + 1, g) for n, g in enumerate(gaps0)]
+    if K > 0:
+        raw, fine = h["raw"][:K], h["fine_stats"][:K]
+        gaps = np.max(np.abs(raw[:, :, 2 * I:] - fine[:, :, 2 * I:]), axis=2).tolist()
+        trace.fraction_gaps += [(k + 1, n + 1, gaps[k][n]) for k in range(K) for n in range(N)]
+        neg = raw[:, :, I:2 * I]
+        trace.clamp_events = [(int(k) + 1, int(n) + 1, int(i), float(neg[k, n, i]))
+                              for k, n, i in np.argwhere(neg < 0.0)]
     trace.timings = timer.resolve()
     return trace
 
