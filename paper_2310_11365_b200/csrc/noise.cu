@@ -438,7 +438,7 @@ __device__ __forceinline__ T pick8(const T (&v)[NW_WORDS], int i) {
 // datapath for the key schedule), there is no block barrier in the loop,
 // and up to 32 streams run per SM.
 template <bool AFFINE>
-__global__ void __launch_bounds__(32, 24)
+__global__ void __launch_bounds__(32, 16)
 normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__restrict__ out, int64_t pitch,
                          double loc, double scale) {
   __shared__ ulonglong2 zig[256];
