@@ -30,6 +30,7 @@
 namespace mmpr {
 
 #define FS_MAX_CLUSTER 16
+#define FS_MAX_STAGES 4
 #define FS_L2_AHEAD 3  // steps of increments kept in flight towards L2 beyond the smem stages
 
 struct FineParams {
@@ -51,6 +52,7 @@ struct FineParams {
   int slots_per_cta;  // 4 * warps per CTA
   int ctas;           // CTAs per slice (cluster size)
   int stage_elems;    // doubles per smem stage (16-B multiple)
+  int nstages;        // increment stages in shared memory (2..FS_MAX_STAGES)
 };
 
 struct __align__(16) ClusterSlot {
@@ -75,15 +77,16 @@ __device__ __forceinline__ double em_update(const FineParams &p, double x, doubl
   return add(moved, noise);
 }
 
-// PPT: accumulator elements per lane (ceil(max leaf / 8) <= 16)
-template <int KIND, int PPT>
-__global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p) {
-  extern __shared__ __align__(128) double s_stage[];  // [2][stage_elems]
-  __shared__ PwVal s_wp[32];
-  __shared__ PwVal s_cta;
-  __shared__ ClusterSlot s_slot[2][FS_MAX_CLUSTER];
-  __shared__ int s_bad[2];
-  __shared__ __align__(8) uint64_t s_bar[2];
+// PPT: accumulator elements per lane (ceil(max leaf / 8) <= 16); HAS_TAIL:
+// P % 8 != 0 (the last leaf adds its trailing elements one by one)
+template <int KIND, int PPT, bool HAS_TAIL, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p) {
+  extern __shared__ __align__(128) double s_stage[];  // [nstages][stage_elems]
+  __shared__ PwVal s_wp[2][32];
+  __shared__ __align__(16) ClusterSlot s_slot[2][FS_MAX_CLUSTER];
+  __shared__ int s_bad[3];
+  __shared__ __align__(8) uint64_t s_bar[FS_MAX_STAGES];
+  __shared__ __align__(8) uint64_t s_red_bar[2];  // cluster partials of call parity 0/1
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -100,7 +103,6 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
   const int tail = (int)(len & 7);       // trailing elements added one by one
   const int64_t tail_off = off + (len & ~int64_t(7));
   const bool slot_ok = len > 0;
-  const bool warp_has_tail = __any_sync(MMPR_FULL_MASK, tail > 0);
 
   int64_t lo, hi;
   {
@@ -110,6 +112,7 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
     else pw_leaf(p.P, p.D, (int64_t)(rank + 1) * p.slots_per_cta, &hi, &o2);
   }
   const uint32_t stage_bytes = (uint32_t)((((hi - lo) * 8) + 15) & ~int64_t(15));
+  const int last_idx = (int)(hi - lo) - 1;
 
   // ---- load positions --------------------------------------------------------
   double x[PPT];
@@ -117,47 +120,58 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
   const double *xin = p.x_in + (int64_t)slice * p.in_pitch;
 #pragma unroll
   for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? xin[off + j8 + 8 * m] : 0.0;
-  if (j8 < tail) xt = xin[tail_off + j8];
+  if (HAS_TAIL && j8 < tail) xt = xin[tail_off + j8];
 
   // ---- increment pipeline -------------------------------------------------------
   const double *xi_slice = p.xi + (int64_t)slice * p.xi_slice_pitch;
+  const int ns = p.nstages;
   if (tid == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
+    for (int q = 0; q < ns; ++q) mbar_init(&s_bar[q], 1);
+    mbar_init(&s_red_bar[0], 1);
+    mbar_init(&s_red_bar[1], 1);
     fence_mbar_init();
     s_bad[0] = 0;
     s_bad[1] = 0;
+    s_bad[2] = 0;
   }
-  __syncthreads();
+  // every CTA's barriers must be initialised before any peer sends to them
+  if (p.ctas > 1) cluster_sync_all();
+  else __syncthreads();
   if (tid == 0) {
-    for (int j = 0; j < 2 && j < p.S; ++j) {
+    for (int j = 0; j < ns && j < p.S; ++j) {
       mbar_arrive_expect_tx(&s_bar[j], stage_bytes);
       bulk_g2s(s_stage + j * p.stage_elems, xi_slice + j * p.xi_row_pitch + lo, stage_bytes, &s_bar[j]);
     }
-    for (int j = 2; j < 2 + FS_L2_AHEAD && j < p.S; ++j)
+    for (int j = ns; j < ns + FS_L2_AHEAD && j < p.S; ++j)
       prefetch_l2(xi_slice + (int64_t)j * p.xi_row_pitch + lo, stage_bytes);
   }
-  int issued = (p.S < 2) ? p.S : 2;
+  int issued = (p.S < ns) ? p.S : ns;
 
   // ---- reduction of sum(x) in numpy order + non-finite flag -------------------
-  // Barriers per call: B1 (__syncthreads) and B2 (__syncthreads, or the
-  // cluster barrier).  s_bad is double-buffered by call parity: slot r&1 is
-  // written before B1 of call r and reset (for call r+2) after B1 of r+1.
+  // One block barrier per call (B1) plus, for clusters, one cluster barrier
+  // (B2).  Every warp reads all warp partials after B1, so s_wp is
+  // double-buffered by call parity; the blow-up flag uses three slots: slot
+  // r%3 is written before B1 of call r, read after it, and reset by thread 0
+  // after B1 of call r+1 (before it can reach B1 of r+2, after which the
+  // slot's next writers run).
   // `refill` (>= 0): step whose increments go into the stage this step just
   // consumed -- issued right after B1, when every thread has read it.
   auto reduce = [&](int r, int bad_local, int refill, double &mean_out, int &bad_out) {
     const int par = r & 1;
+    const int bslot = r % 3;
     double acc = x[0];
 #pragma unroll
-    for (int m = 1; m < PPT; ++m)
-      if (m < cnt) acc = add(acc, x[m]);
+    for (int m = 1; m < PPT; ++m) {
+      const double t = add(acc, x[m]);
+      acc = (m < cnt) ? t : acc;
+    }
     // all 8 lanes of a slot hold cnt elements; shuffles stay warp-uniform
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 1));
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 2));
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 4));
     // a leaf shorter than 8 (P < 8) is summed sequentially from 0.0
     if (cnt == 0) acc = 0.0;
-    if (warp_has_tail) {
+    if (HAS_TAIL) {
 #pragma unroll
       for (int i = 0; i < 7; ++i) {
         const double v = __shfl_sync(MMPR_FULL_MASK, xt, (lane & ~7) | i);
@@ -171,63 +185,59 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
     leaf = pw_xor_level(leaf, lane, 8);
     leaf = pw_xor_level(leaf, lane, 16);
     if (lane == 0) {
-      s_wp[warp] = leaf;
-      if (wbad) s_bad[par] = 1;
+      s_wp[par][warp] = leaf;
+      if (wbad) s_bad[bslot] = 1;
     }
-    __syncthreads();  // B1
-    if (tid == 0 && refill >= 0) {
-      const int st = refill & 1;
-      mbar_arrive_expect_tx(&s_bar[st], stage_bytes);
-      bulk_g2s(s_stage + st * p.stage_elems, xi_slice + (int64_t)refill * p.xi_row_pitch + lo, stage_bytes,
-               &s_bar[st]);
-      ++issued;
-      const int pf = refill + FS_L2_AHEAD;  // pull a later step towards L2
-      if (pf < p.S) prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
-    }
-    PwVal total;
-    int bad;
-    if (warp == 0) {
-      PwVal v;
-      if (lane < nwarps) v = s_wp[lane];
-      else { v.v = 0.0; v.ok = 0; }
-#pragma unroll
-      for (int m = 1; m < 32; m <<= 1)
-        if (m < nwarps) v = pw_xor_level(v, lane, m);
-      if (p.ctas == 1) {
-        if (lane == 0) {
-          s_cta = v;
-          s_bad[par ^ 1] = 0;
-        }
-      } else if (lane < p.ctas) {  // one lane per destination CTA
-        const uint32_t remote = mapa_shared(smem_addr(&s_slot[par][rank]), (uint32_t)lane);
-        st_cluster_v2(remote, __double_as_longlong(v.v),
-                      (unsigned long long)(uint32_t)v.ok | ((unsigned long long)(uint32_t)s_bad[par] << 32));
-        __syncwarp(__activemask());
-        if (lane == 0) s_bad[par ^ 1] = 0;
+    __syncthreads();  // B1 (the only block barrier of a step)
+    if (tid == 0) {
+      s_bad[(r + 2) % 3] = 0;  // slot of call r-1: all its readers passed this B1, its next writers follow B1 of r+1
+      if (refill >= 0) {
+        const int st = refill % ns;
+        mbar_arrive_expect_tx(&s_bar[st], stage_bytes);
+        bulk_g2s(s_stage + st * p.stage_elems, xi_slice + (int64_t)refill * p.xi_row_pitch + lo, stage_bytes,
+                 &s_bar[st]);
+        ++issued;
+        const int pf = refill + FS_L2_AHEAD;  // pull a later step towards L2
+        if (pf < p.S) prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
       }
     }
-    if (p.ctas == 1) {
-      __syncthreads();  // B2
-      total = s_cta;
-      bad = s_bad[par];
-    } else {
-      cluster_sync_all();  // B2
-      // every warp combines the per-CTA partials with the same xor tree
-      PwVal v;
-      v.v = 0.0;
-      v.ok = 0;
+    // every warp folds the CTA's warp partials with the same xor tree
+    PwVal v;
+    if (lane < nwarps) v = s_wp[par][lane];
+    else { v.v = 0.0; v.ok = 0; }
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1)
+      if (m < nwarps) v = pw_xor_level(v, lane, m);
+    PwVal total;
+    int bad = s_bad[bslot];
+    if (p.ctas > 1) {
+      // Each CTA's partial goes to every CTA of the cluster as one 16-byte
+      // st.async that completes tx bytes on the receiver's mbarrier; a CTA
+      // waits only for its own barrier (no cluster-wide barrier per step).
+      if (tid == 0) mbar_arrive_expect_tx(&s_red_bar[par], 16u * (uint32_t)p.ctas);
+      if (warp == 0 && lane < p.ctas) {
+        const uint32_t remote = mapa_shared(smem_addr(&s_slot[par][rank]), (uint32_t)lane);
+        const uint32_t rbar = mapa_shared(smem_addr(&s_red_bar[par]), (uint32_t)lane);
+        st_async_v2(remote, __double_as_longlong(v.v),
+                    (unsigned long long)(uint32_t)v.ok | ((unsigned long long)(uint32_t)bad << 32), rbar);
+      }
+      mbar_wait_parity(&s_red_bar[par], (uint32_t)((r >> 1) & 1));
+      PwVal c;
+      c.v = 0.0;
+      c.ok = 0;
       int b = 0;
       if (lane < p.ctas) {
-        v.v = s_slot[par][lane].v;
-        v.ok = s_slot[par][lane].ok;
+        c.v = s_slot[par][lane].v;
+        c.ok = s_slot[par][lane].ok;
         b = s_slot[par][lane].bad;
       }
 #pragma unroll
       for (int m = 1; m < FS_MAX_CLUSTER; m <<= 1)
-        if (m < p.ctas) v = pw_xor_level(v, lane, m);
-      total.v = __shfl_sync(MMPR_FULL_MASK, v.v, 0);
-      total.ok = 1;
+        if (m < p.ctas) c = pw_xor_level(c, lane, m);
+      total.v = __shfl_sync(MMPR_FULL_MASK, c.v, 0);
       bad = __any_sync(MMPR_FULL_MASK, b);
+    } else {
+      total.v = v.v;
     }
     mean_out = div(total.v, (double)p.P);
     bad_out = bad;
@@ -241,23 +251,26 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
   const double t_start = p.t0[slice];
   (void)t_start;
   for (int j = 0; j < p.S; ++j) {
-    const int stage = j & 1;
-    mbar_wait_parity(&s_bar[stage], (uint32_t)((j >> 1) & 1));
+    const int stage = j % ns;
+    mbar_wait_parity(&s_bar[stage], (uint32_t)((j / ns) & 1));
     const double *xs = s_stage + stage * p.stage_elems;
     int bad_local = 0;
 #pragma unroll
     for (int m = 0; m < PPT; ++m) {
-      if (m < cnt) {
-        x[m] = em_update<KIND>(p, x[m], s, xs[off - lo + j8 + 8 * m]);
-        bad_local |= !finite(x[m]);
-      }
+      // branch-free: lanes past their leaf compute on a clamped index and
+      // keep their (unused) value
+      const int idx = max(0, min((int)(off - lo) + j8 + 8 * m, last_idx));
+      const double nx = em_update<KIND>(p, x[m], s, xs[idx]);
+      const bool live = m < cnt;
+      x[m] = live ? nx : x[m];
+      bad_local |= (live && !finite(nx)) ? 1 : 0;
     }
-    if (j8 < tail) {
+    if (HAS_TAIL && j8 < tail) {
       xt = em_update<KIND>(p, xt, s, xs[tail_off - lo + j8]);
       bad_local |= !finite(xt);
     }
     // B1 inside reduce() orders every read of this stage before its refill
-    reduce(j + 1, bad_local, (j + 2 < p.S) ? j + 2 : -1, s, bad);
+    reduce(j + 1, bad_local, (j + ns < p.S) ? j + ns : -1, s, bad);
     if (bad) {
       first_bad = j;
       break;
@@ -265,14 +278,15 @@ __global__ void __launch_bounds__(1024, 1) fine_sweep_kernel(const FineParams p)
   }
   // Drain copies still in flight after an early exit.
   if (tid == 0 && first_bad != MMPR_STAT_OK) {
-    for (int j = first_bad + 1; j < issued; ++j) mbar_wait_parity(&s_bar[j & 1], (uint32_t)((j >> 1) & 1));
+    for (int j = first_bad + 1; j < issued; ++j) mbar_wait_parity(&s_bar[j % ns], (uint32_t)((j / ns) & 1));
   }
 
+  if (p.ctas > 1) cluster_sync_all();  // no peer may still be writing into this CTA
   double *xo = p.x_out + (int64_t)slice * p.out_pitch;
 #pragma unroll
   for (int m = 0; m < PPT; ++m)
     if (m < cnt) xo[off + j8 + 8 * m] = x[m];
-  if (j8 < tail) xo[tail_off + j8] = xt;
+  if (HAS_TAIL && j8 < tail) xo[tail_off + j8] = xt;
   if (tid == 0 && rank == 0) {
     p.bad_step[slice] = first_bad;
     if (p.final_mean) p.final_mean[slice] = s;
@@ -289,6 +303,7 @@ struct FineGeometry {
   int ctas;
   int threads;
   int stage_elems;
+  int nstages;
   size_t smem_bytes;
 };
 
@@ -334,13 +349,27 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
     if (hi - lo > max_range) max_range = hi - lo;
   }
   g->stage_elems = (int)((max_range + 1) & ~int64_t(1));
-  g->smem_bytes = (size_t)g->stage_elems * 8 * 2;
+  const size_t stage = (size_t)g->stage_elems * 8;
+  g->nstages = (int)(smem_budget / stage);
+  if (g->nstages > FS_MAX_STAGES) g->nstages = FS_MAX_STAGES;
+  if (g->nstages < 2) g->nstages = 2;
+  g->smem_bytes = stage * g->nstages;
   return MMPR_OK;
 }
 
-template <int KIND, int PPT>
+template <void (*KERN)(const FineParams)>
+static int launch_fine_t(const FineParams &p, const FineGeometry &g, cudaStream_t stream);
+
+template <int KIND, int PPT, bool HAS_TAIL>
 static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t stream) {
-  auto kern = fine_sweep_kernel<KIND, PPT>;
+  // <= 512 threads per CTA leaves 128 registers per thread for the particles
+  if (g.threads <= 512) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, 512>>(p, g, stream);
+  return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, 1024>>(p, g, stream);
+}
+
+template <void (*KERN)(const FineParams)>
+static int launch_fine_t(const FineParams &p, const FineGeometry &g, cudaStream_t stream) {
+  auto kern = KERN;
   // attributes are set once per instantiation (never during graph capture
   // of a repeated configuration)
   static int configured_smem = -1;
@@ -372,16 +401,22 @@ static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t 
   return mmpr_check(err, "fine_sweep_kernel launch");
 }
 
-template <int PPT>
+template <int PPT, bool HAS_TAIL>
 static int dispatch_kind(const FineParams &p, const FineGeometry &g, cudaStream_t s) {
   switch (p.model.kind) {
-    case MMPR_MODEL_OU: return launch_fine<MMPR_MODEL_OU, PPT>(p, g, s);
-    case MMPR_MODEL_LINEAR: return launch_fine<MMPR_MODEL_LINEAR, PPT>(p, g, s);
-    case MMPR_MODEL_DOUBLE_WELL: return launch_fine<MMPR_MODEL_DOUBLE_WELL, PPT>(p, g, s);
-    case MMPR_MODEL_CUBIC_MF: return launch_fine<MMPR_MODEL_CUBIC_MF, PPT>(p, g, s);
-    case MMPR_MODEL_DW_MULT: return launch_fine<MMPR_MODEL_DW_MULT, PPT>(p, g, s);
+    case MMPR_MODEL_OU: return launch_fine<MMPR_MODEL_OU, PPT, HAS_TAIL>(p, g, s);
+    case MMPR_MODEL_LINEAR: return launch_fine<MMPR_MODEL_LINEAR, PPT, HAS_TAIL>(p, g, s);
+    case MMPR_MODEL_DOUBLE_WELL: return launch_fine<MMPR_MODEL_DOUBLE_WELL, PPT, HAS_TAIL>(p, g, s);
+    case MMPR_MODEL_CUBIC_MF: return launch_fine<MMPR_MODEL_CUBIC_MF, PPT, HAS_TAIL>(p, g, s);
+    case MMPR_MODEL_DW_MULT: return launch_fine<MMPR_MODEL_DW_MULT, PPT, HAS_TAIL>(p, g, s);
     default: return MMPR_ERR_UNSUPPORTED;
   }
+}
+
+template <int PPT>
+static int dispatch_tail(const FineParams &p, const FineGeometry &g, cudaStream_t s) {
+  if (p.P % 8) return dispatch_kind<PPT, true>(p, g, s);
+  return dispatch_kind<PPT, false>(p, g, s);
 }
 
 }  // namespace mmpr
@@ -431,10 +466,11 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
   p.slots_per_cta = g.slots_per_cta;
   p.ctas = g.ctas;
   p.stage_elems = g.stage_elems;
+  p.nstages = g.nstages;
   cudaStream_t s = (cudaStream_t)stream;
-  if (g.ppt <= 8) return dispatch_kind<8>(p, g, s);
-  if (g.ppt <= 13) return dispatch_kind<13>(p, g, s);
-  return dispatch_kind<16>(p, g, s);
+  if (g.ppt <= 8) return dispatch_tail<8>(p, g, s);
+  if (g.ppt <= 13) return dispatch_tail<13>(p, g, s);
+  return dispatch_tail<16>(p, g, s);
 }
 
 extern "C" int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_out, int32_t *ctas_out) {
@@ -442,7 +478,7 @@ extern "C" int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_ou
   int st = fine_geometry(particles, &g);
   if (st != MMPR_OK) return st;
   if (ctas_out) *ctas_out = g.ctas;
-  auto kern = fine_sweep_kernel<MMPR_MODEL_OU, 16>;
+  auto kern = fine_sweep_kernel<MMPR_MODEL_OU, 16, false, 1024>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
   if (err != cudaSuccess) return mmpr_check(err, "occupancy: smem attribute");
   if (g.ctas > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

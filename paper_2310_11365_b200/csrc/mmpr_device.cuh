@@ -41,7 +41,8 @@ __device__ __forceinline__ double cube(double x) {
   return __dadd_rn(c, __fma_rn(pe, x, ce));
 }
 
-__device__ __forceinline__ bool finite(double x) { return isfinite(x); }
+// exponent field not all ones (integer pipe; keeps the FP64 pipe for the update)
+__device__ __forceinline__ bool finite(double x) { return (__double2hiint(x) & 0x7ff00000) != 0x7ff00000; }
 
 // ---------------------------------------------------------------------------
 // model families (MEAN_OF_F, identity f)
@@ -232,6 +233,17 @@ __device__ __forceinline__ void st_cluster_v2(uint32_t addr, unsigned long long 
 // Bulk prefetch of global memory into L2 (no shared-memory destination).
 __device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// Asynchronous 16-byte store into another CTA's shared memory that
+// completes `bytes` transaction bytes on that CTA's mbarrier (no fence, no
+// cluster barrier: the receiver waits on its own mbarrier).
+__device__ __forceinline__ void st_async_v2(uint32_t remote_addr, unsigned long long a, unsigned long long b,
+                                            uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.u64 [%0], {%1, %2}, [%3];" ::"r"(
+                   remote_addr),
+               "l"(a), "l"(b), "r"(remote_bar)
+               : "memory");
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
