@@ -250,36 +250,57 @@ struct CoarseParams {
   int skip_until;
 };
 
+// The next slice's inputs (times, fine moments, cached prediction) are
+// fetched one slice ahead through the read-only path so the serial chain
+// never waits on a global-memory round trip.
 template <int NV>
 __global__ void coarse_row_kernel(const CoarseParams p) {
   if (threadIdx.x != 0) return;
   constexpr int I = NV / 3;
+  const double *__restrict__ times = p.times;
+  const double *__restrict__ fine = p.fine;
+  const double *__restrict__ cin = p.cache_in;
+  const bool corr = p.iteration >= 1;
   double cur[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    cur[v] = p.rho0[v];
+    cur[v] = __ldg(p.rho0 + v);
     p.macro_out[v] = cur[v];
   }
+  double t0 = __ldg(times), t1 = p.n > 0 ? __ldg(times + 1) : 0.0;
+  double f[NV], c[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    f[v] = (corr && p.n > 0) ? __ldg(fine + v) : 0.0;
+    c[v] = (corr && p.n > 0) ? __ldg(cin + v) : 0.0;
+  }
   for (int n = 0; n < p.n; ++n) {
+    // prefetch slice n+1
+    const bool more = n + 1 < p.n;
+    const double t2 = more ? __ldg(times + n + 2) : 0.0;
+    double fn[NV], cn[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      fn[v] = (corr && more) ? __ldg(fine + (n + 1) * NV + v) : 0.0;
+      cn[v] = (corr && more) ? __ldg(cin + (n + 1) * NV + v) : 0.0;
+    }
     double pred[NV];
     int st = MMPR_STAT_OK;
-    if (p.iteration >= 1 && n < p.skip_until) {
+    if (corr && n < p.skip_until) {
 #pragma unroll
-      for (int v = 0; v < NV; ++v) pred[v] = p.cache_in[n * NV + v];
+      for (int v = 0; v < NV; ++v) pred[v] = c[v];
     } else {
 #pragma unroll
       for (int v = 0; v < NV; ++v) pred[v] = cur[v];
-      st = coarse_step<NV>(p.ode, p.model, p.integ, p.times[n], p.times[n + 1], pred);
+      st = coarse_step<NV>(p.ode, p.model, p.integ, t0, t1, pred);
     }
     p.status[n] = st;
 #pragma unroll
     for (int v = 0; v < NV; ++v) p.cache_out[n * NV + v] = pred[v];
-    if (p.iteration == 0) {
+    if (!corr) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) cur[v] = pred[v];
     } else {
-      const double *f = p.fine + n * NV;
-      const double *c = p.cache_in + n * NV;
       double raw[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) raw[v] = add(f[v], sub(pred[v], c[v]));
@@ -297,6 +318,13 @@ __global__ void coarse_row_kernel(const CoarseParams p) {
     }
 #pragma unroll
     for (int v = 0; v < NV; ++v) p.macro_out[(n + 1) * NV + v] = cur[v];
+    t0 = t1;
+    t1 = t2;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      f[v] = fn[v];
+      c[v] = cn[v];
+    }
   }
 }
 
