@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
       total.v = __shfl_sync(MMPR_FULL_MASK, c.v, 0);
       bad = __any_sync(MMPR_FULL_MASK, b);
     } else {
-      total.v = v.v;
+      total.v = __shfl_sync(MMPR_FULL_MASK, v.v, 0);  // lanes >= nwarps folded empty slots
     }
     mean_out = div(total.v, (double)p.P);
     bad_out = bad;

@@ -178,4 +178,4 @@ def test_occupancy_query(mm):
     import ctypes
     c, k = ctypes.c_int32(0), ctypes.c_int32(0)
     mm._lib.call("mmpr_fine_sweep_occupancy", 100_000, ctypes.byref(c), ctypes.byref(k))
-    assert k.value == 8 and c.value >= 1
+    assert k.value in (8, 16) and c.value >= 1
