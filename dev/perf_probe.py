@@ -25,8 +25,9 @@ x = torch.randn((N, P), dtype=torch.float64, device=dev)
 out = torch.empty_like(x)
 bad = torch.empty(N, dtype=torch.int32, device=dev)
 t0 = torch.zeros(N, dtype=torch.float64, device=dev)
-for spc in ('128', '64', '32'):
+for spc, ns in (('128', '2'), ('64', '2'), ('64', '3'), ('64', '4'), ('32', '4')):
     os.environ['MMPR_FINE_SLOTS_PER_CTA'] = spc
+    os.environ['MMPR_FINE_STAGES'] = ns
     c, k = ctypes.c_int32(0), ctypes.c_int32(0)
     try:
         L.call('mmpr_fine_sweep_occupancy', P, ctypes.byref(c), ctypes.byref(k))
@@ -34,8 +35,8 @@ for spc in ('128', '64', '32'):
         print('spc', spc, e); continue
     ms, all_ = timeit(lambda: kernels.fine_sweep(model, x, out, t0, S, 1e-3, xi, bad))
     byts = N*S*P*8 + 2*N*P*8
-    print(f'fine sweep spc={spc} ctas/slice={k.value} clusters={c.value}: {ms:.3f} ms {N*S*P/ms/1e9*1e3:.3e} p-steps/s {byts/ms/1e6:.0f} GB/s  {all_}')
-os.environ.pop('MMPR_FINE_SLOTS_PER_CTA')
+    print(f'fine sweep ns={ns} spc={spc} ctas/slice={k.value} clusters={c.value}: {ms:.3f} ms {N*S*P/ms/1e9*1e3:.3e} p-steps/s {byts/ms/1e6:.0f} GB/s  {all_}')
+os.environ.pop('MMPR_FINE_SLOTS_PER_CTA'); os.environ.pop('MMPR_FINE_STAGES')
 part = mm.SINGLE_REGION.descriptor()
 stats = torch.empty((N, 3), dtype=torch.float64, device=dev); counts = torch.empty((N, 1), dtype=torch.int64, device=dev)
 ms, _ = timeit(lambda: kernels.restrict(part, x, stats, counts))

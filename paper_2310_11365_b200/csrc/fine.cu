@@ -352,6 +352,10 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
   const size_t stage = (size_t)g->stage_elems * 8;
   g->nstages = (int)(smem_budget / stage);
   if (g->nstages > FS_MAX_STAGES) g->nstages = FS_MAX_STAGES;
+  if (const char *env = getenv("MMPR_FINE_STAGES")) {  // tuning override
+    const int v = atoi(env);
+    if (v >= 2 && v <= FS_MAX_STAGES && (size_t)v * stage <= smem_budget) g->nstages = v;
+  }
   if (g->nstages < 2) g->nstages = 2;
   g->smem_bytes = stage * g->nstages;
   return MMPR_OK;
