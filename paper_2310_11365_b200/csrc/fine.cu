@@ -53,6 +53,7 @@ struct FineParams {
   int ctas;           // CTAs per slice (cluster size)
   int stage_elems;    // doubles per smem stage (16-B multiple)
   int nstages;        // increment stages in shared memory (2..FS_MAX_STAGES)
+  int cnt_min;        // min elements per lane over populated slots
 };
 
 struct __align__(16) ClusterSlot {
@@ -77,12 +78,41 @@ __device__ __forceinline__ double em_update(const FineParams &p, double x, doubl
   return add(moved, noise);
 }
 
+// Partial sums of the pairwise tree.  With PADDED (an irregular tree, or
+// fewer slots than lanes) a partial carries a validity flag so an empty right
+// sibling passes its left sibling through unchanged; a perfect tree (every
+// BASELINE size) uses plain adds.
+template <bool PADDED>
+struct Part;
+
+template <>
+struct Part<true> {
+  double v;
+  int ok;
+  __device__ __forceinline__ static Part make(double v, bool ok) { return {v, ok ? 1 : 0}; }
+  __device__ __forceinline__ Part xor_level(int lane, int m) const {
+    PwVal a{v, ok};
+    PwVal r = pw_xor_level(a, lane, m);
+    return {r.v, r.ok};
+  }
+};
+
+template <>
+struct Part<false> {
+  double v;
+  __device__ __forceinline__ static Part make(double v, bool) { return {v}; }
+  __device__ __forceinline__ Part xor_level(int, int m) const {
+    return {add(v, __shfl_xor_sync(MMPR_FULL_MASK, v, m))};  // IEEE add is commutative
+  }
+};
+
 // PPT: accumulator elements per lane (ceil(max leaf / 8) <= 16); HAS_TAIL:
-// P % 8 != 0 (the last leaf adds its trailing elements one by one)
-template <int KIND, int PPT, bool HAS_TAIL, int MAXT>
+// P % 8 != 0 (the last leaf adds its trailing elements one by one).
+template <int KIND, int PPT, bool HAS_TAIL, bool PADDED, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p) {
+  using PartT = Part<PADDED>;
   extern __shared__ __align__(128) double s_stage[];  // [nstages][stage_elems]
-  __shared__ PwVal s_wp[2][32];
+  __shared__ PartT s_wp[2][32];
   __shared__ __align__(16) ClusterSlot s_slot[2][FS_MAX_CLUSTER];
   __shared__ int s_bad[3];
   __shared__ __align__(8) uint64_t s_bar[FS_MAX_STAGES];
@@ -103,6 +133,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   const int tail = (int)(len & 7);       // trailing elements added one by one
   const int64_t tail_off = off + (len & ~int64_t(7));
   const bool slot_ok = len > 0;
+  const int cmin = p.cnt_min;            // min cnt over the slice's populated slots
 
   int64_t lo, hi;
   {
@@ -113,6 +144,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   }
   const uint32_t stage_bytes = (uint32_t)((((hi - lo) * 8) + 15) & ~int64_t(15));
   const int last_idx = (int)(hi - lo) - 1;
+  const int my_idx = (int)(off - lo) + j8;  // smem index of my first element
 
   // ---- load positions --------------------------------------------------------
   double x[PPT];
@@ -147,30 +179,31 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   }
   int issued = (p.S < ns) ? p.S : ns;
 
-  // ---- reduction of sum(x) in numpy order + non-finite flag -------------------
-  // One block barrier per call (B1) plus, for clusters, one cluster barrier
-  // (B2).  Every warp reads all warp partials after B1, so s_wp is
-  // double-buffered by call parity; the blow-up flag uses three slots: slot
-  // r%3 is written before B1 of call r, read after it, and reset by thread 0
-  // after B1 of call r+1 (before it can reach B1 of r+2, after which the
-  // slot's next writers run).
-  // `refill` (>= 0): step whose increments go into the stage this step just
-  // consumed -- issued right after B1, when every thread has read it.
-  auto reduce = [&](int r, int bad_local, int refill, double &mean_out, int &bad_out) {
+  // ---- sum(x) in numpy's pairwise order + non-finite flag --------------------
+  // One block barrier per call (B1) and, in a cluster, one mbarrier wait for
+  // the peers' partials.  Every warp reads all warp partials after B1, so
+  // s_wp is double-buffered by call parity; the blow-up flag uses three
+  // slots: slot r%3 is written before B1 of call r, read after it, and reset
+  // by thread 0 after B1 of call r+1 (before it reaches B1 of r+2, after
+  // which the slot's next writers run).  `refill` (>= 0) is the step whose
+  // increments go into the stage this step just consumed.
+  auto reduce = [&](int r, int refill, double &mean_out, int &bad_out) {
     const int par = r & 1;
     const int bslot = r % 3;
     double acc = x[0];
 #pragma unroll
     for (int m = 1; m < PPT; ++m) {
-      const double t = add(acc, x[m]);
-      acc = (m < cnt) ? t : acc;
+      if (m < cmin) {
+        acc = add(acc, x[m]);
+      } else {
+        const double t = add(acc, x[m]);
+        acc = (m < cnt) ? t : acc;
+      }
     }
-    // all 8 lanes of a slot hold cnt elements; shuffles stay warp-uniform
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 1));
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 2));
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 4));
-    // a leaf shorter than 8 (P < 8) is summed sequentially from 0.0
-    if (cnt == 0) acc = 0.0;
+    if (cnt == 0) acc = 0.0;  // a leaf shorter than 8 (P < 8) is summed from 0.0
     if (HAS_TAIL) {
 #pragma unroll
       for (int i = 0; i < 7; ++i) {
@@ -178,19 +211,25 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
         if (i < tail) acc = add(acc, v);
       }
     }
-    PwVal leaf;
-    leaf.v = acc;
-    leaf.ok = slot_ok ? 1 : 0;
+    // a finite leaf sum proves every element finite (inf/NaN propagate);
+    // only a non-finite sum needs the exact per-element test
+    int bad_local = 0;
+    if (!finite(acc)) {
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) bad_local |= (m < cnt && !finite(x[m])) ? 1 : 0;
+      if (HAS_TAIL && j8 < tail) bad_local |= !finite(xt);
+    }
     const int wbad = __any_sync(MMPR_FULL_MASK, bad_local);
-    leaf = pw_xor_level(leaf, lane, 8);
-    leaf = pw_xor_level(leaf, lane, 16);
+    PartT leaf = PartT::make(acc, slot_ok);
+    leaf = leaf.xor_level(lane, 8);
+    leaf = leaf.xor_level(lane, 16);
     if (lane == 0) {
       s_wp[par][warp] = leaf;
       if (wbad) s_bad[bslot] = 1;
     }
     __syncthreads();  // B1 (the only block barrier of a step)
     if (tid == 0) {
-      s_bad[(r + 2) % 3] = 0;  // slot of call r-1: all its readers passed this B1, its next writers follow B1 of r+1
+      s_bad[(r + 2) % 3] = 0;
       if (refill >= 0) {
         const int st = refill % ns;
         mbar_arrive_expect_tx(&s_bar[st], stage_bytes);
@@ -202,13 +241,11 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
       }
     }
     // every warp folds the CTA's warp partials with the same xor tree
-    PwVal v;
-    if (lane < nwarps) v = s_wp[par][lane];
-    else { v.v = 0.0; v.ok = 0; }
+    PartT v = (lane < nwarps) ? s_wp[par][lane] : PartT::make(0.0, false);
 #pragma unroll
     for (int m = 1; m < 32; m <<= 1)
-      if (m < nwarps) v = pw_xor_level(v, lane, m);
-    PwVal total;
+      if (m < nwarps) v = v.xor_level(lane, m);
+    double total;
     int bad = s_bad[bslot];
     if (p.ctas > 1) {
       // Each CTA's partial goes to every CTA of the cluster as one 16-byte
@@ -218,59 +255,53 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
       if (warp == 0 && lane < p.ctas) {
         const uint32_t remote = mapa_shared(smem_addr(&s_slot[par][rank]), (uint32_t)lane);
         const uint32_t rbar = mapa_shared(smem_addr(&s_red_bar[par]), (uint32_t)lane);
+        int okv = 1;
+        if constexpr (PADDED) okv = v.ok;
         st_async_v2(remote, __double_as_longlong(v.v),
-                    (unsigned long long)(uint32_t)v.ok | ((unsigned long long)(uint32_t)bad << 32), rbar);
+                    (unsigned long long)(uint32_t)okv | ((unsigned long long)(uint32_t)bad << 32), rbar);
       }
       mbar_wait_parity(&s_red_bar[par], (uint32_t)((r >> 1) & 1));
-      PwVal c;
-      c.v = 0.0;
-      c.ok = 0;
+      PartT c = PartT::make(0.0, false);
       int b = 0;
       if (lane < p.ctas) {
-        c.v = s_slot[par][lane].v;
-        c.ok = s_slot[par][lane].ok;
+        c = PartT::make(s_slot[par][lane].v, s_slot[par][lane].ok != 0);
         b = s_slot[par][lane].bad;
       }
 #pragma unroll
       for (int m = 1; m < FS_MAX_CLUSTER; m <<= 1)
-        if (m < p.ctas) c = pw_xor_level(c, lane, m);
-      total.v = __shfl_sync(MMPR_FULL_MASK, c.v, 0);
+        if (m < p.ctas) c = c.xor_level(lane, m);
+      total = __shfl_sync(MMPR_FULL_MASK, c.v, 0);
       bad = __any_sync(MMPR_FULL_MASK, b);
     } else {
-      total.v = __shfl_sync(MMPR_FULL_MASK, v.v, 0);  // lanes >= nwarps folded empty slots
+      total = __shfl_sync(MMPR_FULL_MASK, v.v, 0);  // lanes >= nwarps folded empty slots
     }
-    mean_out = div(total.v, (double)p.P);
+    mean_out = div(total, (double)p.P);
     bad_out = bad;
   };
 
   double s;
   int bad;
-  reduce(0, 0, -1, s, bad);
+  reduce(0, -1, s, bad);
 
   int first_bad = MMPR_STAT_OK;
-  const double t_start = p.t0[slice];
-  (void)t_start;
   for (int j = 0; j < p.S; ++j) {
     const int stage = j % ns;
     mbar_wait_parity(&s_bar[stage], (uint32_t)((j / ns) & 1));
-    const double *xs = s_stage + stage * p.stage_elems;
-    int bad_local = 0;
+    const double *xb = s_stage + stage * p.stage_elems;
 #pragma unroll
     for (int m = 0; m < PPT; ++m) {
-      // branch-free: lanes past their leaf compute on a clamped index and
-      // keep their (unused) value
-      const int idx = max(0, min((int)(off - lo) + j8 + 8 * m, last_idx));
-      const double nx = em_update<KIND>(p, x[m], s, xs[idx]);
-      const bool live = m < cnt;
-      x[m] = live ? nx : x[m];
-      bad_local |= (live && !finite(nx)) ? 1 : 0;
+      if (m < cmin) {
+        x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
+      } else {
+        // past some lanes' leaves: clamped index, value kept only when live
+        const int idx = max(0, min(my_idx + 8 * m, last_idx));
+        const double nx = em_update<KIND>(p, x[m], s, xb[idx]);
+        x[m] = (m < cnt) ? nx : x[m];
+      }
     }
-    if (HAS_TAIL && j8 < tail) {
-      xt = em_update<KIND>(p, xt, s, xs[tail_off - lo + j8]);
-      bad_local |= !finite(xt);
-    }
+    if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
     // B1 inside reduce() orders every read of this stage before its refill
-    reduce(j + 1, bad_local, (j + ns < p.S) ? j + ns : -1, s, bad);
+    reduce(j + 1, (j + ns < p.S) ? j + ns : -1, s, bad);
     if (bad) {
       first_bad = j;
       break;
@@ -297,7 +328,9 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
 // host-side geometry
 // ---------------------------------------------------------------------------
 struct FineGeometry {
-  int ppt;  // ceil(max leaf / 8)
+  int ppt;      // ceil(max leaf / 8)
+  int cnt_min;  // min leaf / 8 over populated slots
+  bool padded;  // some slot of a CTA is empty
   int D;
   int slots_per_cta;
   int ctas;
@@ -311,12 +344,16 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
   if (P < 1) return MMPR_ERR_ARG;
   g->D = pw_depth(P);
   const int64_t nslots = int64_t(1) << g->D;
-  int64_t max_leaf = 0;
+  int64_t max_leaf = 0, min_leaf = INT64_MAX;
+  bool empty = false;
   for (int64_t s = 0; s < nslots; ++s) {
     int64_t o, l;
     pw_leaf(P, g->D, s, &o, &l);
     if (l > max_leaf) max_leaf = l;
+    if (l > 0 && l < min_leaf) min_leaf = l;
+    empty |= l == 0;
   }
+  g->cnt_min = (int)(min_leaf >> 3);
   g->ppt = (int)((max_leaf + 7) / 8);
   // two increment stages of the CTA's particle range must fit next to the
   // ~1.5 KB of static shared memory (227 KB opt-in per CTA)
@@ -339,6 +376,7 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
   }
   if (g->ctas > FS_MAX_CLUSTER) return MMPR_ERR_UNSUPPORTED;
   g->threads = g->slots_per_cta * 8;
+  g->padded = empty || nslots < g->slots_per_cta;
   // largest per-CTA particle range
   int64_t max_range = 0;
   for (int c = 0; c < g->ctas; ++c) {
@@ -367,8 +405,12 @@ static int launch_fine_t(const FineParams &p, const FineGeometry &g, cudaStream_
 template <int KIND, int PPT, bool HAS_TAIL>
 static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t stream) {
   // <= 512 threads per CTA leaves 128 registers per thread for the particles
-  if (g.threads <= 512) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, 512>>(p, g, stream);
-  return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, 1024>>(p, g, stream);
+  if (g.padded) {
+    if (g.threads <= 512) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 512>>(p, g, stream);
+    return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 1024>>(p, g, stream);
+  }
+  if (g.threads <= 512) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 512>>(p, g, stream);
+  return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 1024>>(p, g, stream);
 }
 
 template <void (*KERN)(const FineParams)>
@@ -471,6 +513,7 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
   p.ctas = g.ctas;
   p.stage_elems = g.stage_elems;
   p.nstages = g.nstages;
+  p.cnt_min = g.cnt_min;
   cudaStream_t s = (cudaStream_t)stream;
   if (g.ppt <= 8) return dispatch_tail<8>(p, g, s);
   if (g.ppt <= 13) return dispatch_tail<13>(p, g, s);
@@ -482,7 +525,7 @@ extern "C" int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_ou
   int st = fine_geometry(particles, &g);
   if (st != MMPR_OK) return st;
   if (ctas_out) *ctas_out = g.ctas;
-  auto kern = fine_sweep_kernel<MMPR_MODEL_OU, 16, false, 1024>;
+  auto kern = fine_sweep_kernel<MMPR_MODEL_OU, 16, false, false, 1024>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
   if (err != cudaSuccess) return mmpr_check(err, "occupancy: smem attribute");
   if (g.ctas > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
