@@ -31,7 +31,6 @@ namespace mmpr {
 
 #define FS_MAX_CLUSTER 16
 #define FS_MAX_STAGES 4
-#define FS_L2_AHEAD 3  // steps of increments kept in flight towards L2 beyond the smem stages
 
 struct FineParams {
   mmpr_model model;
@@ -54,6 +53,7 @@ struct FineParams {
   int stage_elems;    // doubles per smem stage (16-B multiple)
   int nstages;        // increment stages in shared memory (2..FS_MAX_STAGES)
   int cnt_min;        // min elements per lane over populated slots
+  int l2_ahead;       // steps of increments prefetched into L2 beyond the smem stages
 };
 
 struct __align__(16) ClusterSlot {
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
       mbar_arrive_expect_tx(&s_bar[j], stage_bytes);
       bulk_g2s(s_stage + j * p.stage_elems, xi_slice + j * p.xi_row_pitch + lo, stage_bytes, &s_bar[j]);
     }
-    for (int j = ns; j < ns + FS_L2_AHEAD && j < p.S; ++j)
+    for (int j = ns; j < ns + p.l2_ahead && j < p.S; ++j)
       prefetch_l2(xi_slice + (int64_t)j * p.xi_row_pitch + lo, stage_bytes);
   }
   int issued = (p.S < ns) ? p.S : ns;
@@ -236,8 +236,8 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
         bulk_g2s(s_stage + st * p.stage_elems, xi_slice + (int64_t)refill * p.xi_row_pitch + lo, stage_bytes,
                  &s_bar[st]);
         ++issued;
-        const int pf = refill + FS_L2_AHEAD;  // pull a later step towards L2
-        if (pf < p.S) prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
+        const int pf = refill + p.l2_ahead;  // pull a later step towards L2
+        if (p.l2_ahead > 0 && pf < p.S) prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
       }
     }
     // every warp folds the CTA's warp partials with the same xor tree
@@ -358,10 +358,9 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
   // two increment stages of the CTA's particle range must fit next to the
   // ~1.5 KB of static shared memory (227 KB opt-in per CTA)
   const size_t smem_budget = 224 * 1024;
-  // 64 slots (512 threads) per CTA measured faster than 128 on B200
-  // (smaller stages, more CTAs in flight); clusters stay <= 16 CTAs
-  int spc = 64;
-  if ((int64_t(1) << g->D) / spc > FS_MAX_CLUSTER) spc = 128;
+  // 128 slots (1024 threads, one CTA per SM) measured fastest on B200 for
+  // P = 1e5; smaller CTAs when two stages would not fit
+  int spc = 128;
   if (const char *env = getenv("MMPR_FINE_SLOTS_PER_CTA")) {  // tuning override
     const int v = atoi(env);
     if (v >= 4 && v <= 128 && (v & (v - 1)) == 0) spc = v;
@@ -514,6 +513,8 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
   p.stage_elems = g.stage_elems;
   p.nstages = g.nstages;
   p.cnt_min = g.cnt_min;
+  p.l2_ahead = 3;
+  if (const char *env = getenv("MMPR_FINE_L2_AHEAD")) p.l2_ahead = max(0, min(16, atoi(env)));
   cudaStream_t s = (cudaStream_t)stream;
   if (g.ppt <= 8) return dispatch_tail<8>(p, g, s);
   if (g.ppt <= 13) return dispatch_tail<13>(p, g, s);
