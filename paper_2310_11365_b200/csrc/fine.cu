@@ -56,6 +56,16 @@ struct FineParams {
   int l2_ahead;       // steps of increments prefetched into L2 beyond the smem stages
 };
 
+#ifdef MMPR_FINE_PROFILE
+// dev builds only: per-CTA cycle totals of the step phases
+__device__ long long g_fine_prof[4096][6];
+#define PROF_MARK(var) long long var = clock64()
+#define PROF_ADD(k, a, b) if (tid == 0) atomicAdd((unsigned long long *)&g_fine_prof[blockIdx.x & 4095][k], (unsigned long long)((b) - (a)))
+#else
+#define PROF_MARK(var)
+#define PROF_ADD(k, a, b)
+#endif
+
 struct __align__(16) ClusterSlot {
   double v;
   int ok;
@@ -227,7 +237,10 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
       s_wp[par][warp] = leaf;
       if (wbad) s_bad[bslot] = 1;
     }
+    PROF_MARK(tb0);
     __syncthreads();  // B1 (the only block barrier of a step)
+    PROF_MARK(tb1);
+    PROF_ADD(2, tb0, tb1);
     if (tid == 0) {
       s_bad[(r + 2) % 3] = 0;
       if (refill >= 0) {
@@ -260,7 +273,10 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
         st_async_v2(remote, __double_as_longlong(v.v),
                     (unsigned long long)(uint32_t)okv | ((unsigned long long)(uint32_t)bad << 32), rbar);
       }
+      PROF_MARK(tc0);
       mbar_wait_parity(&s_red_bar[par], (uint32_t)((r >> 1) & 1));
+      PROF_MARK(tc1);
+      PROF_ADD(3, tc0, tc1);
       PartT c = PartT::make(0.0, false);
       int b = 0;
       if (lane < p.ctas) {
@@ -286,7 +302,10 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   int first_bad = MMPR_STAT_OK;
   for (int j = 0; j < p.S; ++j) {
     const int stage = j % ns;
+    PROF_MARK(tw0);
     mbar_wait_parity(&s_bar[stage], (uint32_t)((j / ns) & 1));
+    PROF_MARK(tw1);
+    PROF_ADD(0, tw0, tw1);
     const double *xb = s_stage + stage * p.stage_elems;
 #pragma unroll
     for (int m = 0; m < PPT; ++m) {
@@ -300,8 +319,12 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
       }
     }
     if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
+    PROF_MARK(tu1);
+    PROF_ADD(1, tw1, tu1);
     // B1 inside reduce() orders every read of this stage before its refill
     reduce(j + 1, (j + ns < p.S) ? j + ns : -1, s, bad);
+    PROF_MARK(tr1);
+    PROF_ADD(4, tu1, tr1);
     if (bad) {
       first_bad = j;
       break;
@@ -547,3 +570,16 @@ extern "C" int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_ou
   if (clusters_out) *clusters_out = n;
   return MMPR_OK;
 }
+
+#ifdef MMPR_FINE_PROFILE
+// dev builds only: copy out (and reset) the per-CTA phase cycle totals
+extern "C" int mmpr_dev_fine_prof(long long *host_out, int reset) {
+  cudaDeviceSynchronize();
+  if (host_out) cudaMemcpyFromSymbol(host_out, g_fine_prof, sizeof(g_fine_prof));
+  if (reset) {
+    static long long zeros[4096][6];
+    cudaMemcpyToSymbol(g_fine_prof, zeros, sizeof(zeros));
+  }
+  return (int)cudaGetLastError();
+}
+#endif
