@@ -58,7 +58,7 @@ struct FineParams {
 
 #ifdef MMPR_FINE_PROFILE
 // dev builds only: per-CTA cycle totals of the step phases
-__device__ long long g_fine_prof[4096][6];
+__device__ long long g_fine_prof[4096][10];
 #define PROF_MARK(var) long long var = clock64()
 #define PROF_ADD(k, a, b) if (tid == 0) atomicAdd((unsigned long long *)&g_fine_prof[blockIdx.x & 4095][k], (unsigned long long)((b) - (a)))
 #else
@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   // which the slot's next writers run).  `refill` (>= 0) is the step whose
   // increments go into the stage this step just consumed.
   auto reduce = [&](int r, int refill, double &mean_out, int &bad_out) {
+    PROF_MARK(tr0);
     const int par = r & 1;
     const int bslot = r % 3;
     double acc = x[0];
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
       if (wbad) s_bad[bslot] = 1;
     }
     PROF_MARK(tb0);
+    PROF_ADD(5, tr0, tb0);
     __syncthreads();  // B1 (the only block barrier of a step)
     PROF_MARK(tb1);
     PROF_ADD(2, tb0, tb1);
@@ -253,6 +255,8 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
         if (p.l2_ahead > 0 && pf < p.S) prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
       }
     }
+    PROF_MARK(tf0);
+    PROF_ADD(6, tb1, tf0);
     // every warp folds the CTA's warp partials with the same xor tree
     PartT v = (lane < nwarps) ? s_wp[par][lane] : PartT::make(0.0, false);
 #pragma unroll
@@ -274,6 +278,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
                     (unsigned long long)(uint32_t)okv | ((unsigned long long)(uint32_t)bad << 32), rbar);
       }
       PROF_MARK(tc0);
+      PROF_ADD(7, tf0, tc0);
       mbar_wait_parity(&s_red_bar[par], (uint32_t)((r >> 1) & 1));
       PROF_MARK(tc1);
       PROF_ADD(3, tc0, tc1);
@@ -293,6 +298,8 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
     }
     mean_out = div(total, (double)p.P);
     bad_out = bad;
+    PROF_MARK(tr9);
+    PROF_ADD(8, tr0, tr9);
   };
 
   double s;
@@ -577,7 +584,7 @@ extern "C" int mmpr_dev_fine_prof(long long *host_out, int reset) {
   cudaDeviceSynchronize();
   if (host_out) cudaMemcpyFromSymbol(host_out, g_fine_prof, sizeof(g_fine_prof));
   if (reset) {
-    static long long zeros[4096][6];
+    static long long zeros[4096][10];
     cudaMemcpyToSymbol(g_fine_prof, zeros, sizeof(zeros));
   }
   return (int)cudaGetLastError();
