@@ -116,23 +116,51 @@ struct Part<false> {
   }
 };
 
+// Block-level barrier of one slice group: __syncthreads for one group per
+// CTA, a named barrier (id 1 + group) when two groups share the CTA.
+template <int GROUPS>
+__device__ __forceinline__ void group_sync(int grp, int nthreads) {
+  if (GROUPS == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(nthreads) : "memory");
+  }
+}
+
 // PPT: accumulator elements per lane (ceil(max leaf / 8) <= 16); HAS_TAIL:
 // P % 8 != 0 (the last leaf adds its trailing elements one by one).
-template <int KIND, int PPT, bool HAS_TAIL, bool PADDED, int MAXT>
+// GROUPS: slices per cluster.  With two groups each CTA holds particles of
+// two different slices (one per half of its threads) that step
+// independently, so one slice's FP64 update overlaps the other's reduction
+// and exchange latency on the same SM.
+template <int KIND, int PPT, bool HAS_TAIL, bool PADDED, int MAXT, int GROUPS>
 __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p) {
   using PartT = Part<PADDED>;
-  extern __shared__ __align__(128) double s_stage[];  // [nstages][stage_elems]
-  __shared__ PartT s_wp[2][32];
-  __shared__ __align__(16) ClusterSlot s_slot[2][FS_MAX_CLUSTER];
-  __shared__ int s_bad[3];
-  __shared__ __align__(8) uint64_t s_bar[FS_MAX_STAGES];
-  __shared__ __align__(8) uint64_t s_red_bar[2];  // cluster partials of call parity 0/1
+  extern __shared__ __align__(128) double s_dyn[];  // [GROUPS][nstages][stage_elems]
+  __shared__ PartT s_wp_all[GROUPS][2][32];
+  __shared__ __align__(16) ClusterSlot s_slot_all[GROUPS][2][FS_MAX_CLUSTER];
+  __shared__ int s_bad_all[GROUPS][3];
+  __shared__ __align__(8) uint64_t s_bar_all[GROUPS][FS_MAX_STAGES];
+  __shared__ __align__(8) uint64_t s_red_bar_all[GROUPS][2];  // cluster partials of call parity 0/1
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int gthreads = blockDim.x / GROUPS;
+  const int grp = (int)threadIdx.x / gthreads;
+  const int tid = (int)threadIdx.x - grp * gthreads;  // thread index within the group
+  const int warp = tid >> 5;
+  const int nwarps = gthreads >> 5;
   const int rank = (p.ctas > 1) ? (int)cluster_ctarank() : 0;
-  const int slice = blockIdx.x / p.ctas;
+  const int slice = (blockIdx.x / p.ctas) * GROUPS + grp;
+  const bool active = slice < p.n_slices;  // an odd slice count leaves one group idle
   const int64_t nslots = int64_t(1) << p.D;
+
+  const int ns = p.nstages;
+  double *s_stage = s_dyn + (size_t)grp * ns * p.stage_elems;
+  PartT(*s_wp)[32] = s_wp_all[grp];
+  ClusterSlot(*s_slot)[FS_MAX_CLUSTER] = s_slot_all[grp];
+  int *s_bad = s_bad_all[grp];
+  uint64_t *s_bar = s_bar_all[grp];
+  uint64_t *s_red_bar = s_red_bar_all[grp];
 
   // ---- my leaf --------------------------------------------------------------
   const int64_t slot = (int64_t)rank * p.slots_per_cta + warp * 4 + (lane >> 3);
@@ -161,12 +189,11 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   double xt = 0.0;
   const double *xin = p.x_in + (int64_t)slice * p.in_pitch;
 #pragma unroll
-  for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? xin[off + j8 + 8 * m] : 0.0;
-  if (HAS_TAIL && j8 < tail) xt = xin[tail_off + j8];
+  for (int m = 0; m < PPT; ++m) x[m] = (active && m < cnt) ? xin[off + j8 + 8 * m] : 0.0;
+  if (HAS_TAIL && active && j8 < tail) xt = xin[tail_off + j8];
 
   // ---- increment pipeline -------------------------------------------------------
   const double *xi_slice = p.xi + (int64_t)slice * p.xi_slice_pitch;
-  const int ns = p.nstages;
   if (tid == 0) {
     for (int q = 0; q < ns; ++q) mbar_init(&s_bar[q], 1);
     mbar_init(&s_red_bar[0], 1);
@@ -179,7 +206,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   // every CTA's barriers must be initialised before any peer sends to them
   if (p.ctas > 1) cluster_sync_all();
   else __syncthreads();
-  if (tid == 0) {
+  if (tid == 0 && active) {
     for (int j = 0; j < ns && j < p.S; ++j) {
       mbar_arrive_expect_tx(&s_bar[j], stage_bytes);
       bulk_g2s(s_stage + j * p.stage_elems, xi_slice + j * p.xi_row_pitch + lo, stage_bytes, &s_bar[j]);
@@ -190,7 +217,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   int issued = (p.S < ns) ? p.S : ns;
 
   // ---- sum(x) in numpy's pairwise order + non-finite flag --------------------
-  // One block barrier per call (B1) and, in a cluster, one mbarrier wait for
+  // One group barrier per call (B1) and, in a cluster, one mbarrier wait for
   // the peers' partials.  Every warp reads all warp partials after B1, so
   // s_wp is double-buffered by call parity; the blow-up flag uses three
   // slots: slot r%3 is written before B1 of call r, read after it, and reset
@@ -198,7 +225,6 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   // which the slot's next writers run).  `refill` (>= 0) is the step whose
   // increments go into the stage this step just consumed.
   auto reduce = [&](int r, int refill, double &mean_out, int &bad_out) {
-    PROF_MARK(tr0);
     const int par = r & 1;
     const int bslot = r % 3;
     double acc = x[0];
@@ -238,11 +264,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
       s_wp[par][warp] = leaf;
       if (wbad) s_bad[bslot] = 1;
     }
-    PROF_MARK(tb0);
-    PROF_ADD(5, tr0, tb0);
-    __syncthreads();  // B1 (the only block barrier of a step)
-    PROF_MARK(tb1);
-    PROF_ADD(2, tb0, tb1);
+    group_sync<GROUPS>(grp, gthreads);  // B1 (the only block-level barrier of a step)
     if (tid == 0) {
       s_bad[(r + 2) % 3] = 0;
       if (refill >= 0) {
@@ -255,9 +277,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
         if (p.l2_ahead > 0 && pf < p.S) prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
       }
     }
-    PROF_MARK(tf0);
-    PROF_ADD(6, tb1, tf0);
-    // every warp folds the CTA's warp partials with the same xor tree
+    // every warp folds the group's warp partials with the same xor tree
     PartT v = (lane < nwarps) ? s_wp[par][lane] : PartT::make(0.0, false);
 #pragma unroll
     for (int m = 1; m < 32; m <<= 1)
@@ -265,9 +285,9 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
     double total;
     int bad = s_bad[bslot];
     if (p.ctas > 1) {
-      // Each CTA's partial goes to every CTA of the cluster as one 16-byte
-      // st.async that completes tx bytes on the receiver's mbarrier; a CTA
-      // waits only for its own barrier (no cluster-wide barrier per step).
+      // Each CTA's partial goes to the same group of every CTA of the cluster
+      // as one 16-byte st.async that completes tx bytes on the receiver's
+      // mbarrier; a group waits only for its own barrier.
       if (tid == 0) mbar_arrive_expect_tx(&s_red_bar[par], 16u * (uint32_t)p.ctas);
       if (warp == 0 && lane < p.ctas) {
         const uint32_t remote = mapa_shared(smem_addr(&s_slot[par][rank]), (uint32_t)lane);
@@ -277,11 +297,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
         st_async_v2(remote, __double_as_longlong(v.v),
                     (unsigned long long)(uint32_t)okv | ((unsigned long long)(uint32_t)bad << 32), rbar);
       }
-      PROF_MARK(tc0);
-      PROF_ADD(7, tf0, tc0);
       mbar_wait_parity(&s_red_bar[par], (uint32_t)((r >> 1) & 1));
-      PROF_MARK(tc1);
-      PROF_ADD(3, tc0, tc1);
       PartT c = PartT::make(0.0, false);
       int b = 0;
       if (lane < p.ctas) {
@@ -298,51 +314,44 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
     }
     mean_out = div(total, (double)p.P);
     bad_out = bad;
-    PROF_MARK(tr9);
-    PROF_ADD(8, tr0, tr9);
   };
 
-  double s;
-  int bad;
-  reduce(0, -1, s, bad);
-
+  double s = 0.0;
+  int bad = 0;
   int first_bad = MMPR_STAT_OK;
-  for (int j = 0; j < p.S; ++j) {
-    const int stage = j % ns;
-    PROF_MARK(tw0);
-    mbar_wait_parity(&s_bar[stage], (uint32_t)((j / ns) & 1));
-    PROF_MARK(tw1);
-    PROF_ADD(0, tw0, tw1);
-    const double *xb = s_stage + stage * p.stage_elems;
+  if (active) {
+    reduce(0, -1, s, bad);
+    for (int j = 0; j < p.S; ++j) {
+      const int stage = j % ns;
+      mbar_wait_parity(&s_bar[stage], (uint32_t)((j / ns) & 1));
+      const double *xb = s_stage + stage * p.stage_elems;
 #pragma unroll
-    for (int m = 0; m < PPT; ++m) {
-      if (m < cmin) {
-        x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
-      } else {
-        // past some lanes' leaves: clamped index, value kept only when live
-        const int idx = max(0, min(my_idx + 8 * m, last_idx));
-        const double nx = em_update<KIND>(p, x[m], s, xb[idx]);
-        x[m] = (m < cnt) ? nx : x[m];
+      for (int m = 0; m < PPT; ++m) {
+        if (m < cmin) {
+          x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
+        } else {
+          // past some lanes' leaves: clamped index, value kept only when live
+          const int idx = max(0, min(my_idx + 8 * m, last_idx));
+          const double nx = em_update<KIND>(p, x[m], s, xb[idx]);
+          x[m] = (m < cnt) ? nx : x[m];
+        }
+      }
+      if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
+      // B1 inside reduce() orders every read of this stage before its refill
+      reduce(j + 1, (j + ns < p.S) ? j + ns : -1, s, bad);
+      if (bad) {
+        first_bad = j;
+        break;
       }
     }
-    if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
-    PROF_MARK(tu1);
-    PROF_ADD(1, tw1, tu1);
-    // B1 inside reduce() orders every read of this stage before its refill
-    reduce(j + 1, (j + ns < p.S) ? j + ns : -1, s, bad);
-    PROF_MARK(tr1);
-    PROF_ADD(4, tu1, tr1);
-    if (bad) {
-      first_bad = j;
-      break;
+    // Drain copies still in flight after an early exit.
+    if (tid == 0 && first_bad != MMPR_STAT_OK) {
+      for (int j = first_bad + 1; j < issued; ++j) mbar_wait_parity(&s_bar[j % ns], (uint32_t)((j / ns) & 1));
     }
-  }
-  // Drain copies still in flight after an early exit.
-  if (tid == 0 && first_bad != MMPR_STAT_OK) {
-    for (int j = first_bad + 1; j < issued; ++j) mbar_wait_parity(&s_bar[j % ns], (uint32_t)((j / ns) & 1));
   }
 
   if (p.ctas > 1) cluster_sync_all();  // no peer may still be writing into this CTA
+  if (!active) return;
   double *xo = p.x_out + (int64_t)slice * p.out_pitch;
 #pragma unroll
   for (int m = 0; m < PPT; ++m)
@@ -361,8 +370,9 @@ struct FineGeometry {
   int ppt;      // ceil(max leaf / 8)
   int cnt_min;  // min leaf / 8 over populated slots
   bool padded;  // some slot of a CTA is empty
+  int groups;   // slices per cluster (two halves of every CTA when 2)
   int D;
-  int slots_per_cta;
+  int slots_per_cta;  // per group
   int ctas;
   int threads;
   int stage_elems;
@@ -385,17 +395,24 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
   }
   g->cnt_min = (int)(min_leaf >> 3);
   g->ppt = (int)((max_leaf + 7) / 8);
-  // two increment stages of the CTA's particle range must fit next to the
-  // ~1.5 KB of static shared memory (227 KB opt-in per CTA)
+  // increment stages of the CTA's particle range(s) must fit next to the
+  // ~2 KB of static shared memory (227 KB opt-in per CTA)
   const size_t smem_budget = 224 * 1024;
-  // 128 slots (1024 threads, one CTA per SM) measured fastest on B200 for
-  // P = 1e5; smaller CTAs when two stages would not fit
-  int spc = 128;
-  if (const char *env = getenv("MMPR_FINE_SLOTS_PER_CTA")) {  // tuning override
+  // Default: two slice groups per CTA (2 x 64 slots = 1024 threads) so one
+  // slice's update overlaps the other's reduction on every SM; otherwise
+  // one group of 128 slots.
+  g->groups = (nslots >= 128 && nslots / 64 <= FS_MAX_CLUSTER &&
+               (size_t)64 * max_leaf * 8 * 2 * 2 <= smem_budget) ? 2 : 1;
+  if (const char *env = getenv("MMPR_FINE_GROUPS")) {  // tuning override
     const int v = atoi(env);
-    if (v >= 4 && v <= 128 && (v & (v - 1)) == 0) spc = v;
+    if (v == 1 || (v == 2 && nslots >= 128 && nslots / 64 <= FS_MAX_CLUSTER)) g->groups = v;
   }
-  while (spc > 4 && (size_t)spc * max_leaf * 8 * 2 > smem_budget) spc >>= 1;
+  int spc = g->groups == 2 ? 64 : 128;
+  if (const char *env = getenv("MMPR_FINE_SLOTS_PER_CTA")) {  // tuning override (one group)
+    const int v = atoi(env);
+    if (g->groups == 1 && v >= 4 && v <= 128 && (v & (v - 1)) == 0) spc = v;
+  }
+  while (spc > 4 && (size_t)spc * max_leaf * 8 * 2 * g->groups > smem_budget) spc >>= 1;
   if (nslots <= spc) {
     g->slots_per_cta = (int)(nslots < 4 ? 4 : nslots);
     g->ctas = 1;
@@ -404,7 +421,7 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
     g->ctas = (int)(nslots / spc);
   }
   if (g->ctas > FS_MAX_CLUSTER) return MMPR_ERR_UNSUPPORTED;
-  g->threads = g->slots_per_cta * 8;
+  g->threads = g->slots_per_cta * 8 * g->groups;
   g->padded = empty || nslots < g->slots_per_cta;
   // largest per-CTA particle range
   int64_t max_range = 0;
@@ -417,14 +434,14 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
   }
   g->stage_elems = (int)((max_range + 1) & ~int64_t(1));
   const size_t stage = (size_t)g->stage_elems * 8;
-  g->nstages = (int)(smem_budget / stage);
+  g->nstages = (int)(smem_budget / (stage * g->groups));
   if (g->nstages > FS_MAX_STAGES) g->nstages = FS_MAX_STAGES;
   if (const char *env = getenv("MMPR_FINE_STAGES")) {  // tuning override
     const int v = atoi(env);
-    if (v >= 2 && v <= FS_MAX_STAGES && (size_t)v * stage <= smem_budget) g->nstages = v;
+    if (v >= 2 && v <= FS_MAX_STAGES && (size_t)v * stage * g->groups <= smem_budget) g->nstages = v;
   }
   if (g->nstages < 2) g->nstages = 2;
-  g->smem_bytes = stage * g->nstages;
+  g->smem_bytes = stage * g->nstages * g->groups;
   return MMPR_OK;
 }
 
@@ -433,13 +450,17 @@ static int launch_fine_t(const FineParams &p, const FineGeometry &g, cudaStream_
 
 template <int KIND, int PPT, bool HAS_TAIL>
 static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t stream) {
+  if (g.groups == 2) {
+    if (g.padded) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 1024, 2>>(p, g, stream);
+    return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 1024, 2>>(p, g, stream);
+  }
   // <= 512 threads per CTA leaves 128 registers per thread for the particles
   if (g.padded) {
-    if (g.threads <= 512) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 512>>(p, g, stream);
-    return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 1024>>(p, g, stream);
+    if (g.threads <= 512) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 512, 1>>(p, g, stream);
+    return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 1024, 1>>(p, g, stream);
   }
-  if (g.threads <= 512) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 512>>(p, g, stream);
-  return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 1024>>(p, g, stream);
+  if (g.threads <= 512) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 512, 1>>(p, g, stream);
+  return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 1024, 1>>(p, g, stream);
 }
 
 template <void (*KERN)(const FineParams)>
@@ -461,7 +482,7 @@ static int launch_fine_t(const FineParams &p, const FineGeometry &g, cudaStream_
     configured_nonportable = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(p.n_slices * g.ctas), 1, 1);
+  cfg.gridDim = dim3((unsigned)(((p.n_slices + g.groups - 1) / g.groups) * g.ctas), 1, 1);
   cfg.blockDim = dim3((unsigned)g.threads, 1, 1);
   cfg.dynamicSmemBytes = g.smem_bytes;
   cfg.stream = stream;
@@ -556,7 +577,8 @@ extern "C" int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_ou
   int st = fine_geometry(particles, &g);
   if (st != MMPR_OK) return st;
   if (ctas_out) *ctas_out = g.ctas;
-  auto kern = fine_sweep_kernel<MMPR_MODEL_OU, 16, false, false, 1024>;
+  // note: reports the one-group, 1024-thread variant's cluster occupancy
+  auto kern = fine_sweep_kernel<MMPR_MODEL_OU, 16, false, false, 1024, 1>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
   if (err != cudaSuccess) return mmpr_check(err, "occupancy: smem attribute");
   if (g.ctas > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
