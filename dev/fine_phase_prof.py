@@ -17,15 +17,15 @@ out = torch.empty_like(x)
 bad = torch.empty(N, dtype=torch.int32, device='cuda')
 t0 = torch.zeros(N, dtype=torch.float64, device='cuda')
 buf = np.zeros((4096, 10), dtype=np.int64)
-names = ['wait_stage', 'update', 'B1', 'cluster_wait', 'reduce_call', 'leaf+warp', 'refill(tid0)', 'fold+send', 'reduce_inner']
-for l2, spc in (('3', '128'), ('0', '128'), ('3', '64')):
-    os.environ['MMPR_FINE_L2_AHEAD'] = l2
+names = ['wait_stage', 'update', 'B1', 'cluster_wait', '-', 'leaf+warp', '-', 'fold+send', 'reduce_total']
+for grp, spc in (('1', '128'), ('2', '64')):
+    os.environ['MMPR_FINE_GROUPS'] = grp
     os.environ['MMPR_FINE_SLOTS_PER_CTA'] = spc
     kernels.fine_sweep(model, x, out, t0, S, 1e-3, xi, bad)
     lib.mmpr_dev_fine_prof(None, 1)
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(); kernels.fine_sweep(model, x, out, t0, S, 1e-3, xi, bad); e1.record(); torch.cuda.synchronize()
     lib.mmpr_dev_fine_prof(buf.ctypes.data, 1)
-    ctas = 64 * (8 if spc == '128' else 16)
-    per_step = buf[:ctas, :9].sum(axis=0) / ctas / S
-    print(f'l2 {l2} spc {spc}: {e0.elapsed_time(e1):.3f} ms; cycles per CTA-step:', dict(zip(names, per_step.round(0))))
+    ctas = 64 * 8 if grp == '1' else 32 * 16
+    per_step = buf[:ctas, :9].sum(axis=0) / (64 * 8) / S
+    print(f'groups {grp} spc {spc}: {e0.elapsed_time(e1):.3f} ms; cycles per CTA-step:', dict(zip(names, per_step.round(0))))

@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   // which the slot's next writers run).  `refill` (>= 0) is the step whose
   // increments go into the stage this step just consumed.
   auto reduce = [&](int r, int refill, double &mean_out, int &bad_out) {
+    PROF_MARK(tr0);
     const int par = r & 1;
     const int bslot = r % 3;
     double acc = x[0];
@@ -264,8 +265,14 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
       s_wp[par][warp] = leaf;
       if (wbad) s_bad[bslot] = 1;
     }
+    PROF_MARK(tb0);
+    PROF_ADD(5, tr0, tb0);
     group_sync<GROUPS>(grp, gthreads);  // B1 (the only block-level barrier of a step)
-    if (tid == 0) {
+    PROF_MARK(tb1);
+    PROF_ADD(2, tb0, tb1);
+    // the last warp issues the refill so warp 0's path to the cluster
+    // exchange (the step's critical path) carries no TMA issue latency
+    if (tid == gthreads - 32) {
       s_bad[(r + 2) % 3] = 0;
       if (refill >= 0) {
         const int st = refill % ns;
@@ -297,7 +304,11 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
         st_async_v2(remote, __double_as_longlong(v.v),
                     (unsigned long long)(uint32_t)okv | ((unsigned long long)(uint32_t)bad << 32), rbar);
       }
+      PROF_MARK(tc0);
+      PROF_ADD(7, tb1, tc0);
       mbar_wait_parity(&s_red_bar[par], (uint32_t)((r >> 1) & 1));
+      PROF_MARK(tc1);
+      PROF_ADD(3, tc0, tc1);
       PartT c = PartT::make(0.0, false);
       int b = 0;
       if (lane < p.ctas) {
@@ -314,6 +325,8 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
     }
     mean_out = div(total, (double)p.P);
     bad_out = bad;
+    PROF_MARK(tr9);
+    PROF_ADD(8, tr0, tr9);
   };
 
   double s = 0.0;
@@ -323,7 +336,10 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
     reduce(0, -1, s, bad);
     for (int j = 0; j < p.S; ++j) {
       const int stage = j % ns;
+      PROF_MARK(tw0);
       mbar_wait_parity(&s_bar[stage], (uint32_t)((j / ns) & 1));
+      PROF_MARK(tw1);
+      PROF_ADD(0, tw0, tw1);
       const double *xb = s_stage + stage * p.stage_elems;
 #pragma unroll
       for (int m = 0; m < PPT; ++m) {
@@ -337,6 +353,8 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
         }
       }
       if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
+      PROF_MARK(tu1);
+      PROF_ADD(1, tw1, tu1);
       // B1 inside reduce() orders every read of this stage before its refill
       reduce(j + 1, (j + ns < p.S) ? j + ns : -1, s, bad);
       if (bad) {
@@ -344,8 +362,9 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
         break;
       }
     }
-    // Drain copies still in flight after an early exit.
-    if (tid == 0 && first_bad != MMPR_STAT_OK) {
+    // Drain copies still in flight after an early exit (the refill thread
+    // owns the issued count).
+    if (tid == gthreads - 32 && first_bad != MMPR_STAT_OK) {
       for (int j = first_bad + 1; j < issued; ++j) mbar_wait_parity(&s_bar[j % ns], (uint32_t)((j / ns) & 1));
     }
   }
