@@ -25,8 +25,8 @@ x = torch.randn((N, P), dtype=torch.float64, device=dev)
 out = torch.empty_like(x)
 bad = torch.empty(N, dtype=torch.int32, device=dev)
 t0 = torch.zeros(N, dtype=torch.float64, device=dev)
-for grp, spc, ns, l2 in (('1', '128', '2', '0'), ('2', '64', '2', '0'), ('2', '64', '2', '3')):
-    os.environ['MMPR_FINE_GROUPS'] = grp
+for grp, spc, ns, l2 in (('1', '128', '2', '0'), ('0', '128', '2', '0'), ('1', '128', '2', '3'), ('1', '64', '4', '0')):
+    os.environ['MMPR_FINE_DIRECT'] = grp
     os.environ['MMPR_FINE_SLOTS_PER_CTA'] = spc
     os.environ['MMPR_FINE_STAGES'] = ns
     os.environ['MMPR_FINE_L2_AHEAD'] = l2
@@ -37,8 +37,8 @@ for grp, spc, ns, l2 in (('1', '128', '2', '0'), ('2', '64', '2', '0'), ('2', '6
         print('spc', spc, e); continue
     ms, all_ = timeit(lambda: kernels.fine_sweep(model, x, out, t0, S, 1e-3, xi, bad))
     byts = N*S*P*8 + 2*N*P*8
-    print(f'fine sweep groups={grp} l2={l2} ns={ns} spc={spc} ctas/slice={k.value} clusters={c.value}: {ms:.3f} ms {N*S*P/ms/1e9*1e3:.3e} p-steps/s {byts/ms/1e6:.0f} GB/s  {all_}')
-[os.environ.pop(k) for k in ('MMPR_FINE_GROUPS', 'MMPR_FINE_SLOTS_PER_CTA', 'MMPR_FINE_STAGES', 'MMPR_FINE_L2_AHEAD')]
+    print(f'fine sweep direct={grp} l2={l2} ns={ns} spc={spc} ctas/slice={k.value} clusters={c.value}: {ms:.3f} ms {N*S*P/ms/1e9*1e3:.3e} p-steps/s {byts/ms/1e6:.0f} GB/s  {all_}')
+[os.environ.pop(k) for k in ('MMPR_FINE_DIRECT', 'MMPR_FINE_SLOTS_PER_CTA', 'MMPR_FINE_STAGES', 'MMPR_FINE_L2_AHEAD')]
 part = mm.SINGLE_REGION.descriptor()
 stats = torch.empty((N, 3), dtype=torch.float64, device=dev); counts = torch.empty((N, 1), dtype=torch.int64, device=dev)
 ms, _ = timeit(lambda: kernels.restrict(part, x, stats, counts))

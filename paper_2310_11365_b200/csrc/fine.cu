@@ -54,6 +54,7 @@ struct FineParams {
   int nstages;        // increment stages in shared memory (2..FS_MAX_STAGES)
   int cnt_min;        // min elements per lane over populated slots
   int l2_ahead;       // steps of increments prefetched into L2 beyond the smem stages
+  int direct;         // cluster exchange of warp partials (else CTA partials)
 };
 
 #ifdef MMPR_FINE_PROFILE
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   // [2 parities][ctas * nwarps] (after all groups' stages)
   const int nparts = p.ctas * nwarps;
   ClusterSlot *s_part = reinterpret_cast<ClusterSlot *>(s_dyn + (size_t)GROUPS * ns * p.stage_elems) +
-                        (size_t)grp * 2 * nparts;
+                        (size_t)grp * 2 * (p.direct ? nparts : p.ctas);
   PartT(*s_wp)[32] = s_wp_all[grp];
   int *s_bad = s_bad_all[grp];
   uint64_t *s_bar = s_bar_all[grp];
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
     leaf = leaf.xor_level(lane, 16);
     double total;
     int bad;
-    if (p.ctas > 1) {
+    if (p.ctas > 1 && p.direct) {
       // Cluster: every warp sends its partial (16 B st.async, completing tx
       // bytes on the receiver's mbarrier) to every CTA of the cluster, in
       // tree order; each CTA waits for all ctas*nwarps partials and every
@@ -337,6 +338,53 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
           if (m < nparts) v = v.xor_level(lane, m);
       }
       total = __shfl_sync(MMPR_FULL_MASK, v.v, 0);
+      bad = __any_sync(MMPR_FULL_MASK, b);
+    } else if (p.ctas > 1) {
+      // Cluster, CTA-level exchange (when ctas*nwarps partials do not fit
+      // next to the stages): block barrier, CTA fold, one st.async per peer
+      if (lane == 0) {
+        s_wp[par][warp] = leaf;
+        if (wbad) s_bad[bslot] = 1;
+      }
+      group_sync<GROUPS>(grp, gthreads);  // B1
+      if (tid == gthreads - 32) {
+        s_bad[(r + 2) % 3] = 0;
+        if (refill >= 0) {
+          const int st = refill % ns;
+          mbar_arrive_expect_tx(&s_bar[st], stage_bytes);
+          bulk_g2s(s_stage + st * p.stage_elems, xi_slice + (int64_t)refill * p.xi_row_pitch + lo, stage_bytes,
+                   &s_bar[st]);
+          ++issued;
+          const int pf = refill + p.l2_ahead;
+          if (p.l2_ahead > 0 && pf < p.S)
+            prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
+        }
+      }
+      PartT v = (lane < nwarps) ? s_wp[par][lane] : PartT::make(0.0, false);
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1)
+        if (m < nwarps) v = v.xor_level(lane, m);
+      const int cbad = s_bad[bslot];
+      if (tid == 0) mbar_arrive_expect_tx(&s_red_bar[par], 16u * (uint32_t)p.ctas);
+      if (warp == 0 && lane < p.ctas) {
+        const uint32_t remote = mapa_shared(smem_addr(&s_part[par * p.ctas + rank]), (uint32_t)lane);
+        const uint32_t rbar = mapa_shared(smem_addr(&s_red_bar[par]), (uint32_t)lane);
+        const int okv = v.valid() ? 1 : 0;
+        st_async_v2(remote, __double_as_longlong(v.v),
+                    (unsigned long long)(uint32_t)okv | ((unsigned long long)(uint32_t)cbad << 32), rbar);
+      }
+      mbar_wait_parity(&s_red_bar[par], (uint32_t)((r >> 1) & 1));
+      PartT c = PartT::make(0.0, false);
+      int b = 0;
+      if (lane < p.ctas) {
+        const ClusterSlot cs = s_part[par * p.ctas + lane];
+        c = PartT::make(cs.v, cs.ok != 0);
+        b = cs.bad;
+      }
+#pragma unroll
+      for (int m = 1; m < FS_MAX_CLUSTER; m <<= 1)
+        if (m < p.ctas) c = c.xor_level(lane, m);
+      total = __shfl_sync(MMPR_FULL_MASK, c.v, 0);
       bad = __any_sync(MMPR_FULL_MASK, b);
     } else {
       if (lane == 0) {
@@ -429,6 +477,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
 // host-side geometry
 // ---------------------------------------------------------------------------
 struct FineGeometry {
+  bool direct;  // warp-partial cluster exchange fits in shared memory
   int ppt;      // ceil(max leaf / 8)
   int cnt_min;  // min leaf / 8 over populated slots
   bool padded;  // some slot of a CTA is empty
@@ -459,7 +508,7 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
   g->ppt = (int)((max_leaf + 7) / 8);
   // increment stages of the CTA's particle range(s) must fit next to the
   // ~2 KB of static shared memory (227 KB opt-in per CTA)
-  const size_t smem_budget = 224 * 1024;
+  const size_t smem_budget = 226 * 1024;
   // Default: two slice groups per CTA (2 x 64 slots = 1024 threads) so one
   // slice's update overlaps the other's reduction on every SM; otherwise
   // one group of 128 slots.
@@ -473,7 +522,7 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
     const int v = atoi(env);
     if (g->groups == 1 && v >= 4 && v <= 128 && (v & (v - 1)) == 0) spc = v;
   }
-  while (spc > 4 && (size_t)spc * max_leaf * 8 * 2 * g->groups + 16384 > smem_budget) spc >>= 1;
+  while (spc > 4 && (size_t)spc * max_leaf * 8 * 2 * g->groups + 32 * FS_MAX_CLUSTER > smem_budget) spc >>= 1;
   if (nslots <= spc) {
     g->slots_per_cta = (int)(nslots < 4 ? 4 : nslots);
     g->ctas = 1;
@@ -502,8 +551,11 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
     if (v >= 2 && v <= FS_MAX_STAGES && (size_t)v * stage * g->groups <= smem_budget) g->nstages = v;
   }
   if (g->nstages < 2) g->nstages = 2;
-  // + per group two parities of ctas*nwarps 16-byte warp partials
-  const size_t parts = (size_t)g->ctas * (g->slots_per_cta / 4) * 16 * 2 * g->groups;
+  // + per group two parities of ctas*nwarps (direct) or ctas 16-byte partials
+  size_t parts = (size_t)g->ctas * (g->slots_per_cta / 4) * 16 * 2 * g->groups;
+  g->direct = g->ctas > 1 && stage * 2 * g->groups + parts <= smem_budget;
+  if (const char *env = getenv("MMPR_FINE_DIRECT")) g->direct = g->direct && atoi(env) != 0;
+  if (!g->direct) parts = (size_t)g->ctas * 16 * 2 * g->groups;
   while (g->nstages > 2 && stage * g->nstages * g->groups + parts > smem_budget) --g->nstages;
   g->smem_bytes = stage * g->nstages * g->groups + parts;
   return MMPR_OK;
@@ -626,6 +678,7 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
   p.nstages = g.nstages;
   p.cnt_min = g.cnt_min;
   p.l2_ahead = 3;
+  p.direct = g.direct ? 1 : 0;
   if (const char *env = getenv("MMPR_FINE_L2_AHEAD")) p.l2_ahead = max(0, min(16, atoi(env)));
   cudaStream_t s = (cudaStream_t)stream;
   if (g.ppt <= 8) return dispatch_tail<8>(p, g, s);
