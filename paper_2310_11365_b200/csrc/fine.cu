@@ -54,7 +54,6 @@ struct FineParams {
   int nstages;        // increment stages in shared memory (2..FS_MAX_STAGES)
   int cnt_min;        // min elements per lane over populated slots
   int l2_ahead;       // steps of increments prefetched into L2 beyond the smem stages
-  int direct;         // cluster exchange of warp partials (else CTA partials)
 };
 
 #ifdef MMPR_FINE_PROFILE
@@ -106,11 +105,6 @@ struct Part<true> {
     PwVal r = pw_xor_level(a, lane, m);
     return {r.v, r.ok};
   }
-  __device__ __forceinline__ static Part combine(Part l, Part r) {
-    PwVal c = pw_combine(PwVal{l.v, l.ok}, PwVal{r.v, r.ok});
-    return {c.v, c.ok};
-  }
-  __device__ __forceinline__ bool valid() const { return ok != 0; }
 };
 
 template <>
@@ -120,8 +114,6 @@ struct Part<false> {
   __device__ __forceinline__ Part xor_level(int, int m) const {
     return {add(v, __shfl_xor_sync(MMPR_FULL_MASK, v, m))};  // IEEE add is commutative
   }
-  __device__ __forceinline__ static Part combine(Part l, Part r) { return {add(l.v, r.v)}; }
-  __device__ __forceinline__ bool valid() const { return true; }
 };
 
 // Block-level barrier of one slice group: __syncthreads for one group per
@@ -146,13 +138,14 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
   using PartT = Part<PADDED>;
   extern __shared__ __align__(128) double s_dyn[];  // [GROUPS][nstages][stage_elems]
   __shared__ PartT s_wp_all[GROUPS][2][32];
+  __shared__ __align__(16) ClusterSlot s_slot_all[GROUPS][2][FS_MAX_CLUSTER];
   __shared__ int s_bad_all[GROUPS][3];
   __shared__ __align__(8) uint64_t s_bar_all[GROUPS][FS_MAX_STAGES];
   __shared__ __align__(8) uint64_t s_red_bar_all[GROUPS][2];  // cluster partials of call parity 0/1
 
   const int lane = threadIdx.x & 31;
-  const int gthreads = blockDim.x / GROUPS;
-  const int grp = (int)threadIdx.x / gthreads;
+  const int gthreads = GROUPS == 1 ? (int)blockDim.x : (int)blockDim.x / GROUPS;
+  const int grp = GROUPS == 1 ? 0 : (int)threadIdx.x / gthreads;
   const int tid = (int)threadIdx.x - grp * gthreads;  // thread index within the group
   const int warp = tid >> 5;
   const int nwarps = gthreads >> 5;
@@ -163,12 +156,8 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
 
   const int ns = p.nstages;
   double *s_stage = s_dyn + (size_t)grp * ns * p.stage_elems;
-  // cluster path: every warp's partial lands here, in tree order
-  // [2 parities][ctas * nwarps] (after all groups' stages)
-  const int nparts = p.ctas * nwarps;
-  ClusterSlot *s_part = reinterpret_cast<ClusterSlot *>(s_dyn + (size_t)GROUPS * ns * p.stage_elems) +
-                        (size_t)grp * 2 * (p.direct ? nparts : p.ctas);
   PartT(*s_wp)[32] = s_wp_all[grp];
+  ClusterSlot(*s_slot)[FS_MAX_CLUSTER] = s_slot_all[grp];
   int *s_bad = s_bad_all[grp];
   uint64_t *s_bar = s_bar_all[grp];
   uint64_t *s_red_bar = s_red_bar_all[grp];
@@ -272,114 +261,59 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
     PartT leaf = PartT::make(acc, slot_ok);
     leaf = leaf.xor_level(lane, 8);
     leaf = leaf.xor_level(lane, 16);
-    double total;
-    int bad;
-    if (p.ctas > 1 && p.direct) {
-      // Cluster: every warp sends its partial (16 B st.async, completing tx
-      // bytes on the receiver's mbarrier) to every CTA of the cluster, in
-      // tree order; each CTA waits for all ctas*nwarps partials and every
-      // warp folds them itself -- no block barrier in the step at all.
-      if (tid == 0) mbar_arrive_expect_tx(&s_red_bar[par], 16u * (uint32_t)nparts);
-      if (lane < p.ctas) {
-        const int gw = rank * nwarps + warp;
-        const uint32_t remote = mapa_shared(smem_addr(&s_part[par * nparts + gw]), (uint32_t)lane);
-        const uint32_t rbar = mapa_shared(smem_addr(&s_red_bar[par]), (uint32_t)lane);
-        const int okv = leaf.valid() ? 1 : 0;
-        st_async_v2(remote, __double_as_longlong(leaf.v),
-                    (unsigned long long)(uint32_t)okv | ((unsigned long long)(uint32_t)wbad << 32), rbar);
-      }
-      mbar_wait_parity(&s_red_bar[par], (uint32_t)((r >> 1) & 1));
-      // every warp of this CTA has sent, hence finished reading the stage
-      if (tid == gthreads - 32 && refill >= 0) {
+    if (lane == 0) {
+      s_wp[par][warp] = leaf;
+      if (wbad) s_bad[bslot] = 1;
+    }
+    PROF_MARK(tb0);
+    PROF_ADD(5, tr0, tb0);
+    group_sync<GROUPS>(grp, gthreads);  // B1 (the only block-level barrier of a step)
+    PROF_MARK(tb1);
+    PROF_ADD(2, tb0, tb1);
+    // the last warp issues the refill so warp 0's path to the cluster
+    // exchange (the step's critical path) carries no TMA issue latency
+    if (tid == gthreads - 32) {
+      s_bad[(r + 2) % 3] = 0;
+      if (refill >= 0) {
         const int st = refill % ns;
         mbar_arrive_expect_tx(&s_bar[st], stage_bytes);
         bulk_g2s(s_stage + st * p.stage_elems, xi_slice + (int64_t)refill * p.xi_row_pitch + lo, stage_bytes,
                  &s_bar[st]);
         ++issued;
-        const int pf = refill + p.l2_ahead;
+        const int pf = refill + p.l2_ahead;  // pull a later step towards L2
         if (p.l2_ahead > 0 && pf < p.S) prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
       }
-      const ClusterSlot *rp = s_part + par * nparts;
-      PartT v;
-      int b = 0;
-      if (nparts >= 32) {
-        // lane folds its E consecutive partials (E a power of two) with a
-        // binary-counter stack: equal-size subtrees merge left to right,
-        // i.e. exactly the pairwise tree over those E entries
-        const int E = nparts >> 5;
-        PartT st[5];
+    }
+    // every warp folds the group's warp partials with the same xor tree
+    PartT v = (lane < nwarps) ? s_wp[par][lane] : PartT::make(0.0, false);
 #pragma unroll
-        for (int i = 0; i < FS_MAX_CLUSTER; ++i) {
-          if (i < E) {
-            const ClusterSlot cs = rp[lane * E + i];
-            b |= cs.bad;
-            PartT cur = PartT::make(cs.v, cs.ok != 0);
-            int depth = __popc(i);  // entries on the stack before this one
-#pragma unroll
-            for (int bit = 0; bit < 4; ++bit) {
-              if (((i >> bit) & 1) == 0) break;
-              cur = PartT::combine(st[--depth], cur);
-            }
-            st[depth] = cur;
-          }
-        }
-        v = st[0];
-#pragma unroll
-        for (int m = 1; m < 32; m <<= 1) v = v.xor_level(lane, m);
-      } else {
-        v = PartT::make(0.0, false);
-        if (lane < nparts) {
-          const ClusterSlot cs = rp[lane];
-          v = PartT::make(cs.v, cs.ok != 0);
-          b = cs.bad;
-        }
-#pragma unroll
-        for (int m = 1; m < 32; m <<= 1)
-          if (m < nparts) v = v.xor_level(lane, m);
-      }
-      total = __shfl_sync(MMPR_FULL_MASK, v.v, 0);
-      bad = __any_sync(MMPR_FULL_MASK, b);
-    } else if (p.ctas > 1) {
-      // Cluster, CTA-level exchange (when ctas*nwarps partials do not fit
-      // next to the stages): block barrier, CTA fold, one st.async per peer
-      if (lane == 0) {
-        s_wp[par][warp] = leaf;
-        if (wbad) s_bad[bslot] = 1;
-      }
-      group_sync<GROUPS>(grp, gthreads);  // B1
-      if (tid == gthreads - 32) {
-        s_bad[(r + 2) % 3] = 0;
-        if (refill >= 0) {
-          const int st = refill % ns;
-          mbar_arrive_expect_tx(&s_bar[st], stage_bytes);
-          bulk_g2s(s_stage + st * p.stage_elems, xi_slice + (int64_t)refill * p.xi_row_pitch + lo, stage_bytes,
-                   &s_bar[st]);
-          ++issued;
-          const int pf = refill + p.l2_ahead;
-          if (p.l2_ahead > 0 && pf < p.S)
-            prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
-        }
-      }
-      PartT v = (lane < nwarps) ? s_wp[par][lane] : PartT::make(0.0, false);
-#pragma unroll
-      for (int m = 1; m < 32; m <<= 1)
-        if (m < nwarps) v = v.xor_level(lane, m);
-      const int cbad = s_bad[bslot];
+    for (int m = 1; m < 32; m <<= 1)
+      if (m < nwarps) v = v.xor_level(lane, m);
+    double total;
+    int bad = s_bad[bslot];
+    if (p.ctas > 1) {
+      // Each CTA's partial goes to the same group of every CTA of the cluster
+      // as one 16-byte st.async that completes tx bytes on the receiver's
+      // mbarrier; a group waits only for its own barrier.
       if (tid == 0) mbar_arrive_expect_tx(&s_red_bar[par], 16u * (uint32_t)p.ctas);
       if (warp == 0 && lane < p.ctas) {
-        const uint32_t remote = mapa_shared(smem_addr(&s_part[par * p.ctas + rank]), (uint32_t)lane);
+        const uint32_t remote = mapa_shared(smem_addr(&s_slot[par][rank]), (uint32_t)lane);
         const uint32_t rbar = mapa_shared(smem_addr(&s_red_bar[par]), (uint32_t)lane);
-        const int okv = v.valid() ? 1 : 0;
+        int okv = 1;
+        if constexpr (PADDED) okv = v.ok;
         st_async_v2(remote, __double_as_longlong(v.v),
-                    (unsigned long long)(uint32_t)okv | ((unsigned long long)(uint32_t)cbad << 32), rbar);
+                    (unsigned long long)(uint32_t)okv | ((unsigned long long)(uint32_t)bad << 32), rbar);
       }
+      PROF_MARK(tc0);
+      PROF_ADD(7, tb1, tc0);
       mbar_wait_parity(&s_red_bar[par], (uint32_t)((r >> 1) & 1));
+      PROF_MARK(tc1);
+      PROF_ADD(3, tc0, tc1);
       PartT c = PartT::make(0.0, false);
       int b = 0;
       if (lane < p.ctas) {
-        const ClusterSlot cs = s_part[par * p.ctas + lane];
-        c = PartT::make(cs.v, cs.ok != 0);
-        b = cs.bad;
+        c = PartT::make(s_slot[par][lane].v, s_slot[par][lane].ok != 0);
+        b = s_slot[par][lane].bad;
       }
 #pragma unroll
       for (int m = 1; m < FS_MAX_CLUSTER; m <<= 1)
@@ -387,32 +321,7 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
       total = __shfl_sync(MMPR_FULL_MASK, c.v, 0);
       bad = __any_sync(MMPR_FULL_MASK, b);
     } else {
-      if (lane == 0) {
-        s_wp[par][warp] = leaf;
-        if (wbad) s_bad[bslot] = 1;
-      }
-      group_sync<GROUPS>(grp, gthreads);  // B1 (the only block-level barrier of a step)
-      // the last warp issues the refill so warp 0's path carries no TMA issue latency
-      if (tid == gthreads - 32) {
-        s_bad[(r + 2) % 3] = 0;
-        if (refill >= 0) {
-          const int st = refill % ns;
-          mbar_arrive_expect_tx(&s_bar[st], stage_bytes);
-          bulk_g2s(s_stage + st * p.stage_elems, xi_slice + (int64_t)refill * p.xi_row_pitch + lo, stage_bytes,
-                   &s_bar[st]);
-          ++issued;
-          const int pf = refill + p.l2_ahead;
-          if (p.l2_ahead > 0 && pf < p.S)
-            prefetch_l2(xi_slice + (int64_t)pf * p.xi_row_pitch + lo, stage_bytes);
-        }
-      }
-      // every warp folds the group's warp partials with the same xor tree
-      PartT v = (lane < nwarps) ? s_wp[par][lane] : PartT::make(0.0, false);
-#pragma unroll
-      for (int m = 1; m < 32; m <<= 1)
-        if (m < nwarps) v = v.xor_level(lane, m);
       total = __shfl_sync(MMPR_FULL_MASK, v.v, 0);  // lanes >= nwarps folded empty slots
-      bad = s_bad[bslot];
     }
     mean_out = div(total, (double)p.P);
     bad_out = bad;
@@ -477,7 +386,6 @@ __global__ void __launch_bounds__(MAXT, 1) fine_sweep_kernel(const FineParams p)
 // host-side geometry
 // ---------------------------------------------------------------------------
 struct FineGeometry {
-  bool direct;  // warp-partial cluster exchange fits in shared memory
   int ppt;      // ceil(max leaf / 8)
   int cnt_min;  // min leaf / 8 over populated slots
   bool padded;  // some slot of a CTA is empty
@@ -508,10 +416,10 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
   g->ppt = (int)((max_leaf + 7) / 8);
   // increment stages of the CTA's particle range(s) must fit next to the
   // ~2 KB of static shared memory (227 KB opt-in per CTA)
-  const size_t smem_budget = 226 * 1024;
-  // Default: two slice groups per CTA (2 x 64 slots = 1024 threads) so one
-  // slice's update overlaps the other's reduction on every SM; otherwise
-  // one group of 128 slots.
+  const size_t smem_budget = 224 * 1024;
+  // (two groups -- particles of two slices per CTA, stepping independently
+  // -- measured slower than one on B200: they share the SM's FP64 pipe and
+  // double the cluster fan-in; kept behind MMPR_FINE_GROUPS=2 for study)
   g->groups = 1;
   if (const char *env = getenv("MMPR_FINE_GROUPS")) {  // tuning override
     const int v = atoi(env);
@@ -522,7 +430,7 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
     const int v = atoi(env);
     if (g->groups == 1 && v >= 4 && v <= 128 && (v & (v - 1)) == 0) spc = v;
   }
-  while (spc > 4 && (size_t)spc * max_leaf * 8 * 2 * g->groups + 32 * FS_MAX_CLUSTER > smem_budget) spc >>= 1;
+  while (spc > 4 && (size_t)spc * max_leaf * 8 * 2 * g->groups > smem_budget) spc >>= 1;
   if (nslots <= spc) {
     g->slots_per_cta = (int)(nslots < 4 ? 4 : nslots);
     g->ctas = 1;
@@ -551,13 +459,7 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
     if (v >= 2 && v <= FS_MAX_STAGES && (size_t)v * stage * g->groups <= smem_budget) g->nstages = v;
   }
   if (g->nstages < 2) g->nstages = 2;
-  // + per group two parities of ctas*nwarps (direct) or ctas 16-byte partials
-  size_t parts = (size_t)g->ctas * (g->slots_per_cta / 4) * 16 * 2 * g->groups;
-  g->direct = g->ctas > 1 && stage * 2 * g->groups + parts <= smem_budget;
-  if (const char *env = getenv("MMPR_FINE_DIRECT")) g->direct = g->direct && atoi(env) != 0;
-  if (!g->direct) parts = (size_t)g->ctas * 16 * 2 * g->groups;
-  while (g->nstages > 2 && stage * g->nstages * g->groups + parts > smem_budget) --g->nstages;
-  g->smem_bytes = stage * g->nstages * g->groups + parts;
+  g->smem_bytes = stage * g->nstages * g->groups;
   return MMPR_OK;
 }
 
@@ -566,7 +468,14 @@ static int launch_fine_t(const FineParams &p, const FineGeometry &g, cudaStream_
 
 template <int KIND, int PPT, bool HAS_TAIL>
 static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t stream) {
-  if (g.groups != 1) return MMPR_ERR_UNSUPPORTED;  // two-group variant not instantiated (slower on B200)
+#ifdef MMPR_FINE_TWO_GROUPS
+  if (g.groups == 2) {
+    if (g.padded) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 1024, 2>>(p, g, stream);
+    return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 1024, 2>>(p, g, stream);
+  }
+#else
+  if (g.groups != 1) return MMPR_ERR_UNSUPPORTED;
+#endif
   // <= 512 threads per CTA leaves 128 registers per thread for the particles
   if (g.padded) {
     if (g.threads <= 512) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 512, 1>>(p, g, stream);
@@ -678,7 +587,6 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
   p.nstages = g.nstages;
   p.cnt_min = g.cnt_min;
   p.l2_ahead = 3;
-  p.direct = g.direct ? 1 : 0;
   if (const char *env = getenv("MMPR_FINE_L2_AHEAD")) p.l2_ahead = max(0, min(16, atoi(env)));
   cudaStream_t s = (cudaStream_t)stream;
   if (g.ppt <= 8) return dispatch_tail<8>(p, g, s);
