@@ -198,10 +198,10 @@ def our_arm(args):
     ens0_dev = mm.sample_initial(init, plan, P)                    # device-resident input
     ens0_host = ens0_dev.device_positions.cpu().pin_memory()        # pinned host input (e2e)
 
-    def run(ens):
+    def run(ens, timings=False):
         if world > 1:
-            return run_micro_macro_sharded(model, ode, ens, cfg, plan)
-        return mm.run_micro_macro(model, ode, ens, cfg, plan)
+            return run_micro_macro_sharded(model, ode, ens, cfg, plan, record_timings=timings)
+        return mm.run_micro_macro(model, ode, ens, cfg, plan, record_timings=timings)
 
     def barrier():
         torch.cuda.synchronize()
@@ -213,7 +213,6 @@ def our_arm(args):
     barrier()
 
     # ---- device-resident timing ------------------------------------------------
-    fine_ms = []
     launches0 = _lib.launch_count["total"]
     with ClockSampler(local) as clocks:
         barrier()
@@ -222,10 +221,18 @@ def our_arm(args):
         e0.record()
         for _ in range(args.steps):
             tr = run(ens0_dev)
-            fine_ms.extend(1e3 * v for v in tr.timings.get("fine", []))
         e1.record()
         barrier()
     launches = _lib.launch_count["total"] - launches0
+    # per-launch kernel durations (CUDA events on the launching stream) from
+    # two eager runs of the same configuration, for the roofline
+    stage_ms = {}
+    for _ in range(2):
+        tr_t = run(ens0_dev, timings=True)
+        for key, vals in tr_t.timings.items():
+            if isinstance(vals, list):
+                stage_ms.setdefault(key, []).extend(1e3 * v for v in vals)
+    fine_ms = stage_ms.get("fine", [])
     ms = e0.elapsed_time(e1) / args.steps
     ms_all = ms
     if world > 1:
@@ -274,6 +281,7 @@ def our_arm(args):
         "e2e": {"value": psteps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
+        "stage_ms_per_run": {k: round(sum(v) / 2, 4) for k, v in stage_ms.items()},
     }
     if G == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
@@ -286,7 +294,7 @@ def our_arm(args):
 def main():
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
