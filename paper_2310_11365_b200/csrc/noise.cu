@@ -442,6 +442,9 @@ __global__ void __launch_bounds__(32, 16)
 normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__restrict__ out, int64_t pitch,
                          double loc, double scale) {
   __shared__ ulonglong2 zig[256];
+  __shared__ uint64_t s_words[32 * NW_WORDS];  // this sub-chunk's words, stream order
+  __shared__ uint16_t s_item[32 * NW_WORDS];   // positions of the non-fast words
+  __shared__ uint8_t s_res[32 * NW_WORDS];     // per word: bit0 produces, bit1 tail
   const int lane = threadIdx.x;
 #pragma unroll
   for (int i = lane; i < 256; i += 32)
@@ -471,19 +474,57 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
       x[i] = ((rw >> 8) & 1) ? -v : v;
       nf |= (mant >= z.x ? 1u : 0u) << i;
     }
-    // rare words: wedge tests and tail starts (per-lane loop over set bits)
+    // Rare words (~2.2%): wedge tests and tail starts, processed by the whole
+    // warp -- each lane tests one queued word, so the double-precision exp of
+    // the wedge test runs once per sub-chunk instead of once per lane bit.
     uint32_t pr = ~nf & 0xffu, tt = 0;
-    for (uint32_t rem = nf; rem; rem &= rem - 1) {
-      const int i = __ffs(rem) - 1;
-      const uint64_t rw = pick8(w, i);
-      const int layer = (int)(rw & 0xff);
-      if (layer != 0) {
-        const uint64_t nx = (i < NW_WORDS - 1) ? pick8(w, i + 1)
-                            : (lane < 31 ? succ : np::philox_word(word0 + NW_WORDS, k0, k1));
-        if (wedge_accepts(layer, pick8(x, i), nx)) pr |= 1u << i;
-      } else {
-        tt |= 1u << i;
-        pr |= 1u << i;
+    {
+      const int mine = __popc(nf);
+      int incl = mine;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(MMPR_FULL_MASK, incl, d);
+        if (lane >= d) incl += v;
+      }
+      const int n_items = __shfl_sync(MMPR_FULL_MASK, incl, 31);
+      if (n_items > 0) {
+        *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 0]) = make_ulonglong2(w[0], w[1]);
+        *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 2]) = make_ulonglong2(w[2], w[3]);
+        *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 4]) = make_ulonglong2(w[4], w[5]);
+        *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 6]) = make_ulonglong2(w[6], w[7]);
+        int q = incl - mine;
+        for (uint32_t rem = nf; rem; rem &= rem - 1) s_item[q++] = (uint16_t)(lane * NW_WORDS + __ffs(rem) - 1);
+        __syncwarp();
+        for (int base = 0; base < n_items; base += 32) {
+          const int it = base + lane;
+          if (it < n_items) {
+            const int pos = s_item[it];
+            const uint64_t rw = s_words[pos];
+            const int layer = (int)(rw & 0xff);
+            uint8_t res;
+            if (layer != 0) {
+              const uint64_t nx = (pos + 1 < 32 * NW_WORDS) ? s_words[pos + 1]
+                                  : np::philox_word(sub * 32 * NW_WORDS + 32 * NW_WORDS, k0, k1);
+              const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
+              const double wi = c_zig_wi[layer];
+              double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi,
+                                  -0x1.0p52 * wi);
+              if ((rw >> 8) & 1) v = -v;
+              res = wedge_accepts(layer, v, nx) ? 1 : 0;
+            } else {
+              res = 3;  // tail start: always produces
+            }
+            s_res[pos] = res;
+          }
+        }
+        __syncwarp();
+        for (uint32_t rem = nf; rem; rem &= rem - 1) {
+          const int i = __ffs(rem) - 1;
+          const uint8_t res = s_res[lane * NW_WORDS + i];
+          pr |= (uint32_t)(res & 1) << i;
+          tt |= (uint32_t)(res >> 1) << i;
+        }
+        __syncwarp();  // s_words/s_item/s_res are rewritten by the next sub-chunk
       }
     }
     // lane parse from entry 0, then stitch entries lane to lane until stable
