@@ -25,36 +25,10 @@
 #include <stdlib.h>
 
 #include "mmpr_device.cuh"
+#include "fine_common.cuh"
 #include "capi_internal.h"
 
 namespace mmpr {
-
-#define FS_MAX_CLUSTER 16
-#define FS_MAX_STAGES 4
-
-struct FineParams {
-  mmpr_model model;
-  int n_slices;
-  int S;
-  int64_t P;
-  double dt, sqrt_dt, bsd;  // bsd = b*sqrt(dt) for constant-diffusion models
-  const double *t0;
-  const double *x_in;
-  int64_t in_pitch;
-  double *x_out;
-  int64_t out_pitch;
-  const double *xi;
-  int64_t xi_slice_pitch, xi_row_pitch;
-  int32_t *bad_step;
-  double *final_mean;
-  int D;              // tree depth (2^D leaf slots)
-  int slots_per_cta;  // 4 * warps per CTA
-  int ctas;           // CTAs per slice (cluster size)
-  int stage_elems;    // doubles per smem stage (16-B multiple)
-  int nstages;        // increment stages in shared memory (2..FS_MAX_STAGES)
-  int cnt_min;        // min elements per lane over populated slots
-  int l2_ahead;       // steps of increments prefetched into L2 beyond the smem stages
-};
 
 #ifdef MMPR_FINE_PROFILE
 // dev builds only: per-CTA cycle totals of the step phases
@@ -65,56 +39,6 @@ __device__ long long g_fine_prof[4096][10];
 #define PROF_MARK(var)
 #define PROF_ADD(k, a, b)
 #endif
-
-struct __align__(16) ClusterSlot {
-  double v;
-  int ok;
-  int bad;
-};
-
-template <int KIND>
-__device__ __forceinline__ double em_update(const FineParams &p, double x, double s, double xi) {
-  // x + a(x,s)*dt + b(x,s)*sqrt(dt)*xi, left to right, each op rounded
-  mmpr_model m = p.model;
-  m.kind = KIND;  // folds the family switch at compile time
-  const double a = drift(m, x, s);
-  const double moved = add(x, mul(a, p.dt));
-  double noise;
-  if (constant_diffusion(KIND)) {
-    noise = mul(p.bsd, xi);
-  } else {
-    noise = mul(mul(diffusion(m, x, s), p.sqrt_dt), xi);
-  }
-  return add(moved, noise);
-}
-
-// Partial sums of the pairwise tree.  With PADDED (an irregular tree, or
-// fewer slots than lanes) a partial carries a validity flag so an empty right
-// sibling passes its left sibling through unchanged; a perfect tree (every
-// BASELINE size) uses plain adds.
-template <bool PADDED>
-struct Part;
-
-template <>
-struct Part<true> {
-  double v;
-  int ok;
-  __device__ __forceinline__ static Part make(double v, bool ok) { return {v, ok ? 1 : 0}; }
-  __device__ __forceinline__ Part xor_level(int lane, int m) const {
-    PwVal a{v, ok};
-    PwVal r = pw_xor_level(a, lane, m);
-    return {r.v, r.ok};
-  }
-};
-
-template <>
-struct Part<false> {
-  double v;
-  __device__ __forceinline__ static Part make(double v, bool) { return {v}; }
-  __device__ __forceinline__ Part xor_level(int, int m) const {
-    return {add(v, __shfl_xor_sync(MMPR_FULL_MASK, v, m))};  // IEEE add is commutative
-  }
-};
 
 // Block-level barrier of one slice group: __syncthreads for one group per
 // CTA, a named barrier (id 1 + group) when two groups share the CTA.
@@ -555,7 +479,10 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
   if (model->stat_kind != 0) return MMPR_ERR_UNSUPPORTED;
   FineGeometry g;
   int st = fine_geometry(particles, &g);
-  if (st != MMPR_OK) return st;
+  // beyond one cluster (or on request, for testing) the grid variant runs
+  const char *force = getenv("MMPR_FINE_FORCE_GRID");
+  const bool use_grid = (st == MMPR_ERR_UNSUPPORTED && g.ctas > FS_MAX_CLUSTER) || (force && atoi(force) == 1);
+  if (st != MMPR_OK && !use_grid) return st;
   FineParams p;
   p.model = *model;
   p.n_slices = n_slices;
@@ -580,6 +507,8 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
   p.xi_row_pitch = xi_row_pitch;
   p.bad_step = bad_step;
   p.final_mean = final_mean;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (use_grid) return fine_grid_sweep(p, s);
   p.D = g.D;
   p.slots_per_cta = g.slots_per_cta;
   p.ctas = g.ctas;
@@ -588,7 +517,6 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
   p.cnt_min = g.cnt_min;
   p.l2_ahead = 3;
   if (const char *env = getenv("MMPR_FINE_L2_AHEAD")) p.l2_ahead = max(0, min(16, atoi(env)));
-  cudaStream_t s = (cudaStream_t)stream;
   if (g.ppt <= 8) return dispatch_tail<8>(p, g, s);
   if (g.ppt <= 13) return dispatch_tail<13>(p, g, s);
   return dispatch_tail<16>(p, g, s);
@@ -597,6 +525,15 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
 extern "C" int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_out, int32_t *ctas_out) {
   FineGeometry g;
   int st = fine_geometry(particles, &g);
+  if (st == MMPR_ERR_UNSUPPORTED && g.ctas > FS_MAX_CLUSTER) {
+    // grid variant: concurrent teams of co-resident CTAs per slice
+    int teams = 0, c = 0;
+    st = fine_grid_shape(particles, 1 << 30, &teams, &c);
+    if (st != MMPR_OK) return st;
+    if (clusters_out) *clusters_out = teams;
+    if (ctas_out) *ctas_out = c;
+    return MMPR_OK;
+  }
   if (st != MMPR_OK) return st;
   if (ctas_out) *ctas_out = g.ctas;
   // note: reports the one-group, 1024-thread variant's cluster occupancy

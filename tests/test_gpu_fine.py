@@ -179,3 +179,90 @@ def test_occupancy_query(mm):
     c, k = ctypes.c_int32(0), ctypes.c_int32(0)
     mm._lib.call("mmpr_fine_sweep_occupancy", 100_000, ctypes.byref(c), ctypes.byref(k))
     assert k.value in (8, 16) and c.value >= 1
+
+
+# ---- grid variant (teams of co-resident CTAs, fine_grid.cu) ------------------
+GRID_CASES = [
+    # (P, slots per CTA, chunks per step, slices)
+    (100_000, 128, 1, 40),     # C = 8, 18 teams looping over 40 slices
+    (100_000, 128, 2, 5),      # half-step chunks
+    (100_000, 32, 1, 3),       # C = 32
+    (200_003, 64, 2, 3),       # tail, C = 32
+    (5_000, 32, 1, 4),         # padded slot tree, C = 2
+    (1 << 20, 128, 2, 3),      # config 5 shape: C = 64 (two partials per lane)
+    (1 << 20, 64, 1, 2),       # C = 128
+    (1 << 20, 32, 1, 2),       # C = 256 (eight partials per lane)
+]
+
+
+@pytest.mark.parametrize("P,spc,chunks,N", GRID_CASES)
+def test_grid_variant_bitwise_ou(mm, monkeypatch, P, spc, chunks, N):
+    """The grid-reduction kernel reproduces the oracle bit for bit (and so the
+    cluster kernel) for every team size and chunking."""
+    from paper_2310_11365_b200 import kernels
+    import torch
+    monkeypatch.setenv("MMPR_FINE_FORCE_GRID", "1")
+    monkeypatch.setenv("MMPR_FINE_GRID_SLOTS", str(spc))
+    monkeypatch.setenv("MMPR_FINE_GRID_CHUNKS", str(chunks))
+    S = 6
+    rng = np.random.default_rng(P + spc)
+    x0 = rng.normal(1.0, 0.1, (N, P))
+    xi_h = rng.standard_normal((N, S, P))
+    xi = kernels.noise_buffer(N, S, P)
+    xi[:, :, :P] = torch.from_numpy(xi_h).cuda()
+    x = torch.from_numpy(x0).cuda()
+    out = torch.empty_like(x)
+    bad = torch.empty(N, dtype=torch.int32, device="cuda")
+    fmean = torch.empty(N, dtype=torch.float64, device="cuda")
+    t0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+    model = GPU_MODELS["ou"](mm).descriptor
+    kernels.fine_sweep(model, x, out, t0, S, 1e-3, xi, bad, final_mean=fmean)
+    torch.cuda.synchronize()
+    om = O.model_ou(-1.0, 0.5, 0.5)
+    got = out.cpu().numpy()
+    for n in sorted({0, N // 2, N - 1}):
+        ref = O.propagate_fine(om, x0[n], 0, 0.0, 1e-3, S, xi_h[n])
+        assert np.array_equal(got[n], ref), n
+        assert fmean[n].item() == float(np.mean(ref))
+    assert (bad.cpu().numpy() == -1).all()
+
+
+def test_grid_variant_natural_dispatch_and_models(mm):
+    """P = 2^20 exceeds one cluster: dispatched to the grid kernel without
+    any override; every model family within the north-star tolerance."""
+    import ctypes
+    c, k = ctypes.c_int32(0), ctypes.c_int32(0)
+    mm._lib.call("mmpr_fine_sweep_occupancy", 1 << 20, ctypes.byref(c), ctypes.byref(k))
+    assert k.value > 16 and c.value >= 1
+    rng = np.random.default_rng(7)
+    P, S = 1 << 20, 3
+    x0 = np.concatenate([rng.normal(-1.0, 0.2, P // 2), rng.normal(1.0, 0.2, P - P // 2)])
+    xi = rng.standard_normal((S, P))
+    for name, om in [("dw_mult", O.model_dw_mult(0.25, 0.4, 0.2, 0.0, 0.3)),
+                     ("cubic", O.model_cubic(1.0, 1.0, 1.0, 0.4))]:
+        out = mm.propagate_fine(GPU_MODELS[name](mm), mm.ParticleEnsemble(x0), 0, 0.0,
+                                mm.StepConfig(5e-4, S), mm.NoisePlan(0), increments=xi)
+        ref = O.propagate_fine(om, x0, 0, 0.0, 5e-4, S, xi)
+        assert rel_dev(out.positions, ref) <= TOL
+        if name == "cubic":
+            assert np.array_equal(out.positions, ref)
+
+
+def test_grid_variant_blowup(mm, monkeypatch):
+    monkeypatch.setenv("MMPR_FINE_FORCE_GRID", "1")
+    monkeypatch.setenv("MMPR_FINE_GRID_SLOTS", "32")
+    model = mm.make_double_well(mm.DoubleWellSpec(sigma=0.0))
+    cfg = mm.StepConfig(dt=0.5, steps_per_slice=50)
+    x0 = np.full(20_000, 1.0)
+    x0[12_345] = 3.0
+    with pytest.raises(mm.NumericalBlowup) as err:
+        mm.propagate_fine(model, mm.ParticleEnsemble(x0), 6, 0.0, cfg, mm.NoisePlan(1))
+    with np.errstate(over="ignore", invalid="ignore"):
+        with pytest.raises(O.OracleBlowup) as ref:
+            O.propagate_fine(O.model_double_well(0.25, 0.5, 0.3, 0.0, 0.0), x0, 6, 0.0, 0.5, 50,
+                             np.zeros((50, x0.size)))
+    assert err.value.step_index == ref.value.step_index
+    # the same launch configuration still works afterwards (barrier phases drained)
+    out = mm.propagate_fine(mm.make_perturbed_ou(mm.PerturbedOUSpec()), mm.ParticleEnsemble(np.ones(20_000)), 0,
+                            0.0, mm.StepConfig(1e-3, 4), mm.NoisePlan(0), increments=np.zeros((4, 20_000)))
+    assert np.isfinite(out.positions).all()
