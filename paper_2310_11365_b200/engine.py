@@ -18,6 +18,7 @@ noise the increments of all slices are materialised once per run
 from __future__ import annotations
 
 import logging
+import os
 import time
 from collections.abc import Sequence
 from dataclasses import dataclass, field
@@ -150,7 +151,7 @@ class _Workspace:
     I64 = ("micro_counts", "fine_counts", "counts0")
     I32 = ("bad", "coarse_status", "match_status")
 
-    def __init__(self, K: int, N: int, P: int, S: int, I: int, retain: bool):
+    def __init__(self, K: int, N: int, P: int, S: int, I: int, retain: bool, noise_slices: int | None = None):
         dev = device()
         nv = 3 * I
         Kc = max(K, 1)
@@ -169,11 +170,14 @@ class _Workspace:
                 off += size
         self.snap = torch.empty((K + 1 if retain else 2, N + 1, P), dtype=torch.float64, device=dev)
         self.fine = torch.empty((N, P), dtype=torch.float64, device=dev)
-        self.xi = torch.empty((N, S, row_pitch(P)), dtype=torch.float64, device=dev)
         self.cache = torch.empty((K + 1, N, nv), dtype=torch.float64, device=dev)
         self.scratch = torch.empty(((N + 1) * I * P,), dtype=torch.float64, device=dev) if I > 1 else None
         self.x0 = torch.empty((1, P), dtype=torch.float64, device=dev)
         self.host = {dt: torch.empty(t.shape, dtype=dt, pin_memory=True) for dt, t in self.report.items()}
+        # increments of a batch of slices: all N when they fit (frozen noise is
+        # then generated once per run), else batches regenerated per iteration
+        self.noise_slices = noise_slices if noise_slices else _noise_batch(N, S, P)
+        self.xi = torch.empty((self.noise_slices, S, row_pitch(P)), dtype=torch.float64, device=dev)
 
     def reset_status(self):
         self.report[torch.int32].fill_(_lib.STAT_OK)
@@ -198,12 +202,23 @@ class _Workspace:
         return int(sum(t.numel() * t.element_size() for t in self.report.values()))
 
 
+def _noise_batch(N: int, S: int, P: int) -> int:
+    """Slices whose increments are held at once: all of them when they fit in
+    80% of the free device memory (MMPR_NOISE_SLICES overrides)."""
+    env = os.environ.get("MMPR_NOISE_SLICES")
+    if env:
+        return max(1, min(N, int(env)))
+    per_slice = max(1, S) * row_pitch(P) * 8
+    free, _ = torch.cuda.mem_get_info()
+    return max(1, min(N, int(0.8 * free) // per_slice))
+
+
 class _RunPlan:
     """One run configuration: its workspace and its launch sequence
     (replayed from a CUDA graph when the configuration repeats)."""
 
     def __init__(self, model_d, ode_d, ode_model_d, integ_d, part_d, cfg: PararealConfig, plan: NoisePlan,
-                 reuse: bool):
+                 reuse: bool, injected: bool = False):
         self.model_d, self.ode_d, self.ode_model_d, self.integ_d, self.part_d = \
             model_d, ode_d, ode_model_d, integ_d, part_d
         self.cfg, self.plan, self.reuse = cfg, plan, reuse
@@ -212,7 +227,8 @@ class _RunPlan:
         self.N, self.K, self.P, self.S, self.I = N, K, P, S, I
         self.times = tuple(cfg.t_start + n * cfg.slice_length for n in range(N + 1))
         self.times_d = torch.tensor(self.times, dtype=torch.float64, device=device())
-        self.ws = _Workspace(K, N, P, S, I, cfg.retain_snapshots)
+        self.ws = _Workspace(K, N, P, S, I, cfg.retain_snapshots, noise_slices=N if injected else None)
+        self.batch = self.ws.noise_slices
         self.graph = None
         self.launches_per_run = 0
 
@@ -237,21 +253,24 @@ class _RunPlan:
         kernels.match(part_d, ws.macro[0, 1:], ws.rho0, ws.counts0, ws.x0, self.snap(0)[1:], 1, ws.match_status[0])
         timer.stop("match", ev)
         kernels.restrict(part_d, self.snap(0), ws.micro[0], ws.micro_counts[0], ws.scratch)
-        if not injected and not self.plan.fresh:
+        if not injected and not self.plan.fresh and self.batch == N:
             ev = timer.start()
             slice_noise(self.plan.master_seed, 0, N, S, P, 0, False, out=ws.xi)
             timer.stop("noise", ev)
 
     def issue_iteration(self, k, timer, injected=False):
-        ws, part_d, N, S = self.ws, self.part_d, self.N, self.S
-        if not injected and self.plan.fresh:
-            ev = timer.start()
-            slice_noise(self.plan.master_seed, 0, N, S, self.P, k, True, out=ws.xi)
-            timer.stop("noise", ev)
+        ws, part_d, N, S, B = self.ws, self.part_d, self.N, self.S, self.batch
         cur, nxt = self.snap(k), self.snap(k + 1)
-        ev = timer.start()
-        kernels.fine_sweep(self.model_d, cur[:N], ws.fine, self.times_d[:N], S, self.cfg.step.dt, ws.xi, ws.bad[k])
-        timer.stop("fine", ev)
+        for a in range(0, N, B):
+            nb = min(B, N - a)
+            if not injected and (self.plan.fresh or B < N):
+                ev = timer.start()
+                slice_noise(self.plan.master_seed, a, nb, S, self.P, k, self.plan.fresh, out=ws.xi[:nb])
+                timer.stop("noise", ev)
+            ev = timer.start()
+            kernels.fine_sweep(self.model_d, cur[a:a + nb], ws.fine[a:a + nb], self.times_d[a:a + nb], S,
+                               self.cfg.step.dt, ws.xi[:nb], ws.bad[k][a:a + nb])
+            timer.stop("fine", ev)
         ev = timer.start()
         kernels.restrict(part_d, ws.fine, ws.fine_stats[k], ws.fine_counts[k], ws.scratch)
         timer.stop("restrict", ev)
@@ -298,7 +317,8 @@ def clear_graph_cache() -> None:
 def _plan_key(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse):
     return (bytes(model_d), bytes(ode_d), bytes(ode_model_d), bytes(integ_d), bytes(part_d), cfg.n_slices,
             cfg.iterations, cfg.particles, cfg.step.dt, cfg.step.steps_per_slice, cfg.slice_length, cfg.t_start,
-            cfg.retain_snapshots, plan.master_seed, plan.mode, reuse, torch.cuda.current_device())
+            cfg.retain_snapshots, plan.master_seed, plan.mode, reuse, torch.cuda.current_device(),
+            os.environ.get("MMPR_NOISE_SLICES"))
 
 
 def _wasserstein_delta(a, b, part_desc, scratch_stats, scratch_counts) -> float:
@@ -336,7 +356,8 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
     ens0 = _initial_ensemble(initial, cfg, plan)
     eager = record_timings or increments is not None or cfg.stop_wasserstein_tol is not None or not use_graph
     if eager:
-        rp = _RunPlan(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse)
+        rp = _RunPlan(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse,
+                      injected=increments is not None)
     else:
         key = _plan_key(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse)
         rp = _PLANS.get(key)

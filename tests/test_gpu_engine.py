@@ -207,3 +207,48 @@ def test_blowup_raises_first_error_in_reference_order(mm):
     ens = mm.ParticleEnsemble(np.linspace(50.0, 60.0, 16))
     with pytest.raises((mm.NumericalBlowup, mm.IntegrationFailure)):
         mm.run_micro_macro(model, mm.unimodal_rhs(model), ens, cfg, mm.NoisePlan(0))
+
+
+@pytest.mark.parametrize("mode", ["frozen", "fresh"])
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_noise_batching_is_bitwise_neutral(mm, monkeypatch, mode, use_graph):
+    """Increments held for a batch of slices at a time (regenerated per
+    iteration) give the same run as holding every slice's increments."""
+    model, ode, init, cfg, _ = _c1(mm, P=3000)
+    plan = mm.NoisePlan(5, mm.NoiseMode.FRESH if mode == "fresh" else mm.NoiseMode.FROZEN)
+    a = mm.run_micro_macro(model, ode, init, cfg, plan, use_graph=use_graph)
+    sa, ma = _snap(a), _packed(a, "macro")
+    monkeypatch.setenv("MMPR_NOISE_SLICES", "3")
+    b = mm.run_micro_macro(model, ode, init, cfg, plan, use_graph=use_graph)
+    assert np.array_equal(ma, _packed(b, "macro"))
+    assert np.array_equal(sa, _snap(b))
+
+
+def test_config5_large_ensemble_properties(mm):
+    """BASELINE config 5 shape at one GPU (P = 2^20 per slice -- the grid
+    reduction kernel -- bimodal multiplicative noise, dt = 5e-4) with fewer
+    slices and steps: k >= n exactness against the GPU's own serial fine
+    solution, per-region macro/micro consistency after matching, and slice
+    0 -> 1 against the oracle."""
+    P, N, K, S = 1 << 20, 4, 2, 40
+    dw = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.3 * math.sqrt(1.8))
+    model = mm.make_double_well_multiplicative(dw, 0.3)
+    part = dw.default_partition()
+    ode = mm.multimodal_rhs(model, part, dw.potential, dw.sigma)
+    cfg = mm.PararealConfig(n_slices=N, iterations=K, slice_length=S * 5e-4, particles=P,
+                            step=mm.StepConfig(dt=5e-4, steps_per_slice=S), partition=part,
+                            integrator=mm.EulerConfig(1e-2))
+    plan = mm.NoisePlan(0)
+    tr = mm.run_micro_macro(model, ode, _bimodal_init(mm), cfg, plan)
+    seq = mm.sequential_fine(model, _bimodal_init(mm), cfg, plan)
+    for k in range(1, K + 1):
+        for n in range(k + 1):
+            assert np.array_equal(tr.snapshots[k][n].positions, seq[n].positions), (k, n)
+    for k in range(K + 1):
+        for n in range(1, N + 1):
+            mac, mic = tr.macro[k][n], tr.micro_stats[k][n]
+            for i in range(2):
+                assert abs(mac.means[i] - mic.means[i]) < 1e-8, (k, n, i)
+    om = O.model_dw_mult(0.25, 0.4, 0.2, 0.0, 0.3)
+    x1 = O.propagate_fine(om, seq[0].positions, 0, 0.0, 5e-4, S, O.slice_noise(0, 0, S, P))
+    assert _rel(seq[1].positions, x1) <= TRAJ_TOL
