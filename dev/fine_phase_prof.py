@@ -18,14 +18,15 @@ bad = torch.empty(N, dtype=torch.int32, device='cuda')
 t0 = torch.zeros(N, dtype=torch.float64, device='cuda')
 buf = np.zeros((4096, 10), dtype=np.int64)
 names = ['wait_stage', 'update', 'B1', 'cluster_wait', '-', 'leaf+warp', '-', 'fold+send', 'reduce_total']
-for grp, spc in (('1', '128'), ('2', '64')):
+for grp, spc in (('1', '128'), ('1', '64')):
     os.environ['MMPR_FINE_GROUPS'] = grp
     os.environ['MMPR_FINE_SLOTS_PER_CTA'] = spc
+    os.environ['MMPR_FINE_STAGES'] = '2'
     kernels.fine_sweep(model, x, out, t0, S, 1e-3, xi, bad)
     lib.mmpr_dev_fine_prof(None, 1)
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(); kernels.fine_sweep(model, x, out, t0, S, 1e-3, xi, bad); e1.record(); torch.cuda.synchronize()
     lib.mmpr_dev_fine_prof(buf.ctypes.data, 1)
-    ctas = 64 * 8 if grp == '1' else 32 * 16
-    per_step = buf[:ctas, :9].sum(axis=0) / (64 * 8) / S
+    ctas = 64 * (8 if spc == '128' else 16)
+    per_step = buf[:ctas, :9].sum(axis=0) / ctas / S
     print(f'groups {grp} spc {spc}: {e0.elapsed_time(e1):.3f} ms; cycles per CTA-step:', dict(zip(names, per_step.round(0))))

@@ -80,7 +80,9 @@ __device__ __forceinline__ void chunk_range(int64_t len, int h, int64_t *a, int6
   if (*b < *a) *b = *a;
 }
 
-template <int KIND, int PPT, bool HAS_TAIL, bool PADDED, int H>
+// LO: compile-time lower bound on the accumulator elements per lane of every
+// populated leaf (elements LO..PPT-1 carry a predicate); -1 = p.cnt_min.
+template <int KIND, int PPT, bool HAS_TAIL, bool PADDED, int H, int LO>
 __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, const GridExtra e) {
   using PartT = Part<PADDED>;
   constexpr int MH = PPT / H;  // accumulator elements of chunk 0 (chunk H-1 takes the rest)
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
   const int cnt = (int)(len >> 3);
   const int tail = (int)(len & 7);
   const bool slot_ok = len > 0;
-  const int cmin = p.cnt_min;
+  const int cmin = LO >= 0 ? LO : p.cnt_min;
   if (j8 == 0) {
     s_leaf_off[li] = off;
     s_leaf_len[li] = (int)len;
@@ -482,12 +484,16 @@ static int launch_grid_t(const FineParams &p, const GridGeometry &g, cudaStream_
 
 template <int KIND, bool HAS_TAIL>
 static int grid_dispatch_shape(const FineParams &p, const GridGeometry &g, cudaStream_t s) {
+  // P = 2^20: every leaf holds 128 elements, no predicated accumulator element
+  const bool full = !g.padded && g.cnt_min >= 16;
   if (g.H == 1) {
-    if (g.padded) return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, true, 1>>(p, g, s);
-    return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, false, 1>>(p, g, s);
+    if (full) return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, false, 1, 16>>(p, g, s);
+    if (g.padded) return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, true, 1, -1>>(p, g, s);
+    return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, false, 1, -1>>(p, g, s);
   }
-  if (g.padded) return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, true, 2>>(p, g, s);
-  return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, false, 2>>(p, g, s);
+  if (full) return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, false, 2, 16>>(p, g, s);
+  if (g.padded) return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, true, 2, -1>>(p, g, s);
+  return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, false, 2, -1>>(p, g, s);
 }
 
 template <bool HAS_TAIL>
