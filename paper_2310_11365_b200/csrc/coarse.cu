@@ -42,12 +42,16 @@ __device__ double small_pairwise(const double *a, int n) {
   return res;
 }
 
-template <int NV>
-__device__ __forceinline__ void ode_rhs(const mmpr_moment_ode &ode, const mmpr_model &model, double t,
+// OK / MK: ODE and model kinds as compile-time constants, so the serial
+// chain is straight-line code with the parameters in registers.
+template <int NV, int OK, int MK>
+__device__ __forceinline__ void ode_rhs(const mmpr_moment_ode &ode, const mmpr_model &model_in, double t,
                                         const double *y, double *dy) {
   (void)t;
   constexpr int I = NV / 3;
-  switch (ode.kind) {
+  mmpr_model model = model_in;
+  model.kind = MK;  // folds the family switch in coeffs()
+  switch (OK) {
     case MMPR_ODE_UNIMODAL: {  // first-order closure with point statistic s = M
       const double m = y[0], var = y[1];
       const ModelCoeffs c = coeffs(model, m, m);
@@ -102,19 +106,24 @@ __device__ __forceinline__ bool all_finite(const double *v) {
   return ok;
 }
 
-// Forward Euler with n = round((t1 - t0)/dt) >= 1 equal steps.
-template <int NV>
-__device__ int integrate_euler(const mmpr_moment_ode &ode, const mmpr_model &model, double dt, double t0,
-                               double t1, double *y) {
+// Forward-Euler step count and size over [t0, t1]: n = round((t1 - t0)/dt) >= 1.
+__device__ __forceinline__ void euler_grid(double dt, double t0, double t1, long long *n_out, double *h_out) {
   const double span = sub(t1, t0);
-  if (span == 0.0) return MMPR_STAT_OK;
   long long n = llrint(div(span, dt));
   if (n < 1) n = 1;
-  const double h = div(span, (double)n);
+  *n_out = span == 0.0 ? 0 : n;
+  *h_out = div(span, (double)n);
+}
+
+// Forward Euler with n equal steps of size h from t0.
+template <int NV, int OK, int MK>
+__device__ int integrate_euler_n(const mmpr_moment_ode &ode, const mmpr_model &model, long long n, double h,
+                                 double t0, double *y) {
+  if (n == 0) return MMPR_STAT_OK;
   double k[NV];
   for (long long i = 0; i < n; ++i) {
     const double t = add(t0, mul((double)i, h));
-    ode_rhs<NV>(ode, model, t, y, k);
+    ode_rhs<NV, OK, MK>(ode, model, t, y, k);
 #pragma unroll
     for (int v = 0; v < NV; ++v) y[v] = add(y[v], mul(h, k[v]));
   }
@@ -146,7 +155,7 @@ __device__ __forceinline__ double rms_norm(const double *e, const double *scale)
   return __dsqrt_rn(div(small_pairwise(q, NV), (double)NV));
 }
 
-template <int NV>
+template <int NV, int OK, int MK>
 __device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &model, const mmpr_integrator &cfg,
                               double t0, double t1, double *y) {
   constexpr int nv = NV;
@@ -155,7 +164,7 @@ __device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &mode
   if (span == 0.0) return MMPR_STAT_OK;
   double t = t0;
   double k[7][NV];
-  ode_rhs<NV>(ode, model, t, y, k[0]);
+  ode_rhs<NV, OK, MK>(ode, model, t, y, k[0]);
   if (!all_finite<NV>(k[0])) return 1;
   double h;
   if (cfg.first_step > 0.0) {
@@ -187,7 +196,7 @@ __device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &mode
         }
         yi[v] = add(y[v], mul(h, acc));
       }
-      ode_rhs<NV>(ode, model, add(t, mul(c_dp_c[i], h)), yi, k[i]);
+      ode_rhs<NV, OK, MK>(ode, model, add(t, mul(c_dp_c[i], h)), yi, k[i]);
     }
     double y5[NV], err[NV], sc[NV];
 #pragma unroll
@@ -226,11 +235,16 @@ __device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &mode
   return 1;
 }
 
-template <int NV>
+template <int NV, int OK, int MK>
 __device__ __forceinline__ int coarse_step(const mmpr_moment_ode &ode, const mmpr_model &model,
                                            const mmpr_integrator &integ, double t0, double t1, double *y) {
-  if (integ.kind == MMPR_INTEG_EULER) return integrate_euler<NV>(ode, model, integ.dt, t0, t1, y);
-  return integrate_dp54<NV>(ode, model, integ, t0, t1, y);
+  if (integ.kind == MMPR_INTEG_EULER) {
+    long long n;
+    double h;
+    euler_grid(integ.dt, t0, t1, &n, &h);
+    return integrate_euler_n<NV, OK, MK>(ode, model, n, h, t0, y);
+  }
+  return integrate_dp54<NV, OK, MK>(ode, model, integ, t0, t1, y);
 }
 
 struct CoarseParams {
@@ -250,13 +264,31 @@ struct CoarseParams {
   int skip_until;
 };
 
-// The next slice's inputs (times, fine moments, cached prediction) are
-// fetched one slice ahead through the read-only path so the serial chain
-// never waits on a global-memory round trip.
-template <int NV>
+// The row is serial in n and runs on lane 0.  Before it starts, the whole
+// warp computes every slice's Euler grid (step count and size: two
+// divisions per slice) into shared memory, and the next slice's inputs
+// (fine moments, cached prediction) are fetched one slice ahead through the
+// read-only path, so the chain waits on neither.
+#define CR_GRID_MAX 2048
+
+template <int NV, int OK, int MK>
 __global__ void coarse_row_kernel(const CoarseParams p) {
-  if (threadIdx.x != 0) return;
+  __shared__ long long s_n[CR_GRID_MAX];
+  __shared__ double s_h[CR_GRID_MAX];
   constexpr int I = NV / 3;
+  const bool euler = p.integ.kind == MMPR_INTEG_EULER;
+  const bool staged = euler && p.n <= CR_GRID_MAX;
+  if (staged) {
+    for (int n = threadIdx.x; n < p.n; n += blockDim.x) {
+      long long cnt;
+      double h;
+      euler_grid(p.integ.dt, __ldg(p.times + n), __ldg(p.times + n + 1), &cnt, &h);
+      s_n[n] = cnt;
+      s_h[n] = h;
+    }
+    __syncwarp();
+  }
+  if (threadIdx.x != 0) return;
   const double *__restrict__ times = p.times;
   const double *__restrict__ fine = p.fine;
   const double *__restrict__ cin = p.cache_in;
@@ -292,7 +324,8 @@ __global__ void coarse_row_kernel(const CoarseParams p) {
     } else {
 #pragma unroll
       for (int v = 0; v < NV; ++v) pred[v] = cur[v];
-      st = coarse_step<NV>(p.ode, p.model, p.integ, t0, t1, pred);
+      if (staged) st = integrate_euler_n<NV, OK, MK>(p.ode, p.model, s_n[n], s_h[n], t0, pred);
+      else st = coarse_step<NV, OK, MK>(p.ode, p.model, p.integ, t0, t1, pred);
     }
     p.status[n] = st;
 #pragma unroll
@@ -328,7 +361,7 @@ __global__ void coarse_row_kernel(const CoarseParams p) {
   }
 }
 
-template <int NV>
+template <int NV, int OK, int MK>
 __global__ void integrate_macro_kernel(const mmpr_moment_ode ode, const mmpr_model model,
                                        const mmpr_integrator integ, int n_states, const double *t0,
                                        const double *t1, const double *in, double *out, int32_t *status) {
@@ -337,11 +370,80 @@ __global__ void integrate_macro_kernel(const mmpr_moment_ode ode, const mmpr_mod
   double y[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) y[v] = in[s * NV + v];
-  const int st = coarse_step<NV>(ode, model, integ, t0[s], t1[s], y);
+  const int st = coarse_step<NV, OK, MK>(ode, model, integ, t0[s], t1[s], y);
 #pragma unroll
   for (int v = 0; v < NV; ++v) out[s * NV + v] = y[v];
   status[s] = st;
 }
+
+// Kernel selection: (regions, ODE kind, model kind) -> instantiation.
+template <template <int, int, int> class L, int NV, int OK>
+static int by_model(int mk, const typename L<NV, OK, 0>::Args &a) {
+  switch (mk) {
+    case MMPR_MODEL_OU: return L<NV, OK, MMPR_MODEL_OU>::run(a);
+    case MMPR_MODEL_LINEAR: return L<NV, OK, MMPR_MODEL_LINEAR>::run(a);
+    case MMPR_MODEL_DOUBLE_WELL: return L<NV, OK, MMPR_MODEL_DOUBLE_WELL>::run(a);
+    case MMPR_MODEL_CUBIC_MF: return L<NV, OK, MMPR_MODEL_CUBIC_MF>::run(a);
+    case MMPR_MODEL_DW_MULT: return L<NV, OK, MMPR_MODEL_DW_MULT>::run(a);
+    default: return MMPR_ERR_UNSUPPORTED;
+  }
+}
+
+template <template <int, int, int> class L>
+static int dispatch_coarse(int n_regions, int ok, int mk, const typename L<3, 1, 0>::Args &a) {
+  if (n_regions == 1) {
+    switch (ok) {
+      case MMPR_ODE_UNIMODAL: return by_model<L, 3, MMPR_ODE_UNIMODAL>(mk, a);
+      case MMPR_ODE_PERTURBED_OU: return L<3, MMPR_ODE_PERTURBED_OU, 0>::run(a);
+      case MMPR_ODE_GAUSSIAN_CUBIC: return L<3, MMPR_ODE_GAUSSIAN_CUBIC, 0>::run(a);
+      case MMPR_ODE_MULTIMODAL: return by_model<L, 3, MMPR_ODE_MULTIMODAL>(mk, a);
+      default: return MMPR_ERR_UNSUPPORTED;
+    }
+  }
+  if (ok != MMPR_ODE_MULTIMODAL) return MMPR_ERR_ARG;
+  switch (n_regions) {
+    case 2: return by_model<L, 6, MMPR_ODE_MULTIMODAL>(mk, a);
+    case 3: return by_model<L, 9, MMPR_ODE_MULTIMODAL>(mk, a);
+    default: return by_model<L, 12, MMPR_ODE_MULTIMODAL>(mk, a);
+  }
+}
+
+struct RowArgs {
+  CoarseParams p;
+  cudaStream_t stream;
+};
+
+template <int NV, int OK, int MK>
+struct RowLaunch {
+  using Args = RowArgs;
+  static int run(const Args &a) {
+    coarse_row_kernel<NV, OK, MK><<<1, 32, 0, a.stream>>>(a.p);
+    return mmpr_check_launch("coarse_row_kernel");
+  }
+};
+
+struct MacroArgs {
+  mmpr_moment_ode ode;
+  mmpr_model model;
+  mmpr_integrator integ;
+  int n_states;
+  const double *t0, *t1, *in;
+  double *out;
+  int32_t *status;
+  cudaStream_t stream;
+};
+
+template <int NV, int OK, int MK>
+struct MacroLaunch {
+  using Args = MacroArgs;
+  static int run(const Args &a) {
+    const int threads = 64;
+    const int blocks = (a.n_states + threads - 1) / threads;
+    integrate_macro_kernel<NV, OK, MK><<<blocks, threads, 0, a.stream>>>(a.ode, a.model, a.integ, a.n_states, a.t0,
+                                                                         a.t1, a.in, a.out, a.status);
+    return mmpr_check_launch("integrate_macro_kernel");
+  }
+};
 
 }  // namespace mmpr
 
@@ -386,14 +488,10 @@ extern "C" int mmpr_coarse_row(const mmpr_moment_ode *ode, const mmpr_model *mod
   p.raw_out = raw_out;
   p.status = status;
   p.skip_until = skip_until;
-  cudaStream_t st_ = (cudaStream_t)stream;
-  switch (ode->n_regions) {
-    case 1: coarse_row_kernel<3><<<1, 32, 0, st_>>>(p); break;
-    case 2: coarse_row_kernel<6><<<1, 32, 0, st_>>>(p); break;
-    case 3: coarse_row_kernel<9><<<1, 32, 0, st_>>>(p); break;
-    default: coarse_row_kernel<12><<<1, 32, 0, st_>>>(p); break;
-  }
-  return mmpr_check_launch("coarse_row_kernel");
+  RowArgs a;
+  a.p = p;
+  a.stream = (cudaStream_t)stream;
+  return dispatch_coarse<RowLaunch>(ode->n_regions, ode->kind, model->kind, a);
 }
 
 extern "C" int mmpr_integrate_macro(const mmpr_moment_ode *ode, const mmpr_model *model,
@@ -404,14 +502,16 @@ extern "C" int mmpr_integrate_macro(const mmpr_moment_ode *ode, const mmpr_model
   if (st != MMPR_OK) return st;
   if (!model || n_states < 0 || !t0 || !t1 || !state_in || !state_out || !status) return MMPR_ERR_ARG;
   if (n_states == 0) return MMPR_OK;
-  const int threads = 64;
-  const int blocks = (n_states + threads - 1) / threads;
-  cudaStream_t st_ = (cudaStream_t)stream;
-  switch (ode->n_regions) {
-    case 1: integrate_macro_kernel<3><<<blocks, threads, 0, st_>>>(*ode, *model, *integ, n_states, t0, t1, state_in, state_out, status); break;
-    case 2: integrate_macro_kernel<6><<<blocks, threads, 0, st_>>>(*ode, *model, *integ, n_states, t0, t1, state_in, state_out, status); break;
-    case 3: integrate_macro_kernel<9><<<blocks, threads, 0, st_>>>(*ode, *model, *integ, n_states, t0, t1, state_in, state_out, status); break;
-    default: integrate_macro_kernel<12><<<blocks, threads, 0, st_>>>(*ode, *model, *integ, n_states, t0, t1, state_in, state_out, status); break;
-  }
-  return mmpr_check_launch("integrate_macro_kernel");
+  MacroArgs a;
+  a.ode = *ode;
+  a.model = *model;
+  a.integ = *integ;
+  a.n_states = n_states;
+  a.t0 = t0;
+  a.t1 = t1;
+  a.in = state_in;
+  a.out = state_out;
+  a.status = status;
+  a.stream = (cudaStream_t)stream;
+  return dispatch_coarse<MacroLaunch>(ode->n_regions, ode->kind, model->kind, a);
 }
