@@ -18,6 +18,7 @@
 
 #include "mmpr_device.cuh"
 #include "capi_internal.h"
+#include "fine_common.cuh"
 
 namespace mmpr {
 
@@ -278,6 +279,10 @@ extern "C" int mmpr_restrict(const mmpr_partition *part, int32_t n_ens, int64_t 
   if (part->n_regions < 1 || part->n_regions > MMPR_MAX_REGIONS) return MMPR_ERR_ARG;
   if (part->n_regions > 1 && !scratch) return MMPR_ERR_ARG;
   if (n_ens == 0) return MMPR_OK;
+  if (part->n_regions == 1) {
+    const int st = restrict_single_region(n_ens, particles, x, pitch, stats, counts, (cudaStream_t)stream);
+    if (st != MMPR_ERR_UNSUPPORTED) return st;
+  }
   const int D = pw_depth(particles);
   if (D > 7 && ((int64_t(1) << D) / 128) > RS_MAX_CHUNKS) return MMPR_ERR_UNSUPPORTED;
   RestrictParams p;

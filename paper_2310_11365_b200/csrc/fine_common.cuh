@@ -97,4 +97,9 @@ struct Part<false> {
 int fine_grid_sweep(FineParams p, cudaStream_t stream);
 int fine_grid_shape(int64_t P, int n_slices, int *teams_out, int *ctas_out);
 
+// Single-region restriction with one cluster per ensemble, restrict1.cu
+// (MMPR_ERR_UNSUPPORTED beyond one cluster).
+int restrict_single_region(int n_ens, int64_t P, const double *x, int64_t pitch, double *stats, int64_t *counts,
+                           cudaStream_t stream);
+
 }  // namespace mmpr

@@ -135,3 +135,32 @@ def test_restrict_large_bimodal_against_oracle(mm):
     part_m = mm.RegionPartition(separatrices=(0.0,), peaks=(-0.894427, 0.894427))
     part_o = O.Partition((0.0,), (-0.894427, 0.894427))
     assert np.array_equal(mm.restrict(mm.ParticleEnsemble(x), part_m).packed(), O.restrict(x, part_o)[0])
+
+
+@pytest.mark.parametrize("P", [1, 2, 7, 8, 9, 100, 1000, 1001, 4097, 65_537, 100_000, 131_072, 200_003, 1 << 20])
+def test_restrict_single_region_sizes_bitwise(mm, P):
+    """Single-region restriction (cluster kernel up to 16 CTAs, one-CTA
+    kernel beyond) against np.mean / np.var, batched over ensembles."""
+    from paper_2310_11365_b200 import kernels
+    import torch
+    rng = np.random.default_rng(P)
+    E = 3
+    x = rng.normal(0.3, 1.7, (E, P))
+    x[1] *= 1e-3
+    x[2] = np.round(x[2], 2)  # ties and cancellations
+    xd = torch.from_numpy(x).cuda()
+    stats = torch.empty((E, 3), dtype=torch.float64, device="cuda")
+    counts = torch.empty((E, 1), dtype=torch.int64, device="cuda")
+    kernels.restrict(mm.SINGLE_REGION.descriptor(), xd, stats, counts)
+    got = stats.cpu().numpy()
+    for e in range(E):
+        ref, cnt = O.restrict(x[e], O.SINGLE)
+        assert np.array_equal(got[e], ref), (e, got[e], ref)
+        assert counts[e, 0].item() == P
+    # non-finite members propagate like numpy's
+    x[0, P // 2] = np.inf
+    xd = torch.from_numpy(x).cuda()
+    kernels.restrict(mm.SINGLE_REGION.descriptor(), xd, stats, counts)
+    with np.errstate(invalid="ignore"):
+        ref, _ = O.restrict(x[0], O.SINGLE)
+    np.testing.assert_array_equal(stats[0].cpu().numpy(), ref)
