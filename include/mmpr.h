@@ -232,6 +232,25 @@ int mmpr_integrate_macro(const mmpr_moment_ode *ode, const mmpr_model *model,
                          const double *t0, const double *t1, const double *state_in,
                          double *state_out, int32_t *status, void *stream);
 
+/* ------------------------------------------------------------------ */
+/* Error metrics (metrics.py:35-47, 73-130, 133-218)                   */
+/* ------------------------------------------------------------------ */
+
+/* Sort each of n_rows rows (count doubles at in + r*pitch) ascending into
+ * out + r*pitch (np.sort; ties are equal values, so the result is unique up
+ * to the order of +0.0/-0.0).  temp == NULL: writes the required temporary
+ * bytes to *temp_bytes and returns; else temp is a device buffer of
+ * *temp_bytes bytes.  Replaces the np.sort calls of wasserstein_1d and
+ * floor_from_references (metrics.py:46, 185). */
+int mmpr_sort_rows(int32_t n_rows, int64_t count, const double *in, double *out,
+                   int64_t pitch, void *temp, uint64_t *temp_bytes, void *stream);
+
+/* out[r] = np.mean(np.abs(a_r - b_r)) over count doubles (numpy pairwise
+ * order), a_r = a + r*pitch_a, b_r = b + r*pitch_b: the W1 distance of two
+ * sorted equally sized samples (metrics.py:35-47). */
+int mmpr_mean_abs_diff(int32_t n_rows, int64_t count, const double *a, int64_t pitch_a,
+                       const double *b, int64_t pitch_b, double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

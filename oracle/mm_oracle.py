@@ -18,6 +18,9 @@ itself, tests/golden/make_golden.py):
   coarse     unimodal/perturbed-OU/multimodal rhs moments.py:52-68,111-125,145-192
              integrate (DP5(4))                   rk54.py:16-129
   engine     run_micro_macro / sequential_fine    engine.py:127-277
+  metrics    wasserstein_1d / relative_errors /   metrics.py:35-218
+             statistical_floor / moment_spread /
+             floor_from_references
 
 plus the BASELINE-config additions that have no reference counterpart
 ("parity unpinned" by reference tests, pinned only by this restatement and by
@@ -555,3 +558,67 @@ def sequential_fine(model: Model, ens0, n_slices, slice_length, dt, steps, seed,
         x = propagate_fine(model, x, n, t_start + n * slice_length, dt, steps, xi)
         out.append(x)
     return out
+
+
+# ---------------------------------------------------------------------------
+# error metrics (metrics.py:35-218)
+# ---------------------------------------------------------------------------
+def w1(a, b):
+    """W1 of two equally sized samples: mean |sort(a) - sort(b)| (metrics.py:35-47)."""
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    return float(np.mean(np.abs(np.sort(a) - np.sort(b))))
+
+
+def l2(v):
+    return float(np.sqrt(np.sum(np.asarray(v) ** 2)))
+
+
+def relative_errors(snapshots, k, ref_k, var_denominator="variance"):
+    """(e_mean, e_var, e_wass, norm_mean, norm_var, norm_wass), per-slice
+    |mean err|, |var err|, W1 of iterate k against iterate ref_k over the
+    interior boundaries n = 1..N (metrics.py:73-130)."""
+    cur, ref = snapshots[k], snapshots[ref_k]
+    N = len(cur) - 1
+    me = np.array([np.mean(cur[n]) - np.mean(ref[n]) for n in range(1, N + 1)])
+    ve = np.array([np.var(cur[n]) - np.var(ref[n]) for n in range(1, N + 1)])
+    wa = np.array([w1(cur[n], ref[n]) for n in range(1, N + 1)])
+    rm = l2([np.mean(ref[n]) for n in range(1, N + 1)])
+    rv = l2([np.var(ref[n]) for n in range(1, N + 1)]) if var_denominator == "variance" else rm
+    q = math.sqrt(N)
+    scal = np.array([l2(me) / rm, l2(ve) / rv, l2(wa) / rm, l2(me) / q, l2(ve) / q, l2(wa) / q])
+    return scal, np.array([np.abs(me), np.abs(ve), wa])
+
+
+def statistical_floor(finals):
+    pairs = [(i, j) for i in range(len(finals)) for j in range(i + 1, len(finals))]
+    tot = 0.0
+    for i, j in pairs:
+        tot += w1(finals[i], finals[j])
+    return tot / len(pairs)
+
+
+def moment_spread(finals):
+    pairs = [(i, j) for i in range(len(finals)) for j in range(i + 1, len(finals))]
+    m = [float(np.mean(f)) for f in finals]
+    v = [float(np.var(f)) for f in finals]
+    return (sum(abs(m[i] - m[j]) for i, j in pairs) / len(pairs),
+            sum(abs(v[i] - v[j]) for i, j in pairs) / len(pairs))
+
+
+def floor_from_references(paths, var_denominator="variance"):
+    """(e_mean, e_var, e_wass, replicas) from >= 2 serial fine trajectories
+    (metrics.py:165-218): moments of the SORTED ensembles, W1 between them."""
+    N = len(paths[0]) - 1
+    srt = [[np.sort(np.asarray(p[n], dtype=float)) for n in range(1, N + 1)] for p in paths]
+    means = np.array([[float(np.mean(x)) for x in s] for s in srt])
+    varis = np.array([[float(np.var(x)) for x in s] for s in srt])
+    dm = float(np.mean([l2(m) for m in means]))
+    dv = float(np.mean([l2(v) for v in varis])) if var_denominator == "variance" else dm
+    pairs = [(i, j) for i in range(len(paths)) for j in range(i + 1, len(paths))]
+    nm = nv = nw = 0.0
+    for i, j in pairs:
+        nm += l2(means[i] - means[j])
+        nv += l2(varis[i] - varis[j])
+        nw += l2(np.array([float(np.mean(np.abs(srt[i][n] - srt[j][n]))) for n in range(N)]))
+    c = len(pairs)
+    return np.array([nm / c / dm, nv / c / dv, nw / c / dm, len(paths)])

@@ -87,6 +87,8 @@ SIGNATURES = {
     "mmpr_coarse_row": (ctypes.c_int, [_P, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
                                         _I32, _P]),
     "mmpr_integrate_macro": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),
+    "mmpr_sort_rows": (ctypes.c_int, [_I32, _I64, _P, _P, _I64, _P, _P, _P]),
+    "mmpr_mean_abs_diff": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I64, _P, _P]),
 }
 
 _lib = None
@@ -116,7 +118,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
 
 # entry points that launch exactly one kernel each (bench.py counts them)
 LAUNCHING = frozenset({"mmpr_noise_keys", "mmpr_entropy_key", "mmpr_normals_fill", "mmpr_fine_sweep",
-                       "mmpr_restrict", "mmpr_match", "mmpr_coarse_row", "mmpr_integrate_macro"})
+                       "mmpr_restrict", "mmpr_match", "mmpr_coarse_row", "mmpr_integrate_macro",
+                       "mmpr_mean_abs_diff"})
 launch_count = {"total": 0}
 
 

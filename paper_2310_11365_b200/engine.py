@@ -30,7 +30,7 @@ from ._device import device, require_cuda, torch
 from .errors import ConfigError, DegenerateMatch, IntegrationFailure, NumericalBlowup
 from .models import InitialDistribution, McKeanVlasovModel, device_model
 from .moments import MomentODE, device_ode
-from .noise import row_pitch, slice_noise
+from .noise import fill_normals, row_pitch, slice_noise, step_keys
 from .particles import NoisePlan, ParticleEnsemble, StepConfig, sample_initial
 from .rk54 import EulerConfig, IntegratorConfig, integrator_descriptor
 from .state import SINGLE_REGION, MacroState, RegionPartition
@@ -321,11 +321,9 @@ def _plan_key(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse):
             os.environ.get("MMPR_NOISE_SLICES"))
 
 
-def _wasserstein_delta(a, b, part_desc, scratch_stats, scratch_counts) -> float:
+def _wasserstein_delta(a, b) -> float:
     """max_n mean|sort(a_n) - sort(b_n)| (engine.py:244-253) on the device."""
-    diff = (torch.sort(a, dim=1).values - torch.sort(b, dim=1).values).abs_()
-    kernels.restrict(part_desc, diff, scratch_stats, scratch_counts)
-    return float(scratch_stats[:, 0].max().cpu())
+    return float(kernels.mean_abs_diff(kernels.sort_rows(a), kernels.sort_rows(b)).max().cpu())
 
 
 def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: InitialDistribution | ParticleEnsemble,
@@ -387,9 +385,7 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
             rp.issue_iteration(k, timer, injected)
             iterations_done = k + 1
             if cfg.stop_wasserstein_tol is not None:
-                st = torch.empty((N, 3), dtype=torch.float64, device=device())
-                ct = torch.empty((N, 1), dtype=torch.int64, device=device())
-                delta = _wasserstein_delta(rp.snap(k + 1)[1:], rp.snap(k)[1:], SINGLE_REGION.descriptor(), st, ct)
+                delta = _wasserstein_delta(rp.snap(k + 1)[1:], rp.snap(k)[1:])
                 if delta <= cfg.stop_wasserstein_tol:
                     stopped_at = k + 1
                     logger.info("stopping after iteration %d: max slice Wasserstein delta %.3e", k + 1, delta)
@@ -511,25 +507,56 @@ def _fine_sweep(model, ensembles, times, cfg: PararealConfig, plan: NoisePlan, i
     return [ParticleEnsemble._wrap(out[n]) for n in range(N)], [elapsed] * N
 
 
+def _serial_chains(desc, ens0, plans, cfg: PararealConfig, iteration: int):
+    """R independent serial fine chains advanced together: one fine-sweep
+    launch per slice over all R chains.  Increments are generated for a
+    batch of slices of every chain at a time (one key launch per chain, one
+    fill launch), within the device-memory budget of _noise_batch."""
+    R, N, S = len(plans), cfg.n_slices, cfg.step.steps_per_slice
+    P = ens0[0].size
+    pitch = row_pitch(P)
+    xs = torch.empty((R, N + 1, P), dtype=torch.float64, device=device())
+    for r, e in enumerate(ens0):
+        xs[r, 0].copy_(e.device_positions)
+    B = max(1, min(N, _noise_batch(N * R, S, P) // R)) if N else 1
+    xi = torch.empty((B, R, S, pitch), dtype=torch.float64, device=device())
+    bad = torch.empty((max(N, 1), R), dtype=torch.int32, device=device())
+    t0 = [torch.full((R,), cfg.t_start + n * cfg.slice_length, dtype=torch.float64, device=device())
+          for n in range(N)]
+    for a in range(0, N, B):
+        nb = min(B, N - a)
+        keys = torch.stack([step_keys(pl.master_seed, pl.fresh, iteration, a, nb, S) for pl in plans], dim=1)
+        fill_normals(keys, P, xi[:nb], pitch)
+        for n in range(a, a + nb):
+            kernels.fine_sweep(desc, xs[:, n], xs[:, n + 1], t0[n], S, cfg.step.dt, xi[n - a], bad[n])
+    b = bad.cpu().numpy()
+    for r in range(R):  # chain by chain, as separate serial runs would raise
+        for n in range(N):
+            if b[n, r] != _lib.STAT_OK:
+                raise NumericalBlowup(f"non-finite particle position in slice {n}, step {int(b[n, r])}",
+                                      slice_index=n, step_index=int(b[n, r]))
+    return [[ens0[r]] + [ParticleEnsemble._wrap(xs[r, n]) for n in range(1, N + 1)] for r in range(R)]
+
+
 def sequential_fine(model: McKeanVlasovModel, initial: InitialDistribution | ParticleEnsemble,
                     cfg: PararealConfig, plan: NoisePlan, iteration: int = 0) -> list[ParticleEnsemble]:
     """Serial fine propagation over all slices (engine.py:262-277): one
-    launch per slice, increments of every slice generated in one launch."""
+    launch per slice, increments generated per batch of slices."""
     desc = device_model(model)
     ens = initial if isinstance(initial, ParticleEnsemble) else sample_initial(initial, plan, cfg.particles)
-    N, P, S = cfg.n_slices, ens.size, cfg.step.steps_per_slice
-    xs = torch.empty((N + 1, P), dtype=torch.float64, device=device())
-    xs[0].copy_(ens.device_positions)
-    xi = slice_noise(plan.master_seed, 0, N, S, P, iteration, plan.fresh)
-    t0 = torch.tensor([cfg.t_start + n * cfg.slice_length for n in range(N)], dtype=torch.float64,
-                      device=device())
-    bad = torch.empty(N, dtype=torch.int32, device=device())
-    for n in range(N):
-        kernels.fine_sweep(desc, xs[n:n + 1], xs[n + 1:n + 2], t0[n:n + 1], S, cfg.step.dt, xi[n:n + 1],
-                           bad[n:n + 1])
-    b = bad.cpu().numpy()
-    for n in range(N):
-        if b[n] != _lib.STAT_OK:
-            raise NumericalBlowup(f"non-finite particle position in slice {n}, step {int(b[n])}",
-                                  slice_index=n, step_index=int(b[n]))
-    return [ens] + [ParticleEnsemble._wrap(xs[n]) for n in range(1, N + 1)]
+    return _serial_chains(desc, [ens], [plan], cfg, iteration)[0]
+
+
+def sequential_fine_batch(model: McKeanVlasovModel, initial: InitialDistribution | ParticleEnsemble,
+                          cfg: PararealConfig, plans, iteration: int = 0) -> list[list[ParticleEnsemble]]:
+    """``[sequential_fine(model, initial, cfg, plan) for plan in plans]`` --
+    the floor replicas of harness.run_experiment (harness.py:257-265) --
+    with the replicas advanced together (one launch per slice for all of
+    them).  Results are bit-identical to the separate serial runs."""
+    desc = device_model(model)
+    plans = list(plans)
+    if not plans:
+        return []
+    ens0 = [initial if isinstance(initial, ParticleEnsemble) else sample_initial(initial, pl, cfg.particles)
+            for pl in plans]
+    return _serial_chains(desc, ens0, plans, cfg, iteration)

@@ -121,5 +121,40 @@ def integrate_macro(ode: _lib.MomentOde, model: _lib.Model, integ: _lib.Integrat
               _lib.stream_handle(stream))
 
 
+def sort_rows(x, out=None, stream=None):
+    """Ascending sort of every row of x (R, P) into out (same shape and row
+    pitch): np.sort per row."""
+    require_cuda()
+    _f64(x, "x")
+    R, P = x.shape
+    pitch = _rows(x, "x")
+    if out is None:
+        out = torch.empty_strided(x.shape, x.stride(), dtype=torch.float64, device=x.device)
+    if out.shape != x.shape or _rows(out, "out") != pitch:
+        raise ValueError("out must match x in shape and row pitch")
+    nbytes = ctypes.c_uint64(0)
+    _lib.call("mmpr_sort_rows", int(R), int(P), None, None, int(pitch), None, ctypes.byref(nbytes),
+              _lib.stream_handle(stream))
+    temp = torch.empty(max(1, nbytes.value), dtype=torch.uint8, device=x.device)
+    _lib.call("mmpr_sort_rows", int(R), int(P), x.data_ptr(), out.data_ptr(), int(pitch), temp.data_ptr(),
+              ctypes.byref(nbytes), _lib.stream_handle(stream))
+    return out
+
+
+def mean_abs_diff(a, b, out=None, stream=None):
+    """out[r] = np.mean(np.abs(a[r] - b[r])) (numpy pairwise order)."""
+    require_cuda()
+    _f64(a, "a")
+    _f64(b, "b")
+    if a.shape != b.shape:
+        raise ValueError("a and b must have the same shape")
+    R, P = a.shape
+    if out is None:
+        out = torch.empty(R, dtype=torch.float64, device=a.device)
+    _lib.call("mmpr_mean_abs_diff", int(R), int(P), a.data_ptr(), _rows(a, "a"), b.data_ptr(), _rows(b, "b"),
+              out.data_ptr(), _lib.stream_handle(stream))
+    return out
+
+
 def noise_buffer(n_slices: int, steps: int, P: int):
     return torch.empty((n_slices, steps, row_pitch(P)), dtype=torch.float64, device=device())

@@ -286,15 +286,62 @@ def trace_fixture():
     return out
 
 
+def report_to_arrays(rep, prefix, out):
+    out[prefix + "scalars"] = np.array([rep.e_mean, rep.e_var, rep.e_wass, rep.normalized_mean, rep.normalized_var,
+                                        rep.normalized_wass])
+    out[prefix + "per_slice"] = np.array([rep.mean_err_per_slice, rep.var_err_per_slice, rep.wass_per_slice])
+
+
+def metrics_fixture():
+    """mcparareal.metrics on reference traces and serial fine replicas."""
+    from mcparareal import metrics as M
+    out = {}
+    spec = ref.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5)
+    model = ref.make_perturbed_ou(spec)
+    cfg = ref.PararealConfig(n_slices=10, iterations=5, slice_length=0.1, particles=1000,
+                             step=ref.StepConfig(dt=1e-3, steps_per_slice=100))
+    initial = ref.InitialDistribution.normal(1.0, 0.01)
+    with euler_coarse(1e-2):
+        tr = ref.run_micro_macro(model, ref.unimodal_rhs(model), initial, cfg, ref.NoisePlan(0))
+    for k in range(tr.iterations + 1):
+        report_to_arrays(M.relative_errors(tr, k), f"rel_c1_k{k}_", out)
+        report_to_arrays(M.relative_errors(tr, k, var_denominator="mean"), f"relm_c1_k{k}_", out)
+    report_to_arrays(M.relative_errors(tr, 1, reference_k=3), "rel_c1_k1_ref3_", out)
+    # floor replicas exactly as harness.replicate_seeds derives them (harness.py:158-165)
+    base = ref.NoisePlan(0)
+    seeds = [base.derived_seed(10_000 + j) for j in range(3)]
+    out["floor_seeds"] = np.array(seeds, dtype=np.uint64)
+    paths = [ref.sequential_fine(model, initial, cfg, ref.NoisePlan(s)) for s in seeds]
+    for vd in ("variance", "mean"):
+        fl = M.floor_from_references(paths, vd)
+        out[f"floor_{vd}"] = np.array([fl.e_mean, fl.e_var, fl.e_wass, fl.n_replicas])
+    finals = [p[-1] for p in paths]
+    out["floor_raw"] = np.array([M.statistical_floor(finals)])
+    out["floor_spread"] = np.array(M.moment_spread(finals))
+    out["floor_final_positions"] = np.array([f.positions for f in finals])
+    # W1 examples: ties, signed zeros, different scales
+    rng = np.random.default_rng(5)
+    a = np.round(rng.normal(0.0, 1.0, 3001), 1)
+    b = np.round(rng.normal(0.2, 1.5, 3001), 1)
+    a[:5] = [0.0, -0.0, 0.0, -0.0, 1.0]
+    out["w1_a"], out["w1_b"] = a, b
+    out["w1_ab"] = np.array([M.wasserstein_1d(a, b), M.wasserstein_1d(b, a), M.wasserstein_1d(a, a)])
+    return out
+
+
 def main():
     np.savez_compressed(os.path.join(OUT, "noise.npz"), **noise_fixture())
     np.savez_compressed(os.path.join(OUT, "fine.npz"), **fine_fixture())
     np.savez_compressed(os.path.join(OUT, "coupling.npz"), **coupling_fixture())
     np.savez_compressed(os.path.join(OUT, "traces.npz"), **trace_fixture())
+    np.savez_compressed(os.path.join(OUT, "metrics.npz"), **metrics_fixture())
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
 
 
 if __name__ == "__main__":
-    sys.exit(main())
+    if len(sys.argv) > 1 and sys.argv[1] == "metrics":
+        np.savez_compressed(os.path.join(OUT, "metrics.npz"), **metrics_fixture())
+    else:
+        sys.exit(main())

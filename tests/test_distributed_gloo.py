@@ -53,6 +53,9 @@ class OracleBackend:
             stats[i] = torch.from_numpy(st)
             counts[i] = torch.from_numpy(c)
 
+    def w1_rows(self, a, b):
+        return torch.tensor([O.w1(a[i].numpy(), b[i].numpy()) for i in range(a.shape[0])], dtype=torch.float64)
+
     def coarse_row(self, times, iteration, rho0, fine_stats, cache_in, macro_out, cache_out, raw_out, status,
                    skip_until):
         I = self.part.n_regions
@@ -124,11 +127,14 @@ def _case(bimodal):
     return mm, model, ode, cfg, om, oode, opart
 
 
-def _worker(rank, world, port, bimodal, result_q):
+def _worker(rank, world, port, bimodal, result_q, tol=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         mm, model, ode, cfg, om, oode, opart = _case(bimodal)
+        if tol is not None:
+            import dataclasses
+            cfg = dataclasses.replace(cfg, stop_wasserstein_tol=tol)
         from paper_2310_11365_b200.distributed import TorchComm, run_micro_macro_sharded
         rng = np.random.default_rng(3)
         ens0 = (np.where(rng.random(cfg.particles) < 0.5, -1.0, 1.0) + 0.2 * rng.standard_normal(cfg.particles)
@@ -139,7 +145,8 @@ def _worker(rank, world, port, bimodal, result_q):
         macro = np.array([[s.packed() for s in row] for row in tr.macro])
         micro = np.array([[s.packed() for s in row] for row in tr.micro_stats])
         snaps = np.array([[e.device_positions.numpy() for e in row] for row in tr.snapshots])
-        result_q.put((rank, macro, micro, snaps, tr.timings["slice_offset"], tr.clamp_events, tr.fraction_gaps))
+        result_q.put((rank, macro, micro, snaps, tr.timings["slice_offset"], tr.clamp_events, tr.fraction_gaps,
+                      tr.stopped_at))
     finally:
         dist.destroy_process_group()
 
@@ -164,10 +171,38 @@ def test_sharded_run_matches_single_process_oracle(world, bimodal):
                             cfg.step.steps_per_slice, 5, part=opart, integ=O.Euler(cfg.integrator.dt))
     ref_snaps = np.array([[e for e in row] for row in ref.snapshots])
     Ng = cfg.n_slices // world
-    for rank, macro, micro, snaps, offset, clamps, gaps in results:
+    for rank, macro, micro, snaps, offset, clamps, gaps, _ in results:
         assert np.array_equal(macro, ref.macro), rank
         assert np.array_equal(micro, ref.micro), rank
         assert offset == rank * Ng
         assert np.array_equal(snaps, ref_snaps[:, offset:offset + Ng + 1]), rank
         assert clamps == ref.clamp_events
         assert [g[:2] for g in gaps] == [g[:2] for g in ref.fraction_gaps]
+
+
+def test_sharded_wasserstein_stop():
+    """stop_wasserstein_tol across ranks: the max slice W1 change is reduced
+    over all ranks (engine.py:244-253), every rank stops at the same k."""
+    mm, model, ode, cfg, om, oode, opart = _case(False)
+    rng = np.random.default_rng(3)
+    ens0 = rng.normal(1.0, 0.1, cfg.particles)
+    ref = O.run_micro_macro(om, oode, ens0, cfg.n_slices, cfg.iterations, cfg.slice_length, cfg.step.dt,
+                            cfg.step.steps_per_slice, 5, part=opart, integ=O.Euler(cfg.integrator.dt))
+    snaps = ref.snapshots
+    deltas = [max(O.w1(snaps[k][n], snaps[k - 1][n]) for n in range(1, cfg.n_slices + 1))
+              for k in range(1, cfg.iterations + 1)]
+    tol = deltas[1]
+    want = 1 + next(i for i, d in enumerate(deltas) if d <= tol)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, False, q, tol)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, macro, micro, snaps_r, offset, clamps, gaps, stopped in results:
+        assert stopped == want, rank
+        assert np.array_equal(macro, ref.macro[:want + 1]), rank

@@ -252,3 +252,24 @@ def test_config5_large_ensemble_properties(mm):
     om = O.model_dw_mult(0.25, 0.4, 0.2, 0.0, 0.3)
     x1 = O.propagate_fine(om, seq[0].positions, 0, 0.0, 5e-4, S, O.slice_noise(0, 0, S, P))
     assert _rel(seq[1].positions, x1) <= TRAJ_TOL
+
+
+def test_wasserstein_stop_criterion(mm, golden):
+    """stop_wasserstein_tol (engine.py:244-253): stop after the first
+    iteration whose max slice W1 change is <= tol; rows up to it unchanged."""
+    import dataclasses
+    g = golden("traces")
+    model, ode, init, cfg, plan = _c1(mm)
+    full = mm.run_micro_macro(model, ode, init, cfg, plan)
+    N = cfg.n_slices
+    deltas = [max(mm.wasserstein_1d(full.snapshots[k][n], full.snapshots[k - 1][n]) for n in range(1, N + 1))
+              for k in range(1, cfg.iterations + 1)]
+    big = mm.run_micro_macro(model, ode, init, dataclasses.replace(cfg, stop_wasserstein_tol=1e9), plan)
+    assert big.stopped_at == 1 and big.iterations == 1
+    assert np.array_equal(_packed(big, "macro"), g["c1_macro"][:2])
+    tol = deltas[2]
+    want = 1 + next(i for i, d in enumerate(deltas) if d <= tol)
+    tr = mm.run_micro_macro(model, ode, init, dataclasses.replace(cfg, stop_wasserstein_tol=tol), plan)
+    assert tr.stopped_at == want
+    assert np.array_equal(_packed(tr, "macro"), g["c1_macro"][:want + 1])
+    assert np.array_equal(_snap(tr), g["c1_snap"][:want + 1])

@@ -180,3 +180,34 @@ def test_trace_config5_shape_multiplicative(golden):
     ens0 = _bimodal(0, 1000)
     tr = O.run_micro_macro(m, ode, ens0, 4, 3, 0.1, 5e-4, 200, 0, part=part, integ=O.Euler(1e-2))
     _check_trace(tr, g, "c5_")
+
+
+# ---- metrics (metrics.py:35-218) ---------------------------------------------
+def test_oracle_metrics_match_reference(golden):
+    g, tr = golden("metrics"), golden("traces")
+    snaps = tr["c1_snap"]  # the reference trace the metrics fixture was computed on
+    K = snaps.shape[0] - 1
+    for k in range(K + 1):
+        for pre, vd in (("rel_", "variance"), ("relm_", "mean")):
+            scal, per = O.relative_errors(snaps, k, K, vd)
+            assert np.array_equal(scal, g[f"{pre}c1_k{k}_scalars"]), (k, vd)
+            assert np.array_equal(per, g[f"{pre}c1_k{k}_per_slice"]), (k, vd)
+    scal, per = O.relative_errors(snaps, 1, 3)
+    assert np.array_equal(scal, g["rel_c1_k1_ref3_scalars"])
+    a, b = g["w1_a"], g["w1_b"]
+    assert [O.w1(a, b), O.w1(b, a), O.w1(a, a)] == list(g["w1_ab"])
+
+
+def test_oracle_floor_matches_reference(golden):
+    g = golden("metrics")
+    om = O.model_ou(-1.0, 0.5, 0.5)
+    paths = []
+    for s in g["floor_seeds"]:
+        x0 = O.sample_normal_initial(int(s), 1.0, 0.01, 1000)
+        paths.append(O.sequential_fine(om, x0, 10, 0.1, 1e-3, 100, int(s)))
+    assert np.array_equal(np.array([p[-1] for p in paths]), g["floor_final_positions"])
+    for vd in ("variance", "mean"):
+        assert np.array_equal(O.floor_from_references(paths, vd), g[f"floor_{vd}"]), vd
+    finals = [p[-1] for p in paths]
+    assert O.statistical_floor(finals) == g["floor_raw"][0]
+    assert np.array_equal(np.array(O.moment_spread(finals)), g["floor_spread"])
