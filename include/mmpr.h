@@ -47,18 +47,32 @@ typedef enum {
  *  CUBIC_MF    builder model for BASELINE config 2, a = cE*s - c1*x - c3*x^3:
  *              p = {c1, c3, cE, sigma}
  *  DW_MULT     double-well drift with b = s0*sqrt(1+x^2) (BASELINE config 5):
- *              p = {4*alpha, 2*gamma, beta, tilt, s0, 12*alpha} */
+ *              p = {4*alpha, 2*gamma, beta, tilt, s0, 12*alpha}
+ *  ROTATOR     make_plane_rotator (models.py:286-314), ROTATOR_SUM statistic:
+ *              p = {K, sqrt(2 kBT), wrap (0/1), 2 kBT}
+ *  BURGERS     make_burgers (models.py:317-334), EMPIRICAL_CDF statistic:
+ *              p = {0, sigma} */
 enum {
   MMPR_MODEL_OU = 1,
   MMPR_MODEL_LINEAR = 2,
   MMPR_MODEL_DOUBLE_WELL = 3,
   MMPR_MODEL_CUBIC_MF = 4,
-  MMPR_MODEL_DW_MULT = 5
+  MMPR_MODEL_DW_MULT = 5,
+  MMPR_MODEL_ROTATOR = 6,
+  MMPR_MODEL_BURGERS = 7
+};
+
+/* Interaction statistics (models.py:30-33, ensemble_statistic :61-83). */
+enum {
+  MMPR_STAT_MEAN_OF_F = 0,     /* np.mean(x) (f = identity) */
+  MMPR_STAT_EMPIRICAL_CDF = 1, /* per-particle mid-rank CDF, stable argsort */
+  MMPR_STAT_ROTATOR_SUM = 2    /* (np.mean(sin x), np.mean(cos x)) */
 };
 
 typedef struct {
   int32_t kind;
-  int32_t stat_kind; /* 0 = MEAN_OF_F with identity f (only supported kind) */
+  int32_t stat_kind; /* MMPR_STAT_*; mmpr_fine_sweep takes MEAN_OF_F, the
+                        other two go through mmpr_fine_sweep_stepwise */
   double p[MMPR_MAX_PARAMS];
 } mmpr_model;
 
@@ -79,12 +93,22 @@ typedef struct {
  *  MULTIMODAL      multimodal_rhs(model, ...) (moments.py:145-192):
  *                  p = {targets[I], rates[I]}
  *  GAUSSIAN_CUBIC  builder Gaussian closure for CUBIC_MF (BASELINE config 2):
- *                  p = {c1, c3, cE, sigma}, I = 1 */
+ *                  p = {c1, c3, cE, sigma}, I = 1
+ *  TAYLOR          taylor_enriched_rhs(model) for a MEAN_OF_F model without
+ *                  its own closure (moments.py:71-108), I = 1
+ *  ROTATOR_TAYLOR  the plane rotator's enriched closure (models.py:299-306):
+ *                  p = {K, sigma_sq}, I = 1; status MMPR_STAT_SINGULAR at
+ *                  |sin M| or |cos M| < 1e-8 (SingularityError)
+ *  BURGERS         burgers_rhs(sigma) (moments.py:128-142):
+ *                  p = {sigma^2, -(2/sqrt(2 pi))}, I = 1 */
 enum {
   MMPR_ODE_UNIMODAL = 1,
   MMPR_ODE_PERTURBED_OU = 2,
   MMPR_ODE_MULTIMODAL = 3,
-  MMPR_ODE_GAUSSIAN_CUBIC = 4
+  MMPR_ODE_GAUSSIAN_CUBIC = 4,
+  MMPR_ODE_TAYLOR = 5,
+  MMPR_ODE_ROTATOR_TAYLOR = 6,
+  MMPR_ODE_BURGERS = 7
 };
 
 typedef struct {
@@ -107,8 +131,13 @@ typedef struct {
   double first_step;   /* DP54; <= 0 selects the initial-step heuristic */
 } mmpr_integrator;
 
-/* Status codes written to device status arrays. */
+/* Status codes written to device status arrays: MMPR_STAT_OK, else the
+ * failing step / region (fine sweep, match) or, for the coarse propagator,
+ * MMPR_STAT_INTEG_FAILED (IntegrationFailure) / MMPR_STAT_SINGULAR
+ * (SingularityError). */
 #define MMPR_STAT_OK (-1)
+#define MMPR_STAT_INTEG_FAILED 1
+#define MMPR_STAT_SINGULAR 2
 
 /* ------------------------------------------------------------------ */
 /* Library / device queries (host-synchronous)                         */
@@ -171,6 +200,19 @@ int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_t particles
                     int64_t out_pitch, const double *xi, int64_t xi_slice_pitch,
                     int64_t xi_row_pitch, int32_t *bad_step, double *final_mean,
                     void *stream);
+
+/* Fine sweep for the ROTATOR_SUM / EMPIRICAL_CDF models (plane rotator,
+ * Burgers), same buffers and status convention as mmpr_fine_sweep (no
+ * final_mean).  Step-synchronous: per EM step one statistic pass (pairwise
+ * sin/cos means, or a stable segmented sort giving mid-rank CDF values) and
+ * one update pass with the reference's post_step (np.mod(x, 2 pi)).
+ * workspace == NULL: writes the required bytes to *workspace_bytes. */
+int mmpr_fine_sweep_stepwise(const mmpr_model *model, int32_t n_slices, int64_t particles,
+                             int32_t steps, double dt, double sqrt_dt, const double *x_in,
+                             int64_t in_pitch, double *x_out, int64_t out_pitch,
+                             const double *xi, int64_t xi_slice_pitch, int64_t xi_row_pitch,
+                             int32_t *bad_step, void *workspace, uint64_t *workspace_bytes,
+                             void *stream);
 
 /* ------------------------------------------------------------------ */
 /* Restriction / matching (particles.py:176-205, coupling.py:26-95)    */

@@ -94,7 +94,8 @@ def slice_noise(seed, slice_index, steps, count, iteration=0, fresh=False):
 # ---------------------------------------------------------------------------
 # models (descriptor = (kind, params)); factory closures' op order
 # ---------------------------------------------------------------------------
-OU, LINEAR, DOUBLE_WELL, CUBIC_MF, DW_MULT = 1, 2, 3, 4, 5
+OU, LINEAR, DOUBLE_WELL, CUBIC_MF, DW_MULT, ROTATOR, BURGERS = 1, 2, 3, 4, 5, 6, 7
+TWO_PI = 2.0 * math.pi
 
 
 @dataclass(frozen=True)
@@ -125,8 +126,35 @@ def model_dw_mult(alpha, gamma, beta, J, s0):
     return Model(DW_MULT, (4.0 * alpha, 2.0 * gamma, float(beta), tilt, float(s0), 12.0 * alpha))
 
 
+def model_rotator(K, kBT, wrap=True):
+    """Plane rotator (models.py:286-314): p = (K, sqrt(2 kBT), wrap)."""
+    return Model(ROTATOR, (float(K), math.sqrt(2.0 * kBT), 1.0 if wrap else 0.0))
+
+
+def model_burgers(sigma):
+    """Burgers rank interaction (models.py:317-334): p = (0, sigma)."""
+    return Model(BURGERS, (0.0, float(sigma)))
+
+
+def statistic(m: Model, x):
+    """ensemble_statistic (models.py:61-83) for every statistic kind."""
+    if m.kind == ROTATOR:
+        return float(np.mean(np.sin(x))), float(np.mean(np.cos(x)))
+    if m.kind == BURGERS:  # mid-rank CDF, ties by index
+        order = np.argsort(x, kind="stable")
+        ranks = np.empty(len(x), dtype=float)
+        ranks[order] = np.arange(len(x), dtype=float)
+        return (ranks + 0.5) / len(x)
+    return float(np.mean(x))
+
+
 def drift(m: Model, x, s):
     p = m.p
+    if m.kind == ROTATOR:                 # K (cos x S - sin x C) - sin x
+        S, C = s
+        return p[0] * (np.cos(x) * S - np.sin(x) * C) - np.sin(x)
+    if m.kind == BURGERS:                 # 1 - s
+        return 1.0 - s
     if m.kind == OU:                      # a * x + a_E * s
         return p[0] * x + p[1] * s
     if m.kind == LINEAR:                  # A x + A_E s + A_0
@@ -151,6 +179,8 @@ def diffusion(m: Model, x, s):
         return np.full_like(x, p[3])
     if m.kind == DW_MULT:
         return p[4] * np.sqrt(1.0 + x * x)
+    if m.kind in (ROTATOR, BURGERS):
+        return np.full_like(x, p[1])
     raise ValueError(m.kind)
 
 
@@ -180,8 +210,11 @@ def coefficients(m: Model, x, s):
 
 
 def em_step_raw(m: Model, x, t, dt, noise):
-    s = float(np.mean(x))
-    return x + drift(m, x, s) * dt + diffusion(m, x, s) * math.sqrt(dt) * noise
+    s = statistic(m, x)
+    y = x + drift(m, x, s) * dt + diffusion(m, x, s) * math.sqrt(dt) * noise
+    if m.kind == ROTATOR and m.p[2]:      # post_step: np.mod(x, 2 pi)
+        y = np.mod(y, TWO_PI)
+    return y
 
 
 def propagate_fine(m: Model, x0, slice_index, t0, dt, steps, noise):
@@ -275,7 +308,7 @@ def match(target, x, part: Partition = SINGLE, policy="raise"):
 # ---------------------------------------------------------------------------
 # moment ODEs (moments.py) and integrators
 # ---------------------------------------------------------------------------
-UNIMODAL, PERTURBED_OU, MULTIMODAL, GAUSSIAN_CUBIC = 1, 2, 3, 4
+UNIMODAL, PERTURBED_OU, MULTIMODAL, GAUSSIAN_CUBIC, TAYLOR, ROTATOR_TAYLOR, BURGERS_ODE = 1, 2, 3, 4, 5, 6, 7
 
 
 @dataclass(frozen=True)
@@ -317,13 +350,43 @@ def ode_gaussian_cubic(c1, c3, cE, sigma):
     return Ode(GAUSSIAN_CUBIC, 1, (float(c1), float(c3), float(cE), float(sigma)))
 
 
+def ode_rotator_taylor(K, kBT):
+    """The plane rotator's enriched closure (models.py:299-306)."""
+    return Ode(ROTATOR_TAYLOR, 1, (float(K), 2.0 * kBT))
+
+
+def ode_burgers(sigma):
+    """burgers_rhs (moments.py:128-142)."""
+    return Ode(BURGERS_ODE, 1, (float(sigma) ** 2,))
+
+
+class OracleSingular(Exception):
+    pass
+
+
 def rhs(ode: Ode, t, y):
     y = np.asarray(y, dtype=float)
     n = ode.n_regions
     if ode.kind == UNIMODAL:
         m, var, _ = y
+        if ode.model.kind == ROTATOR:  # point statistic (sin M, cos M)
+            K, b = ode.model.p[0], ode.model.p[1]
+            S, C = math.sin(m), math.cos(m)
+            a = float(K * (np.cos(m) * S - np.sin(m) * C) - np.sin(m))
+            a_x = float(K * (-np.sin(m) * S - np.cos(m) * C) - np.cos(m))
+            return np.array([a + 0.5 * 0.0, (2.0 * a_x + 0.0 * 0.0) * var + b * b, 0.0])
         a, b, a_x, b_x, b_xx = coefficients(ode.model, m, float(m))
         return np.array([a + 0.5 * b_xx, (2.0 * a_x + b_x * b_x) * var + b * b, 0.0])
+    if ode.kind == ROTATOR_TAYLOR:
+        m, var, _ = y
+        K, sigma_sq = ode.p
+        sm, cm = math.sin(m), math.cos(m)
+        if abs(sm) < 1e-8 or abs(cm) < 1e-8:
+            raise OracleSingular(m)
+        return np.array([-sm + var / (2.0 * sm), -2.0 * (-K - cm + var / (2.0 * cm)) * var + sigma_sq, 0.0])
+    if ode.kind == BURGERS_ODE:
+        _, var, _ = y
+        return np.array([0.5, -(2.0 / math.sqrt(2.0 * math.pi)) * math.sqrt(max(var, 0.0)) + ode.p[0], 0.0])
     if ode.kind == PERTURBED_OU:
         m, var, _ = y
         mr, vr, vs = ode.p

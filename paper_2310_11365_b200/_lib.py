@@ -25,16 +25,27 @@ MODEL_LINEAR = 2
 MODEL_DOUBLE_WELL = 3
 MODEL_CUBIC_MF = 4
 MODEL_DW_MULT = 5
+MODEL_ROTATOR = 6
+MODEL_BURGERS = 7
+
+STAT_MEAN_OF_F = 0
+STAT_EMPIRICAL_CDF = 1
+STAT_ROTATOR_SUM = 2
 
 ODE_UNIMODAL = 1
 ODE_PERTURBED_OU = 2
 ODE_MULTIMODAL = 3
 ODE_GAUSSIAN_CUBIC = 4
+ODE_TAYLOR = 5
+ODE_ROTATOR_TAYLOR = 6
+ODE_BURGERS = 7
 
 INTEG_EULER = 1
 INTEG_DP54 = 2
 
 STAT_OK = -1
+STAT_INTEG_FAILED = 1
+STAT_SINGULAR = 2
 
 STATUS_TEXT = {0: "ok", 1: "invalid argument", 2: "CUDA error", 3: "unsupported"}
 
@@ -87,6 +98,8 @@ SIGNATURES = {
     "mmpr_coarse_row": (ctypes.c_int, [_P, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
                                         _I32, _P]),
     "mmpr_integrate_macro": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),
+    "mmpr_fine_sweep_stepwise": (ctypes.c_int, [_P, _I32, _I64, _I32, _D, _D, _P, _I64, _P, _I64, _P, _I64,
+                                                 _I64, _P, _P, _P, _P]),
     "mmpr_sort_rows": (ctypes.c_int, [_I32, _I64, _P, _P, _I64, _P, _P, _P]),
     "mmpr_mean_abs_diff": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I64, _P, _P]),
 }

@@ -23,6 +23,7 @@
 namespace mmpr {
 
 #define CS_MAXV (3 * MMPR_MAX_REGIONS)
+#define MMPR_COARSE_SINGULAR 2
 
 // numpy pairwise sum for n <= 128 (short vectors: sequential from 0 when
 // n < 8, else 8 accumulators)
@@ -44,9 +45,11 @@ __device__ double small_pairwise(const double *a, int n) {
 
 // OK / MK: ODE and model kinds as compile-time constants, so the serial
 // chain is straight-line code with the parameters in registers.
+// Returns 0, or MMPR_COARSE_SINGULAR when a closure is evaluated at its
+// removable singularity (the reference raises SingularityError).
 template <int NV, int OK, int MK>
-__device__ __forceinline__ void ode_rhs(const mmpr_moment_ode &ode, const mmpr_model &model_in, double t,
-                                        const double *y, double *dy) {
+__device__ __forceinline__ int ode_rhs(const mmpr_moment_ode &ode, const mmpr_model &model_in, double t,
+                                       const double *y, double *dy) {
   (void)t;
   constexpr int I = NV / 3;
   mmpr_model model = model_in;
@@ -92,10 +95,39 @@ __device__ __forceinline__ void ode_rhs(const mmpr_moment_ode &ode, const mmpr_m
       dy[2] = 0.0;
       break;
     }
+    case MMPR_ODE_TAYLOR: {  // first-order closure at the enriched statistic s = M + (S/2) f''(M), f'' = 0
+      const double m = y[0], var = y[1];
+      const double s = add(m, mul(mul(0.5, var), 0.0));
+      const ModelCoeffs c = coeffs(model, m, s);
+      dy[0] = add(c.drift, mul(0.5, c.diff_dxx));
+      dy[1] = add(mul(add(mul(2.0, c.drift_dx), mul(c.diff_dx, c.diff_dx)), var), mul(c.diff, c.diff));
+      dy[2] = 0.0;
+      break;
+    }
+    case MMPR_ODE_ROTATOR_TAYLOR: {  // the rotator's enriched closure (models.py:299-306)
+      const double m = y[0], var = y[1];
+      double sm, cm;
+      sincos(m, &sm, &cm);
+      if (fabs(sm) < 1e-8 || fabs(cm) < 1e-8) return MMPR_COARSE_SINGULAR;
+      const double K = ode.p[0], sigma_sq = ode.p[1];
+      dy[0] = add(-sm, div(var, mul(2.0, sm)));
+      dy[1] = add(mul(mul(-2.0, add(sub(-K, cm), div(var, mul(2.0, cm)))), var), sigma_sq);
+      dy[2] = 0.0;
+      break;
+    }
+    case MMPR_ODE_BURGERS: {  // dM = 1/2, dS = -(2/sqrt(2 pi)) sqrt(max(S, 0)) + sigma^2
+      const double var = y[1];
+      const double v = (0.0 > var) ? 0.0 : var;  // Python max(var, 0.0)
+      dy[0] = 0.5;
+      dy[1] = add(mul(ode.p[1], __dsqrt_rn(v)), ode.p[0]);
+      dy[2] = 0.0;
+      break;
+    }
     default:
 #pragma unroll
       for (int i = 0; i < NV; ++i) dy[i] = __longlong_as_double(0x7ff8000000000000ULL);
   }
+  return 0;
 }
 
 template <int NV>
@@ -123,7 +155,7 @@ __device__ int integrate_euler_n(const mmpr_moment_ode &ode, const mmpr_model &m
   double k[NV];
   for (long long i = 0; i < n; ++i) {
     const double t = add(t0, mul((double)i, h));
-    ode_rhs<NV, OK, MK>(ode, model, t, y, k);
+    if (ode_rhs<NV, OK, MK>(ode, model, t, y, k)) return MMPR_COARSE_SINGULAR;
 #pragma unroll
     for (int v = 0; v < NV; ++v) y[v] = add(y[v], mul(h, k[v]));
   }
@@ -164,7 +196,7 @@ __device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &mode
   if (span == 0.0) return MMPR_STAT_OK;
   double t = t0;
   double k[7][NV];
-  ode_rhs<NV, OK, MK>(ode, model, t, y, k[0]);
+  if (ode_rhs<NV, OK, MK>(ode, model, t, y, k[0])) return MMPR_COARSE_SINGULAR;
   if (!all_finite<NV>(k[0])) return 1;
   double h;
   if (cfg.first_step > 0.0) {
@@ -196,7 +228,7 @@ __device__ int integrate_dp54(const mmpr_moment_ode &ode, const mmpr_model &mode
         }
         yi[v] = add(y[v], mul(h, acc));
       }
-      ode_rhs<NV, OK, MK>(ode, model, add(t, mul(c_dp_c[i], h)), yi, k[i]);
+      if (ode_rhs<NV, OK, MK>(ode, model, add(t, mul(c_dp_c[i], h)), yi, k[i])) return MMPR_COARSE_SINGULAR;
     }
     double y5[NV], err[NV], sc[NV];
 #pragma unroll
@@ -385,6 +417,9 @@ static int by_model(int mk, const typename L<NV, OK, 0>::Args &a) {
     case MMPR_MODEL_DOUBLE_WELL: return L<NV, OK, MMPR_MODEL_DOUBLE_WELL>::run(a);
     case MMPR_MODEL_CUBIC_MF: return L<NV, OK, MMPR_MODEL_CUBIC_MF>::run(a);
     case MMPR_MODEL_DW_MULT: return L<NV, OK, MMPR_MODEL_DW_MULT>::run(a);
+    case MMPR_MODEL_ROTATOR:
+      if (OK == MMPR_ODE_MULTIMODAL) return MMPR_ERR_UNSUPPORTED;  // mixture closure needs MEAN_OF_F
+      return L<NV, OK, MMPR_MODEL_ROTATOR>::run(a);
     default: return MMPR_ERR_UNSUPPORTED;
   }
 }
@@ -396,6 +431,9 @@ static int dispatch_coarse(int n_regions, int ok, int mk, const typename L<3, 1,
       case MMPR_ODE_UNIMODAL: return by_model<L, 3, MMPR_ODE_UNIMODAL>(mk, a);
       case MMPR_ODE_PERTURBED_OU: return L<3, MMPR_ODE_PERTURBED_OU, 0>::run(a);
       case MMPR_ODE_GAUSSIAN_CUBIC: return L<3, MMPR_ODE_GAUSSIAN_CUBIC, 0>::run(a);
+      case MMPR_ODE_TAYLOR: return by_model<L, 3, MMPR_ODE_TAYLOR>(mk, a);
+      case MMPR_ODE_ROTATOR_TAYLOR: return L<3, MMPR_ODE_ROTATOR_TAYLOR, 0>::run(a);
+      case MMPR_ODE_BURGERS: return L<3, MMPR_ODE_BURGERS, 0>::run(a);
       case MMPR_ODE_MULTIMODAL: return by_model<L, 3, MMPR_ODE_MULTIMODAL>(mk, a);
       default: return MMPR_ERR_UNSUPPORTED;
     }
@@ -452,7 +490,7 @@ using namespace mmpr;
 static int check_ode(const mmpr_moment_ode *ode, const mmpr_integrator *integ) {
   if (!ode || !integ) return MMPR_ERR_ARG;
   if (ode->n_regions < 1 || ode->n_regions > MMPR_MAX_REGIONS) return MMPR_ERR_ARG;
-  if (ode->kind < MMPR_ODE_UNIMODAL || ode->kind > MMPR_ODE_GAUSSIAN_CUBIC) return MMPR_ERR_UNSUPPORTED;
+  if (ode->kind < MMPR_ODE_UNIMODAL || ode->kind > MMPR_ODE_BURGERS) return MMPR_ERR_UNSUPPORTED;
   if (ode->kind != MMPR_ODE_MULTIMODAL && ode->n_regions != 1) return MMPR_ERR_ARG;
   if (integ->kind == MMPR_INTEG_EULER) {
     if (!(integ->dt > 0.0)) return MMPR_ERR_ARG;

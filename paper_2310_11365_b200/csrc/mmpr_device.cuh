@@ -102,6 +102,18 @@ __host__ __device__ __forceinline__ bool constant_diffusion(int kind) {
 __device__ inline ModelCoeffs coeffs(const mmpr_model &m, double x, double s) {
   const double *p = m.p;
   ModelCoeffs c;
+  if (m.kind == MMPR_MODEL_ROTATOR) {
+    // point statistic of a mass at x: (S, C) = (sin x, cos x) (models.py:86-96)
+    // a = K (cos x S - sin x C) - sin x, a_x = K (-sin x S - cos x C) - cos x
+    double sx, cx;
+    sincos(x, &sx, &cx);
+    c.drift = sub(mul(p[0], sub(mul(cx, sx), mul(sx, cx))), sx);
+    c.drift_dx = sub(mul(p[0], sub(mul(-sx, sx), mul(cx, cx))), cx);
+    c.diff = p[1];
+    c.diff_dx = 0.0;
+    c.diff_dxx = 0.0;
+    return c;
+  }
   c.drift = drift(m, x, s);
   c.diff = diffusion(m, x, s);
   switch (m.kind) {

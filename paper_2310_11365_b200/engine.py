@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _lib, kernels
 from ._device import device, require_cuda, torch
-from .errors import ConfigError, DegenerateMatch, IntegrationFailure, NumericalBlowup
+from .errors import ConfigError, DegenerateMatch, IntegrationFailure, NumericalBlowup, SingularityError
 from .models import InitialDistribution, McKeanVlasovModel, device_model
 from .moments import MomentODE, device_ode
 from .noise import fill_normals, row_pitch, slice_noise, step_keys
@@ -402,10 +402,16 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
     return trace
 
 
+def _coarse_error(status: int, n: int, k: int):
+    if status == _lib.STAT_SINGULAR:
+        return SingularityError(f"moment closure singular on slice {n} (iteration {k})")
+    return IntegrationFailure(f"coarse integration failed on slice {n} (iteration {k})")
+
+
 def _raise_first_error(h, N: int, K: int, I: int) -> None:
     for n in range(N):
         if h["coarse_status"][0, n] != _lib.STAT_OK:
-            raise IntegrationFailure(f"coarse integration failed on slice {n} (iteration 0)")
+            raise _coarse_error(int(h["coarse_status"][0, n]), n, 0)
     for k in range(K):
         bad = h["bad"][k]
         for n in range(N):
@@ -414,7 +420,7 @@ def _raise_first_error(h, N: int, K: int, I: int) -> None:
                                       slice_index=n, step_index=int(bad[n]))
         for n in range(N):
             if h["coarse_status"][k + 1, n] != _lib.STAT_OK:
-                raise IntegrationFailure(f"coarse integration failed on slice {n} (iteration {k + 1})")
+                raise _coarse_error(int(h["coarse_status"][k + 1, n]), n, k + 1)
             region = int(h["match_status"][k + 1, n])
             if region >= 0:
                 var_t = h["macro"][k + 1, n + 1, I + region]

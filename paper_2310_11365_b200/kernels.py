@@ -45,6 +45,18 @@ def fine_sweep(model: _lib.Model, x_in, x_out, t0, steps: int, dt: float, xi, ba
         raise ValueError("xi row pitch must be even and >= P")
     if bad_step.dtype != torch.int32 or bad_step.numel() < E:
         raise ValueError("bad_step must be int32 (E,)")
+    if model.stat_kind != _lib.STAT_MEAN_OF_F:  # plane rotator / Burgers
+        if final_mean is not None:
+            raise ValueError("final_mean is defined for MEAN_OF_F models only")
+        nbytes = ctypes.c_uint64(0)
+        args = (ctypes.byref(model), int(E), int(P), int(steps), float(dt), float(math.sqrt(dt)), x_in.data_ptr(),
+                int(in_pitch), x_out.data_ptr(), int(out_pitch), xi.data_ptr(), int(xi.stride(0)), int(pitch),
+                bad_step.data_ptr())
+        _lib.call("mmpr_fine_sweep_stepwise", *args, None, ctypes.byref(nbytes), _lib.stream_handle(stream))
+        work = torch.empty(max(1, nbytes.value), dtype=torch.uint8, device=x_in.device)
+        _lib.call("mmpr_fine_sweep_stepwise", *args, work.data_ptr(), ctypes.byref(nbytes),
+                  _lib.stream_handle(stream))
+        return
     _lib.call("mmpr_fine_sweep", ctypes.byref(model), int(E), int(P), int(steps), float(dt),
               float(math.sqrt(dt)), t0.data_ptr(), x_in.data_ptr(), int(in_pitch), x_out.data_ptr(),
               int(out_pitch), xi.data_ptr(), int(xi.stride(0)), int(pitch), bad_step.data_ptr(),

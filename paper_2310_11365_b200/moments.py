@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib, kernels
 from ._device import device, torch
-from .errors import IntegrationFailure, McPararealError
+from .errors import IntegrationFailure, McPararealError, SingularityError
 from .models import (McKeanVlasovModel, PerturbedOUSpec, StatisticKind, device_model, mixture_statistic,
                      point_statistic)
 from .rk54 import EulerConfig, IntegratorConfig, integrator_descriptor
@@ -150,7 +150,10 @@ def multimodal_rhs(model: McKeanVlasovModel, partition: RegionPartition, potenti
 
 
 def taylor_enriched_rhs(model: McKeanVlasovModel) -> MomentODE:
-    """Host-only variance-enriched closure (outside the device path)."""
+    """Variance-enriched single-region closure (moments.py:71-108): the
+    model's own closure when it has one (plane rotator: ODE_ROTATOR_TAYLOR),
+    else the first-order closure at s = f(M) + (S/2) f''(M) (ODE_TAYLOR)."""
+    desc_m = getattr(model, "descriptor", None)
     if model.enriched_moment_rhs is not None:
         custom = model.enriched_moment_rhs
 
@@ -159,7 +162,10 @@ def taylor_enriched_rhs(model: McKeanVlasovModel) -> MomentODE:
             d_mean, d_var = custom(m, var, t)
             return np.array([float(d_mean), float(d_var), 0.0])
 
-        return MomentODE(rhs, 1, "taylor")
+        desc = None
+        if desc_m is not None and desc_m.kind == _lib.MODEL_ROTATOR:
+            desc = _ode(_lib.ODE_ROTATOR_TAYLOR, 1, (desc_m.p[0], desc_m.p[3]))
+        return MomentODE(rhs, 1, "taylor", descriptor=desc)
     if model.statistic_kind is not StatisticKind.MEAN_OF_F:
         raise ValueError(f"model {model.name!r} has no enriched closure and no mean-of-f statistic to enrich")
 
@@ -172,18 +178,22 @@ def taylor_enriched_rhs(model: McKeanVlasovModel) -> MomentODE:
         b_x = float(model.diffusion_dx(m, s, t))
         return np.array([d_mean, (2.0 * float(model.drift_dx(m, s, t)) + b_x * b_x) * var + b * b, 0.0])
 
-    return MomentODE(rhs, 1, "taylor")
+    desc = None
+    if desc_m is not None and model.f is None and model.f_dd is None:
+        desc = _ode(_lib.ODE_TAYLOR, 1)
+    return MomentODE(rhs, 1, "taylor", descriptor=desc, model=model if desc is not None else None)
 
 
 def burgers_rhs(sigma: float) -> MomentODE:
-    """Host-only rank-interaction moment model (outside the device path)."""
+    """Rank-interaction moment model (moments.py:128-142): dM = 1/2,
+    dS = -(2/sqrt(2 pi)) sqrt(max(S, 0)) + sigma^2 (device ODE_BURGERS)."""
     sig_sq = float(sigma) ** 2
 
     def rhs(t, y):
         _, var, _ = y
         return np.array([0.5, -(2.0 / SQRT_2PI) * math.sqrt(max(var, 0.0)) + sig_sq, 0.0])
 
-    return MomentODE(rhs, 1, "first-order")
+    return MomentODE(rhs, 1, "first-order", descriptor=_ode(_lib.ODE_BURGERS, 1, (sig_sq, -(2.0 / SQRT_2PI))))
 
 
 def integrate_macro(ode: MomentODE, state: MacroState, t0: float, t1: float,
@@ -200,6 +210,9 @@ def integrate_macro(ode: MomentODE, state: MacroState, t0: float, t1: float,
     ta = torch.tensor([float(t0)], dtype=torch.float64, device=device())
     tb = torch.tensor([float(t1)], dtype=torch.float64, device=device())
     kernels.integrate_macro(ode_d, model_d, integrator_descriptor(cfg), ta, tb, y, out, status)
-    if int(status.cpu()[0]) != _lib.STAT_OK:
+    st = int(status.cpu()[0])
+    if st == _lib.STAT_SINGULAR:
+        raise SingularityError(f"moment closure singular on [{t0}, {t1}]")
+    if st != _lib.STAT_OK:
         raise IntegrationFailure(f"coarse integration failed on [{t0}, {t1}]")
     return unpack_state(out.cpu().numpy()[0], ode.n_regions)

@@ -286,6 +286,42 @@ def trace_fixture():
     return out
 
 
+def stats_fixture():
+    """ROTATOR_SUM and EMPIRICAL_CDF models: propagate_fine and the
+    statistics themselves, from the reference factories."""
+    out = {}
+    models = {"rotator": ref.make_plane_rotator(ref.PlaneRotatorSpec(K=0.5, kBT=0.1, wrap=True)),
+              "rotator_nowrap": ref.make_plane_rotator(ref.PlaneRotatorSpec(K=1.5, kBT=0.3, wrap=False)),
+              "burgers": ref.make_burgers(ref.BurgersSpec())}
+    for name, model in models.items():
+        for P, S, dt, n, t0 in [(1, 4, 1e-2, 0, 0.0), (7, 5, 1e-2, 2, 0.5), (1000, 20, 1e-3, 3, 0.3),
+                                (4099, 12, 2.0 ** -8, 1, 0.0)]:
+            plan = ref.NoisePlan(13)
+            x0 = ref.sample_initial(ref.InitialDistribution.normal(3.0, 1.5), plan, P)
+            x1 = ref.propagate_fine(model, x0, n, t0, ref.StepConfig(dt=dt, steps_per_slice=S), plan)
+            key = f"{name}_P{P}"
+            out[key + "_meta"] = np.array([P, S, dt, n, t0, 13.0])
+            out[key + "_x0"] = x0.positions
+            out[key + "_x1"] = x1.positions
+    # full mM runs (Euler coarse plugged in as for the BASELINE configs)
+    runs = {"rot_uni": (models["rotator"], ref.unimodal_rhs(models["rotator"])),
+            "rot_taylor": (models["rotator"], ref.taylor_enriched_rhs(models["rotator"])),
+            "burgers": (models["burgers"], ref.burgers_rhs(math.sqrt(0.2)))}
+    for name, (model, ode) in runs.items():
+        cfg = ref.PararealConfig(n_slices=6, iterations=3, slice_length=25 * 2.0 ** -8, particles=1000,
+                                 step=ref.StepConfig(dt=2.0 ** -8, steps_per_slice=25))
+        init = ref.InitialDistribution.normal(2.5, 0.04)
+        with euler_coarse(2.0 ** -6):
+            tr = ref.run_micro_macro(model, ode, init, cfg, ref.NoisePlan(21))
+        trace_to_arrays(tr, f"run_{name}_", out)
+    # statistics with ties and signed zeros (ranks are stable by index)
+    x = np.array([0.5, -0.0, 0.0, 0.5, -1.0, 0.0, 2.0, 0.5, -0.0])
+    out["cdf_x"] = x
+    out["cdf_s"] = ref.ensemble_statistic(models["burgers"], x)
+    out["rot_s"] = np.array(ref.ensemble_statistic(models["rotator"], x))
+    return out
+
+
 def report_to_arrays(rep, prefix, out):
     out[prefix + "scalars"] = np.array([rep.e_mean, rep.e_var, rep.e_wass, rep.normalized_mean, rep.normalized_var,
                                         rep.normalized_wass])
@@ -335,13 +371,15 @@ def main():
     np.savez_compressed(os.path.join(OUT, "coupling.npz"), **coupling_fixture())
     np.savez_compressed(os.path.join(OUT, "traces.npz"), **trace_fixture())
     np.savez_compressed(os.path.join(OUT, "metrics.npz"), **metrics_fixture())
+    np.savez_compressed(os.path.join(OUT, "stats.npz"), **stats_fixture())
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "metrics":
-        np.savez_compressed(os.path.join(OUT, "metrics.npz"), **metrics_fixture())
+    if len(sys.argv) > 1 and sys.argv[1] in ("metrics", "stats"):
+        fixture = {"metrics": metrics_fixture, "stats": stats_fixture}[sys.argv[1]]
+        np.savez_compressed(os.path.join(OUT, sys.argv[1] + ".npz"), **fixture())
     else:
         sys.exit(main())

@@ -67,9 +67,13 @@ def test_descriptors_follow_factory_closures():
 def test_models_without_descriptor_are_rejected():
     from paper_2310_11365_b200.models import device_model
     with pytest.raises(TypeError):
-        device_model(mm.make_plane_rotator(mm.PlaneRotatorSpec()))
-    with pytest.raises(TypeError):
-        mm.moments.device_ode(mm.burgers_rhs(0.4))
+        device_model(mm.make_linear(mm.LinearMcKVSpec(A=lambda t: -1.0 - t)))
+    with pytest.raises(TypeError):  # the closure of a closure-built model
+        mm.moments.device_ode(mm.taylor_enriched_rhs(mm.make_linear(mm.LinearMcKVSpec(A=lambda t: -t))))
+    # the ROTATOR_SUM / EMPIRICAL_CDF models now carry device descriptors
+    rot = device_model(mm.make_plane_rotator(mm.PlaneRotatorSpec(K=0.7, kBT=0.2)))
+    assert (rot.kind, rot.stat_kind, list(rot.p)[:4]) == (6, 2, [0.7, math.sqrt(0.4), 1.0, 0.4])
+    assert mm.moments.device_ode(mm.burgers_rhs(0.4))[0].kind == 7
 
 
 def test_partition_and_state_semantics():

@@ -211,3 +211,38 @@ def test_oracle_floor_matches_reference(golden):
     finals = [p[-1] for p in paths]
     assert O.statistical_floor(finals) == g["floor_raw"][0]
     assert np.array_equal(np.array(O.moment_spread(finals)), g["floor_spread"])
+
+
+# ---- ROTATOR_SUM / EMPIRICAL_CDF models (models.py:61-83, 286-334) -----------
+STAT_MODELS = {"rotator": lambda: O.model_rotator(0.5, 0.1, True),
+               "rotator_nowrap": lambda: O.model_rotator(1.5, 0.3, False),
+               "burgers": lambda: O.model_burgers(math.sqrt(0.2))}
+
+
+@pytest.mark.parametrize("name", sorted(STAT_MODELS))
+@pytest.mark.parametrize("P", [1, 7, 1000, 4099])
+def test_oracle_stat_models_propagate_fine(golden, name, P):
+    g = golden("stats")
+    Pm, S, dt, n, t0, seed = g[f"{name}_P{P}_meta"]
+    xi = O.slice_noise(int(seed), int(n), int(S), int(Pm))
+    got = O.propagate_fine(STAT_MODELS[name](), g[f"{name}_P{P}_x0"], int(n), t0, dt, int(S), xi)
+    assert np.array_equal(got, g[f"{name}_P{P}_x1"])
+
+
+def test_oracle_statistics(golden):
+    g = golden("stats")
+    assert np.array_equal(O.statistic(O.model_burgers(1.0), g["cdf_x"]), g["cdf_s"])
+    assert np.array_equal(np.array(O.statistic(O.model_rotator(0.5, 0.1), g["cdf_x"])), g["rot_s"])
+
+
+@pytest.mark.parametrize("name", ["rot_uni", "rot_taylor", "burgers"])
+def test_oracle_stat_model_runs(golden, name):
+    g = golden("stats")
+    om = O.model_burgers(math.sqrt(0.2)) if name == "burgers" else O.model_rotator(0.5, 0.1, True)
+    ode = {"rot_uni": O.ode_unimodal(om), "rot_taylor": O.ode_rotator_taylor(0.5, 0.1),
+           "burgers": O.ode_burgers(math.sqrt(0.2))}[name]
+    x0 = O.sample_normal_initial(21, 2.5, 0.04, 1000)
+    tr = O.run_micro_macro(om, ode, x0, 6, 3, 25 * 2.0 ** -8, 2.0 ** -8, 25, 21, integ=O.Euler(2.0 ** -6))
+    assert np.array_equal(tr.macro, g[f"run_{name}_macro"])
+    assert np.array_equal(tr.micro, g[f"run_{name}_micro"])
+    assert np.array_equal(np.array([[e for e in row] for row in tr.snapshots]), g[f"run_{name}_snap"])
