@@ -426,6 +426,10 @@ __device__ __noinline__ void general_parse8(uint32_t nf, uint32_t tt, int e, uin
   *exit_out = pos - NW_WORDS;
 }
 
+__device__ __noinline__ uint64_t successor_word(uint64_t i, uint64_t k0, uint64_t k1) {
+  return np::philox_word(i, k0, k1);
+}
+
 template <typename T>
 __device__ __forceinline__ T pick8(const T (&v)[NW_WORDS], int i) {
   T r = v[0];
@@ -471,7 +475,8 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
       const ulonglong2 z = zig[rw & 0xff];
       const double wi = __longlong_as_double((long long)z.y);
       const double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
-      x[i] = ((rw >> 8) & 1) ? -v : v;
+      // sign bit 8 of the word -> sign of the double (one LOP3 on the high half)
+      x[i] = __hiloint2double(__double2hiint(v) ^ (int)(((uint32_t)rw << 23) & 0x80000000u), __double2loint(v));
       nf |= (mant >= z.x ? 1u : 0u) << i;
     }
     // Rare words (~2.2%): wedge tests and tail starts, processed by the whole
@@ -503,8 +508,10 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
             const int layer = (int)(rw & 0xff);
             uint8_t res;
             if (layer != 0) {
+              // the last word's successor opens the next sub-chunk: computed
+              // out of line (hoisted, it cost 14% of the kernel's instructions)
               const uint64_t nx = (pos + 1 < 32 * NW_WORDS) ? s_words[pos + 1]
-                                  : np::philox_word(sub * 32 * NW_WORDS + 32 * NW_WORDS, k0, k1);
+                                  : successor_word(sub * 32 * NW_WORDS + 32 * NW_WORDS, k0, k1);
               const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
               const double wi = c_zig_wi[layer];
               double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi,
@@ -563,10 +570,16 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
     const int total = __shfl_sync(MMPR_FULL_MASK, incl, 31);
     carry = __shfl_sync(MMPR_FULL_MASK, ex, 31);
     const int64_t base = produced + incl - cnt;
+    if (O == 0xffu && base + NW_WORDS <= count) {  // common case (~84% of lanes): 8 consecutive outputs
+      double *dst = o + base;
 #pragma unroll
-    for (int i = 0; i < NW_WORDS; ++i) {
-      const int64_t idx = base + __popc(O & ((1u << i) - 1u));
-      if (((O >> i) & 1u) && idx < count) o[idx] = AFFINE ? add(loc, mul(scale, x[i])) : x[i];
+      for (int i = 0; i < NW_WORDS; ++i) dst[i] = AFFINE ? add(loc, mul(scale, x[i])) : x[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < NW_WORDS; ++i) {
+        const int64_t idx = base + __popc(O & ((1u << i) - 1u));
+        if (((O >> i) & 1u) && idx < count) o[idx] = AFFINE ? add(loc, mul(scale, x[i])) : x[i];
+      }
     }
     for (uint32_t rem = O & tt; rem; rem &= rem - 1) {  // rare: tail values overwrite
       const int i = __ffs(rem) - 1;
