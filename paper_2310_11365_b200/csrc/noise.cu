@@ -570,10 +570,14 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
     const int total = __shfl_sync(MMPR_FULL_MASK, incl, 31);
     carry = __shfl_sync(MMPR_FULL_MASK, ex, 31);
     const int64_t base = produced + incl - cnt;
-    if (O == 0xffu && base + NW_WORDS <= count) {  // common case (~84% of lanes): 8 consecutive outputs
-      double *dst = o + base;
+    if (produced + 32 * NW_WORDS <= count) {  // warp-uniform: no bound checks in this sub-chunk
+      double *dst = o + base;  // produced values are consecutive from base
 #pragma unroll
-      for (int i = 0; i < NW_WORDS; ++i) dst[i] = AFFINE ? add(loc, mul(scale, x[i])) : x[i];
+      for (int i = 0; i < NW_WORDS; ++i) {
+        const uint32_t take = (O >> i) & 1u;
+        if (take) *dst = AFFINE ? add(loc, mul(scale, x[i])) : x[i];
+        dst += take;
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < NW_WORDS; ++i) {
