@@ -152,6 +152,28 @@ template <int NV, int OK, int MK>
 __device__ int integrate_euler_n(const mmpr_moment_ode &ode, const mmpr_model &model, long long n, double h,
                                  double t0, double *y) {
   if (n == 0) return MMPR_STAT_OK;
+  if constexpr (OK == MMPR_ODE_UNIMODAL && MK == MMPR_MODEL_OU) {
+    // the OU closure's coefficients do not depend on the state: the same
+    // products the generic path forms every step, formed once
+    const double a = model.p[0], aE = model.p[1], B = model.p[2];
+    const double c0 = mul(0.5, 0.0);                    // 0.5 * b_xx
+    const double c1 = add(mul(2.0, a), mul(0.0, 0.0));  // 2 a_x + b_x^2
+    const double c2 = mul(B, B);                        // b^2
+    const double z = mul(h, 0.0);                       // h * dF (fractions are constant)
+    double m = y[0], v = y[1], f = y[2];
+#pragma unroll 2
+    for (long long i = 0; i < n; ++i) {
+      const double dm = add(add(mul(a, m), mul(aE, m)), c0);
+      const double dv = add(mul(c1, v), c2);
+      m = add(m, mul(h, dm));
+      v = add(v, mul(h, dv));
+      f = add(f, z);
+    }
+    y[0] = m;
+    y[1] = v;
+    y[2] = f;
+    return all_finite<NV>(y) ? MMPR_STAT_OK : 1;
+  }
   double k[NV];
   for (long long i = 0; i < n; ++i) {
     const double t = add(t0, mul((double)i, h));
