@@ -201,6 +201,17 @@ int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_t particles
                     int64_t xi_row_pitch, int32_t *bad_step, double *final_mean,
                     void *stream);
 
+/* mmpr_fine_sweep followed by the single-region restriction of every
+ * slice-end ensemble (restrict(F_n), engine.py:205), fused into the sweep:
+ * stats + 3*n = [np.mean, np.var, 1.0] of x_out row n, counts[n] = P
+ * (counts may be NULL).  Written only for slices without a blow-up. */
+int mmpr_fine_sweep_restrict(const mmpr_model *model, int32_t n_slices, int64_t particles,
+                             int32_t steps, double dt, double sqrt_dt, const double *t0,
+                             const double *x_in, int64_t in_pitch, double *x_out,
+                             int64_t out_pitch, const double *xi, int64_t xi_slice_pitch,
+                             int64_t xi_row_pitch, int32_t *bad_step, double *stats,
+                             int64_t *counts, void *stream);
+
 /* Fine sweep for the ROTATOR_SUM / EMPIRICAL_CDF models (plane rotator,
  * Burgers), same buffers and status convention as mmpr_fine_sweep (no
  * final_mean).  Step-synchronous: per EM step one statistic pass (pairwise

@@ -296,16 +296,45 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
     }
   }
 
+  if (active) {
+    double *xo = p.x_out + (int64_t)slice * p.out_pitch;
+#pragma unroll
+    for (int m = 0; m < PPT; ++m)
+      if (m < cnt) xo[off + j8 + 8 * m] = x[m];
+    if (HAS_TAIL && j8 < tail) xo[tail_off + j8] = xt;
+  }
+  // Fused restriction of the slice-end ensemble (restrict, coupling.py:26;
+  // np.mean / two-pass np.var): the mean is the last step's statistic, the
+  // variance one more pass of the same tree over (x - mean)^2 from registers.
+  // first_bad is cluster-uniform, so every CTA of the cluster takes part.
+  double var = 0.0;
+  const bool want_stats = p.stats != nullptr && active && first_bad == MMPR_STAT_OK;
+  if (want_stats) {
+#pragma unroll
+    for (int m = 0; m < PPT; ++m) {
+      const double d = sub(x[m], s);
+      x[m] = mul(d, d);
+    }
+    if (HAS_TAIL) {
+      const double d = sub(xt, s);
+      xt = mul(d, d);
+    }
+    int bad2 = 0;
+    reduce(p.S + 1, -1, var, bad2);
+  }
+
   if (p.ctas > 1) cluster_sync_all();  // no peer may still be writing into this CTA
   if (!active) return;
-  double *xo = p.x_out + (int64_t)slice * p.out_pitch;
-#pragma unroll
-  for (int m = 0; m < PPT; ++m)
-    if (m < cnt) xo[off + j8 + 8 * m] = x[m];
-  if (HAS_TAIL && j8 < tail) xo[tail_off + j8] = xt;
   if (tid == 0 && rank == 0) {
     p.bad_step[slice] = first_bad;
     if (p.final_mean) p.final_mean[slice] = s;
+    if (want_stats) {
+      double *st = p.stats + 3 * (int64_t)slice;
+      st[0] = s;
+      st[1] = p.P == 1 ? 0.0 : var;  // one member: S = 0 (particles.py:196-199)
+      st[2] = div((double)p.P, (double)p.P);
+      if (p.counts) p.counts[slice] = p.P;
+    }
   }
 }
 
@@ -476,11 +505,11 @@ static int dispatch_tail(const FineParams &p, const FineGeometry &g, cudaStream_
 
 using namespace mmpr;
 
-extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_t particles, int32_t steps,
-                               double dt, double sqrt_dt, const double *t0, const double *x_in,
-                               int64_t in_pitch, double *x_out, int64_t out_pitch, const double *xi,
-                               int64_t xi_slice_pitch, int64_t xi_row_pitch, int32_t *bad_step,
-                               double *final_mean, void *stream) {
+static int fine_sweep_impl(const mmpr_model *model, int32_t n_slices, int64_t particles, int32_t steps,
+                           double dt, double sqrt_dt, const double *t0, const double *x_in, int64_t in_pitch,
+                           double *x_out, int64_t out_pitch, const double *xi, int64_t xi_slice_pitch,
+                           int64_t xi_row_pitch, int32_t *bad_step, double *final_mean, double *stats,
+                           int64_t *counts, void *stream) {
   if (!model || n_slices < 0 || particles < 1 || steps < 0 || !x_in || !x_out || !bad_step || !t0)
     return MMPR_ERR_ARG;
   if (n_slices == 0) return MMPR_OK;
@@ -518,6 +547,8 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
   p.xi_row_pitch = xi_row_pitch;
   p.bad_step = bad_step;
   p.final_mean = final_mean;
+  p.stats = stats;
+  p.counts = counts;
   cudaStream_t s = (cudaStream_t)stream;
   if (use_grid) return fine_grid_sweep(p, s);
   p.D = g.D;
@@ -531,6 +562,25 @@ extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_
   if (g.ppt <= 8) return dispatch_tail<8>(p, g, s);
   if (g.ppt <= 13) return dispatch_tail<13>(p, g, s);
   return dispatch_tail<16>(p, g, s);
+}
+
+extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_t particles, int32_t steps,
+                               double dt, double sqrt_dt, const double *t0, const double *x_in,
+                               int64_t in_pitch, double *x_out, int64_t out_pitch, const double *xi,
+                               int64_t xi_slice_pitch, int64_t xi_row_pitch, int32_t *bad_step,
+                               double *final_mean, void *stream) {
+  return fine_sweep_impl(model, n_slices, particles, steps, dt, sqrt_dt, t0, x_in, in_pitch, x_out, out_pitch, xi,
+                         xi_slice_pitch, xi_row_pitch, bad_step, final_mean, nullptr, nullptr, stream);
+}
+
+extern "C" int mmpr_fine_sweep_restrict(const mmpr_model *model, int32_t n_slices, int64_t particles,
+                                        int32_t steps, double dt, double sqrt_dt, const double *t0,
+                                        const double *x_in, int64_t in_pitch, double *x_out, int64_t out_pitch,
+                                        const double *xi, int64_t xi_slice_pitch, int64_t xi_row_pitch,
+                                        int32_t *bad_step, double *stats, int64_t *counts, void *stream) {
+  if (!stats) return MMPR_ERR_ARG;
+  return fine_sweep_impl(model, n_slices, particles, steps, dt, sqrt_dt, t0, x_in, in_pitch, x_out, out_pitch, xi,
+                         xi_slice_pitch, xi_row_pitch, bad_step, nullptr, stats, counts, stream);
 }
 
 extern "C" int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_out, int32_t *ctas_out) {

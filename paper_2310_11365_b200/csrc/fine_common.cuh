@@ -27,6 +27,8 @@ struct FineParams {
   int64_t xi_slice_pitch, xi_row_pitch;
   int32_t *bad_step;
   double *final_mean;
+  double *stats;      // optional single-region restriction of x_out: [mean, var, fraction] per slice
+  int64_t *counts;    // optional member counts (= P) per slice
   int D;              // tree depth (2^D leaf slots)
   int slots_per_cta;  // 4 * warps per CTA
   int ctas;           // CTAs per slice (cluster size)

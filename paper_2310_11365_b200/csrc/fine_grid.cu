@@ -347,9 +347,33 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
     for (int m = 0; m < PPT; ++m)
       if (m < cnt) xo[off + j8 + 8 * m] = x[m];
     if (HAS_TAIL && j8 < tail) xo[off + 8 * cnt + j8] = xt;
+    // fused single-region restriction (see fine.cu): one more team reduction
+    // of (x - mean)^2; first_bad is team-uniform
+    double var = 0.0;
+    const bool want_stats = p.stats != nullptr && first_bad == MMPR_STAT_OK;
+    if (want_stats) {
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) {
+        const double d = sub(x[m], s);
+        x[m] = mul(d, d);
+      }
+      if (HAS_TAIL) {
+        const double d = sub(xt, s);
+        xt = mul(d, d);
+      }
+      int bad2 = 0;
+      reduce(-1, var, bad2);
+    }
     if (tid == 0 && rank == 0) {
       p.bad_step[slice] = first_bad;
       if (p.final_mean) p.final_mean[slice] = s;
+      if (want_stats) {
+        double *st = p.stats + 3 * (int64_t)slice;
+        st[0] = s;
+        st[1] = p.P == 1 ? 0.0 : var;
+        st[2] = div((double)p.P, (double)p.P);
+        if (p.counts) p.counts[slice] = p.P;
+      }
     }
   }
 }

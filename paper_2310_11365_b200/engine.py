@@ -228,6 +228,8 @@ class _RunPlan:
         self.times = tuple(cfg.t_start + n * cfg.slice_length for n in range(N + 1))
         self.times_d = torch.tensor(self.times, dtype=torch.float64, device=device())
         self.ws = _Workspace(K, N, P, S, I, cfg.retain_snapshots, noise_slices=N if injected else None)
+        # single-region restriction of the fine outputs fused into the sweep
+        self.fused_restrict = I == 1 and model_d.stat_kind == _lib.STAT_MEAN_OF_F
         self.batch = self.ws.noise_slices
         self.graph = None
         self.launches_per_run = 0
@@ -268,12 +270,18 @@ class _RunPlan:
                 slice_noise(self.plan.master_seed, a, nb, S, self.P, k, self.plan.fresh, out=ws.xi[:nb])
                 timer.stop("noise", ev)
             ev = timer.start()
-            kernels.fine_sweep(self.model_d, cur[a:a + nb], ws.fine[a:a + nb], self.times_d[a:a + nb], S,
-                               self.cfg.step.dt, ws.xi[:nb], ws.bad[k][a:a + nb])
+            if self.fused_restrict:  # R(F_n) computed by the sweep from registers
+                kernels.fine_sweep(self.model_d, cur[a:a + nb], ws.fine[a:a + nb], self.times_d[a:a + nb], S,
+                                   self.cfg.step.dt, ws.xi[:nb], ws.bad[k][a:a + nb],
+                                   stats=ws.fine_stats[k][a:a + nb], counts=ws.fine_counts[k][a:a + nb])
+            else:
+                kernels.fine_sweep(self.model_d, cur[a:a + nb], ws.fine[a:a + nb], self.times_d[a:a + nb], S,
+                                   self.cfg.step.dt, ws.xi[:nb], ws.bad[k][a:a + nb])
             timer.stop("fine", ev)
-        ev = timer.start()
-        kernels.restrict(part_d, ws.fine, ws.fine_stats[k], ws.fine_counts[k], ws.scratch)
-        timer.stop("restrict", ev)
+        if not self.fused_restrict:
+            ev = timer.start()
+            kernels.restrict(part_d, ws.fine, ws.fine_stats[k], ws.fine_counts[k], ws.scratch)
+            timer.stop("restrict", ev)
         ev = timer.start()
         kernels.coarse_row(self.ode_d, self.ode_model_d, self.integ_d, self.times_d, k + 1, ws.rho0,
                            ws.fine_stats[k], ws.cache[k], ws.macro[k + 1], ws.cache[k + 1], ws.raw[k],

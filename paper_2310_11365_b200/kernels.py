@@ -28,9 +28,11 @@ def _rows(t, name):
 
 
 def fine_sweep(model: _lib.Model, x_in, x_out, t0, steps: int, dt: float, xi, bad_step, final_mean=None,
-               stream=None) -> None:
+               stats=None, counts=None, stream=None) -> None:
     """EM over ``steps`` steps for every row of x_in (E, P) -> x_out (E, P).
-    xi: (E, steps, pitch) increments; t0: (E,) float64; bad_step: (E,) int32."""
+    xi: (E, steps, pitch) increments; t0: (E,) float64; bad_step: (E,) int32.
+    stats (E, 3) / counts (E, 1): single-region restriction of x_out fused
+    into the sweep (MEAN_OF_F models)."""
     require_cuda()
     E, P = x_in.shape
     in_pitch = _rows(x_in, "x_in")
@@ -56,6 +58,19 @@ def fine_sweep(model: _lib.Model, x_in, x_out, t0, steps: int, dt: float, xi, ba
         work = torch.empty(max(1, nbytes.value), dtype=torch.uint8, device=x_in.device)
         _lib.call("mmpr_fine_sweep_stepwise", *args, work.data_ptr(), ctypes.byref(nbytes),
                   _lib.stream_handle(stream))
+        if stats is not None:
+            restrict(_single_region(), x_out, stats, counts)
+        return
+    if stats is not None:
+        _f64(stats, "stats")
+        if stats.numel() < 3 * E or not stats.is_contiguous():
+            raise ValueError("stats must be contiguous float64 (E, 3)")
+        if counts is not None and (counts.dtype != torch.int64 or counts.numel() < E):
+            raise ValueError("counts must be int64 (E, 1)")
+        _lib.call("mmpr_fine_sweep_restrict", ctypes.byref(model), int(E), int(P), int(steps), float(dt),
+                  float(math.sqrt(dt)), t0.data_ptr(), x_in.data_ptr(), int(in_pitch), x_out.data_ptr(),
+                  int(out_pitch), xi.data_ptr(), int(xi.stride(0)), int(pitch), bad_step.data_ptr(),
+                  stats.data_ptr(), _lib.ptr(counts), _lib.stream_handle(stream))
         return
     _lib.call("mmpr_fine_sweep", ctypes.byref(model), int(E), int(P), int(steps), float(dt),
               float(math.sqrt(dt)), t0.data_ptr(), x_in.data_ptr(), int(in_pitch), x_out.data_ptr(),
@@ -166,6 +181,12 @@ def mean_abs_diff(a, b, out=None, stream=None):
     _lib.call("mmpr_mean_abs_diff", int(R), int(P), a.data_ptr(), _rows(a, "a"), b.data_ptr(), _rows(b, "b"),
               out.data_ptr(), _lib.stream_handle(stream))
     return out
+
+
+def _single_region() -> _lib.Partition:
+    d = _lib.Partition()
+    d.n_regions = 1
+    return d
 
 
 def noise_buffer(n_slices: int, steps: int, P: int):

@@ -266,3 +266,34 @@ def test_grid_variant_blowup(mm, monkeypatch):
     out = mm.propagate_fine(mm.make_perturbed_ou(mm.PerturbedOUSpec()), mm.ParticleEnsemble(np.ones(20_000)), 0,
                             0.0, mm.StepConfig(1e-3, 4), mm.NoisePlan(0), increments=np.zeros((4, 20_000)))
     assert np.isfinite(out.positions).all()
+
+
+@pytest.mark.parametrize("P,grid", [(1, False), (7, False), (1000, False), (1001, False), (100_000, False),
+                                    (200_003, False), (100_000, True), (1 << 20, False)])
+def test_fused_restriction_equals_restrict(mm, monkeypatch, P, grid):
+    """mmpr_fine_sweep_restrict: the stats the sweep computes from registers
+    equal restrict() of its output bit for bit (np.mean / np.var)."""
+    from paper_2310_11365_b200 import kernels
+    import torch
+    if grid:
+        monkeypatch.setenv("MMPR_FINE_FORCE_GRID", "1")
+    N, S = 3, 5
+    rng = np.random.default_rng(P)
+    x = torch.from_numpy(rng.normal(0.5, 1.0, (N, P))).cuda()
+    xi = kernels.noise_buffer(N, S, P)
+    xi[:, :, :P] = torch.from_numpy(rng.standard_normal((N, S, P))).cuda()
+    t0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+    out = torch.empty_like(x)
+    bad = torch.empty(N, dtype=torch.int32, device="cuda")
+    stats = torch.empty((N, 3), dtype=torch.float64, device="cuda")
+    counts = torch.empty((N, 1), dtype=torch.int64, device="cuda")
+    model = GPU_MODELS["double_well"](mm).descriptor
+    kernels.fine_sweep(model, x, out, t0, S, 1e-3, xi, bad, stats=stats, counts=counts)
+    ref_stats = torch.empty_like(stats)
+    ref_counts = torch.empty_like(counts)
+    kernels.restrict(mm.SINGLE_REGION.descriptor(), out, ref_stats, ref_counts)
+    assert torch.equal(stats, ref_stats)
+    assert torch.equal(counts, ref_counts)
+    plain = torch.empty_like(x)
+    kernels.fine_sweep(model, x, plain, t0, S, 1e-3, xi, bad)
+    assert torch.equal(plain, out)
