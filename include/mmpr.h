@@ -253,6 +253,17 @@ int mmpr_match(const mmpr_partition *part, int32_t n_ens, int64_t particles,
                const double *x_src, int64_t src_pitch, double *x_out, int64_t out_pitch,
                int32_t policy, int32_t *status, int32_t *clamped, void *stream);
 
+/* Single-region match followed by the restriction of the matched ensembles,
+ * fused (engine.py:232-238: match then micro_stats = restrict): arguments of
+ * mmpr_match for a one-region partition, plus stats + 3*e = [np.mean, np.var,
+ * 1.0] of x_out row e and counts[e] = P (counts may be NULL). */
+int mmpr_match_restrict(int32_t n_ens, int64_t particles, const double *targets,
+                        int64_t tgt_stride, const double *cur_stats, int64_t cur_stride,
+                        const int64_t *cur_counts, int64_t cnt_stride, const double *x_src,
+                        int64_t src_pitch, double *x_out, int64_t out_pitch, int32_t policy,
+                        int32_t *status, int32_t *clamped, double *stats, int64_t *counts,
+                        void *stream);
+
 /* ------------------------------------------------------------------ */
 /* Coarse propagator and Parareal correction (moments.py:195-203,      */
 /* engine.py:170-236), one warp, no host round-trip                    */

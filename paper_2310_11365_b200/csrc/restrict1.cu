@@ -30,9 +30,23 @@ struct Restrict1Params {
   int D;
   int slots_per_cta;
   int ctas;
+  // match prologue (MATCH kernels): x_out = match(target, x) then restrict(x_out)
+  const double *targets;
+  int64_t tgt_stride;
+  const double *cur;
+  int64_t cur_stride;
+  const int64_t *cur_counts;
+  int64_t cnt_stride;
+  double *x_out;
+  int64_t out_pitch;
+  int policy;  // 0 raise, 1 collapse
+  int32_t *status;
+  int32_t *clamped;
 };
 
-template <int PPT, bool HAS_TAIL, bool PADDED>
+enum { R1_KEEP = 0, R1_SET = 1, R1_AFFINE = 2 };
+
+template <int PPT, bool HAS_TAIL, bool PADDED, bool MATCH>
 __global__ void __launch_bounds__(1024, 1) restrict1_kernel(const Restrict1Params p) {
   using PartT = Part<PADDED>;
   __shared__ PartT s_wp[32];
@@ -57,6 +71,47 @@ __global__ void __launch_bounds__(1024, 1) restrict1_kernel(const Restrict1Param
 #pragma unroll
   for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? xs[off + j8 + 8 * m] : 0.0;
   if (HAS_TAIL && j8 < tail) xt = xs[off + 8 * cnt + j8];
+  if constexpr (MATCH) {
+    // single-region match (coupling.py:32-95; same rules as match_kernel in
+    // coupling.cu), evaluated redundantly by every thread from broadcast loads
+    const double *tg = p.targets + (int64_t)e * p.tgt_stride;
+    const double *cs = p.cur + (int64_t)e * p.cur_stride;
+    const int64_t cn = p.cur_counts[(int64_t)e * p.cnt_stride];
+    int mode = R1_KEEP, status = MMPR_STAT_OK, clamped = 0;
+    double scale = 1.0, mc = 0.0, mu = 0.0;
+    if (cn != 0) {
+      mu = tg[0];
+      double var_t = tg[1];
+      if (var_t < 0.0) {
+        clamped = 1;
+        var_t = 0.0;
+      }
+      mc = cs[0];
+      const double cur_var = cs[1];
+      if (cur_var == 0.0) {
+        if (var_t > 0.0 && p.policy == 0) status = 0;
+        mode = R1_SET;
+      } else {
+        scale = __dsqrt_rn(div(var_t, cur_var));
+        if (!(scale == 1.0 && mu == mc)) mode = R1_AFFINE;  // exact identity keeps bits
+      }
+    }
+    auto apply = [&](double v) {
+      return mode == R1_SET ? mu : (mode == R1_AFFINE ? add(mul(scale, sub(v, mc)), mu) : v);
+    };
+#pragma unroll
+    for (int m = 0; m < PPT; ++m) x[m] = apply(x[m]);
+    if (HAS_TAIL) xt = apply(xt);
+    double *xo = p.x_out + (int64_t)e * p.out_pitch;
+#pragma unroll
+    for (int m = 0; m < PPT; ++m)
+      if (m < cnt) xo[off + j8 + 8 * m] = x[m];
+    if (HAS_TAIL && j8 < tail) xo[off + 8 * cnt + j8] = xt;
+    if (rank == 0 && tid == 0) {
+      p.status[e] = status;
+      if (p.clamped) p.clamped[e] = clamped;
+    }
+  }
   // peers' shared memory is written below: every CTA of the cluster must run
   if (p.ctas > 1) cluster_sync_all();
 
@@ -133,6 +188,57 @@ __global__ void __launch_bounds__(1024, 1) restrict1_kernel(const Restrict1Param
 }
 
 template <void (*KERN)(const Restrict1Params)>
+static int launch_r1(const Restrict1Params &p, int n_ens, int threads, cudaStream_t stream);
+
+// cluster geometry of one particle count (cached per host thread)
+struct R1Geometry {
+  int D, spc, ctas, ppt;
+  bool padded;
+};
+
+static const R1Geometry &r1_geometry(int64_t P) {
+  thread_local int64_t last_P = -1;
+  thread_local R1Geometry g;
+  if (P != last_P) {
+    const int D = pw_depth(P);
+    const int64_t nslots = int64_t(1) << D;
+    int64_t max_leaf = 0;
+    bool empty = false;
+    for (int64_t s = 0; s < nslots; ++s) {
+      int64_t o, l;
+      pw_leaf(P, D, s, &o, &l);
+      if (l > max_leaf) max_leaf = l;
+      empty |= l == 0;
+    }
+    const int spc = nslots < 128 ? (nslots < 4 ? 4 : (int)nslots) : 128;
+    g.D = D;
+    g.spc = spc;
+    g.ctas = nslots <= spc ? 1 : (int)(nslots / spc);
+    g.ppt = (int)((max_leaf + 7) / 8);
+    g.padded = empty || nslots < spc;
+    last_P = P;
+  }
+  return g;
+}
+
+template <bool MATCH>
+static int launch_r1_shape(Restrict1Params p, int n_ens, cudaStream_t stream) {
+  const R1Geometry &g = r1_geometry(p.P);
+  if (g.ctas > FS_MAX_CLUSTER || g.ppt > 16) return MMPR_ERR_UNSUPPORTED;
+  p.D = g.D;
+  p.slots_per_cta = g.spc;
+  p.ctas = g.ctas;
+  const int threads = g.spc * 8;
+  const bool tail = (p.P % 8) != 0;
+  if (g.padded) {
+    if (tail) return launch_r1<restrict1_kernel<16, true, true, MATCH>>(p, n_ens, threads, stream);
+    return launch_r1<restrict1_kernel<16, false, true, MATCH>>(p, n_ens, threads, stream);
+  }
+  if (tail) return launch_r1<restrict1_kernel<16, true, false, MATCH>>(p, n_ens, threads, stream);
+  return launch_r1<restrict1_kernel<16, false, false, MATCH>>(p, n_ens, threads, stream);
+}
+
+template <void (*KERN)(const Restrict1Params)>
 static int launch_r1(const Restrict1Params &p, int n_ens, int threads, cudaStream_t stream) {
   static bool configured = false;
   cudaError_t err;
@@ -161,47 +267,52 @@ static int launch_r1(const Restrict1Params &p, int n_ens, int threads, cudaStrea
 // (the caller then uses the one-CTA-per-ensemble kernel).
 int restrict_single_region(int n_ens, int64_t P, const double *x, int64_t pitch, double *stats, int64_t *counts,
                            cudaStream_t stream) {
-  // geometry of the last particle count (fixed within a run)
-  thread_local int64_t last_P = -1;
-  thread_local int g_D, g_spc, g_ctas, g_ppt;
-  thread_local bool g_padded;
-  if (P != last_P) {
-    const int D = pw_depth(P);
-    const int64_t nslots = int64_t(1) << D;
-    int64_t max_leaf = 0;
-    bool empty = false;
-    for (int64_t s = 0; s < nslots; ++s) {
-      int64_t o, l;
-      pw_leaf(P, D, s, &o, &l);
-      if (l > max_leaf) max_leaf = l;
-      empty |= l == 0;
-    }
-    const int spc = nslots < 128 ? (nslots < 4 ? 4 : (int)nslots) : 128;
-    g_D = D;
-    g_spc = spc;
-    g_ctas = nslots <= spc ? 1 : (int)(nslots / spc);
-    g_ppt = (int)((max_leaf + 7) / 8);
-    g_padded = empty || nslots < spc;
-    last_P = P;
-  }
-  if (g_ctas > FS_MAX_CLUSTER || g_ppt > 16) return MMPR_ERR_UNSUPPORTED;
-  Restrict1Params p;
+  Restrict1Params p = {};
   p.P = P;
   p.x = x;
   p.pitch = pitch;
   p.stats = stats;
   p.counts = counts;
-  p.D = g_D;
-  p.slots_per_cta = g_spc;
-  p.ctas = g_ctas;
-  const int threads = g_spc * 8;
-  const bool tail = (P % 8) != 0;
-  if (g_padded) {
-    if (tail) return launch_r1<restrict1_kernel<16, true, true>>(p, n_ens, threads, stream);
-    return launch_r1<restrict1_kernel<16, false, true>>(p, n_ens, threads, stream);
-  }
-  if (tail) return launch_r1<restrict1_kernel<16, true, false>>(p, n_ens, threads, stream);
-  return launch_r1<restrict1_kernel<16, false, false>>(p, n_ens, threads, stream);
+  return launch_r1_shape<false>(p, n_ens, stream);
 }
 
 }  // namespace mmpr
+
+using namespace mmpr;
+
+extern "C" int mmpr_match_restrict(int32_t n_ens, int64_t particles, const double *targets, int64_t tgt_stride,
+                                   const double *cur_stats, int64_t cur_stride, const int64_t *cur_counts,
+                                   int64_t cnt_stride, const double *x_src, int64_t src_pitch, double *x_out,
+                                   int64_t out_pitch, int32_t policy, int32_t *status, int32_t *clamped,
+                                   double *stats, int64_t *counts, void *stream) {
+  if (n_ens < 0 || particles < 1 || !targets || !cur_stats || !cur_counts || !x_src || !x_out || !status ||
+      !stats || (policy != 0 && policy != 1))
+    return MMPR_ERR_ARG;
+  if (n_ens == 0) return MMPR_OK;
+  Restrict1Params p = {};
+  p.P = particles;
+  p.x = x_src;
+  p.pitch = src_pitch;
+  p.stats = stats;
+  p.counts = counts;
+  p.targets = targets;
+  p.tgt_stride = tgt_stride;
+  p.cur = cur_stats;
+  p.cur_stride = cur_stride;
+  p.cur_counts = cur_counts;
+  p.cnt_stride = cnt_stride;
+  p.x_out = x_out;
+  p.out_pitch = out_pitch;
+  p.policy = policy;
+  p.status = status;
+  p.clamped = clamped;
+  const int st = launch_r1_shape<true>(p, n_ens, (cudaStream_t)stream);
+  if (st != MMPR_ERR_UNSUPPORTED) return st;
+  // beyond one cluster: the two separate passes
+  mmpr_partition single = {};
+  single.n_regions = 1;
+  const int sm = mmpr_match(&single, n_ens, particles, targets, tgt_stride, cur_stats, cur_stride, cur_counts,
+                            cnt_stride, x_src, src_pitch, x_out, out_pitch, policy, status, clamped, stream);
+  if (sm != MMPR_OK) return sm;
+  return mmpr_restrict(&single, n_ens, particles, x_out, out_pitch, stats, counts, nullptr, stream);
+}

@@ -252,9 +252,17 @@ class _RunPlan:
                            ws.macro[0], ws.cache[0], None, ws.coarse_status[0])
         timer.stop("coarse", ev)
         ev = timer.start()
-        kernels.match(part_d, ws.macro[0, 1:], ws.rho0, ws.counts0, ws.x0, self.snap(0)[1:], 1, ws.match_status[0])
+        if self.fused_restrict:  # lift and micro restriction in one pass; row 0 is ens0 itself
+            kernels.match_restrict(ws.macro[0, 1:], ws.rho0, ws.counts0, ws.x0, self.snap(0)[1:], 1,
+                                   ws.match_status[0], ws.micro[0, 1:], ws.micro_counts[0, 1:])
+            ws.micro[0, 0].copy_(ws.rho0[0])
+            ws.micro_counts[0, 0].copy_(ws.counts0[0])
+        else:
+            kernels.match(part_d, ws.macro[0, 1:], ws.rho0, ws.counts0, ws.x0, self.snap(0)[1:], 1,
+                          ws.match_status[0])
         timer.stop("match", ev)
-        kernels.restrict(part_d, self.snap(0), ws.micro[0], ws.micro_counts[0], ws.scratch)
+        if not self.fused_restrict:
+            kernels.restrict(part_d, self.snap(0), ws.micro[0], ws.micro_counts[0], ws.scratch)
         if not injected and not self.plan.fresh and self.batch == N:
             ev = timer.start()
             slice_noise(self.plan.master_seed, 0, N, S, P, 0, False, out=ws.xi)
@@ -288,11 +296,18 @@ class _RunPlan:
                            ws.coarse_status[k + 1], skip_until=(k + 1) if self.reuse else 0)
         timer.stop("coarse", ev)
         ev = timer.start()
-        kernels.match(part_d, ws.macro[k + 1, 1:], ws.fine_stats[k], ws.fine_counts[k], ws.fine, nxt[1:], 0,
-                      ws.match_status[k + 1])
+        if self.fused_restrict:  # match and micro restriction in one pass; row 0 is ens0 itself
+            kernels.match_restrict(ws.macro[k + 1, 1:], ws.fine_stats[k], ws.fine_counts[k], ws.fine, nxt[1:], 0,
+                                   ws.match_status[k + 1], ws.micro[k + 1, 1:], ws.micro_counts[k + 1, 1:])
+            ws.micro[k + 1, 0].copy_(ws.rho0[0])
+            ws.micro_counts[k + 1, 0].copy_(ws.counts0[0])
+        else:
+            kernels.match(part_d, ws.macro[k + 1, 1:], ws.fine_stats[k], ws.fine_counts[k], ws.fine, nxt[1:], 0,
+                          ws.match_status[k + 1])
         nxt[0].copy_(ws.x0[0])
         timer.stop("match", ev)
-        kernels.restrict(part_d, nxt, ws.micro[k + 1], ws.micro_counts[k + 1], ws.scratch)
+        if not self.fused_restrict:
+            kernels.restrict(part_d, nxt, ws.micro[k + 1], ws.micro_counts[k + 1], ws.scratch)
 
     def issue_all(self, timer):
         self.issue_prologue(timer)

@@ -127,6 +127,38 @@ def match(part: _lib.Partition, targets, cur_stats, cur_counts, x_src, x_out, po
               _lib.ptr(clamped), _lib.stream_handle(stream))
 
 
+def match_restrict(targets, cur_stats, cur_counts, x_src, x_out, policy: int, status, stats, counts=None,
+                   clamped=None, stream=None) -> None:
+    """Single-region match of E ensembles and the restriction of the matched
+    ensembles in one pass (stats (E, 3), counts (E, 1))."""
+    require_cuda()
+    E, P = x_out.shape
+    out_pitch = _rows(x_out, "x_out")
+    src_pitch = _rows(x_src, "x_src") if x_src.shape[0] > 1 else 0
+    if x_src.shape[1] != P or x_src.shape[0] not in (1, E):
+        raise ValueError("x_src must be (1 or E, P)")
+    for t, name in ((targets, "targets"), (cur_stats, "cur_stats")):
+        _f64(t, name)
+        if t.dim() != 2 or t.shape[1] != 3 or t.stride(1) != 1 or t.shape[0] not in (1, E):
+            raise ValueError(f"{name} must be (1 or E, 3)")
+    tgt_stride = targets.stride(0) if targets.shape[0] > 1 else 0
+    cur_stride = cur_stats.stride(0) if cur_stats.shape[0] > 1 else 0
+    if cur_counts.dtype != torch.int64 or cur_counts.shape[1] != 1 or cur_counts.shape[0] not in (1, E):
+        raise ValueError("cur_counts must be int64 (1 or E, 1)")
+    cnt_stride = cur_counts.stride(0) if cur_counts.shape[0] > 1 else 0
+    if status.dtype != torch.int32 or status.numel() < E:
+        raise ValueError("status must be int32 (E,)")
+    _f64(stats, "stats")
+    if stats.shape != (E, 3) or not stats.is_contiguous():
+        raise ValueError("stats must be contiguous float64 (E, 3)")
+    if counts is not None and (counts.dtype != torch.int64 or counts.numel() < E or not counts.is_contiguous()):
+        raise ValueError("counts must be contiguous int64 (E, 1)")
+    _lib.call("mmpr_match_restrict", int(E), int(P), targets.data_ptr(), int(tgt_stride), cur_stats.data_ptr(),
+              int(cur_stride), cur_counts.data_ptr(), int(cnt_stride), x_src.data_ptr(), int(src_pitch),
+              x_out.data_ptr(), int(out_pitch), int(policy), status.data_ptr(), _lib.ptr(clamped),
+              stats.data_ptr(), _lib.ptr(counts), _lib.stream_handle(stream))
+
+
 def coarse_row(ode: _lib.MomentOde, model: _lib.Model, integ: _lib.Integrator, times, iteration: int, rho0,
                fine_stats, cache_in, macro_out, cache_out, raw_out, status, skip_until: int = 0,
                stream=None) -> None:

@@ -164,3 +164,44 @@ def test_restrict_single_region_sizes_bitwise(mm, P):
     with np.errstate(invalid="ignore"):
         ref, _ = O.restrict(x[0], O.SINGLE)
     np.testing.assert_array_equal(stats[0].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("P", [1, 9, 1000, 100_000, 200_003, 1 << 20])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_match_restrict_fused_equals_separate(mm, P, policy):
+    """mmpr_match_restrict == mmpr_match then mmpr_restrict, bit for bit,
+    including the identity shortcut, a degenerate (zero-variance) source,
+    a negative target variance and a shared source (lift)."""
+    from paper_2310_11365_b200 import kernels
+    import torch
+    rng = np.random.default_rng(P + policy)
+    E = 5
+    x = rng.normal(0.2, 1.3, (E, P))
+    x[3] = 0.7  # zero variance: SET (collapse) or status 0 (raise)
+    xd = torch.from_numpy(x).cuda()
+    part = mm.SINGLE_REGION.descriptor()
+    cur = torch.empty((E, 3), dtype=torch.float64, device="cuda")
+    cnt = torch.empty((E, 1), dtype=torch.int64, device="cuda")
+    kernels.restrict(part, xd, cur, cnt)
+    tg = cur.clone()
+    tg[0, 0] += 0.25
+    tg[1, 1] *= 1.7
+    tg[4, 1] = -0.5  # clamped to 0
+    # row 2: identity (target == current) keeps the bits
+    for src, s_cur, s_cnt in ((xd, cur, cnt), (xd[:1], cur[:1], cnt[:1])):
+        out_a = torch.empty_like(xd)
+        st_a = torch.empty(E, dtype=torch.int32, device="cuda")
+        kernels.match(part, tg, s_cur, s_cnt, src, out_a, policy, st_a)
+        stats_a = torch.empty((E, 3), dtype=torch.float64, device="cuda")
+        cnt_a = torch.empty((E, 1), dtype=torch.int64, device="cuda")
+        kernels.restrict(part, out_a, stats_a, cnt_a)
+        out_b = torch.empty_like(xd)
+        st_b = torch.empty(E, dtype=torch.int32, device="cuda")
+        stats_b = torch.empty((E, 3), dtype=torch.float64, device="cuda")
+        cnt_b = torch.empty((E, 1), dtype=torch.int64, device="cuda")
+        kernels.match_restrict(tg, s_cur, s_cnt, src, out_b, policy, st_b, stats_b, cnt_b)
+        assert torch.equal(out_a, out_b)
+        assert torch.equal(st_a, st_b)
+        assert torch.equal(stats_a.nan_to_num(7.0), stats_b.nan_to_num(7.0))
+        assert torch.equal(cnt_a, cnt_b)
+    assert torch.equal(out_b[2], xd[0]) or src.shape[0] == 1
