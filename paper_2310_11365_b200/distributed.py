@@ -54,6 +54,15 @@ class GpuBackend:
     def fine(self, x_in, x_out, t0, steps, dt, xi, bad):
         kernels.fine_sweep(self.model_d, x_in, x_out, t0, steps, dt, xi, bad)
 
+    def fine_restrict(self, x_in, x_out, t0, steps, dt, xi, bad, stats, counts):
+        """Sweep plus the single-region restriction of its outputs, fused
+        (MEAN_OF_F models; the restriction kernel otherwise)."""
+        if self.model_d.stat_kind == _lib.STAT_MEAN_OF_F:
+            kernels.fine_sweep(self.model_d, x_in, x_out, t0, steps, dt, xi, bad, stats=stats, counts=counts)
+        else:
+            kernels.fine_sweep(self.model_d, x_in, x_out, t0, steps, dt, xi, bad)
+            kernels.restrict(SINGLE_REGION.descriptor(), x_out, stats, counts)
+
     def restrict(self, x, stats, counts, scratch):
         kernels.restrict(self.part_d, x, stats, counts, scratch)
 
@@ -178,9 +187,13 @@ def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: N
             be.noise(plan.master_seed, a, Ng, S, P, k, True, xi)
         cur, nxt = sn(k), sn(k + 1)
         ev = timer.start()
-        be.fine(cur[:Ng], fine, times_d[a:a + Ng], S, dt, xi, bad_local[k])
-        timer.stop("fine", ev)
-        be.restrict(fine, fine_local, fine_counts, scratch)
+        if I == 1:
+            be.fine_restrict(cur[:Ng], fine, times_d[a:a + Ng], S, dt, xi, bad_local[k], fine_local, fine_counts)
+            timer.stop("fine", ev)
+        else:
+            be.fine(cur[:Ng], fine, times_d[a:a + Ng], S, dt, xi, bad_local[k])
+            timer.stop("fine", ev)
+            be.restrict(fine, fine_local, fine_counts, scratch)
         fine_all[k].copy_(comm.all_gather_rows(fine_local))
         be.coarse_row(times_d, k + 1, rho0, fine_all[k], cache[k], macro[k + 1], cache[k + 1], raw[k],
                       coarse_status[k + 1], (k + 1) if reuse_converged_coarse else 0)

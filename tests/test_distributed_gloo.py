@@ -41,6 +41,10 @@ class OracleBackend:
             except O.OracleBlowup as e:
                 bad[i] = e.step_index
 
+    def fine_restrict(self, x_in, x_out, t0, steps, dt, xi, bad, stats, counts):
+        self.fine(x_in, x_out, t0, steps, dt, xi, bad)
+        self.restrict_single(x_out, stats, counts)
+
     def restrict(self, x, stats, counts, scratch):
         for i in range(x.shape[0]):
             st, c = O.restrict(x[i].numpy(), self.part)
