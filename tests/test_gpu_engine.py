@@ -273,3 +273,41 @@ def test_wasserstein_stop_criterion(mm, golden):
     assert tr.stopped_at == want
     assert np.array_equal(_packed(tr, "macro"), g["c1_macro"][:want + 1])
     assert np.array_equal(_snap(tr), g["c1_snap"][:want + 1])
+
+
+class _LocalComm:
+    """Single-rank stand-in for TorchComm (no process group needed)."""
+    rank, world = 0, 1
+
+    def all_gather_rows(self, local):
+        return local.clone()
+
+    def shift_right(self, send, recv):
+        pass
+
+    def all_max(self, value):
+        return value
+
+
+@pytest.mark.parametrize("bimodal", [False, True])
+def test_sharded_path_on_gpu_backend_equals_engine(mm, bimodal):
+    """The multi-GPU driver's per-rank code (GpuBackend kernels, fused
+    restriction, statuses, end-of-run gather) at world size 1 reproduces the
+    single-GPU engine bit for bit."""
+    from paper_2310_11365_b200.distributed import GpuBackend, run_micro_macro_sharded
+    if bimodal:
+        dw = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.5)
+        model = mm.make_double_well(dw)
+        part = dw.default_partition()
+        ode = mm.multimodal_rhs(model, part, dw.potential, dw.sigma)
+        cfg = mm.PararealConfig(n_slices=8, iterations=3, slice_length=0.0625, particles=3000,
+                                step=mm.StepConfig(2.0 ** -10, 64), partition=part, integrator=mm.EulerConfig(2.0 ** -6))
+        init = _bimodal_init(mm)
+    else:
+        model, ode, init, cfg, _ = _c1(mm, P=3000)
+    plan = mm.NoisePlan(9)
+    a = mm.run_micro_macro(model, ode, init, cfg, plan)
+    b = run_micro_macro_sharded(model, ode, init, cfg, plan, comm=_LocalComm(), backend=GpuBackend(model, ode, cfg))
+    assert np.array_equal(_packed(a, "macro"), _packed(b, "macro"))
+    assert np.array_equal(_packed(a, "micro_stats"), _packed(b, "micro_stats"))
+    assert np.array_equal(_snap(a), _snap(b))
