@@ -124,6 +124,7 @@ def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: N
     macro/micro trace, snapshots hold the rank's own slices only
     (``trace.snapshots[k][m]`` is global slice boundary ``offset + m``)."""
     comm = comm if comm is not None else TorchComm()
+    reuse_converged_coarse = reuse_converged_coarse and not plan.fresh  # see engine.run_micro_macro
     be = backend if backend is not None else GpuBackend(model, coarse, cfg)
     R, G = comm.rank, comm.world
     N, K, P, S, I = cfg.n_slices, cfg.iterations, cfg.particles, cfg.step.steps_per_slice, cfg.partition.n_regions

@@ -375,6 +375,10 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
     integ_d = integrator_descriptor(cfg.integrator)
     part_d = cfg.partition.descriptor()
     ens0 = _initial_ensemble(initial, cfg, plan)
+    # Reusing C(rho_n) of converged slices relies on their inputs being
+    # bitwise unchanged, which holds only when every iteration sees the same
+    # increments (FROZEN noise, or one injected array for all iterations).
+    reuse_converged_coarse = reuse_converged_coarse and not plan.fresh and not callable(increments)
     eager = record_timings or increments is not None or cfg.stop_wasserstein_tol is not None or not use_graph
     if eager:
         rp = _RunPlan(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse,

@@ -311,3 +311,57 @@ def test_sharded_path_on_gpu_backend_equals_engine(mm, bimodal):
     assert np.array_equal(_packed(a, "macro"), _packed(b, "macro"))
     assert np.array_equal(_packed(a, "micro_stats"), _packed(b, "micro_stats"))
     assert np.array_equal(_snap(a), _snap(b))
+
+
+@pytest.mark.parametrize("N,K", [(1, 0), (1, 1), (3, 0), (4, 4), (5, 2)])
+def test_small_shapes_against_oracle(mm, N, K):
+    """Degenerate run shapes (K = 0, N = 1, K = N) against the oracle, bitwise."""
+    P = 777
+    model, ode, init, _, _ = _c1(mm, P=P)
+    cfg = mm.PararealConfig(n_slices=N, iterations=K, slice_length=0.05, particles=P,
+                            step=mm.StepConfig(dt=1e-3, steps_per_slice=50), integrator=mm.EulerConfig(1e-2))
+    rng = np.random.default_rng(N * 10 + K)
+    ens0 = rng.normal(1.0, 0.1, P)
+    tr = mm.run_micro_macro(model, ode, mm.ParticleEnsemble(ens0), cfg, mm.NoisePlan(3))
+    om = O.model_ou(-1.0, 0.5, 0.5)
+    ref = O.run_micro_macro(om, O.ode_unimodal(om), ens0, N, K, 0.05, 1e-3, 50, 3, integ=O.Euler(1e-2))
+    assert tr.iterations == K and tr.n_slices == N
+    assert np.array_equal(_packed(tr, "macro"), ref.macro)
+    assert np.array_equal(_packed(tr, "micro_stats"), ref.micro)
+    assert np.array_equal(_snap(tr), np.array([[e for e in row] for row in ref.snapshots]))
+
+
+def test_fresh_noise_against_oracle(mm):
+    """FRESH noise (a new stream per iteration, particles.py:55-60) against
+    the oracle, bitwise, eager and graph-replayed."""
+    P, N, K = 1500, 6, 3
+    model, ode, init, _, _ = _c1(mm, P=P)
+    cfg = mm.PararealConfig(n_slices=N, iterations=K, slice_length=0.05, particles=P,
+                            step=mm.StepConfig(dt=1e-3, steps_per_slice=50), integrator=mm.EulerConfig(1e-2))
+    ens0 = np.random.default_rng(1).normal(1.0, 0.1, P)
+    om = O.model_ou(-1.0, 0.5, 0.5)
+    ref = O.run_micro_macro(om, O.ode_unimodal(om), ens0, N, K, 0.05, 1e-3, 50, 8, integ=O.Euler(1e-2), fresh=True)
+    ref_snap = np.array([[e for e in row] for row in ref.snapshots])
+    for use_graph in (False, True, True):
+        tr = mm.run_micro_macro(model, ode, mm.ParticleEnsemble(ens0), cfg, mm.NoisePlan(8, mm.NoiseMode.FRESH),
+                                use_graph=use_graph)
+        # (Marsaglia-tail draws may differ by one ulp: libm log1p, see DESIGN.md)
+        assert _rel(_packed(tr, "macro"), ref.macro) <= MOM_TOL
+        assert _rel(_snap(tr), ref_snap) <= TRAJ_TOL
+    # converged-slice coarse reuse is disabled for FRESH noise (inputs change)
+    a = mm.run_micro_macro(model, ode, mm.ParticleEnsemble(ens0), cfg, mm.NoisePlan(8, mm.NoiseMode.FRESH),
+                           reuse_converged_coarse=True)
+    b = mm.run_micro_macro(model, ode, mm.ParticleEnsemble(ens0), cfg, mm.NoisePlan(8, mm.NoiseMode.FRESH),
+                           reuse_converged_coarse=False)
+    assert np.array_equal(_packed(a, "macro"), _packed(b, "macro"))
+
+
+def test_graph_cache_eviction_and_reuse(mm):
+    """Alternating configurations (plan cache of 2, eviction) keep results exact."""
+    model, ode, init, cfg, plan = _c1(mm)
+    import dataclasses
+    cfgs = [cfg, dataclasses.replace(cfg, iterations=2), dataclasses.replace(cfg, n_slices=6, iterations=3)]
+    first = [_packed(mm.run_micro_macro(model, ode, init, c, plan), "macro") for c in cfgs]
+    for _ in range(2):
+        for c, ref in zip(cfgs, first):
+            assert np.array_equal(_packed(mm.run_micro_macro(model, ode, init, c, plan), "macro"), ref)
