@@ -103,6 +103,26 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+# SURVEY 8(d) canonical FP64 accounting of the Philox-mode fine propagator:
+# I_fp64 = dynamics (OU: fma drift 1 + update 2 + mean 1 = 4) + the dynamic
+# FP64 instruction count of curand_normal2_double per normal, measured on
+# B200 with dev/curand_fp64.cu under ncu (31.0); peak = measured FP64 issue
+# rate, dev/fp64_peak.cu (63.7 DADD/clk/SM) x 148 SMs x the run's SM clock.
+FP64_DYNAMICS = 4
+FP64_PER_NORMAL = 31.0
+FP64_PER_CLK_SM = 63.7
+N_SM = 148
+
+
+def fp64_canonical(psteps_per_s, sm_mhz):
+    peak = FP64_PER_CLK_SM * N_SM * sm_mhz * 1e6
+    achieved = psteps_per_s * (FP64_DYNAMICS + FP64_PER_NORMAL)
+    return {"achieved": achieved, "peak": peak, "unit": "FP64 instr/s", "frac": achieved / peak,
+            "model": "SURVEY 8(d): particle-steps/s x (4 dynamics + 31.0 curand_normal2_double FP64 instr per "
+                     "normal, dev/curand_fp64.cu) vs measured 63.7 FP64/clk/SM (dev/fp64_peak.cu) at the run's "
+                     "SM clock; whole run (noise generation and all sweeps)"}
+
+
 def ncu_traffic():
     """Per-launch DRAM bytes of the fine sweep from the committed ncu summary."""
     path = os.path.join(ROOT, "profiles", "fine_sweep_ncu.json")
@@ -281,6 +301,7 @@ def our_arm(args):
         "e2e": {"value": psteps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
+        "fp64_canonical": fp64_canonical(value / G, clocks.summary().get("sm_mhz") or 1965.0),
         "stage_ms_per_run": {k: round(sum(v) / 2, 4) for k, v in stage_ms.items()},
     }
     if G == 1 and not args.no_cpu_baseline:
