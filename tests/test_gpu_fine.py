@@ -297,3 +297,33 @@ def test_fused_restriction_equals_restrict(mm, monkeypatch, P, grid):
     plain = torch.empty_like(x)
     kernels.fine_sweep(model, x, plain, t0, S, 1e-3, xi, bad)
     assert torch.equal(plain, out)
+
+
+def test_random_sizes_sweep_bitwise(mm):
+    """Forty particle counts drawn over 1..3e5 (every geometry: single CTA,
+    clusters of 2..16, padded slot trees, tails, the compile-time and the
+    run-time accumulator bound): injected-mode OU bitwise against the oracle."""
+    from paper_2310_11365_b200 import kernels
+    import torch
+    rng = np.random.default_rng(2024)
+    sizes = sorted(set(int(v) for v in np.exp(rng.uniform(0, np.log(3e5), 40))))
+    om = O.model_ou(-1.0, 0.5, 0.5)
+    model = GPU_MODELS["ou"](mm).descriptor
+    S = 3
+    for P in sizes:
+        x0 = rng.normal(0.0, 1.0, (2, P))
+        xi_h = rng.standard_normal((2, S, P))
+        xi = kernels.noise_buffer(2, S, P)
+        xi[:, :, :P] = torch.from_numpy(xi_h).cuda()
+        x = torch.from_numpy(x0).cuda()
+        out = torch.empty_like(x)
+        bad = torch.empty(2, dtype=torch.int32, device="cuda")
+        stats = torch.empty((2, 3), dtype=torch.float64, device="cuda")
+        t0 = torch.zeros(2, dtype=torch.float64, device="cuda")
+        kernels.fine_sweep(model, x, out, t0, S, 1e-3, xi, bad, stats=stats)
+        got = out.cpu().numpy()
+        st = stats.cpu().numpy()
+        for n in range(2):
+            ref = O.propagate_fine(om, x0[n], 0, 0.0, 1e-3, S, xi_h[n])
+            assert np.array_equal(got[n], ref), P
+            assert np.array_equal(st[n], O.restrict(ref)[0]), P
