@@ -315,6 +315,13 @@ int mmpr_sort_rows(int32_t n_rows, int64_t count, const double *in, double *out,
 int mmpr_mean_abs_diff(int32_t n_rows, int64_t count, const double *a, int64_t pitch_a,
                        const double *b, int64_t pitch_b, double *out, void *stream);
 
+/* Cumulative histogram of sorted rows (np.histogram with explicit edges,
+ * harness.py:314-316): cum[r*n_edges + e] = #{x in row r : x < edges[e]},
+ * the last edge inclusive (x <= edges[n_edges-1]); bin counts are the
+ * differences.  NaNs (sorted last) are never counted. */
+int mmpr_histogram_sorted(int32_t n_rows, int64_t count, const double *sorted, int64_t pitch,
+                          const double *edges, int32_t n_edges, int64_t *cum, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

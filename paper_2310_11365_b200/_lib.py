@@ -106,6 +106,7 @@ SIGNATURES = {
                                                  _I64, _P, _P, _P, _P]),
     "mmpr_sort_rows": (ctypes.c_int, [_I32, _I64, _P, _P, _I64, _P, _P, _P]),
     "mmpr_mean_abs_diff": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I64, _P, _P]),
+    "mmpr_histogram_sorted": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I32, _P, _P]),
 }
 
 _lib = None

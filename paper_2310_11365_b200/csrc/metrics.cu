@@ -88,9 +88,41 @@ __global__ void __launch_bounds__(MA_THREADS) mean_absdiff_kernel(int64_t n, con
   if (threadIdx.x == 0) out[r] = div(s, (double)n);
 }
 
+// cum[r][e] = #{sorted_r < edge_e} (last edge: <=), one thread per (row, edge)
+__global__ void hist_cum_kernel(int32_t n_rows, int64_t count, const double *__restrict__ sorted, int64_t pitch,
+                                const double *__restrict__ edges, int32_t n_edges, int64_t *__restrict__ cum) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= (int64_t)n_rows * n_edges) return;
+  const int64_t r = g / n_edges;
+  const int e = (int)(g - r * n_edges);
+  const double *a = sorted + r * pitch;
+  const double v = edges[e];
+  const bool right = e == n_edges - 1;
+  int64_t lo = 0, hi = count;  // first index whose element is >= v (> v for the last edge)
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const double x = a[mid];
+    if (right ? !(x > v) : (x < v)) lo = mid + 1;
+    else hi = mid;
+  }
+  cum[g] = lo;
+}
+
 }  // namespace mmpr
 
 using namespace mmpr;
+
+extern "C" int mmpr_histogram_sorted(int32_t n_rows, int64_t count, const double *sorted, int64_t pitch,
+                                     const double *edges, int32_t n_edges, int64_t *counts, void *stream) {
+  if (n_rows < 0 || count < 0 || !sorted || !edges || n_edges < 2 || !counts) return MMPR_ERR_ARG;
+  if (n_rows == 0) return MMPR_OK;
+  // counts is used as the cumulative scratch: [n_rows][n_edges]; the host
+  // differences it (n_edges - 1 bins per row)
+  const int64_t total = (int64_t)n_rows * n_edges;
+  hist_cum_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_rows, count, sorted, pitch,
+                                                                                    edges, n_edges, counts);
+  return mmpr_check_launch("hist_cum_kernel");
+}
 
 extern "C" int mmpr_sort_rows(int32_t n_rows, int64_t count, const double *in, double *out, int64_t pitch,
                               void *temp, uint64_t *temp_bytes, void *stream) {

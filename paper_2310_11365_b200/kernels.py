@@ -221,5 +221,19 @@ def _single_region() -> _lib.Partition:
     return d
 
 
+def histogram_sorted(sorted_rows, edges, stream=None):
+    """Cumulative counts (R, E) int64 of every sorted row below each edge
+    (the last edge inclusive)."""
+    require_cuda()
+    R, P = sorted_rows.shape
+    pitch = _rows(sorted_rows, "sorted_rows")
+    _f64(edges, "edges")
+    E = edges.numel()
+    cum = torch.empty((R, E), dtype=torch.int64, device=sorted_rows.device)
+    _lib.call("mmpr_histogram_sorted", int(R), int(P), sorted_rows.data_ptr(), int(pitch),
+              edges.contiguous().data_ptr(), int(E), cum.data_ptr(), _lib.stream_handle(stream))
+    return cum
+
+
 def noise_buffer(n_slices: int, steps: int, P: int):
     return torch.empty((n_slices, steps, row_pitch(P)), dtype=torch.float64, device=device())

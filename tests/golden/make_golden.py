@@ -343,6 +343,14 @@ def metrics_fixture():
         report_to_arrays(M.relative_errors(tr, k), f"rel_c1_k{k}_", out)
         report_to_arrays(M.relative_errors(tr, k, var_denominator="mean"), f"relm_c1_k{k}_", out)
     report_to_arrays(M.relative_errors(tr, 1, reference_k=3), "rel_c1_k1_ref3_", out)
+    # histogram artefacts (harness.py:300-323): FD edges on the final iterate
+    from mcparareal import harness as H
+    for n in (1, 5, 10):
+        data = [tr.snapshots[k][n].positions for k in range(tr.iterations + 1)]
+        reference = tr.snapshots[tr.iterations][n].positions
+        edges = H._fd_edges(reference, data + [reference])
+        out[f"hist_c1_n{n}_edges"] = edges
+        out[f"hist_c1_n{n}_counts"] = np.array([np.histogram(d, edges)[0] for d in data])
     # floor replicas exactly as harness.replicate_seeds derives them (harness.py:158-165)
     base = ref.NoisePlan(0)
     seeds = [base.derived_seed(10_000 + j) for j in range(3)]

@@ -95,3 +95,24 @@ def test_floor_config4_size(mm):
     host = [[e.positions for e in p] for p in paths]
     fl = mm.floor_from_references(paths)
     assert np.array_equal(np.array([fl.e_mean, fl.e_var, fl.e_wass, fl.n_replicas]), O.floor_from_references(host))
+
+
+def test_fd_histograms_match_reference(mm, golden):
+    """Freedman-Diaconis edges and histogram counts of the harness's
+    histogram.csv (harness.py:209-227, 300-323) on the device."""
+    g = golden("metrics")
+    model, ode, init, cfg = _c1(mm)
+    tr = mm.run_micro_macro(model, ode, init, cfg, mm.NoisePlan(0))
+    for n in (1, 5, 10):
+        data = [tr.snapshots[k][n] for k in range(tr.iterations + 1)]
+        edges = mm.metrics.fd_edges(tr.snapshots[tr.iterations][n], data + [tr.snapshots[tr.iterations][n]])
+        assert np.array_equal(edges, g[f"hist_c1_n{n}_edges"]), n
+        assert np.array_equal(mm.metrics.histograms(data, edges), g[f"hist_c1_n{n}_counts"]), n
+
+
+@pytest.mark.parametrize("P", [1, 10, 4097, 100_000])
+def test_histogram_edge_cases_against_numpy(mm, P):
+    rng = np.random.default_rng(P)
+    x = np.round(rng.normal(0.0, 1.0, P), 2)  # values on the edges
+    for edges in (np.linspace(-1.0, 1.0, 11), np.array([-5.0, 0.0, 0.0, 5.0]), np.array([0.0, 0.01])):
+        assert np.array_equal(mm.metrics.histogram(x, edges), np.histogram(x, edges)[0])
