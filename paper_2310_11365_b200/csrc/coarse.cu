@@ -24,6 +24,9 @@ namespace mmpr {
 
 #define CS_MAXV (3 * MMPR_MAX_REGIONS)
 #define MMPR_COARSE_SINGULAR 2
+#ifdef MMPR_COARSE_PROFILE
+__device__ long long g_coarse_prof[4];  // dev builds: cycles in the Euler loops, calls, total
+#endif
 
 // numpy pairwise sum for n <= 128 (short vectors: sequential from 0 when
 // n < 8, else 8 accumulators)
@@ -343,6 +346,9 @@ __global__ void coarse_row_kernel(const CoarseParams p) {
     __syncwarp();
   }
   if (threadIdx.x != 0) return;
+#ifdef MMPR_COARSE_PROFILE
+  const long long ct0 = clock64();
+#endif
   const double *__restrict__ times = p.times;
   const double *__restrict__ fine = p.fine;
   const double *__restrict__ cin = p.cache_in;
@@ -378,8 +384,16 @@ __global__ void coarse_row_kernel(const CoarseParams p) {
     } else {
 #pragma unroll
       for (int v = 0; v < NV; ++v) pred[v] = cur[v];
+#ifdef MMPR_COARSE_PROFILE
+      const long long c0 = clock64();
+#endif
       if (staged) st = integrate_euler_n<NV, OK, MK>(p.ode, p.model, s_n[n], s_h[n], t0, pred);
       else st = coarse_step<NV, OK, MK>(p.ode, p.model, p.integ, t0, t1, pred);
+#ifdef MMPR_COARSE_PROFILE
+      const long long c1 = clock64();
+      g_coarse_prof[0] += c1 - c0;
+      g_coarse_prof[1] += 1;
+#endif
     }
     p.status[n] = st;
 #pragma unroll
@@ -413,6 +427,9 @@ __global__ void coarse_row_kernel(const CoarseParams p) {
       c[v] = cn[v];
     }
   }
+#ifdef MMPR_COARSE_PROFILE
+  g_coarse_prof[2] += clock64() - ct0;
+#endif
 }
 
 template <int NV, int OK, int MK>
@@ -575,3 +592,13 @@ extern "C" int mmpr_integrate_macro(const mmpr_moment_ode *ode, const mmpr_model
   a.stream = (cudaStream_t)stream;
   return dispatch_coarse<MacroLaunch>(ode->n_regions, ode->kind, model->kind, a);
 }
+
+#ifdef MMPR_COARSE_PROFILE
+extern "C" int mmpr_dev_coarse_prof(long long *host_out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host_out, mmpr::g_coarse_prof, sizeof(mmpr::g_coarse_prof));
+  static long long zeros[4];
+  cudaMemcpyToSymbol(mmpr::g_coarse_prof, zeros, sizeof(zeros));
+  return (int)cudaGetLastError();
+}
+#endif
