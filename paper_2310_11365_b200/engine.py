@@ -95,6 +95,7 @@ class PararealTrace:
     timings: dict = field(default_factory=dict)
     stopped_at: int | None = None
     d2h_bytes: int = 0
+    snapshot_positions: np.ndarray | None = None  # host copy streamed during the run (snapshots_to_host)
 
     @property
     def n_slices(self) -> int:
@@ -218,7 +219,7 @@ class _RunPlan:
     (replayed from a CUDA graph when the configuration repeats)."""
 
     def __init__(self, model_d, ode_d, ode_model_d, integ_d, part_d, cfg: PararealConfig, plan: NoisePlan,
-                 reuse: bool, injected: bool = False):
+                 reuse: bool, injected: bool = False, host_snapshots: bool = False):
         self.model_d, self.ode_d, self.ode_model_d, self.integ_d, self.part_d = \
             model_d, ode_d, ode_model_d, integ_d, part_d
         self.cfg, self.plan, self.reuse = cfg, plan, reuse
@@ -230,6 +231,13 @@ class _RunPlan:
         self.ws = _Workspace(K, N, P, S, I, cfg.retain_snapshots, noise_slices=N if injected else None)
         # single-region restriction of the fine outputs fused into the sweep
         self.fused_restrict = I == 1 and model_d.stat_kind == _lib.STAT_MEAN_OF_F
+        # snapshot rows streamed to pinned host memory on a side stream while
+        # the next iteration computes (harness artefacts need them on the host)
+        self.host_snap = None
+        self.copy_stream = None
+        if host_snapshots:
+            self.host_snap = torch.empty((K + 1, N + 1, P), dtype=torch.float64, pin_memory=True)
+            self.copy_stream = torch.cuda.Stream()
         self.batch = self.ws.noise_slices
         self.graph = None
         self.launches_per_run = 0
@@ -309,10 +317,26 @@ class _RunPlan:
         if not self.fused_restrict:
             kernels.restrict(part_d, nxt, ws.micro[k + 1], ws.micro_counts[k + 1], ws.scratch)
 
+    def stream_row(self, k):
+        """Copy snapshot row k to pinned host memory on the side stream."""
+        if self.host_snap is None:
+            return
+        main = torch.cuda.current_stream()
+        self.copy_stream.wait_stream(main)
+        with torch.cuda.stream(self.copy_stream):
+            self.host_snap[k].copy_(self.snap(k), non_blocking=True)
+
+    def join(self):
+        if self.copy_stream is not None:
+            torch.cuda.current_stream().wait_stream(self.copy_stream)
+
     def issue_all(self, timer):
         self.issue_prologue(timer)
+        self.stream_row(0)
         for k in range(self.K):
             self.issue_iteration(k, timer)
+            self.stream_row(k + 1)
+        self.join()
 
     def replay(self):
         """Launch the whole run as one CUDA graph (captured on first use)."""
@@ -351,7 +375,8 @@ def _wasserstein_delta(a, b) -> float:
 
 def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: InitialDistribution | ParticleEnsemble,
                     cfg: PararealConfig, plan: NoisePlan, *, reuse_converged_coarse: bool = True,
-                    record_timings: bool = False, increments=None, use_graph: bool = True) -> PararealTrace:
+                    record_timings: bool = False, increments=None, use_graph: bool = True,
+                    snapshots_to_host: bool = False) -> PararealTrace:
     """Run the micro-macro Parareal iteration on the GPU and record every iterate.
 
     ``increments`` (optional) injects the Brownian increments as a callable
@@ -360,6 +385,10 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
     ``reuse_converged_coarse`` copies C(rho_n) for n < k from the previous
     row instead of re-integrating (bitwise identical: those inputs have
     converged exactly, engine.py:11-14).
+    ``snapshots_to_host`` streams every iterate's snapshot row to pinned host
+    memory on a side stream while the next iteration computes; the result is
+    ``trace.snapshot_positions`` ((K+1, N+1, P) numpy, reused by the next run
+    of the same configuration like the device snapshots).
     ``use_graph`` replays the run's launch sequence as one CUDA graph, cached
     per configuration (eager launches when timings are recorded, increments
     are injected or the Wasserstein stop criterion is active).
@@ -380,16 +409,20 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
     # increments (FROZEN noise, or one injected array for all iterations).
     reuse_converged_coarse = reuse_converged_coarse and not plan.fresh and not callable(increments)
     eager = record_timings or increments is not None or cfg.stop_wasserstein_tol is not None or not use_graph
+    if snapshots_to_host and not cfg.retain_snapshots:
+        raise ConfigError("snapshots_to_host needs retain_snapshots=True")
     if eager:
         rp = _RunPlan(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse,
-                      injected=increments is not None)
+                      injected=increments is not None, host_snapshots=snapshots_to_host)
     else:
-        key = _plan_key(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse)
+        key = _plan_key(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse) + \
+            (snapshots_to_host,)
         rp = _PLANS.get(key)
         if rp is None:
             while len(_PLANS) >= _PLANS_MAX:
                 _PLANS.pop(next(iter(_PLANS)))
-            rp = _RunPlan(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse)
+            rp = _RunPlan(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse,
+                          host_snapshots=snapshots_to_host)
             _PLANS[key] = rp
     ws = rp.ws
     ws.x0.copy_(ens0.device_positions.reshape(1, -1))
@@ -405,11 +438,13 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
         if injected and not callable(increments):
             ws.xi = increments
         rp.issue_prologue(timer, injected)
+        rp.stream_row(0)
         for k in range(K):
             if callable(increments):
                 for n in range(N):
                     ws.xi[n, :, :P] = torch.as_tensor(np.asarray(increments(n, k), dtype=float)).to(device())
             rp.issue_iteration(k, timer, injected)
+            rp.stream_row(k + 1)
             iterations_done = k + 1
             if cfg.stop_wasserstein_tol is not None:
                 delta = _wasserstein_delta(rp.snap(k + 1)[1:], rp.snap(k)[1:])
@@ -418,6 +453,7 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
                     logger.info("stopping after iteration %d: max slice Wasserstein delta %.3e", k + 1, delta)
                     break
 
+    rp.join()
     # ---- one device->host transfer, then the reference's error order --------
     h = ws.read_back()
     Kd = iterations_done
@@ -426,6 +462,9 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
     _raise_first_error(h, N, Kd, cfg.partition.n_regions)
     trace = _build_trace(h, ws, cfg, plan, rp.times, Kd, cfg.partition.n_regions, timer, stopped_at)
     trace.d2h_bytes = ws.report_bytes()
+    if rp.host_snap is not None:
+        trace.snapshot_positions = rp.host_snap.numpy()[:Kd + 1]
+        trace.d2h_bytes += int(rp.host_snap[:Kd + 1].numel()) * 8
     return trace
 
 

@@ -365,3 +365,15 @@ def test_graph_cache_eviction_and_reuse(mm):
     for _ in range(2):
         for c, ref in zip(cfgs, first):
             assert np.array_equal(_packed(mm.run_micro_macro(model, ode, init, c, plan), "macro"), ref)
+
+
+@pytest.mark.parametrize("use_graph", [False, True])
+def test_snapshots_streamed_to_host(mm, golden, use_graph):
+    """snapshots_to_host: every iterate's ensembles reach pinned host memory
+    during the run (side-stream copies), equal to the device snapshots."""
+    g = golden("traces")
+    model, ode, init, cfg, plan = _c1(mm)
+    for _ in range(2):  # second pass replays the cached graph
+        tr = mm.run_micro_macro(model, ode, init, cfg, plan, snapshots_to_host=True, use_graph=use_graph)
+        assert np.array_equal(tr.snapshot_positions, g["c1_snap"])
+        assert np.array_equal(_snap(tr), g["c1_snap"])
