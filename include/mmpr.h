@@ -193,7 +193,11 @@ int mmpr_normals_fill(const uint64_t *keys, int32_t n_streams, int64_t count,
  *  t0    : device double[n_slices] slice start times
  *  bad_step : device int32[n_slices]; MMPR_STAT_OK or the first step whose
  *          positions were not all finite (NumericalBlowup(slice, step))
- *  final_mean : device double[n_slices] (may be NULL): mean of the output. */
+ *  final_mean : device double[n_slices] (may be NULL): mean of the output.
+ * Ensembles larger than one 16-CTA cluster (P = 2^20) run the grid variant:
+ * co-resident teams of CTAs exchanging per-step partials through a
+ * library-owned device buffer, so two such launches must not run
+ * concurrently on one device (stream order them). */
 int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_t particles,
                     int32_t steps, double dt, double sqrt_dt, const double *t0,
                     const double *x_in, int64_t in_pitch, double *x_out,

@@ -25,3 +25,13 @@ static inline int mmpr_check(cudaError_t err, const char *what) {
   }
   return MMPR_OK;
 }
+
+// Per-device memo of kernel attributes already applied (cudaFuncSetAttribute
+// acts on the current device; attributes are set outside graph captures on
+// the first launch of a configuration and only raised afterwards).
+#define MMPR_MAX_DEVICES 64
+static inline int mmpr_current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return (dev >= 0 && dev < MMPR_MAX_DEVICES) ? dev : 0;
+}

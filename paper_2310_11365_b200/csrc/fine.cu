@@ -454,8 +454,11 @@ static int launch_fine_t(const FineParams &p, const FineGeometry &g, cudaStream_
   auto kern = KERN;
   // attributes are set once per instantiation (never during graph capture
   // of a repeated configuration)
-  static int configured_smem = -1;
-  static bool configured_nonportable = false;
+  static int configured_smem_dev[MMPR_MAX_DEVICES] = {};
+  static bool configured_nonportable_dev[MMPR_MAX_DEVICES] = {};
+  const int dev = mmpr_current_device();
+  int &configured_smem = configured_smem_dev[dev];
+  bool &configured_nonportable = configured_nonportable_dev[dev];
   cudaError_t err;
   if ((int)g.smem_bytes > configured_smem) {
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);

@@ -464,7 +464,8 @@ static int grid_geometry(int64_t P, int n_slices, GridGeometry *g) {
 
 template <void (*KERN)(const FineParams, const GridExtra)>
 static int launch_grid_t(const FineParams &p, const GridGeometry &g, cudaStream_t stream) {
-  static int configured_smem = -1;
+  static int configured_smem_dev[MMPR_MAX_DEVICES] = {};
+  int &configured_smem = configured_smem_dev[mmpr_current_device()];
   cudaError_t err;
   if ((int)g.smem > configured_smem) {
     err = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);

@@ -240,7 +240,8 @@ static int launch_r1_shape(Restrict1Params p, int n_ens, cudaStream_t stream) {
 
 template <void (*KERN)(const Restrict1Params)>
 static int launch_r1(const Restrict1Params &p, int n_ens, int threads, cudaStream_t stream) {
-  static bool configured = false;
+  static bool configured_dev[MMPR_MAX_DEVICES] = {};
+  bool &configured = configured_dev[mmpr_current_device()];
   cudaError_t err;
   if (p.ctas > 8 && !configured) {
     err = cudaFuncSetAttribute(KERN, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
