@@ -18,7 +18,7 @@ bad = torch.empty(N, dtype=torch.int32, device='cuda')
 t0 = torch.zeros(N, dtype=torch.float64, device='cuda')
 buf = np.zeros((4096, 10), dtype=np.int64)
 names = ['wait_stage', 'update', 'B1', 'cluster_wait', '-', 'leaf+warp', '-', 'fold+send', 'reduce_total']
-for grp, spc in (('1', '128'), ('1', '64')):
+for grp, spc in (('1', '64'),):
     os.environ['MMPR_FINE_GROUPS'] = grp
     os.environ['MMPR_FINE_SLOTS_PER_CTA'] = spc
     os.environ['MMPR_FINE_STAGES'] = '2'
