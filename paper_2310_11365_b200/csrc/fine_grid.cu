@@ -32,6 +32,16 @@
 
 namespace mmpr {
 
+#ifdef MMPR_FINE_PROFILE
+// dev builds only: per-CTA cycle totals of the step phases
+__device__ long long g_grid_prof[2048][8];
+#define GPROF_MARK(var) long long var = clock64()
+#define GPROF_ADD(k, a, b) if (threadIdx.x == 0) g_grid_prof[blockIdx.x & 2047][k] += (b) - (a)
+#else
+#define GPROF_MARK(var)
+#define GPROF_ADD(k, a, b)
+#endif
+
 #define FG_MAX_CTAS 2048   // teams * C
 #define FG_MAX_TEAM 256    // C (8 partials per lane in the final fold)
 #define FG_MAX_TEAMS 64
@@ -217,7 +227,10 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
       leaf = leaf.xor_level(lane, 8);
       leaf = leaf.xor_level(lane, 16);
       if (lane == 0) s_wp[warp] = leaf;
+      GPROF_MARK(pb0);
       const int cta_bad = __syncthreads_or(bad_local);  // B1
+      GPROF_MARK(pb1);
+      GPROF_ADD(1, pb0, pb1);
       // B1 orders every read of the consumed buffers before their refill; the
       // copies overlap the team exchange below
       if (issuer && refill_step >= 0) {
@@ -241,9 +254,12 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
           w.z = okv;
           w.w = cta_bad;
           __stcg(reinterpret_cast<int4 *>(&parts[rank]), w);
+          GPROF_MARK(pp0);
           red_release_gpu_add(counter, 1u);
           const unsigned int target = (epoch + 1) * (unsigned int)C;
           const unsigned long long t0 = globaltimer();
+          GPROF_MARK(pp1);
+          GPROF_ADD(2, pp0, pp1);
           while (ld_acquire_gpu(counter) < target) {
             // a team member that never arrives (not co-resident) would hang
             // the device: fail the launch instead
@@ -293,7 +309,11 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
           s_tbad = any;
         }
       }
+      GPROF_MARK(pb2);
       __syncthreads();  // B2
+      GPROF_MARK(pb3);
+      GPROF_ADD(4, pb1, pb2);
+      GPROF_ADD(5, pb2, pb3);
       ++epoch;
       mean_out = s_mean;
       bad_out = s_tbad;
@@ -305,6 +325,7 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
     int issued = min(NB, total_chunks);
     reduce(-1, s, bad);
     for (int j = 0; j < p.S; ++j) {
+      GPROF_MARK(pu0);
 #pragma unroll
           for (int h = 0; h < H; ++h) {
             const uint32_t q = qbase + (uint32_t)(j * H + h);
@@ -325,7 +346,11 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
             }
             if (h == H - 1 && HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[tail_idx]);
           }
+      GPROF_MARK(pu1);
+      GPROF_ADD(0, pu0, pu1);
       reduce(j, s, bad);  // refills the buffers step j consumed
+      GPROF_MARK(pu2);
+      GPROF_ADD(6, pu1, pu2);
       issued = min(total_chunks, NB + (j + 1) * H);
       if (bad) {
         first_bad = j;
@@ -557,3 +582,15 @@ int fine_grid_sweep(FineParams p, cudaStream_t stream) {
 }
 
 }  // namespace mmpr
+
+#ifdef MMPR_FINE_PROFILE
+extern "C" int mmpr_dev_grid_prof(long long *host_out, int reset) {
+  cudaDeviceSynchronize();
+  if (host_out) cudaMemcpyFromSymbol(host_out, mmpr::g_grid_prof, sizeof(mmpr::g_grid_prof));
+  if (reset) {
+    static long long zeros[2048][8];
+    cudaMemcpyToSymbol(mmpr::g_grid_prof, zeros, sizeof(zeros));
+  }
+  return (int)cudaGetLastError();
+}
+#endif
