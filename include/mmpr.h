@@ -236,10 +236,16 @@ int mmpr_fine_sweep_stepwise(const mmpr_model *model, int32_t n_slices, int64_t 
 /* Per-region fraction, mean and two-pass population variance of n_ens
  * ensembles, numpy summation order.  stats: device double[n_ens][3I] packed
  * [means, variances, fractions]; counts: device int64[n_ens][I]; scratch:
- * device double, >= n_ens*I*particles values when I > 1 (NULL when I = 1). */
+ * device double, >= mmpr_restrict_scratch_doubles(n_ens, particles, I)
+ * values when I > 1 (NULL when I = 1). */
 int mmpr_restrict(const mmpr_partition *part, int32_t n_ens, int64_t particles,
                   const double *x, int64_t pitch, double *stats, int64_t *counts,
                   double *scratch, void *stream);
+
+/* Scratch (in doubles) mmpr_restrict needs for n_regions > 1: the region
+ * arrays compacted in index order plus per-chunk counts and subtree
+ * partials of the multi-CTA reduction; 0 for one region. */
+int64_t mmpr_restrict_scratch_doubles(int32_t n_ens, int64_t particles, int32_t n_regions);
 
 /* Per-region affine match x -> sqrt(var_t/var_c)(x - M_c) + mu_t with the
  * reference's clamp / degenerate / identity rules.  Ensemble e reads source

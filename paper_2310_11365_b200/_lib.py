@@ -93,6 +93,7 @@ SIGNATURES = {
     "mmpr_fine_sweep": (ctypes.c_int, [_P, _I32, _I64, _I32, _D, _D, _P, _P, _I64, _P, _I64,
                                         _P, _I64, _I64, _P, _P, _P]),
     "mmpr_restrict": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _P, _P, _P, _P]),
+    "mmpr_restrict_scratch_doubles": (ctypes.c_int64, [_I32, _I64, _I32]),
     "mmpr_match": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _P,
                                    _I64, _I32, _P, _P, _P]),
     "mmpr_match_restrict": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _I32,

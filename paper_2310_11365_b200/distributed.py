@@ -66,6 +66,9 @@ class GpuBackend:
     def restrict(self, x, stats, counts, scratch):
         kernels.restrict(self.part_d, x, stats, counts, scratch)
 
+    def restrict_scratch(self, n_ens, P, I):
+        return kernels.restrict_scratch(n_ens, P, I)
+
     def coarse_row(self, times, iteration, rho0, fine_stats, cache_in, macro_out, cache_out, raw_out, status,
                    skip_until):
         kernels.coarse_row(self.ode_d, self.ode_model_d, self.integ_d, times, iteration, rho0, fine_stats,
@@ -163,7 +166,7 @@ def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: N
     lift_first = torch.full((1,), _lib.STAT_OK, dtype=i32, device=be.device)
     rho0 = be.empty((1, nv))
     counts0 = be.empty((1, I), i64)
-    scratch = be.empty(((Ng + 1) * I * P,)) if I > 1 else None
+    scratch = be.empty((be.restrict_scratch(Ng + 1, P, I),)) if I > 1 else None
 
     def sn(k):
         return snap[k if retain else k % 2]

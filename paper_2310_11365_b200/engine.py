@@ -172,7 +172,8 @@ class _Workspace:
         self.snap = torch.empty((K + 1 if retain else 2, N + 1, P), dtype=torch.float64, device=dev)
         self.fine = torch.empty((N, P), dtype=torch.float64, device=dev)
         self.cache = torch.empty((K + 1, N, nv), dtype=torch.float64, device=dev)
-        self.scratch = torch.empty(((N + 1) * I * P,), dtype=torch.float64, device=dev) if I > 1 else None
+        self.scratch = (torch.empty((kernels.restrict_scratch(N + 1, P, I),), dtype=torch.float64, device=dev)
+                        if I > 1 else None)
         self.x0 = torch.empty((1, P), dtype=torch.float64, device=dev)
         self.host = {dt: torch.empty(t.shape, dtype=dt, pin_memory=True) for dt, t in self.report.items()}
         # increments of a batch of slices: all N when they fit (frozen noise is

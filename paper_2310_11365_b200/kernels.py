@@ -78,6 +78,11 @@ def fine_sweep(model: _lib.Model, x_in, x_out, t0, steps: int, dt: float, xi, ba
               _lib.ptr(final_mean), _lib.stream_handle(stream))
 
 
+def restrict_scratch(n_ens: int, P: int, n_regions: int) -> int:
+    """Doubles of scratch mmpr_restrict needs (0 for one region)."""
+    return int(_lib.load().mmpr_restrict_scratch_doubles(int(n_ens), int(P), int(n_regions)))
+
+
 def restrict(part: _lib.Partition, x, stats, counts, scratch=None, stream=None) -> None:
     """stats (E, 3I) and counts (E, I) int64 of every row of x (E, P)."""
     require_cuda()
@@ -90,7 +95,7 @@ def restrict(part: _lib.Partition, x, stats, counts, scratch=None, stream=None) 
     if counts.dtype != torch.int64 or counts.shape != (E, I) or not counts.is_contiguous():
         raise ValueError("counts must be contiguous int64 (E, I)")
     if I > 1:
-        need = E * I * P
+        need = restrict_scratch(E, P, I)
         if scratch is None:
             scratch = torch.empty(need, dtype=torch.float64, device=device())
         elif scratch.numel() < need:

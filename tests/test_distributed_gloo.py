@@ -41,6 +41,9 @@ class OracleBackend:
             except O.OracleBlowup as e:
                 bad[i] = e.step_index
 
+    def restrict_scratch(self, n_ens, P, I):
+        return n_ens * I * P
+
     def fine_restrict(self, x_in, x_out, t0, steps, dt, xi, bad, stats, counts):
         self.fine(x_in, x_out, t0, steps, dt, xi, bad)
         self.restrict_single(x_out, stats, counts)

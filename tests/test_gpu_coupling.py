@@ -205,3 +205,32 @@ def test_match_restrict_fused_equals_separate(mm, P, policy):
         assert torch.equal(stats_a.nan_to_num(7.0), stats_b.nan_to_num(7.0))
         assert torch.equal(cnt_a, cnt_b)
     assert torch.equal(out_b[2], xd[0]) or src.shape[0] == 1
+
+
+def test_multi_region_restrict_random_sizes(mm):
+    """The multi-CTA multi-region restriction against the oracle, bitwise:
+    random sizes, 2-4 regions, empty and one-member regions, many ensembles."""
+    from paper_2310_11365_b200 import kernels
+    import torch
+    rng = np.random.default_rng(77)
+    parts = [((0.0,), (-1.0, 1.0)), ((-0.5, 0.5), (-1.0, 0.0, 1.0)), ((-2.0, 0.0, 2.0), (-3.0, -1.0, 1.0, 3.0)),
+             ((50.0,), (0.0, 60.0))]  # second region empty
+    for P in sorted(set(int(v) for v in np.exp(rng.uniform(0, np.log(3e5), 12))) | {1, 2, 9}):
+        for seps, peaks in parts:
+            E = 3
+            x = rng.normal(0.0, 1.5, (E, P))
+            if P > 3:
+                x[1, : P - 1] = -9.0  # region 0 takes all but one particle
+                x[1, -1] = 9.0
+            xd = torch.from_numpy(x).cuda()
+            part_m = mm.RegionPartition(separatrices=seps, peaks=peaks)
+            I = len(peaks)
+            stats = torch.empty((E, 3 * I), dtype=torch.float64, device="cuda")
+            counts = torch.empty((E, I), dtype=torch.int64, device="cuda")
+            kernels.restrict(part_m.descriptor(), xd, stats, counts)
+            got, gc = stats.cpu().numpy(), counts.cpu().numpy()
+            part_o = O.Partition(seps, peaks)
+            for e in range(E):
+                ref, rc = O.restrict(x[e], part_o)
+                assert np.array_equal(got[e], ref), (P, seps, e)
+                assert np.array_equal(gc[e], rc), (P, seps, e)
