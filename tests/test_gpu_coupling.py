@@ -234,3 +234,47 @@ def test_multi_region_restrict_random_sizes(mm):
                 ref, rc = O.restrict(x[e], part_o)
                 assert np.array_equal(got[e], ref), (P, seps, e)
                 assert np.array_equal(gc[e], rc), (P, seps, e)
+
+
+# ---- hypothesis: coupling operators against the oracle (test_coupling.py:180-248) ----
+from hypothesis import given, settings, strategies as hst  # noqa: E402
+
+_positions = hst.lists(hst.floats(min_value=-50.0, max_value=50.0, allow_nan=False, allow_infinity=False),
+                       min_size=2, max_size=40).filter(lambda xs: max(xs) - min(xs) > 1e-3)
+_targets = hst.tuples(hst.floats(min_value=-100.0, max_value=100.0), hst.floats(min_value=1e-6, max_value=1e4))
+
+
+@settings(max_examples=300, deadline=None)
+@given(_positions, _targets)
+def test_hypothesis_match_restrict_bitwise_oracle(mm, xs, target):
+    """Random small ensembles and targets: match, restrict and their
+    composition equal the oracle (the reference's arithmetic) bit for bit;
+    matching an ensemble to its own restriction is the identity."""
+    mu, var = target
+    x = np.array(xs)
+    ens = mm.ParticleEnsemble(x)
+    out = mm.match(mm.MacroState((mu,), (var,), (1.0,)), ens)
+    ref = O.match(np.array([mu, var, 1.0]), x)[0]
+    assert np.array_equal(out.positions, ref)
+    assert np.array_equal(mm.restrict(out).packed(), O.restrict(ref)[0])
+    assert np.array_equal(mm.match(mm.restrict(ens), ens).positions, x)
+
+
+@settings(max_examples=200, deadline=None)
+@given(hst.lists(hst.floats(min_value=-20.0, max_value=20.0, allow_nan=False, allow_infinity=False),
+                 min_size=4, max_size=40), hst.floats(min_value=-5.0, max_value=5.0))
+def test_hypothesis_two_region_match_bitwise_oracle(mm, xs, sep):
+    x = np.array(xs)
+    part_m = mm.RegionPartition(separatrices=(sep,), peaks=(sep - 1.0, sep + 1.0))
+    part_o = O.Partition((sep,), (sep - 1.0, sep + 1.0))
+    target = mm.MacroState((sep - 0.5, sep + 0.5), (0.01, 0.01), (0.5, 0.5))
+    try:
+        ref = O.match(np.array(target.packed()), x, part_o)[0]
+    except O.OracleDegenerateMatch as e:
+        with pytest.raises(mm.DegenerateMatch) as err:
+            mm.match(target, mm.ParticleEnsemble(x), part_m)
+        assert err.value.region == e.region
+        return
+    out = mm.match(target, mm.ParticleEnsemble(x), part_m)
+    assert np.array_equal(out.positions, ref)
+    assert np.array_equal(mm.restrict(out, part_m).packed(), O.restrict(ref, part_o)[0])
