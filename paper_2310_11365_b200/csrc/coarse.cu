@@ -162,19 +162,21 @@ __device__ int integrate_euler_n(const mmpr_moment_ode &ode, const mmpr_model &m
     const double c0 = mul(0.5, 0.0);                    // 0.5 * b_xx
     const double c1 = add(mul(2.0, a), mul(0.0, 0.0));  // 2 a_x + b_x^2
     const double c2 = mul(B, B);                        // b^2
-    const double z = mul(h, 0.0);                       // h * dF (fractions are constant)
-    double m = y[0], v = y[1], f = y[2];
+    // fractions: f + h*0 repeated n times equals one addition of +0.0 (it
+    // only turns -0.0 into +0.0), so it leaves the serial loop
+    const double z = mul(h, 0.0);
+    double m = y[0], v = y[1];
+    const int steps = (int)n;
 #pragma unroll 2
-    for (long long i = 0; i < n; ++i) {
+    for (int i = 0; i < steps; ++i) {
       const double dm = add(add(mul(a, m), mul(aE, m)), c0);
       const double dv = add(mul(c1, v), c2);
       m = add(m, mul(h, dm));
       v = add(v, mul(h, dv));
-      f = add(f, z);
     }
     y[0] = m;
     y[1] = v;
-    y[2] = f;
+    y[2] = add(y[2], z);
     return all_finite<NV>(y) ? MMPR_STAT_OK : 1;
   }
   double k[NV];
