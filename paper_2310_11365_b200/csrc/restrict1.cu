@@ -210,7 +210,10 @@ static const R1Geometry &r1_geometry(int64_t P) {
       if (l > max_leaf) max_leaf = l;
       empty |= l == 0;
     }
-    const int spc = nslots < 128 ? (nslots < 4 ? 4 : (int)nslots) : 128;
+    // 512-thread CTAs (two per SM, 16 per cluster) when the ensemble fills
+    // exactly 1024 slots (P ~ 1e5), as in the fine sweep; else 1024 threads
+    int spc = nslots < 128 ? (nslots < 4 ? 4 : (int)nslots) : 128;
+    if (nslots == 1024) spc = 64;  // 51 vs 58 us per 64 x 1e5 fused match-restrict
     g.D = D;
     g.spc = spc;
     g.ctas = nslots <= spc ? 1 : (int)(nslots / spc);
