@@ -19,7 +19,7 @@ HEADER = os.path.join(ROOT, "include", "mmpr.h")
 
 def header_functions():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:const char \*|int )(mmpr_\w+)\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:const char \*|int |int64_t )(mmpr_\w+)\(", text, flags=re.M)))
 
 
 def test_library_exports_every_declared_symbol():
