@@ -327,3 +327,26 @@ def test_random_sizes_sweep_bitwise(mm):
             ref = O.propagate_fine(om, x0[n], 0, 0.0, 1e-3, S, xi_h[n])
             assert np.array_equal(got[n], ref), P
             assert np.array_equal(st[n], O.restrict(ref)[0]), P
+
+
+@pytest.mark.parametrize("cl", ["1", "4", "8"])
+def test_grid_cluster_levels_bitwise(mm, monkeypatch, cl):
+    """The grid sweep's first reduction level in clusters of 1/4/8 CTAs (the
+    default is 2) gives the same bits (P = 2^20, 128 CTAs per team)."""
+    from paper_2310_11365_b200 import kernels
+    import torch
+    monkeypatch.setenv("MMPR_FINE_GRID_CLUSTER", cl)
+    P, N, S = 1 << 20, 3, 4
+    rng = np.random.default_rng(int(cl))
+    x0 = rng.normal(0.0, 1.0, (N, P))
+    xi_h = rng.standard_normal((N, S, P))
+    xi = kernels.noise_buffer(N, S, P)
+    xi[:, :, :P] = torch.from_numpy(xi_h).cuda()
+    out = torch.empty((N, P), dtype=torch.float64, device="cuda")
+    bad = torch.empty(N, dtype=torch.int32, device="cuda")
+    kernels.fine_sweep(GPU_MODELS["ou"](mm).descriptor, torch.from_numpy(x0).cuda(), out,
+                       torch.zeros(N, dtype=torch.float64, device="cuda"), S, 1e-3, xi, bad)
+    got = out.cpu().numpy()
+    om = O.model_ou(-1.0, 0.5, 0.5)
+    for n in (0, N - 1):
+        assert np.array_equal(got[n], O.propagate_fine(om, x0[n], 0, 0.0, 1e-3, S, xi_h[n]))
