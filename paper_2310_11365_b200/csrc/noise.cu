@@ -168,7 +168,14 @@ __device__ __noinline__ double tail_token(uint64_t wi, uint64_t mant, uint64_t k
 __device__ __forceinline__ bool wedge_accepts(int layer, double x, uint64_t next_word) {
   const double u = np::unit_double(next_word);
   const double lhs = add(mul(sub(c_zig_fi[layer - 1], c_zig_fi[layer]), u), c_zig_fi[layer]);
-  return lhs < exp(mul(mul(-0.5, x), x));
+  const double q = mul(mul(-0.5, x), x);  // in [-6.7, 0] for wedge draws
+  // single-precision filter: expf((float)q) is within 1e-6 of exp(q)
+  // relative here (rounding of q times |q|, plus expf's 2 ulp), so only
+  // draws within 4e-6 of the boundary need the double-precision exp
+  const double ef = (double)expf((float)q);
+  if (lhs < ef * (1.0 - 0x1.0p-18)) return true;
+  if (lhs > ef * (1.0 + 0x1.0p-18)) return false;
+  return lhs < exp(q);
 }
 
 // ---------------------------------------------------------------------------
@@ -405,21 +412,16 @@ __device__ __forceinline__ void wedge_parse8(uint32_t nf, int e, uint32_t &S, in
   exit = (((w & s_rel) >> (width - 1)) & 1u) ? 1 : 0;
 }
 
-// Exact lane parse from entry e with tail tokens present (rare path).
-__device__ __noinline__ void general_parse8(uint32_t nf, uint32_t tt, int e, uint64_t word0, uint64_t k0,
-                                            uint64_t k1, uint32_t *S_out, int *exit_out) {
+// Exact lane parse from entry e with tail tokens present (rare path); the
+// tail lengths were measured once by the work-list pass (tlen).
+__device__ __noinline__ void general_parse8(uint32_t nf, uint32_t tt, int e, const uint16_t *tlen,
+                                            uint32_t *S_out, int *exit_out) {
   uint32_t S = 0;
   int pos = e;
   while (pos < NW_WORDS) {
     S |= 1u << pos;
     int L = 1;
-    if ((nf >> pos) & 1u) {
-      if ((tt >> pos) & 1u) {
-        tail_token(word0 + pos, 0, k0, k1, &L);  // length only
-      } else {
-        L = 2;
-      }
-    }
+    if ((nf >> pos) & 1u) L = ((tt >> pos) & 1u) ? (int)tlen[pos] : 2;
     pos += L;
   }
   *S_out = S;
@@ -449,6 +451,8 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
   __shared__ uint64_t s_words[32 * NW_WORDS];  // this sub-chunk's words, stream order
   __shared__ uint16_t s_item[32 * NW_WORDS];   // positions of the non-fast words
   __shared__ uint8_t s_res[32 * NW_WORDS];     // per word: bit0 produces, bit1 tail
+  __shared__ double s_tval[32 * NW_WORDS];     // tail starts: value and length in words
+  __shared__ uint16_t s_tlen[32 * NW_WORDS];
   const int lane = threadIdx.x;
 #pragma unroll
   for (int i = lane; i < 256; i += 32)
@@ -493,6 +497,7 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
       }
       const int n_items = __shfl_sync(MMPR_FULL_MASK, incl, 31);
       if (n_items > 0) {
+        __syncwarp();  // the previous sub-chunk's tail reads are done
         *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 0]) = make_ulonglong2(w[0], w[1]);
         *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 2]) = make_ulonglong2(w[2], w[3]);
         *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 4]) = make_ulonglong2(w[4], w[5]);
@@ -518,8 +523,11 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
                                   -0x1.0p52 * wi);
               if ((rw >> 8) & 1) v = -v;
               res = wedge_accepts(layer, v, nx) ? 1 : 0;
-            } else {
-              res = 3;  // tail start: always produces
+            } else {  // tail start: always produces; value and length once, here
+              int L;
+              s_tval[pos] = tail_token(sub * 32 * NW_WORDS + pos, (rw >> 9) & 0x000fffffffffffffULL, k0, k1, &L);
+              s_tlen[pos] = (uint16_t)L;
+              res = 3;
             }
             s_res[pos] = res;
           }
@@ -538,7 +546,7 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
     uint32_t S;
     int ex, ecur = 0;
     if (tt == 0) wedge_parse8(nf, 0, S, ex);
-    else general_parse8(nf, tt, 0, word0, k0, k1, &S, &ex);
+    else general_parse8(nf, tt, 0, &s_tlen[lane * NW_WORDS], &S, &ex);
     for (;;) {
       int e = __shfl_up_sync(MMPR_FULL_MASK, ex, 1);
       if (lane == 0) e = carry;
@@ -553,7 +561,7 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
         } else if (tt == 0) {
           wedge_parse8(nf, e, S, ex);
         } else {
-          general_parse8(nf, tt, e, word0, k0, k1, &S, &ex);
+          general_parse8(nf, tt, e, &s_tlen[lane * NW_WORDS], &S, &ex);
         }
         ecur = e;
       }
@@ -589,8 +597,7 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
       const int i = __ffs(rem) - 1;
       const int64_t idx = base + __popc(O & ((1u << i) - 1u));
       if (idx < count) {
-        int L;
-        const double v = tail_token(word0 + i, (pick8(w, i) >> 9) & 0x000fffffffffffffULL, k0, k1, &L);
+        const double v = s_tval[lane * NW_WORDS + i];
         o[idx] = AFFINE ? add(loc, mul(scale, v)) : v;
       }
     }
