@@ -164,10 +164,12 @@ __device__ __noinline__ double tail_token(uint64_t wi, uint64_t mant, uint64_t k
   }
 }
 
-// Wedge test of layer `layer` at x with the next word's uniform.
-__device__ __forceinline__ bool wedge_accepts(int layer, double x, uint64_t next_word) {
+// Wedge test of layer `layer` at x with the next word's uniform (fi: the
+// fi table, constant or shared memory).
+__device__ __forceinline__ bool wedge_accepts(int layer, double x, uint64_t next_word,
+                                              const double *fi = c_zig_fi) {
   const double u = np::unit_double(next_word);
-  const double lhs = add(mul(sub(c_zig_fi[layer - 1], c_zig_fi[layer]), u), c_zig_fi[layer]);
+  const double lhs = add(mul(sub(fi[layer - 1], fi[layer]), u), fi[layer]);
   const double q = mul(mul(-0.5, x), x);  // in [-6.7, 0] for wedge draws
   // single-precision filter: expf((float)q) is within 1e-6 of exp(q)
   // relative here (rounding of q times |q|, plus expf's 2 ulp), so only
@@ -448,15 +450,15 @@ __global__ void __launch_bounds__(32, 16)
 normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__restrict__ out, int64_t pitch,
                          double loc, double scale) {
   __shared__ ulonglong2 zig[256];
-  __shared__ uint64_t s_words[32 * NW_WORDS];  // this sub-chunk's words, stream order
-  __shared__ uint16_t s_item[32 * NW_WORDS];   // positions of the non-fast words
-  __shared__ uint8_t s_res[32 * NW_WORDS];     // per word: bit0 produces, bit1 tail
-  __shared__ double s_tval[32 * NW_WORDS];     // tail starts: value and length in words
+  __shared__ double s_fi[256];
+  __shared__ double s_tval[32 * NW_WORDS];  // tail starts (lane-private slots): value, length in words
   __shared__ uint16_t s_tlen[32 * NW_WORDS];
   const int lane = threadIdx.x;
 #pragma unroll
-  for (int i = lane; i < 256; i += 32)
+  for (int i = lane; i < 256; i += 32) {
     zig[i] = make_ulonglong2(c_zig_ki[i], (unsigned long long)__double_as_longlong(c_zig_wi[i]));
+    s_fi[i] = c_zig_fi[i];
+  }
   __syncwarp();
   const uint64_t k0 = keys[2 * blockIdx.x], k1 = keys[2 * blockIdx.x + 1];
   double *o = out + (int64_t)blockIdx.x * pitch;
@@ -483,63 +485,38 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
       x[i] = __hiloint2double(__double2hiint(v) ^ (int)(((uint32_t)rw << 23) & 0x80000000u), __double2loint(v));
       nf |= (mant >= z.x ? 1u : 0u) << i;
     }
-    // Rare words (~2.2%): wedge tests and tail starts, processed by the whole
-    // warp -- each lane tests one queued word, so the double-precision exp of
-    // the wedge test runs once per sub-chunk instead of once per lane bit.
+    // Rare words (~2.2%, ~0.2 per lane): each lane tests its own non-fast
+    // words in order, all lanes together, so the wedge test's arithmetic runs
+    // once per round for the warp (one round in ~2/3 of the sub-chunks, two
+    // in most of the rest); tail values and lengths go to lane-private slots.
     uint32_t pr = ~nf & 0xffu, tt = 0;
-    {
-      const int mine = __popc(nf);
-      int incl = mine;
+    for (uint32_t rem = nf; __any_sync(MMPR_FULL_MASK, rem != 0);) {
+      if (rem) {
+        const int i = __ffs(rem) - 1;
+        rem &= rem - 1;
+        uint64_t rw = w[0], nx = w[1];
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int v = __shfl_up_sync(MMPR_FULL_MASK, incl, d);
-        if (lane >= d) incl += v;
-      }
-      const int n_items = __shfl_sync(MMPR_FULL_MASK, incl, 31);
-      if (n_items > 0) {
-        __syncwarp();  // the previous sub-chunk's tail reads are done
-        *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 0]) = make_ulonglong2(w[0], w[1]);
-        *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 2]) = make_ulonglong2(w[2], w[3]);
-        *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 4]) = make_ulonglong2(w[4], w[5]);
-        *reinterpret_cast<ulonglong2 *>(&s_words[lane * NW_WORDS + 6]) = make_ulonglong2(w[6], w[7]);
-        int q = incl - mine;
-        for (uint32_t rem = nf; rem; rem &= rem - 1) s_item[q++] = (uint16_t)(lane * NW_WORDS + __ffs(rem) - 1);
-        __syncwarp();
-        for (int base = 0; base < n_items; base += 32) {
-          const int it = base + lane;
-          if (it < n_items) {
-            const int pos = s_item[it];
-            const uint64_t rw = s_words[pos];
-            const int layer = (int)(rw & 0xff);
-            uint8_t res;
-            if (layer != 0) {
-              // the last word's successor opens the next sub-chunk: computed
-              // out of line (hoisted, it cost 14% of the kernel's instructions)
-              const uint64_t nx = (pos + 1 < 32 * NW_WORDS) ? s_words[pos + 1]
-                                  : successor_word(sub * 32 * NW_WORDS + 32 * NW_WORDS, k0, k1);
-              const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
-              const double wi = c_zig_wi[layer];
-              double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi,
-                                  -0x1.0p52 * wi);
-              if ((rw >> 8) & 1) v = -v;
-              res = wedge_accepts(layer, v, nx) ? 1 : 0;
-            } else {  // tail start: always produces; value and length once, here
-              int L;
-              s_tval[pos] = tail_token(sub * 32 * NW_WORDS + pos, (rw >> 9) & 0x000fffffffffffffULL, k0, k1, &L);
-              s_tlen[pos] = (uint16_t)L;
-              res = 3;
-            }
-            s_res[pos] = res;
+        for (int k = 1; k < NW_WORDS; ++k)
+          if (i == k) {
+            rw = w[k];
+            nx = k + 1 < NW_WORDS ? w[k + 1] : succ;
           }
+        const int layer = (int)(rw & 0xff);
+        const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
+        if (layer != 0) {
+          // the last lane's last word: its successor opens the next sub-chunk
+          if (i == NW_WORDS - 1 && lane == 31) nx = successor_word(word0 + NW_WORDS, k0, k1);
+          const double wi = __longlong_as_double((long long)zig[layer].y);
+          double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
+          if ((rw >> 8) & 1) v = -v;
+          pr |= (wedge_accepts(layer, v, nx, s_fi) ? 1u : 0u) << i;
+        } else {  // tail start: always produces
+          int L;
+          s_tval[lane * NW_WORDS + i] = tail_token(word0 + i, mant, k0, k1, &L);
+          s_tlen[lane * NW_WORDS + i] = (uint16_t)L;
+          pr |= 1u << i;
+          tt |= 1u << i;
         }
-        __syncwarp();
-        for (uint32_t rem = nf; rem; rem &= rem - 1) {
-          const int i = __ffs(rem) - 1;
-          const uint8_t res = s_res[lane * NW_WORDS + i];
-          pr |= (uint32_t)(res & 1) << i;
-          tt |= (uint32_t)(res >> 1) << i;
-        }
-        __syncwarp();  // s_words/s_item/s_res are rewritten by the next sub-chunk
       }
     }
     // lane parse from entry 0, then stitch entries lane to lane until stable
