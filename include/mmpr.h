@@ -307,6 +307,63 @@ int mmpr_integrate_macro(const mmpr_moment_ode *ode, const mmpr_model *model,
                          double *state_out, int32_t *status, void *stream);
 
 /* ------------------------------------------------------------------ */
+/* Iterations 1..K of run_micro_macro in one persistent kernel         */
+/* (engine.py:197-238: fine sweep, serial correction, match, micro     */
+/* restriction of every iteration, dependency-driven per (k, n) unit)  */
+/* ------------------------------------------------------------------ */
+
+/* Device buffers of one run (all caller-owned; shapes in doubles/ints).
+ * The prologue (iteration 0: rho0 = R(ens0), macro/cache row 0 by
+ * mmpr_coarse_row, the lifted snapshot row 0 with micro row 0, the
+ * increments) must already be on the stream; the pipeline writes every
+ * row k >= 1 of macro/micro/micro_counts/cache/coarse_status/match_status,
+ * all rows of fine_stats/fine_counts/raw/bad, and snapshot rows 1..K. */
+typedef struct mmpr_pipeline_io {
+  const double *times;        /* [N+1] slice boundaries */
+  const double *x0;           /* [P] ens0 */
+  const double *rho0;         /* [3] R(ens0) */
+  const int64_t *counts0;     /* [1] */
+  const double *xi;           /* increments, slice n step j at xi + n*xi_slice_pitch + j*xi_row_pitch */
+  int64_t xi_slice_pitch, xi_row_pitch;
+  double *snap;               /* snapshot row k slice n at snap + k'*snap_iter_stride + n*snap_slice_pitch */
+  int64_t snap_iter_stride, snap_slice_pitch;
+  int32_t snap_rows;          /* K+1 (k' = k) or 2 (k' = k % 2, retain_snapshots=False) */
+  double *fine;               /* [2][N] rows of fine_pitch: F^k_n in row (k%2)*N + n */
+  int64_t fine_pitch;
+  double *macro;              /* [K+1][N+1][3] */
+  double *micro;              /* [K+1][N+1][3] */
+  int64_t *micro_counts;      /* [K+1][N+1] */
+  double *fine_stats;         /* [K][N][3] */
+  int64_t *fine_counts;       /* [K][N] */
+  double *raw;                /* [K][N][3] */
+  double *cache;              /* [K+1][N][3] (row 0 from the prologue) */
+  int32_t *bad;               /* [K][N] */
+  int32_t *coarse_status;     /* [K+1][N] */
+  int32_t *match_status;      /* [K+1][N] */
+  int32_t *flags;             /* [mmpr_pipeline_flags_size(N, K)] scratch, reset by the call */
+} mmpr_pipeline_io;
+
+/* int32 scratch words the pipeline needs for (n_slices, iterations). */
+int64_t mmpr_pipeline_flags_size(int32_t n_slices, int32_t iterations);
+
+/* MMPR_OK when (model, ode, ode_model, integrator, particles) has a pipeline
+ * instantiation (single region, MEAN_OF_F, forward-Euler coarse, the
+ * 16 x 512-thread cluster geometry of P ~ 1e5); else MMPR_ERR_UNSUPPORTED
+ * and the caller runs the per-iteration kernels. */
+int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_moment_ode *ode,
+                            const mmpr_model *ode_model, const mmpr_integrator *integ,
+                            int64_t particles);
+
+/* Runs iterations 1..iterations (raise policy for the matches, predictions
+ * of converged slices reused when reuse_converged != 0, as mmpr_coarse_row's
+ * skip_until).  Bitwise identical to the per-iteration kernel sequence. */
+int mmpr_parareal_pipeline(const mmpr_model *model, const mmpr_moment_ode *ode,
+                           const mmpr_model *ode_model, const mmpr_integrator *integ,
+                           int32_t n_slices, int32_t iterations,
+                           int64_t particles, int32_t steps, double dt, double sqrt_dt,
+                           int32_t reuse_converged, const mmpr_pipeline_io *io, void *stream);
+
+/* ------------------------------------------------------------------ */
 /* Error metrics (metrics.py:35-47, 73-130, 133-218)                   */
 /* ------------------------------------------------------------------ */
 

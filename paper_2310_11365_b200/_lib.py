@@ -76,6 +76,19 @@ class Integrator(ctypes.Structure):
                 ("abs_tol", ctypes.c_double), ("first_step", ctypes.c_double)]
 
 
+class PipelineIO(ctypes.Structure):
+    """mmpr_pipeline_io: device buffers of one run of the iteration pipeline."""
+    _fields_ = [("times", ctypes.c_void_p), ("x0", ctypes.c_void_p), ("rho0", ctypes.c_void_p),
+                ("counts0", ctypes.c_void_p), ("xi", ctypes.c_void_p), ("xi_slice_pitch", ctypes.c_int64),
+                ("xi_row_pitch", ctypes.c_int64), ("snap", ctypes.c_void_p), ("snap_iter_stride", ctypes.c_int64),
+                ("snap_slice_pitch", ctypes.c_int64), ("snap_rows", ctypes.c_int32), ("fine", ctypes.c_void_p),
+                ("fine_pitch", ctypes.c_int64), ("macro", ctypes.c_void_p), ("micro", ctypes.c_void_p),
+                ("micro_counts", ctypes.c_void_p), ("fine_stats", ctypes.c_void_p),
+                ("fine_counts", ctypes.c_void_p), ("raw", ctypes.c_void_p), ("cache", ctypes.c_void_p),
+                ("bad", ctypes.c_void_p), ("coarse_status", ctypes.c_void_p), ("match_status", ctypes.c_void_p),
+                ("flags", ctypes.c_void_p)]
+
+
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -108,6 +121,9 @@ SIGNATURES = {
     "mmpr_sort_rows": (ctypes.c_int, [_I32, _I64, _P, _P, _I64, _P, _P, _P]),
     "mmpr_mean_abs_diff": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I64, _P, _P]),
     "mmpr_histogram_sorted": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I32, _P, _P]),
+    "mmpr_pipeline_flags_size": (ctypes.c_int64, [_I32, _I32]),
+    "mmpr_pipeline_supported": (ctypes.c_int, [_P, _P, _P, _P, _I64]),
+    "mmpr_parareal_pipeline": (ctypes.c_int, [_P, _P, _P, _P, _I32, _I32, _I64, _I32, _D, _D, _I32, _P, _P]),
 }
 
 _lib = None
@@ -139,7 +155,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
 LAUNCHING = frozenset({"mmpr_noise_keys", "mmpr_entropy_key", "mmpr_normals_fill", "mmpr_fine_sweep",
                        "mmpr_fine_sweep_restrict", "mmpr_match_restrict",
                        "mmpr_restrict", "mmpr_match", "mmpr_coarse_row", "mmpr_integrate_macro",
-                       "mmpr_mean_abs_diff"})
+                       "mmpr_mean_abs_diff", "mmpr_parareal_pipeline"})
 launch_count = {"total": 0}
 
 

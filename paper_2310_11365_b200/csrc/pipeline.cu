@@ -1,0 +1,702 @@
+// Iterations 1..K of mM-Parareal as one persistent, dependency-driven kernel.
+//
+// Replaces, for single-region MEAN_OF_F runs, the per-iteration launch
+// sequence fine sweep -> coarse row -> match + micro restriction of
+// engine.run_micro_macro (/root/reference/pkg/src/mcparareal/engine.py:
+// 197-238; particles.propagate_fine particles.py:146-159; coupling.match /
+// restrict coupling.py:26-95; the serial correction engine.py:210-236).
+//
+// Work unit (k, n), k = 0..K, n = 0..N, one thread-block cluster per unit
+// (same leaf-slot layout and per-step cluster reduction as fine.cu):
+//   match part (k >= 1, n >= 1): the serial correction of boundary n of row
+//     k -- pred = C(macro[k][n-1]) (or the cached prediction of a converged
+//     slice, n-1 < k), corrected = R(F^{k-1}_{n-1}) + (pred - cache[k-1][n-1]),
+//     negative variance clamped -- then u^k_n = match(corrected, F^{k-1}_{n-1})
+//     and micro[k][n] = R(u^k_n), from registers;
+//   fine part (k < K, n < N): F^k_n = F(u^k_n) with the particles still in
+//     registers, and R(F^k_n) fused as in fine.cu.
+// Units are taken in ticket order (k-major) by whichever cluster is free, and
+// a unit waits only on units with smaller tickets:
+//   fine_done[k-1][n-1]  (F^{k-1}_{n-1} and its restriction),
+//   chain_done[k][n-1]   (macro[k][n-1], the serial chain of row k),
+//   chain_done[k-1][n]   (cache[k-1][n-1]),
+//   consumed[k-1][n+1]   (the reader of the fine buffer slot this unit
+//                          overwrites has loaded it).
+// So row k+1 starts on the SMs that row k's last wave leaves idle, the serial
+// coarse chain and the match run inside the units that need them, and no
+// kernel boundary separates the iterations.  Every value is computed with
+// the same operations in the same order as the per-iteration kernels, so the
+// trace is bitwise identical to theirs (tests/test_gpu_pipeline.py).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <type_traits>
+
+#include "capi_internal.h"
+#include "coarse_device.cuh"
+#include "fine_common.cuh"
+#include "mmpr_device.cuh"
+
+namespace mmpr {
+
+struct PipeParams {
+  FineParams f;  // model, S, P, dt, sqrt_dt, bsd, increments, cluster geometry
+  mmpr_moment_ode ode;
+  mmpr_model ode_model;  // the model the moment ODE was built from
+  mmpr_integrator integ;
+  mmpr_pipeline_io io;
+  int N, K;
+  int units;
+  int reuse;  // cached predictions for converged slices (engine skip_until)
+  int retain;
+  int *ticket;
+  int *fine_done;   // [K][N]
+  int *chain_done;  // [K+1][N+1]
+  int *consumed;    // [K+1][N+1]
+};
+
+__device__ __forceinline__ int pl_ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void pl_red_release(int *p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Spin until *p >= target.  A dependency that never arrives is a bug; the
+// watchdog (~9 s) turns it into a kernel fault instead of a hung device.
+__device__ __forceinline__ void pl_wait(const int *p, int target) {
+  if (pl_ld_acquire(p) >= target) return;
+  const long long t0 = clock64();
+  while (pl_ld_acquire(p) < target) {
+    __nanosleep(64);
+    if (clock64() - t0 > (1LL << 34)) __trap();
+  }
+}
+
+enum { PL_KEEP = 0, PL_SET = 1, PL_AFFINE = 2 };
+
+template <int KIND, int PPT, bool HAS_TAIL, int OK, int MK>
+__global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
+  constexpr int LO = PPT - 1;  // every leaf has PPT-1 or PPT accumulator elements per lane
+  using PartT = Part<false>;
+  const FineParams &p = pp.f;
+  const mmpr_pipeline_io &io = pp.io;
+  extern __shared__ __align__(128) double s_stage[];  // [nstages][stage_elems]
+  __shared__ PartT s_wp[2][32];
+  __shared__ __align__(16) ClusterSlot s_slot[2][FS_MAX_CLUSTER];
+  __shared__ int s_bad[3];
+  __shared__ __align__(8) uint64_t s_bar[FS_MAX_STAGES];
+  __shared__ __align__(8) uint64_t s_red_bar[2];
+  __shared__ int s_ticket[2];
+  __shared__ double s_match[3];  // mu, scale, mc
+  __shared__ int s_mode;
+  __shared__ const double *s_xi_base;  // this CTA's increments of the unit's slice, step 0
+  __shared__ uint32_t s_stage_bytes;
+
+  const int lane = threadIdx.x & 31;
+  const int gthreads = (int)blockDim.x;
+  const int tid = (int)threadIdx.x;
+  const int warp = tid >> 5;
+  const int nwarps = gthreads >> 5;
+  const int rank = (p.ctas > 1) ? (int)cluster_ctarank() : 0;
+  const int N = pp.N, K = pp.K;
+
+  // ---- my leaf (fine.cu layout; P < 2^31 here, so 32-bit offsets) ------------
+  const int64_t slot = (int64_t)rank * p.slots_per_cta + warp * 4 + (lane >> 3);
+  const int j8 = lane & 7;
+  int off, cnt, tail, tail_off, lo;
+  int last_idx;
+  {
+    int64_t o64 = 0, l64 = 0, lo64, hi64, o2, l2;
+    pw_leaf(p.P, p.D, slot, &o64, &l64);
+    pw_leaf(p.P, p.D, (int64_t)rank * p.slots_per_cta, &lo64, &l2);
+    if (rank == p.ctas - 1) hi64 = p.P;
+    else pw_leaf(p.P, p.D, (int64_t)(rank + 1) * p.slots_per_cta, &hi64, &o2);
+    off = (int)o64;
+    cnt = (int)(l64 >> 3);
+    tail = (int)(l64 & 7);
+    tail_off = (int)(o64 + (l64 & ~int64_t(7)));
+    lo = (int)lo64;
+    last_idx = (int)(hi64 - lo64) - 1;
+    if (tid == 0) s_stage_bytes = (uint32_t)((((hi64 - lo64) * 8) + 15) & ~int64_t(15));
+  }
+  const int my_idx = off - lo + j8;
+  const int ns = p.nstages;
+
+  if (tid == 0) {
+    for (int q = 0; q < ns; ++q) mbar_init(&s_bar[q], 1);
+    mbar_init(&s_red_bar[0], 1);
+    mbar_init(&s_red_bar[1], 1);
+    fence_mbar_init();
+    s_bad[0] = s_bad[1] = s_bad[2] = 0;
+  }
+  if (p.ctas > 1) cluster_sync_all();
+  else __syncthreads();
+
+  double x[PPT];
+  double xt = 0.0;
+  uint32_t ld = 0;  // increment loads issued (and completed) before this unit
+  uint32_t r = 0;   // reduction calls made by this CTA (cluster-uniform sequence)
+
+  // Pairwise-tree sum of x (or of (x - c)^2) over the ensemble, then / P;
+  // as fine.cu's reduce (B1, warp fold, one st.async per peer CTA).
+  // `refill` >= 0: the unit's step whose increments go into the stage freed
+  // by the step just taken.
+  auto reduce = [&](auto centered, double c, int refill, double &mean_out, int &bad_out) {
+    constexpr bool CEN = decltype(centered)::value;
+    auto f = [&](double v) {
+      if constexpr (CEN) {
+        const double d = sub(v, c);
+        return mul(d, d);
+      } else {
+        return v;
+      }
+    };
+    const int par = r & 1;
+    const int bslot = r % 3;
+    double acc = f(x[0]);
+#pragma unroll
+    for (int m = 1; m < PPT; ++m) {
+      if (m < LO) {
+        acc = add(acc, f(x[m]));
+      } else {
+        const double t = add(acc, f(x[m]));
+        acc = (m < cnt) ? t : acc;
+      }
+    }
+    acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 1));
+    acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 2));
+    acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 4));
+    if (HAS_TAIL) {
+      const double ft = f(xt);
+#pragma unroll
+      for (int i = 0; i < 7; ++i) {
+        const double v = __shfl_sync(MMPR_FULL_MASK, ft, (lane & ~7) | i);
+        if (i < tail) acc = add(acc, v);
+      }
+    }
+    int bad_local = 0;
+    if (!CEN && !finite(acc)) {
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) bad_local |= (m < cnt && !finite(x[m])) ? 1 : 0;
+      if (HAS_TAIL && j8 < tail) bad_local |= !finite(xt);
+    }
+    const int wbad = __any_sync(MMPR_FULL_MASK, bad_local);
+    PartT leaf = PartT::make(acc, true);
+    leaf = leaf.xor_level(lane, 8);
+    leaf = leaf.xor_level(lane, 16);
+    if (lane == 0) {
+      s_wp[par][warp] = leaf;
+      if (wbad) s_bad[bslot] = 1;
+    }
+    __syncthreads();  // B1
+    if (tid == gthreads - 32) {
+      s_bad[(r + 2) % 3] = 0;
+      if (refill >= 0) {
+        const uint32_t q = ld + (uint32_t)refill;
+        const int st = (int)(q % (uint32_t)ns);
+        const uint32_t bytes = s_stage_bytes;
+        const double *base = s_xi_base;
+        mbar_arrive_expect_tx(&s_bar[st], bytes);
+        bulk_g2s(s_stage + st * p.stage_elems, base + (int64_t)refill * p.xi_row_pitch, bytes, &s_bar[st]);
+        const int pf = refill + p.l2_ahead;
+        if (p.l2_ahead > 0 && pf < p.S) prefetch_l2(base + (int64_t)pf * p.xi_row_pitch, bytes);
+      }
+    }
+    PartT v = (lane < nwarps) ? s_wp[par][lane] : PartT::make(0.0, false);
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1)
+      if (m < nwarps) v = v.xor_level(lane, m);
+    double total;
+    int bad = s_bad[bslot];
+    if (p.ctas > 1) {
+      if (tid == 0) mbar_arrive_expect_tx(&s_red_bar[par], 16u * (uint32_t)p.ctas);
+      if (warp == 0 && lane < p.ctas) {
+        const uint32_t remote = mapa_shared(smem_addr(&s_slot[par][rank]), (uint32_t)lane);
+        const uint32_t rbar = mapa_shared(smem_addr(&s_red_bar[par]), (uint32_t)lane);
+        st_async_v2(remote, __double_as_longlong(v.v),
+                    (unsigned long long)1u | ((unsigned long long)(uint32_t)bad << 32), rbar);
+      }
+      mbar_wait_parity(&s_red_bar[par], (r >> 1) & 1u);
+      PartT cc = PartT::make(0.0, false);
+      int b = 0;
+      if (lane < p.ctas) {
+        cc = PartT::make(s_slot[par][lane].v, true);
+        b = s_slot[par][lane].bad;
+      }
+#pragma unroll
+      for (int m = 1; m < FS_MAX_CLUSTER; m <<= 1)
+        if (m < p.ctas) cc = cc.xor_level(lane, m);
+      total = __shfl_sync(MMPR_FULL_MASK, cc.v, 0);
+      bad = __any_sync(MMPR_FULL_MASK, b);
+    } else {
+      total = __shfl_sync(MMPR_FULL_MASK, v.v, 0);
+    }
+    mean_out = div(total, (double)p.P);
+    bad_out = bad;
+    ++r;
+  };
+  using Plain = std::integral_constant<bool, false>;
+  using Centered = std::integral_constant<bool, true>;
+
+  const int64_t fpitch = io.fine_pitch;
+  for (int it = 0;; ++it) {
+    // ---- next ticket, broadcast to the cluster ---------------------------------
+    if (rank == 0 && tid == 0) {
+      const int t = atomicAdd(pp.ticket, 1);
+      if (p.ctas > 1) {
+        for (int c = 0; c < p.ctas; ++c) st_cluster_u32(mapa_shared(smem_addr(&s_ticket[it & 1]), (uint32_t)c), t);
+      } else {
+        s_ticket[it & 1] = t;
+      }
+    }
+    if (p.ctas > 1) cluster_sync_all();
+    else __syncthreads();
+    const int t = s_ticket[it & 1];
+    if (t >= pp.units) break;
+    const int k = t / (N + 1), n = t % (N + 1);
+    const bool has_match = k >= 1 && n >= 1;
+    const bool has_fine = k < K && n < N;
+    const int64_t srow = pp.retain ? k : (k & 1);
+    double *snap_kn = io.snap + srow * io.snap_iter_stride + (int64_t)n * io.snap_slice_pitch;
+
+    // the increments do not depend on anything: start their copies first
+    if (has_fine && tid == 0) {
+      const double *base = io.xi + (int64_t)n * io.xi_slice_pitch + lo;
+      const uint32_t bytes = s_stage_bytes;
+      s_xi_base = base;  // read by the refill thread after the next block barrier
+      for (int j = 0; j < ns && j < p.S; ++j) {
+        const int st = (int)((ld + (uint32_t)j) % (uint32_t)ns);
+        mbar_arrive_expect_tx(&s_bar[st], bytes);
+        bulk_g2s(s_stage + st * p.stage_elems, base + (int64_t)j * p.xi_row_pitch, bytes, &s_bar[st]);
+      }
+      for (int j = ns; j < ns + p.l2_ahead && j < p.S; ++j) prefetch_l2(base + (int64_t)j * p.xi_row_pitch, bytes);
+    }
+
+    double s = 0.0;
+    bool mean_known = false;
+    if (has_match) {
+      // ---- serial correction of boundary n, then the match parameters ---------
+      if (tid == 0) {
+        pl_wait(pp.fine_done + (int64_t)(k - 1) * N + (n - 1), p.ctas);
+        if (n - 1 >= 1) pl_wait(pp.chain_done + (int64_t)k * (N + 1) + (n - 1), 1);
+        if (k - 1 >= 1) pl_wait(pp.chain_done + (int64_t)(k - 1) * (N + 1) + n, 1);
+        // row 0's reader of this snapshot slot (units (0, n < N) read it)
+        if (!pp.retain && k == 2 && n < N) pl_wait(pp.consumed + n, p.ctas);
+        const double *prev = (n - 1 == 0) ? io.rho0 : io.macro + ((int64_t)k * (N + 1) + (n - 1)) * 3;
+        const double *fs = io.fine_stats + ((int64_t)(k - 1) * N + (n - 1)) * 3;
+        const double *cin = io.cache + ((int64_t)(k - 1) * N + (n - 1)) * 3;
+        double cur[3], f[3], c[3], pred[3], raw[3];
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          cur[v] = __ldcg(prev + v);
+          f[v] = __ldcg(fs + v);
+          c[v] = __ldcg(cin + v);
+        }
+        int st = MMPR_STAT_OK;
+        if (pp.reuse && n - 1 < k) {
+#pragma unroll
+          for (int v = 0; v < 3; ++v) pred[v] = c[v];
+        } else {
+#pragma unroll
+          for (int v = 0; v < 3; ++v) pred[v] = cur[v];
+          long long steps;
+          double h;
+          const double t0 = __ldg(io.times + n - 1);
+          euler_grid(pp.integ.dt, t0, __ldg(io.times + n), &steps, &h);
+          st = integrate_euler_n<3, OK, MK>(pp.ode, pp.ode_model, steps, h, t0, pred);
+        }
+#pragma unroll
+        for (int v = 0; v < 3; ++v) raw[v] = add(f[v], sub(pred[v], c[v]));
+        const bool neg = raw[1] < 0.0;
+        double nxt[3] = {raw[0], (neg && raw[1] < 0.0) ? 0.0 : raw[1], f[2]};
+        if (rank == 0) {
+          const int64_t e = (int64_t)(k - 1) * N + (n - 1);
+          io.coarse_status[(int64_t)k * N + (n - 1)] = st;
+#pragma unroll
+          for (int v = 0; v < 3; ++v) {
+            io.cache[((int64_t)k * N + (n - 1)) * 3 + v] = pred[v];
+            io.raw[e * 3 + v] = raw[v];
+            io.macro[((int64_t)k * (N + 1) + n) * 3 + v] = nxt[v];
+          }
+          __threadfence();
+          pl_red_release(pp.chain_done + (int64_t)k * (N + 1) + n, 1);
+        }
+        // match(corrected, F^{k-1}_{n-1}), raise policy (coupling.py:32-95)
+        const int64_t cn = __ldcg(io.fine_counts + (int64_t)(k - 1) * N + (n - 1));
+        int mode = PL_KEEP, status = MMPR_STAT_OK;
+        double scale = 1.0, mc = 0.0, mu = 0.0;
+        if (cn != 0) {
+          mu = nxt[0];
+          double var_t = nxt[1];
+          if (var_t < 0.0) var_t = 0.0;
+          mc = f[0];
+          const double cur_var = f[1];
+          if (cur_var == 0.0) {
+            if (var_t > 0.0) status = 0;
+            mode = PL_SET;
+          } else {
+            scale = __dsqrt_rn(div(var_t, cur_var));
+            if (!(scale == 1.0 && mu == mc)) mode = PL_AFFINE;
+          }
+        }
+        if (rank == 0) io.match_status[(int64_t)k * N + (n - 1)] = status;
+        s_match[0] = mu;
+        s_match[1] = scale;
+        s_match[2] = mc;
+        s_mode = mode;
+      }
+      __syncthreads();
+      const double mu = s_match[0], scale = s_match[1], mc = s_match[2];
+      const int mode = s_mode;
+      const double *src = io.fine + ((int64_t)((k - 1) & 1) * N + (n - 1)) * fpitch;
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? __ldcg(src + off + j8 + 8 * m) : 0.0;
+      if (HAS_TAIL && j8 < tail) xt = __ldcg(src + tail_off + j8);
+      auto apply = [&](double v) {
+        return mode == PL_SET ? mu : (mode == PL_AFFINE ? add(mul(scale, sub(v, mc)), mu) : v);
+      };
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) x[m] = apply(x[m]);
+      if (HAS_TAIL) xt = apply(xt);
+      __syncthreads();  // every load of the source slot has returned
+      if (tid == 0) pl_red_release(pp.consumed + (int64_t)k * (N + 1) + n, 1);
+#pragma unroll
+      for (int m = 0; m < PPT; ++m)
+        if (m < cnt) snap_kn[off + j8 + 8 * m] = x[m];
+      if (HAS_TAIL && j8 < tail) snap_kn[tail_off + j8] = xt;
+      // micro restriction R(u^k_n) from registers (np.mean, two-pass np.var)
+      double var;
+      int b0;
+      reduce(Plain{}, 0.0, -1, s, b0);
+      reduce(Centered{}, s, -1, var, b0);
+      mean_known = true;
+      if (rank == 0 && tid == 0) {
+        double *mo = io.micro + ((int64_t)k * (N + 1) + n) * 3;
+        mo[0] = s;
+        mo[1] = var;
+        mo[2] = div((double)p.P, (double)p.P);
+        io.micro_counts[(int64_t)k * (N + 1) + n] = p.P;
+      }
+    } else if (k >= 1) {
+      // n == 0: u^k_0 = ens0 (engine.py:208); boundary-0 rows of the trace
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? io.x0[off + j8 + 8 * m] : 0.0;
+      if (HAS_TAIL && j8 < tail) xt = io.x0[tail_off + j8];
+#pragma unroll
+      for (int m = 0; m < PPT; ++m)
+        if (m < cnt) snap_kn[off + j8 + 8 * m] = x[m];
+      if (HAS_TAIL && j8 < tail) snap_kn[tail_off + j8] = xt;
+      if (rank == 0 && tid == 0) {
+        const int64_t e = (int64_t)k * (N + 1);
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          io.macro[e * 3 + v] = io.rho0[v];
+          io.micro[e * 3 + v] = io.rho0[v];
+        }
+        io.micro_counts[e] = io.counts0[0];
+      }
+    } else if (has_fine) {
+      // row 0: the lifted ensembles written by the prologue
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? snap_kn[off + j8 + 8 * m] : 0.0;
+      if (HAS_TAIL && j8 < tail) xt = snap_kn[tail_off + j8];
+      if (!pp.retain) {
+        __syncthreads();
+        if (tid == 0) pl_red_release(pp.consumed + n, 1);
+      }
+    }
+
+    if (has_fine) {
+      // ---- F(u^k_n): S Euler-Maruyama steps, particles in registers ------------
+      int bad = 0;
+      if (!mean_known) reduce(Plain{}, 0.0, -1, s, bad);
+      int first_bad = MMPR_STAT_OK;
+      for (int j = 0; j < p.S; ++j) {
+        const uint32_t lj = ld + (uint32_t)j;
+        const int stage = (int)(lj % (uint32_t)ns);
+        mbar_wait_parity(&s_bar[stage], (lj / (uint32_t)ns) & 1u);
+        const double *xb = s_stage + stage * p.stage_elems;
+#pragma unroll
+        for (int m = 0; m < PPT; ++m) {
+          if (m < LO) {
+            x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
+          } else {
+            const int idx = max(0, min(my_idx + 8 * m, last_idx));
+            const double nx = em_update<KIND>(p, x[m], s, xb[idx]);
+            x[m] = (m < cnt) ? nx : x[m];
+          }
+        }
+        if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
+        reduce(Plain{}, 0.0, (j + ns < p.S) ? j + ns : -1, s, bad);
+        if (bad) {
+          first_bad = j;
+          break;
+        }
+      }
+      // loads issued for this unit: the first min(ns, S) plus one refill per
+      // completed step while j + ns < S
+      const int init = ns < p.S ? ns : p.S;
+      const int done_steps = first_bad == MMPR_STAT_OK ? p.S : first_bad + 1;
+      const int refills = max(0, min(done_steps, p.S - ns));
+      const int issued = init + refills;
+      if (tid == gthreads - 32 && first_bad != MMPR_STAT_OK) {
+        for (int j = first_bad + 1; j < issued; ++j) {
+          const uint32_t lj = ld + (uint32_t)j;
+          mbar_wait_parity(&s_bar[lj % (uint32_t)ns], (lj / (uint32_t)ns) & 1u);
+        }
+      }
+      ld += (uint32_t)issued;
+      // the unit's coordinates again from shared memory (not held in
+      // registers across the step loop)
+      const int tt = *(volatile int *)&s_ticket[it & 1];
+      const int k = tt / (N + 1), n = tt % (N + 1);
+
+      // ---- write F^k_n into the parity buffer, restriction, publish -------------
+      if (k >= 2) {
+        if (tid == 0) pl_wait(pp.consumed + (int64_t)(k - 1) * (N + 1) + (n + 1), p.ctas);
+        __syncthreads();
+      }
+      double *xo = io.fine + ((int64_t)(k & 1) * N + n) * fpitch;
+#pragma unroll
+      for (int m = 0; m < PPT; ++m)
+        if (m < cnt) xo[off + j8 + 8 * m] = x[m];
+      if (HAS_TAIL && j8 < tail) xo[tail_off + j8] = xt;
+      double var = 0.0;
+      const bool ok = first_bad == MMPR_STAT_OK;
+      if (ok) {
+        int b2;
+        reduce(Centered{}, s, -1, var, b2);
+      }
+      if (rank == 0 && tid == 0) {
+        const int64_t e = (int64_t)k * N + n;
+        io.bad[e] = first_bad;
+        if (ok) {
+          io.fine_stats[e * 3 + 0] = s;
+          io.fine_stats[e * 3 + 1] = var;
+          io.fine_stats[e * 3 + 2] = div((double)p.P, (double)p.P);
+          io.fine_counts[e] = p.P;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        pl_red_release(pp.fine_done + (int64_t)k * N + n, 1);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+struct PipeGeometry {
+  int D, spc, ctas, threads, stage_elems, nstages;
+  size_t smem;
+  bool tail;
+};
+
+// The pipeline covers the fine-sweep geometry of the BASELINE ensembles
+// (P ~ 1e5: 1024 leaf slots of 96..104 particles, 16 CTAs x 512 threads,
+// 13 accumulator elements per lane); other sizes keep the per-iteration
+// kernels.
+static int pipe_geometry(int64_t P, PipeGeometry *g) {
+  if (P < 1) return MMPR_ERR_ARG;
+  const int D = pw_depth(P);
+  const int64_t nslots = int64_t(1) << D;
+  if (nslots != 1024) return MMPR_ERR_UNSUPPORTED;
+  int64_t max_leaf = 0, min_leaf = INT64_MAX;
+  for (int64_t s = 0; s < nslots; ++s) {
+    int64_t o, l;
+    pw_leaf(P, D, s, &o, &l);
+    if (l > max_leaf) max_leaf = l;
+    if (l < min_leaf) min_leaf = l;
+  }
+  if ((max_leaf + 7) / 8 != 13 || (min_leaf >> 3) < 12) return MMPR_ERR_UNSUPPORTED;
+  g->D = D;
+  g->spc = 64;
+  g->ctas = 16;
+  g->threads = 512;
+  int64_t max_range = 0;
+  for (int c = 0; c < g->ctas; ++c) {
+    int64_t lo, hi, l;
+    pw_leaf(P, D, (int64_t)c * g->spc, &lo, &l);
+    if (c == g->ctas - 1) hi = P;
+    else pw_leaf(P, D, (int64_t)(c + 1) * g->spc, &hi, &l);
+    if (hi - lo > max_range) max_range = hi - lo;
+  }
+  g->stage_elems = (int)((max_range + 1) & ~int64_t(1));
+  g->nstages = 2;
+  g->smem = (size_t)g->stage_elems * 8 * g->nstages;
+  if (g->smem > 112 * 1024) return MMPR_ERR_UNSUPPORTED;  // two CTAs per SM
+  g->tail = (P % 8) != 0;
+  return MMPR_OK;
+}
+
+template <void (*KERN)(const PipeParams)>
+static int launch_pipe(const PipeParams &pp, const PipeGeometry &g, cudaStream_t stream) {
+  static int configured_smem_dev[MMPR_MAX_DEVICES] = {};
+  static int clusters_dev[MMPR_MAX_DEVICES] = {};
+  const int dev = mmpr_current_device();
+  cudaError_t err;
+  if ((int)g.smem > configured_smem_dev[dev]) {
+    err = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    if (err != cudaSuccess) return mmpr_check(err, "pipeline: smem attribute");
+    err = cudaFuncSetAttribute(KERN, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err != cudaSuccess) return mmpr_check(err, "pipeline: non-portable cluster");
+    configured_smem_dev[dev] = (int)g.smem;
+    clusters_dev[dev] = 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3((unsigned)g.threads, 1, 1);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)g.ctas;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (clusters_dev[dev] == 0) {
+    // persistent grid: the clusters that can be co-resident (tickets are
+    // taken at run time, so a cluster that is not resident never blocks one
+    // that is)
+    cfg.gridDim = dim3((unsigned)g.ctas, 1, 1);
+    int n = 0;
+    err = cudaOccupancyMaxActiveClusters(&n, KERN, &cfg);
+    if (err != cudaSuccess) return mmpr_check(err, "pipeline: cudaOccupancyMaxActiveClusters");
+    if (n < 1) return MMPR_ERR_UNSUPPORTED;
+    clusters_dev[dev] = n;
+  }
+  int clusters = clusters_dev[dev];
+  if (const char *env = getenv("MMPR_PIPELINE_CLUSTERS")) {  // tuning override
+    const int v = atoi(env);
+    if (v >= 1 && v < clusters) clusters = v;
+  }
+  if (clusters > pp.units) clusters = pp.units;
+  cfg.gridDim = dim3((unsigned)(clusters * g.ctas), 1, 1);
+  err = cudaLaunchKernelEx(&cfg, KERN, pp);
+  return mmpr_check(err, "pipeline_kernel launch");
+}
+
+template <int KIND, int OK, int MK>
+static int dispatch_pipe_tail(const PipeParams &pp, const PipeGeometry &g, cudaStream_t s) {
+  if (g.tail) return launch_pipe<pipeline_kernel<KIND, 13, true, OK, MK>>(pp, g, s);
+  return launch_pipe<pipeline_kernel<KIND, 13, false, OK, MK>>(pp, g, s);
+}
+
+// (fine model kind, ODE kind, ODE model kind) combinations with a pipeline
+// instantiation: the BASELINE unimodal configs and their close relatives.
+static int dispatch_pipe(const mmpr_model &model, const mmpr_moment_ode &ode, const mmpr_model &ode_model,
+                         const PipeParams *pp, const PipeGeometry &g, cudaStream_t s) {
+  const int fk = model.kind, ok = ode.kind, mk = ode_model.kind;
+  const bool run = pp != nullptr;
+  if (fk == MMPR_MODEL_OU && ok == MMPR_ODE_UNIMODAL && mk == MMPR_MODEL_OU)
+    return run ? dispatch_pipe_tail<MMPR_MODEL_OU, MMPR_ODE_UNIMODAL, MMPR_MODEL_OU>(*pp, g, s) : MMPR_OK;
+  if (fk == MMPR_MODEL_OU && ok == MMPR_ODE_PERTURBED_OU)
+    return run ? dispatch_pipe_tail<MMPR_MODEL_OU, MMPR_ODE_PERTURBED_OU, 0>(*pp, g, s) : MMPR_OK;
+  if (fk == MMPR_MODEL_LINEAR && ok == MMPR_ODE_UNIMODAL && mk == MMPR_MODEL_LINEAR)
+    return run ? dispatch_pipe_tail<MMPR_MODEL_LINEAR, MMPR_ODE_UNIMODAL, MMPR_MODEL_LINEAR>(*pp, g, s) : MMPR_OK;
+  if (fk == MMPR_MODEL_CUBIC_MF && ok == MMPR_ODE_GAUSSIAN_CUBIC)
+    return run ? dispatch_pipe_tail<MMPR_MODEL_CUBIC_MF, MMPR_ODE_GAUSSIAN_CUBIC, 0>(*pp, g, s) : MMPR_OK;
+  if (fk == MMPR_MODEL_CUBIC_MF && ok == MMPR_ODE_UNIMODAL && mk == MMPR_MODEL_CUBIC_MF)
+    return run ? dispatch_pipe_tail<MMPR_MODEL_CUBIC_MF, MMPR_ODE_UNIMODAL, MMPR_MODEL_CUBIC_MF>(*pp, g, s)
+               : MMPR_OK;
+  return MMPR_ERR_UNSUPPORTED;
+}
+
+}  // namespace mmpr
+
+using namespace mmpr;
+
+extern "C" int64_t mmpr_pipeline_flags_size(int32_t n_slices, int32_t iterations) {
+  if (n_slices < 1 || iterations < 0) return 0;
+  const int64_t N = n_slices, K = iterations;
+  return 1 + K * N + 2 * (K + 1) * (N + 1);
+}
+
+extern "C" int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_moment_ode *ode,
+                                       const mmpr_model *ode_model, const mmpr_integrator *integ,
+                                       int64_t particles) {
+  if (!model || !ode || !ode_model || !integ) return MMPR_ERR_ARG;
+  if (model->stat_kind != MMPR_STAT_MEAN_OF_F || ode->n_regions != 1) return MMPR_ERR_UNSUPPORTED;
+  if (integ->kind != MMPR_INTEG_EULER || !(integ->dt > 0.0)) return MMPR_ERR_UNSUPPORTED;
+  PipeGeometry g;
+  const int st = pipe_geometry(particles, &g);
+  if (st != MMPR_OK) return st;
+  return dispatch_pipe(*model, *ode, *ode_model, nullptr, g, nullptr);
+}
+
+extern "C" int mmpr_parareal_pipeline(const mmpr_model *model, const mmpr_moment_ode *ode,
+                                      const mmpr_model *ode_model, const mmpr_integrator *integ,
+                                      int32_t n_slices, int32_t iterations,
+                                      int64_t particles, int32_t steps, double dt, double sqrt_dt,
+                                      int32_t reuse_converged, const mmpr_pipeline_io *io, void *stream) {
+  int st = mmpr_pipeline_supported(model, ode, ode_model, integ, particles);
+  if (st != MMPR_OK) return st;
+  if (!io || n_slices < 1 || iterations < 1 || steps < 0) return MMPR_ERR_ARG;
+  if (!io->times || !io->x0 || !io->rho0 || !io->counts0 || !io->snap || !io->fine || !io->macro || !io->micro ||
+      !io->micro_counts || !io->fine_stats || !io->fine_counts || !io->raw || !io->cache || !io->bad ||
+      !io->coarse_status || !io->match_status || !io->flags)
+    return MMPR_ERR_ARG;
+  if (io->snap_rows != iterations + 1 && io->snap_rows != 2) return MMPR_ERR_ARG;
+  if (io->fine_pitch < particles || io->snap_slice_pitch < particles ||
+      io->snap_iter_stride < (int64_t)(n_slices + 1) * io->snap_slice_pitch)
+    return MMPR_ERR_ARG;
+  if (steps > 0 && (!io->xi || (io->xi_row_pitch & 1) || io->xi_row_pitch < particles ||
+                    (reinterpret_cast<uintptr_t>(io->xi) & 15) ||
+                    (steps > 1 && io->xi_slice_pitch < steps * io->xi_row_pitch)))
+    return MMPR_ERR_ARG;
+  PipeGeometry g;
+  pipe_geometry(particles, &g);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nflags = mmpr_pipeline_flags_size(n_slices, iterations);
+  cudaError_t err = cudaMemsetAsync(io->flags, 0, (size_t)nflags * sizeof(int32_t), s);
+  if (err != cudaSuccess) return mmpr_check(err, "pipeline: flag reset");
+
+  PipeParams pp = {};
+  FineParams &p = pp.f;
+  p.model = *model;
+  p.n_slices = n_slices;
+  p.S = steps;
+  p.P = particles;
+  p.dt = dt;
+  p.sqrt_dt = sqrt_dt;
+  p.bsd = 0.0;
+  switch (model->kind) {
+    case MMPR_MODEL_OU: p.bsd = model->p[2] * sqrt_dt; break;
+    case MMPR_MODEL_CUBIC_MF: p.bsd = model->p[3] * sqrt_dt; break;
+    default: break;
+  }
+  p.xi = io->xi;
+  p.xi_slice_pitch = io->xi_slice_pitch;
+  p.xi_row_pitch = io->xi_row_pitch;
+  p.D = g.D;
+  p.slots_per_cta = g.spc;
+  p.ctas = g.ctas;
+  p.stage_elems = g.stage_elems;
+  p.nstages = g.nstages;
+  p.cnt_min = 12;
+  p.l2_ahead = 3;
+  if (const char *env = getenv("MMPR_FINE_L2_AHEAD")) p.l2_ahead = max(0, min(16, atoi(env)));
+  pp.ode = *ode;
+  pp.ode_model = *ode_model;
+  pp.integ = *integ;
+  pp.io = *io;
+  pp.N = n_slices;
+  pp.K = iterations;
+  pp.units = (iterations + 1) * (n_slices + 1);
+  pp.reuse = reuse_converged ? 1 : 0;
+  pp.retain = io->snap_rows == iterations + 1 ? 1 : 0;
+  if (iterations == 1 && io->snap_rows == 2) pp.retain = 1;  // two rows are all of them
+  pp.ticket = io->flags;
+  pp.fine_done = io->flags + 1;
+  pp.chain_done = pp.fine_done + (int64_t)iterations * n_slices;
+  pp.consumed = pp.chain_done + (int64_t)(iterations + 1) * (n_slices + 1);
+  return dispatch_pipe(*model, *ode, *ode_model, &pp, g, s);
+}

@@ -242,6 +242,15 @@ class _RunPlan:
         self.batch = self.ws.noise_slices
         self.graph = None
         self.launches_per_run = 0
+        # iterations 1..K as one persistent kernel (mmpr_parareal_pipeline)
+        # when the configuration has an instantiation; every iterate is
+        # bitwise the one of the per-iteration kernel sequence
+        self.pipeline = (K >= 1 and self.fused_restrict and not plan.fresh and self.batch == N
+                         and not host_snapshots and os.environ.get("MMPR_PIPELINE", "1") != "0"
+                         and kernels.pipeline_supported(model_d, ode_d, ode_model_d, integ_d, P))
+        if self.pipeline:
+            self.ws.fine = torch.empty((2, N, P), dtype=torch.float64, device=device())
+            self.flags = torch.empty((kernels.pipeline_flags_size(N, K),), dtype=torch.int32, device=device())
 
     def snap(self, k):
         return self.ws.snap[k if self.cfg.retain_snapshots else k % 2]
@@ -318,6 +327,17 @@ class _RunPlan:
         if not self.fused_restrict:
             kernels.restrict(part_d, nxt, ws.micro[k + 1], ws.micro_counts[k + 1], ws.scratch)
 
+    def issue_pipeline(self, timer):
+        """Iterations 1..K in one launch (after issue_prologue)."""
+        ws = self.ws
+        ev = timer.start()
+        kernels.parareal_pipeline(self.model_d, self.ode_d, self.ode_model_d, self.integ_d,
+                                  self.cfg.step.dt, self.S, self.reuse, self.times_d, ws.x0, ws.rho0, ws.counts0,
+                                  ws.xi, ws.snap, ws.fine, ws.macro, ws.micro, ws.micro_counts, ws.fine_stats,
+                                  ws.fine_counts, ws.raw, ws.cache, ws.bad, ws.coarse_status, ws.match_status,
+                                  self.flags)
+        timer.stop("iterations", ev)
+
     def stream_row(self, k):
         """Copy snapshot row k to pinned host memory on the side stream."""
         if self.host_snap is None:
@@ -334,9 +354,12 @@ class _RunPlan:
     def issue_all(self, timer):
         self.issue_prologue(timer)
         self.stream_row(0)
-        for k in range(self.K):
-            self.issue_iteration(k, timer)
-            self.stream_row(k + 1)
+        if self.pipeline:
+            self.issue_pipeline(timer)
+        else:
+            for k in range(self.K):
+                self.issue_iteration(k, timer)
+                self.stream_row(k + 1)
         self.join()
 
     def replay(self):
@@ -355,6 +378,8 @@ class _RunPlan:
 
 _PLANS: dict = {}
 _PLANS_MAX = 2
+# how the last run_micro_macro executed (tests and bench read it)
+last_run_info: dict = {"pipeline": False}
 
 
 def clear_graph_cache() -> None:
@@ -426,6 +451,7 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
                           host_snapshots=snapshots_to_host)
             _PLANS[key] = rp
     ws = rp.ws
+    last_run_info["pipeline"] = rp.pipeline
     ws.x0.copy_(ens0.device_positions.reshape(1, -1))
     timer = _StageTimer(record_timings)
     N, K, P = rp.N, rp.K, rp.P
@@ -440,7 +466,9 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
             ws.xi = increments
         rp.issue_prologue(timer, injected)
         rp.stream_row(0)
-        for k in range(K):
+        if rp.pipeline:
+            rp.issue_pipeline(timer)
+        for k in range(0 if rp.pipeline else K):
             if callable(increments):
                 for n in range(N):
                     ws.xi[n, :, :P] = torch.as_tensor(np.asarray(increments(n, k), dtype=float)).to(device())

@@ -176,6 +176,70 @@ def coarse_row(ode: _lib.MomentOde, model: _lib.Model, integ: _lib.Integrator, t
               _lib.stream_handle(stream))
 
 
+def pipeline_supported(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Model, integ: _lib.Integrator,
+                       particles: int) -> bool:
+    """True when iterations 1..K of this configuration run as one persistent
+    kernel (mmpr_parareal_pipeline).  Host-only query."""
+    return _lib.load().mmpr_pipeline_supported(ctypes.byref(model), ctypes.byref(ode), ctypes.byref(ode_model),
+                                               ctypes.byref(integ), int(particles)) == 0
+
+
+def pipeline_flags_size(n_slices: int, iterations: int) -> int:
+    return int(_lib.load().mmpr_pipeline_flags_size(int(n_slices), int(iterations)))
+
+
+def parareal_pipeline(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Model, integ: _lib.Integrator,
+                      dt: float, steps: int,
+                      reuse: bool, times, x0, rho0, counts0, xi, snap, fine, macro, micro, micro_counts,
+                      fine_stats, fine_counts, raw, cache, bad, coarse_status, match_status, flags,
+                      stream=None) -> None:
+    """Iterations 1..K of run_micro_macro in one launch (after the prologue).
+
+    snap: (K+1 or 2, N+1, P); fine: (2, N, P); macro/micro: (K+1, N+1, 3);
+    micro_counts (K+1, N+1, 1); fine_stats/raw: (K, N, 3); fine_counts
+    (K, N, 1); cache (K+1, N, 3); bad (K, N); coarse_status/match_status
+    (K+1, N) int32; flags: int32 scratch of pipeline_flags_size(N, K)."""
+    require_cuda()
+    K1, N1, _ = macro.shape
+    K, N = K1 - 1, N1 - 1
+    P = x0.shape[-1]
+    _f64(snap, "snap")
+    if snap.dim() != 3 or snap.shape[1:] != (N + 1, P) or snap.shape[0] not in (K + 1, 2) or snap.stride(2) != 1:
+        raise ValueError("snap must be (K+1 or 2, N+1, P)")
+    _f64(fine, "fine")
+    if fine.shape != (2, N, P) or fine.stride(2) != 1 or fine.stride(0) != N * fine.stride(1):
+        raise ValueError("fine must be (2, N, P) with uniform row pitch")
+    _f64(xi, "xi")
+    if xi.dim() != 3 or xi.shape[0] < N or xi.shape[1] < steps or xi.stride(2) != 1:
+        raise ValueError("xi must be (N, >=steps, pitch)")
+    for t, shape, dtype, name in ((macro, (K + 1, N + 1, 3), torch.float64, "macro"),
+                                  (micro, (K + 1, N + 1, 3), torch.float64, "micro"),
+                                  (micro_counts, (K + 1, N + 1, 1), torch.int64, "micro_counts"),
+                                  (fine_stats, (K, N, 3), torch.float64, "fine_stats"),
+                                  (fine_counts, (K, N, 1), torch.int64, "fine_counts"),
+                                  (raw, (K, N, 3), torch.float64, "raw"),
+                                  (cache, (K + 1, N, 3), torch.float64, "cache"),
+                                  (bad, (K, N), torch.int32, "bad"),
+                                  (coarse_status, (K + 1, N), torch.int32, "coarse_status"),
+                                  (match_status, (K + 1, N), torch.int32, "match_status")):
+        if tuple(t.shape) != shape or t.dtype != dtype or not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous {dtype} {shape}")
+    if flags.dtype != torch.int32 or flags.numel() < pipeline_flags_size(N, K):
+        raise ValueError("flags must be int32 of pipeline_flags_size(N, K)")
+    io = _lib.PipelineIO(times=times.data_ptr(), x0=x0.data_ptr(), rho0=rho0.data_ptr(), counts0=counts0.data_ptr(),
+                         xi=xi.data_ptr(), xi_slice_pitch=xi.stride(0), xi_row_pitch=xi.stride(1),
+                         snap=snap.data_ptr(), snap_iter_stride=snap.stride(0), snap_slice_pitch=snap.stride(1),
+                         snap_rows=snap.shape[0], fine=fine.data_ptr(), fine_pitch=fine.stride(1),
+                         macro=macro.data_ptr(), micro=micro.data_ptr(), micro_counts=micro_counts.data_ptr(),
+                         fine_stats=fine_stats.data_ptr(), fine_counts=fine_counts.data_ptr(), raw=raw.data_ptr(),
+                         cache=cache.data_ptr(), bad=bad.data_ptr(), coarse_status=coarse_status.data_ptr(),
+                         match_status=match_status.data_ptr(), flags=flags.data_ptr())
+    _lib.call("mmpr_parareal_pipeline", ctypes.byref(model), ctypes.byref(ode), ctypes.byref(ode_model),
+              ctypes.byref(integ), int(N), int(K),
+              int(P), int(steps), float(dt), float(math.sqrt(dt)), 1 if reuse else 0, ctypes.byref(io),
+              _lib.stream_handle(stream))
+
+
 def integrate_macro(ode: _lib.MomentOde, model: _lib.Model, integ: _lib.Integrator, t0, t1, state_in, state_out,
                     status, stream=None) -> None:
     require_cuda()

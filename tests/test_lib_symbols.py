@@ -38,6 +38,33 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.Partition) == 8 + 8 * (_lib.MAX_REGIONS - 1) + 8 * _lib.MAX_REGIONS
     assert ctypes.sizeof(_lib.MomentOde) == 8 + 8 * _lib.MAX_ODE_PARAMS
     assert ctypes.sizeof(_lib.Integrator) == 8 + 4 * 8
+    assert ctypes.sizeof(_lib.PipelineIO) == 24 * 8  # 21 pointers / int64 + snap_rows padded to 8
+
+
+def test_pipeline_support_query_without_a_gpu():
+    """mmpr_pipeline_supported / mmpr_pipeline_flags_size are host-only."""
+    from paper_2310_11365_b200 import engine, kernels, moments
+    m = mm.make_perturbed_ou(mm.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5))
+    ode, ode_model = moments.device_ode(mm.unimodal_rhs(m))
+    euler = engine.integrator_descriptor(mm.EulerConfig(1e-2))
+    assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 100_000)
+    assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 98_307)
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 10_000)  # other geometry
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 20)
+    dp54 = engine.integrator_descriptor(mm.IntegratorConfig())
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, dp54, 100_000)
+    spec = mm.CubicMeanFieldSpec(1.0, 1.0, 1.0, 0.4)
+    cub = mm.make_cubic_meanfield(spec)
+    ode_c, odm_c = moments.device_ode(mm.gaussian_closure_rhs(spec))
+    assert kernels.pipeline_supported(cub.descriptor, ode_c, odm_c, euler, 100_000)
+    dw = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.5)
+    dwm = mm.make_double_well(dw)
+    ode_m, odm_m = moments.device_ode(mm.multimodal_rhs(dwm, dw.default_partition(), dw.potential, dw.sigma))
+    assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 100_000)  # two regions
+    assert kernels.pipeline_flags_size(64, 5) == 1 + 5 * 64 + 2 * 6 * 65
+    lib = _lib.load()
+    assert lib.mmpr_pipeline_supported(None, None, None, None, 100_000) == 1
+    assert lib.mmpr_parareal_pipeline(None, None, None, None, 4, 2, 100_000, 10, 1e-3, 0.03, 1, None, None) == 1
 
 
 def test_invalid_arguments_are_rejected_without_a_gpu():
