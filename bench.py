@@ -321,7 +321,7 @@ def our_arm(args):
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "fp64_canonical": fp64_canonical(value / G, clocks.summary().get("sm_mhz") or 1965.0),
-        "stage_ms_per_run": {k: round(sum(v) / 2, 4) for k, v in stage_ms.items()},
+        "stage_ms_per_run": {k: round(sum(v) / 2, 4) for k, v in stage_ms.items() if v},
     }
     if G == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)

@@ -19,7 +19,7 @@ for l in dis[start + 1:]:
     m = re.match(r'\s+/\*([0-9a-f]{4,})\*/\s+(.*)', l)
     if m and cur:
         addr2line[int(m.group(1), 16)] = cur
-out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'sass'],
+out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'sass'] + (['-k', 'regex:' + __import__('os').environ['NCU_KERNEL']] if __import__('os').environ.get('NCU_KERNEL') else []),
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]

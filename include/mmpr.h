@@ -363,6 +363,44 @@ int mmpr_parareal_pipeline(const mmpr_model *model, const mmpr_moment_ode *ode,
                            int64_t particles, int32_t steps, double dt, double sqrt_dt,
                            int32_t reuse_converged, const mmpr_pipeline_io *io, void *stream);
 
+/* The same pipeline over n_ranks ranks, each owning n_slices / n_ranks
+ * contiguous slices (the last rank also boundary N): ios[r] are rank r's
+ * buffers, every array indexed by GLOBAL slice/boundary (rank r writes only
+ * the entries of its own units), except xi, which holds rank r's own slices
+ * (slice n at xi + (n - r*Ng)*xi_slice_pitch).  The launch processes the
+ * units of ranks [first_rank, first_rank + launch_ranks) in (k, n) order and
+ * reads the first slice's inputs of each rank -- F^{k-1}_{n-1}, its
+ * restriction, macro[k][n-1] -- from the previous rank's buffers, waiting on
+ * that rank's flag words; the only cross-rank traffic is one ensemble and a
+ * few doubles per (rank boundary, iteration).
+ *  - multi-GPU: each process launches its own rank (launch_ranks = 1) with
+ *    the other ranks' ios pointing into their exchange memory opened with
+ *    mmpr_ipc_open (flags, macro, fine_stats, fine_counts, fine); multi_gpu=1
+ *    selects system-scope release/acquire;
+ *  - one GPU: one launch over all ranks (first_rank = 0, launch_ranks =
+ *    n_ranks) -- the emulation the tests use.
+ * Flags accumulate across runs: run `epoch` (1, 2, ...) waits for epoch
+ * times the per-run count, so no rank resets a word a peer may still read;
+ * reset_flags=1 (epoch 1 only) zeroes the launch's flags first.  The ticket
+ * word (flags[0] of ios[first_rank]) is reset by every call. */
+int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_moment_ode *ode,
+                                 const mmpr_model *ode_model, const mmpr_integrator *integ,
+                                 int32_t n_slices, int32_t iterations, int64_t particles,
+                                 int32_t steps, double dt, double sqrt_dt, int32_t reuse_converged,
+                                 int32_t n_ranks, const mmpr_pipeline_io *ios, int32_t first_rank,
+                                 int32_t launch_ranks, int32_t epoch, int32_t reset_flags,
+                                 int32_t multi_gpu, void *stream);
+
+/* Exchange memory of the multi-GPU pipeline: a cudaMalloc'd block (so one
+ * IPC handle covers it), its 64-byte cudaIpcMemHandle, and the peer
+ * mapping of another process's block (cudaIpcMemLazyEnablePeerAccess). */
+int mmpr_exchange_alloc(int64_t bytes, void **dev_ptr);
+int mmpr_exchange_free(void *dev_ptr);
+int mmpr_ipc_handle(void *dev_ptr, unsigned char *handle_out);
+int mmpr_ipc_open(const unsigned char *handle, void **dev_ptr);
+int mmpr_ipc_close(void *dev_ptr);
+int mmpr_device_can_access_peer(int32_t device, int32_t peer, int32_t *out);
+
 /* ------------------------------------------------------------------ */
 /* Error metrics (metrics.py:35-47, 73-130, 133-218)                   */
 /* ------------------------------------------------------------------ */

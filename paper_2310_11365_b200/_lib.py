@@ -124,6 +124,14 @@ SIGNATURES = {
     "mmpr_pipeline_flags_size": (ctypes.c_int64, [_I32, _I32]),
     "mmpr_pipeline_supported": (ctypes.c_int, [_P, _P, _P, _P, _I64]),
     "mmpr_parareal_pipeline": (ctypes.c_int, [_P, _P, _P, _P, _I32, _I32, _I64, _I32, _D, _D, _I32, _P, _P]),
+    "mmpr_parareal_pipeline_ranks": (ctypes.c_int, [_P, _P, _P, _P, _I32, _I32, _I64, _I32, _D, _D, _I32, _I32, _P,
+                                                     _I32, _I32, _I32, _I32, _I32, _P]),
+    "mmpr_exchange_alloc": (ctypes.c_int, [_I64, _P]),
+    "mmpr_exchange_free": (ctypes.c_int, [_P]),
+    "mmpr_ipc_handle": (ctypes.c_int, [_P, _P]),
+    "mmpr_ipc_open": (ctypes.c_int, [_P, _P]),
+    "mmpr_ipc_close": (ctypes.c_int, [_P]),
+    "mmpr_device_can_access_peer": (ctypes.c_int, [_I32, _I32, _P]),
 }
 
 _lib = None
@@ -144,6 +152,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
                 "g.build()'` (there is no CPU fallback)")
         lib = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
+            if path != LIB_PATH and not hasattr(lib, name):
+                continue  # an older build loaded for an A/B experiment
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
@@ -155,7 +165,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
 LAUNCHING = frozenset({"mmpr_noise_keys", "mmpr_entropy_key", "mmpr_normals_fill", "mmpr_fine_sweep",
                        "mmpr_fine_sweep_restrict", "mmpr_match_restrict",
                        "mmpr_restrict", "mmpr_match", "mmpr_coarse_row", "mmpr_integrate_macro",
-                       "mmpr_mean_abs_diff", "mmpr_parareal_pipeline"})
+                       "mmpr_mean_abs_diff", "mmpr_parareal_pipeline", "mmpr_parareal_pipeline_ranks"})
 launch_count = {"total": 0}
 
 

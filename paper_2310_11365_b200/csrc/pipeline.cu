@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <type_traits>
 
@@ -40,51 +41,91 @@
 
 namespace mmpr {
 
+#define PL_MAX_RANKS 8
+
+// One launch processes the units of ranks [r0, r0 + nr): every unit (k, n)
+// with owner(n) in that range, in k-major order.  io[r] are rank r's
+// buffers -- this process's own, or another GPU's mapped through CUDA IPC
+// (peer pointers), or, in the one-GPU emulation, another set of local
+// buffers.  Flags accumulate over runs: run `epoch` (1, 2, ...) waits for
+// epoch * count, so ranks never reset a word a peer may still be reading.
 struct PipeParams {
   FineParams f;  // model, S, P, dt, sqrt_dt, bsd, increments, cluster geometry
   mmpr_moment_ode ode;
   mmpr_model ode_model;  // the model the moment ODE was built from
   mmpr_integrator integ;
-  mmpr_pipeline_io io;
-  int N, K;
+  mmpr_pipeline_io io[PL_MAX_RANKS];
+  int N, K, G, Ng;  // slices, iterations, ranks, slices per rank (N = G * Ng)
+  int r0;           // first rank of this launch
+  int lo_n;         // first boundary index of the launch's units
+  int row_units;    // units per row for this launch
   int units;
   int reuse;  // cached predictions for converged slices (engine skip_until)
   int retain;
-  int *ticket;
-  int *fine_done;   // [K][N]
-  int *chain_done;  // [K+1][N+1]
-  int *consumed;    // [K+1][N+1]
+  int epoch;
+  int sys;  // ranks on several GPUs: system-scope ordering
 };
 
-__device__ __forceinline__ int pl_ld_acquire(const int *p) {
+__device__ __forceinline__ int pl_ld_acquire(const int *p, bool sys) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  if (sys) asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-__device__ __forceinline__ void pl_red_release(int *p, int v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// Publish after this thread's (and, through the preceding block barrier,
+// the CTA's) stores: fence at the consumers' scope, then a release add.
+// fence=false for "consumed" signals, which order only loads whose values
+// the CTA has already used (the release alone orders this thread's).
+__device__ __forceinline__ void pl_publish(int *p, int v, bool sys, bool fence = true) {
+  if (sys) {
+    if (fence) __threadfence_system();
+    asm volatile("red.release.sys.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  } else {
+    if (fence) __threadfence();
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  }
 }
 
 // Spin until *p >= target.  A dependency that never arrives is a bug; the
 // watchdog (~9 s) turns it into a kernel fault instead of a hung device.
-__device__ __forceinline__ void pl_wait(const int *p, int target) {
-  if (pl_ld_acquire(p) >= target) return;
+__device__ __forceinline__ void pl_wait(const int *p, int target, bool sys) {
+  if (pl_ld_acquire(p, sys) >= target) return;
   const long long t0 = clock64();
-  while (pl_ld_acquire(p) < target) {
+  while (pl_ld_acquire(p, sys) < target) {
     __nanosleep(64);
     if (clock64() - t0 > (1LL << 34)) __trap();
   }
 }
 
+// data another rank produced: L2 (same GPU) or uncached (peer GPU)
+__device__ __forceinline__ double pl_ld(const double *p, bool remote) { return remote ? __ldcv(p) : __ldcg(p); }
+__device__ __forceinline__ int64_t pl_ld64(const int64_t *p, bool remote) {
+  return remote ? (int64_t)__ldcv((const long long *)p) : (int64_t)__ldcg((const long long *)p);
+}
+
+// flag words of one rank: [0] ticket, then fine_done[K][N], chain_done[K+1][N+1], consumed[K+1][N+1]
+struct PlFlags {
+  int *base;
+  int N, K;
+  __device__ int *fine_done(int k, int n) const { return base + 1 + (int64_t)k * N + n; }
+  __device__ int *chain_done(int k, int n) const {
+    return base + 1 + (int64_t)K * N + (int64_t)k * (N + 1) + n;
+  }
+  __device__ int *consumed(int k, int n) const {
+    return base + 1 + (int64_t)K * N + (int64_t)(K + 1) * (N + 1) + (int64_t)k * (N + 1) + n;
+  }
+};
+
 enum { PL_KEEP = 0, PL_SET = 1, PL_AFFINE = 2 };
 
-template <int KIND, int PPT, bool HAS_TAIL, int OK, int MK>
+// MULTI = false: one rank (the single-GPU engine); the rank table collapses
+// to io[0] at compile time and the step loop keeps every value in registers.
+template <int KIND, int PPT, bool HAS_TAIL, int OK, int MK, bool MULTI>
 __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
   constexpr int LO = PPT - 1;  // every leaf has PPT-1 or PPT accumulator elements per lane
   using PartT = Part<false>;
   const FineParams &p = pp.f;
-  const mmpr_pipeline_io &io = pp.io;
   extern __shared__ __align__(128) double s_stage[];  // [nstages][stage_elems]
   __shared__ PartT s_wp[2][32];
   __shared__ __align__(16) ClusterSlot s_slot[2][FS_MAX_CLUSTER];
@@ -243,11 +284,20 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
   using Plain = std::integral_constant<bool, false>;
   using Centered = std::integral_constant<bool, true>;
 
-  const int64_t fpitch = io.fine_pitch;
+  // (read from the parameter bank at each use: nothing here stays live in
+  // registers across the step loop)
+#define sys (MULTI && pp.sys != 0)
+#define ep (pp.epoch)
+#define cdone (pp.epoch * p.ctas)  // a flag every CTA of a unit's cluster adds to
+  auto owner = [&](int m) {
+    if constexpr (!MULTI) return 0;
+    const int o = m / pp.Ng;
+    return o < pp.G ? o : pp.G - 1;
+  };
   for (int it = 0;; ++it) {
     // ---- next ticket, broadcast to the cluster ---------------------------------
     if (rank == 0 && tid == 0) {
-      const int t = atomicAdd(pp.ticket, 1);
+      const int t = atomicAdd(pp.io[pp.r0].flags, 1);
       if (p.ctas > 1) {
         for (int c = 0; c < p.ctas; ++c) st_cluster_u32(mapa_shared(smem_addr(&s_ticket[it & 1]), (uint32_t)c), t);
       } else {
@@ -258,7 +308,10 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
     else __syncthreads();
     const int t = s_ticket[it & 1];
     if (t >= pp.units) break;
-    const int k = t / (N + 1), n = t % (N + 1);
+    const int k = t / pp.row_units, n = pp.lo_n + t % pp.row_units;
+    const int r = owner(n);
+    const mmpr_pipeline_io &io = pp.io[r];
+    const PlFlags fl{io.flags, N, K};
     const bool has_match = k >= 1 && n >= 1;
     const bool has_fine = k < K && n < N;
     const int64_t srow = pp.retain ? k : (k & 1);
@@ -266,7 +319,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
 
     // the increments do not depend on anything: start their copies first
     if (has_fine && tid == 0) {
-      const double *base = io.xi + (int64_t)n * io.xi_slice_pitch + lo;
+      const double *base = io.xi + (int64_t)(n - r * pp.Ng) * io.xi_slice_pitch + lo;
       const uint32_t bytes = s_stage_bytes;
       s_xi_base = base;  // read by the refill thread after the next block barrier
       for (int j = 0; j < ns && j < p.S; ++j) {
@@ -280,21 +333,27 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
     double s = 0.0;
     bool mean_known = false;
     if (has_match) {
+      // F^{k-1}_{n-1}, its restriction and macro[k][n-1] belong to the owner
+      // of slice n-1 (another rank for the first slice of a rank)
+      const int rp = owner(n - 1);
+      const mmpr_pipeline_io &iop = pp.io[rp];
+      const PlFlags flp{iop.flags, N, K};
+      const bool remote = rp != r;
+      const bool rsys = sys && remote;
       // ---- serial correction of boundary n, then the match parameters ---------
       if (tid == 0) {
-        pl_wait(pp.fine_done + (int64_t)(k - 1) * N + (n - 1), p.ctas);
-        if (n - 1 >= 1) pl_wait(pp.chain_done + (int64_t)k * (N + 1) + (n - 1), 1);
-        if (k - 1 >= 1) pl_wait(pp.chain_done + (int64_t)(k - 1) * (N + 1) + n, 1);
+        pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys);
+        if (n - 1 >= 1) pl_wait(flp.chain_done(k, n - 1), ep, rsys);
+        if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, n), ep, false);
         // row 0's reader of this snapshot slot (units (0, n < N) read it)
-        if (!pp.retain && k == 2 && n < N) pl_wait(pp.consumed + n, p.ctas);
-        const double *prev = (n - 1 == 0) ? io.rho0 : io.macro + ((int64_t)k * (N + 1) + (n - 1)) * 3;
-        const double *fs = io.fine_stats + ((int64_t)(k - 1) * N + (n - 1)) * 3;
+        if (!pp.retain && k == 2 && n < N) pl_wait(fl.consumed(0, n), cdone, false);
+        const double *fs = iop.fine_stats + ((int64_t)(k - 1) * N + (n - 1)) * 3;
         const double *cin = io.cache + ((int64_t)(k - 1) * N + (n - 1)) * 3;
         double cur[3], f[3], c[3], pred[3], raw[3];
 #pragma unroll
         for (int v = 0; v < 3; ++v) {
-          cur[v] = __ldcg(prev + v);
-          f[v] = __ldcg(fs + v);
+          cur[v] = (n - 1 == 0) ? io.rho0[v] : pl_ld(iop.macro + ((int64_t)k * (N + 1) + (n - 1)) * 3 + v, remote);
+          f[v] = pl_ld(fs + v, remote);
           c[v] = __ldcg(cin + v);
         }
         int st = MMPR_STAT_OK;
@@ -323,11 +382,10 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
             io.raw[e * 3 + v] = raw[v];
             io.macro[((int64_t)k * (N + 1) + n) * 3 + v] = nxt[v];
           }
-          __threadfence();
-          pl_red_release(pp.chain_done + (int64_t)k * (N + 1) + n, 1);
+          pl_publish(fl.chain_done(k, n), 1, sys);
         }
         // match(corrected, F^{k-1}_{n-1}), raise policy (coupling.py:32-95)
-        const int64_t cn = __ldcg(io.fine_counts + (int64_t)(k - 1) * N + (n - 1));
+        const int64_t cn = pl_ld64(iop.fine_counts + (int64_t)(k - 1) * N + (n - 1), remote);
         int mode = PL_KEEP, status = MMPR_STAT_OK;
         double scale = 1.0, mc = 0.0, mu = 0.0;
         if (cn != 0) {
@@ -353,10 +411,10 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       __syncthreads();
       const double mu = s_match[0], scale = s_match[1], mc = s_match[2];
       const int mode = s_mode;
-      const double *src = io.fine + ((int64_t)((k - 1) & 1) * N + (n - 1)) * fpitch;
+      const double *src = iop.fine + ((int64_t)((k - 1) & 1) * N + (n - 1)) * iop.fine_pitch;
 #pragma unroll
-      for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? __ldcg(src + off + j8 + 8 * m) : 0.0;
-      if (HAS_TAIL && j8 < tail) xt = __ldcg(src + tail_off + j8);
+      for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? pl_ld(src + off + j8 + 8 * m, remote) : 0.0;
+      if (HAS_TAIL && j8 < tail) xt = pl_ld(src + tail_off + j8, remote);
       auto apply = [&](double v) {
         return mode == PL_SET ? mu : (mode == PL_AFFINE ? add(mul(scale, sub(v, mc)), mu) : v);
       };
@@ -364,7 +422,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       for (int m = 0; m < PPT; ++m) x[m] = apply(x[m]);
       if (HAS_TAIL) xt = apply(xt);
       __syncthreads();  // every load of the source slot has returned
-      if (tid == 0) pl_red_release(pp.consumed + (int64_t)k * (N + 1) + n, 1);
+      if (tid == 0) pl_publish(flp.consumed(k, n), 1, sys, false);  // the slot's owner waits on it
 #pragma unroll
       for (int m = 0; m < PPT; ++m)
         if (m < cnt) snap_kn[off + j8 + 8 * m] = x[m];
@@ -407,7 +465,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       if (HAS_TAIL && j8 < tail) xt = snap_kn[tail_off + j8];
       if (!pp.retain) {
         __syncthreads();
-        if (tid == 0) pl_red_release(pp.consumed + n, 1);
+        if (tid == 0) pl_publish(fl.consumed(0, n), 1, false, false);
       }
     }
 
@@ -426,8 +484,14 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
           if (m < LO) {
             x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
           } else {
-            const int idx = max(0, min(my_idx + 8 * m, last_idx));
-            const double nx = em_update<KIND>(p, x[m], s, xb[idx]);
+#ifdef PL_CLAMP
+            const double nx = em_update<KIND>(p, x[m], s, xb[max(0, min(my_idx + 8 * m, last_idx))]);
+#else
+            // past a 12-element leaf this reads up to 8 doubles beyond the
+            // CTA's range (into the next stage or the 64-byte pad after the
+            // last): the value is discarded, so no clamp is needed
+            const double nx = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
+#endif
             x[m] = (m < cnt) ? nx : x[m];
           }
         }
@@ -454,14 +518,18 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       // the unit's coordinates again from shared memory (not held in
       // registers across the step loop)
       const int tt = *(volatile int *)&s_ticket[it & 1];
-      const int k = tt / (N + 1), n = tt % (N + 1);
+      const int k = tt / pp.row_units, n = pp.lo_n + tt % pp.row_units;
+      const int r = owner(n);
+      const mmpr_pipeline_io &io = pp.io[r];
+      const PlFlags fl{io.flags, N, K};
 
       // ---- write F^k_n into the parity buffer, restriction, publish -------------
       if (k >= 2) {
-        if (tid == 0) pl_wait(pp.consumed + (int64_t)(k - 1) * (N + 1) + (n + 1), p.ctas);
+        // the reader of F^{k-2}_n (unit (k-1, n+1), owner of slice n+1) is done
+        if (tid == 0) pl_wait(fl.consumed(k - 1, n + 1), cdone, sys && owner(n + 1) != r);
         __syncthreads();
       }
-      double *xo = io.fine + ((int64_t)(k & 1) * N + n) * fpitch;
+      double *xo = io.fine + ((int64_t)(k & 1) * N + n) * io.fine_pitch;
 #pragma unroll
       for (int m = 0; m < PPT; ++m)
         if (m < cnt) xo[off + j8 + 8 * m] = x[m];
@@ -483,13 +551,13 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
         }
       }
       __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        pl_red_release(pp.fine_done + (int64_t)k * N + n, 1);
-      }
+      if (tid == 0) pl_publish(fl.fine_done(k, n), 1, sys);
     }
   }
 }
+#undef sys
+#undef ep
+#undef cdone
 
 // ---------------------------------------------------------------------------
 // host side
@@ -531,7 +599,7 @@ static int pipe_geometry(int64_t P, PipeGeometry *g) {
   }
   g->stage_elems = (int)((max_range + 1) & ~int64_t(1));
   g->nstages = 2;
-  g->smem = (size_t)g->stage_elems * 8 * g->nstages;
+  g->smem = (size_t)g->stage_elems * 8 * g->nstages + 64;  // + pad for the unclamped last element
   if (g->smem > 112 * 1024) return MMPR_ERR_UNSUPPORTED;  // two CTAs per SM
   g->tail = (P % 8) != 0;
   return MMPR_OK;
@@ -586,8 +654,12 @@ static int launch_pipe(const PipeParams &pp, const PipeGeometry &g, cudaStream_t
 
 template <int KIND, int OK, int MK>
 static int dispatch_pipe_tail(const PipeParams &pp, const PipeGeometry &g, cudaStream_t s) {
-  if (g.tail) return launch_pipe<pipeline_kernel<KIND, 13, true, OK, MK>>(pp, g, s);
-  return launch_pipe<pipeline_kernel<KIND, 13, false, OK, MK>>(pp, g, s);
+  if (pp.G > 1) {
+    if (g.tail) return launch_pipe<pipeline_kernel<KIND, 13, true, OK, MK, true>>(pp, g, s);
+    return launch_pipe<pipeline_kernel<KIND, 13, false, OK, MK, true>>(pp, g, s);
+  }
+  if (g.tail) return launch_pipe<pipeline_kernel<KIND, 13, true, OK, MK, false>>(pp, g, s);
+  return launch_pipe<pipeline_kernel<KIND, 13, false, OK, MK, false>>(pp, g, s);
 }
 
 // (fine model kind, ODE kind, ODE model kind) combinations with a pipeline
@@ -632,14 +704,8 @@ extern "C" int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_momen
   return dispatch_pipe(*model, *ode, *ode_model, nullptr, g, nullptr);
 }
 
-extern "C" int mmpr_parareal_pipeline(const mmpr_model *model, const mmpr_moment_ode *ode,
-                                      const mmpr_model *ode_model, const mmpr_integrator *integ,
-                                      int32_t n_slices, int32_t iterations,
-                                      int64_t particles, int32_t steps, double dt, double sqrt_dt,
-                                      int32_t reuse_converged, const mmpr_pipeline_io *io, void *stream) {
-  int st = mmpr_pipeline_supported(model, ode, ode_model, integ, particles);
-  if (st != MMPR_OK) return st;
-  if (!io || n_slices < 1 || iterations < 1 || steps < 0) return MMPR_ERR_ARG;
+static int check_io(const mmpr_pipeline_io *io, int32_t n_slices, int32_t iterations, int64_t particles,
+                    int32_t steps) {
   if (!io->times || !io->x0 || !io->rho0 || !io->counts0 || !io->snap || !io->fine || !io->macro || !io->micro ||
       !io->micro_counts || !io->fine_stats || !io->fine_counts || !io->raw || !io->cache || !io->bad ||
       !io->coarse_status || !io->match_status || !io->flags)
@@ -652,12 +718,44 @@ extern "C" int mmpr_parareal_pipeline(const mmpr_model *model, const mmpr_moment
                     (reinterpret_cast<uintptr_t>(io->xi) & 15) ||
                     (steps > 1 && io->xi_slice_pitch < steps * io->xi_row_pitch)))
     return MMPR_ERR_ARG;
+  return MMPR_OK;
+}
+
+extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_moment_ode *ode,
+                                            const mmpr_model *ode_model, const mmpr_integrator *integ,
+                                            int32_t n_slices, int32_t iterations, int64_t particles,
+                                            int32_t steps, double dt, double sqrt_dt, int32_t reuse_converged,
+                                            int32_t n_ranks, const mmpr_pipeline_io *ios, int32_t first_rank,
+                                            int32_t launch_ranks, int32_t epoch, int32_t reset_flags,
+                                            int32_t multi_gpu, void *stream) {
+  int st = mmpr_pipeline_supported(model, ode, ode_model, integ, particles);
+  if (st != MMPR_OK) return st;
+  if (!ios || n_slices < 1 || iterations < 1 || steps < 0 || n_ranks < 1 || n_ranks > PL_MAX_RANKS ||
+      n_slices % n_ranks != 0 || first_rank < 0 || launch_ranks < 1 || first_rank + launch_ranks > n_ranks ||
+      epoch < 1 || (reset_flags && epoch != 1))
+    return MMPR_ERR_ARG;
+  const int retain = ios[first_rank].snap_rows == iterations + 1 || iterations == 1;
+  for (int r = 0; r < n_ranks; ++r) {
+    const mmpr_pipeline_io &io = ios[r];
+    if (r >= first_rank && r < first_rank + launch_ranks) {  // ranks whose units run here: everything
+      st = check_io(&io, n_slices, iterations, particles, steps);
+      if (st != MMPR_OK) return st;
+      if ((io.snap_rows == iterations + 1 || iterations == 1) != (retain != 0)) return MMPR_ERR_ARG;
+    } else if (!io.flags || !io.macro || !io.fine_stats || !io.fine_counts || !io.fine ||
+               io.fine_pitch < particles) {  // peers: their exchange arrays
+      return MMPR_ERR_ARG;
+    }
+  }
   PipeGeometry g;
   pipe_geometry(particles, &g);
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t nflags = mmpr_pipeline_flags_size(n_slices, iterations);
-  cudaError_t err = cudaMemsetAsync(io->flags, 0, (size_t)nflags * sizeof(int32_t), s);
-  if (err != cudaSuccess) return mmpr_check(err, "pipeline: flag reset");
+  for (int r = first_rank; r < first_rank + launch_ranks; ++r) {
+    // the ticket always; every flag only when the caller resets per run
+    const size_t bytes = reset_flags ? (size_t)nflags * sizeof(int32_t) : sizeof(int32_t);
+    cudaError_t err = cudaMemsetAsync(ios[r].flags, 0, bytes, s);
+    if (err != cudaSuccess) return mmpr_check(err, "pipeline: flag reset");
+  }
 
   PipeParams pp = {};
   FineParams &p = pp.f;
@@ -673,9 +771,8 @@ extern "C" int mmpr_parareal_pipeline(const mmpr_model *model, const mmpr_moment
     case MMPR_MODEL_CUBIC_MF: p.bsd = model->p[3] * sqrt_dt; break;
     default: break;
   }
-  p.xi = io->xi;
-  p.xi_slice_pitch = io->xi_slice_pitch;
-  p.xi_row_pitch = io->xi_row_pitch;
+  p.xi_slice_pitch = ios[first_rank].xi_slice_pitch;
+  p.xi_row_pitch = ios[first_rank].xi_row_pitch;
   p.D = g.D;
   p.slots_per_cta = g.spc;
   p.ctas = g.ctas;
@@ -684,19 +781,76 @@ extern "C" int mmpr_parareal_pipeline(const mmpr_model *model, const mmpr_moment
   p.cnt_min = 12;
   p.l2_ahead = 3;
   if (const char *env = getenv("MMPR_FINE_L2_AHEAD")) p.l2_ahead = max(0, min(16, atoi(env)));
+  for (int r = 0; r < n_ranks; ++r) {
+    const bool local = r >= first_rank && r < first_rank + launch_ranks;
+    if (local && (ios[r].xi_row_pitch != p.xi_row_pitch || ios[r].xi_slice_pitch != p.xi_slice_pitch))
+      return MMPR_ERR_ARG;
+    pp.io[r] = ios[r];
+  }
   pp.ode = *ode;
   pp.ode_model = *ode_model;
   pp.integ = *integ;
-  pp.io = *io;
   pp.N = n_slices;
   pp.K = iterations;
-  pp.units = (iterations + 1) * (n_slices + 1);
+  pp.G = n_ranks;
+  pp.Ng = n_slices / n_ranks;
+  pp.r0 = first_rank;
+  pp.lo_n = first_rank * pp.Ng;
+  const int hi_n = (first_rank + launch_ranks == n_ranks) ? n_slices : (first_rank + launch_ranks) * pp.Ng - 1;
+  pp.row_units = hi_n - pp.lo_n + 1;
+  pp.units = (iterations + 1) * pp.row_units;
   pp.reuse = reuse_converged ? 1 : 0;
-  pp.retain = io->snap_rows == iterations + 1 ? 1 : 0;
-  if (iterations == 1 && io->snap_rows == 2) pp.retain = 1;  // two rows are all of them
-  pp.ticket = io->flags;
-  pp.fine_done = io->flags + 1;
-  pp.chain_done = pp.fine_done + (int64_t)iterations * n_slices;
-  pp.consumed = pp.chain_done + (int64_t)(iterations + 1) * (n_slices + 1);
+  pp.retain = retain;
+  pp.epoch = epoch;
+  pp.sys = multi_gpu ? 1 : 0;
   return dispatch_pipe(*model, *ode, *ode_model, &pp, g, s);
+}
+
+extern "C" int mmpr_parareal_pipeline(const mmpr_model *model, const mmpr_moment_ode *ode,
+                                      const mmpr_model *ode_model, const mmpr_integrator *integ,
+                                      int32_t n_slices, int32_t iterations, int64_t particles, int32_t steps,
+                                      double dt, double sqrt_dt, int32_t reuse_converged,
+                                      const mmpr_pipeline_io *io, void *stream) {
+  return mmpr_parareal_pipeline_ranks(model, ode, ode_model, integ, n_slices, iterations, particles, steps, dt,
+                                      sqrt_dt, reuse_converged, 1, io, 0, 1, 1, 1, 0, stream);
+}
+
+// ---- exchange memory for the multi-GPU pipeline (CUDA IPC) -------------------
+extern "C" int mmpr_exchange_alloc(int64_t bytes, void **dev_ptr) {
+  if (bytes < 1 || !dev_ptr) return MMPR_ERR_ARG;
+  return mmpr_check(cudaMalloc(dev_ptr, (size_t)bytes), "exchange: cudaMalloc");
+}
+
+extern "C" int mmpr_exchange_free(void *dev_ptr) {
+  if (!dev_ptr) return MMPR_OK;
+  return mmpr_check(cudaFree(dev_ptr), "exchange: cudaFree");
+}
+
+extern "C" int mmpr_ipc_handle(void *dev_ptr, unsigned char *handle_out) {
+  if (!dev_ptr || !handle_out) return MMPR_ERR_ARG;
+  cudaIpcMemHandle_t h;
+  const int st = mmpr_check(cudaIpcGetMemHandle(&h, dev_ptr), "exchange: cudaIpcGetMemHandle");
+  if (st != MMPR_OK) return st;
+  memcpy(handle_out, &h, sizeof(h));
+  return MMPR_OK;
+}
+
+extern "C" int mmpr_ipc_open(const unsigned char *handle, void **dev_ptr) {
+  if (!handle || !dev_ptr) return MMPR_ERR_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return mmpr_check(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "exchange: cudaIpcOpenMemHandle");
+}
+
+extern "C" int mmpr_ipc_close(void *dev_ptr) {
+  if (!dev_ptr) return MMPR_OK;
+  return mmpr_check(cudaIpcCloseMemHandle(dev_ptr), "exchange: cudaIpcCloseMemHandle");
+}
+
+extern "C" int mmpr_device_can_access_peer(int32_t device, int32_t peer, int32_t *out) {
+  if (!out) return MMPR_ERR_ARG;
+  int v = 0;
+  const int st = mmpr_check(cudaDeviceCanAccessPeer(&v, device, peer), "cudaDeviceCanAccessPeer");
+  *out = v;
+  return st;
 }

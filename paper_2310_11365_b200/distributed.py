@@ -19,7 +19,9 @@ the oracle (gloo).  Production uses ``GpuBackend`` only.
 
 from __future__ import annotations
 
+import ctypes
 import dataclasses
+import os
 
 import numpy as np
 import torch
@@ -113,6 +115,20 @@ class TorchComm:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
 
+    def _device(self):
+        return "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+
+    def all_min_int(self, value: int) -> int:
+        t = torch.tensor([int(value)], dtype=torch.int64, device=self._device())
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return int(t.item())
+
+    def all_gather_bytes(self, payload: bytes) -> list:
+        """Fixed-size byte strings from every rank (IPC handles)."""
+        t = torch.tensor(list(payload), dtype=torch.uint8, device=self._device()).reshape(1, -1)
+        out = self.all_gather_rows(t).cpu().numpy()
+        return [bytes(row) for row in out]
+
     def all_max(self, value: float) -> float:
         t = torch.tensor([value], dtype=torch.float64,
                          device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
@@ -120,15 +136,146 @@ class TorchComm:
         return float(t.item())
 
 
+_PIPE_STATE: dict = {}
+last_run_info: dict = {"pipeline": False}
+
+
+def _pipeline_sharded_ok(be, cfg: PararealConfig, plan: NoisePlan, comm) -> bool:
+    """Every rank agrees to run the multi-GPU iteration pipeline: GPU
+    backend, an instantiated configuration, FROZEN noise, no Wasserstein
+    stop, N divisible by the world size, at most 8 ranks."""
+    if (not isinstance(be, GpuBackend) or os.environ.get("MMPR_PIPELINE", "1") == "0"
+            or not hasattr(comm, "all_min_int")):
+        return False
+    G = comm.world
+    ok = (G <= 8 and cfg.n_slices % G == 0 and cfg.iterations >= 1 and not plan.fresh
+          and cfg.stop_wasserstein_tol is None
+          and kernels.pipeline_supported(be.model_d, be.ode_d, be.ode_model_d, be.integ_d, cfg.particles))
+    return comm.all_min_int(1 if ok else 0) == 1
+
+
+def _pipeline_state(be, cfg: PararealConfig, comm):
+    """Per-configuration rank buffers with an IPC-exportable exchange block,
+    and the previous rank's exchange block mapped into this process (the
+    only peer memory a rank touches: it reads rank r-1's outputs for its first
+    slice and adds its "consumed" signals to rank r-1's flags)."""
+    from . import sharded_pipeline as SP
+    R, G = comm.rank, comm.world
+    key = (cfg.n_slices, cfg.iterations, cfg.particles, cfg.step.steps_per_slice, cfg.retain_snapshots, R, G,
+           torch.cuda.current_device())
+    st = _PIPE_STATE.get(key)
+    if st is not None:
+        return st
+    for old in list(_PIPE_STATE.values()):  # one configuration at a time
+        old["rb"].free()
+    _PIPE_STATE.clear()
+    rb = SP.RankBuffers(R, G, cfg.n_slices, cfg.iterations, cfg.particles, cfg.step.steps_per_slice,
+                        cfg.retain_snapshots, raw_exchange=G > 1)
+    prev_base = None
+    if G > 1:
+        handle = (ctypes.c_ubyte * 64)()
+        _lib.call("mmpr_ipc_handle", ctypes.c_void_p(rb.block.ptr), handle)
+        handles = comm.all_gather_bytes(bytes(handle))
+        ok = 1
+        if R > 0:
+            ptr = ctypes.c_void_p()
+            st_open = _lib.load().mmpr_ipc_open((ctypes.c_ubyte * 64).from_buffer_copy(handles[R - 1]),
+                                                ctypes.byref(ptr))
+            ok = 1 if st_open == 0 else 0
+            prev_base = int(ptr.value) if ok else None
+        if comm.all_min_int(ok) != 1:
+            if prev_base is not None:
+                _lib.load().mmpr_ipc_close(ctypes.c_void_p(prev_base))
+            rb.free()
+            return None
+    st = {"rb": rb, "prev_base": prev_base}
+    _PIPE_STATE[key] = st
+    return st
+
+
+def _run_pipeline_sharded(be, initial, cfg: PararealConfig, plan: NoisePlan, comm, reuse: bool,
+                          record_timings: bool, st) -> PararealTrace:
+    """Iterations 1..K as one persistent kernel per GPU; the first slice of
+    rank r waits on rank r-1's flags and reads its last fine output, its
+    restriction and macro value through the mapped exchange block
+    (mmpr_parareal_pipeline_ranks).  One all-gather at the end merges the
+    per-slice trace arrays."""
+    from . import sharded_pipeline as SP
+    R, G = comm.rank, comm.world
+    N, K, P, S = cfg.n_slices, cfg.iterations, cfg.particles, cfg.step.steps_per_slice
+    Ng = N // G
+    rb = st["rb"]
+    times = tuple(cfg.t_start + n * cfg.slice_length for n in range(N + 1))
+    times_d = torch.tensor(times, dtype=torch.float64, device=be.device)
+    if isinstance(initial, ParticleEnsemble):
+        x0 = initial.device_positions.to(be.device)
+    else:
+        x0 = sample_initial(initial, plan, P).device_positions
+    timer = _StageTimer(record_timings)
+    ev = timer.start()
+    rb.prologue(be.ode_d, be.ode_model_d, be.integ_d, times_d, x0, plan.master_seed)
+    timer.stop("prologue", ev)
+    own = rb.io(times_d)
+    ios = [own] * G
+    if R > 0:
+        ios[R - 1] = rb.peer_io(st["prev_base"], own)
+    rb.epoch += 1
+    ev = timer.start()
+    SP.launch(be.model_d, be.ode_d, be.ode_model_d, be.integ_d, cfg.step.dt, S, reuse, ios, R, 1, rb.epoch,
+              False, G > 1, N, K, P)
+    timer.stop("iterations", ev)
+    # ---- one gather of the per-slice arrays, merged by ownership -------------------
+    names = (("macro", "boundary"), ("micro", "boundary"), ("micro_counts", "boundary"), ("fine_stats", "slice"),
+             ("fine_counts", "slice"), ("bad", "slice"), ("raw", "shifted"), ("coarse_status", "shifted"),
+             ("match_status", "shifted"))
+    h = {}
+    by_dtype = {}
+    for name, kind in names:
+        by_dtype.setdefault(getattr(rb, name).dtype, []).append((name, kind))
+    for dtype, items in by_dtype.items():  # one gather and one read-back per dtype
+        flat = torch.cat([getattr(rb, name).reshape(-1) for name, _ in items]).reshape(1, -1)
+        rows = (comm.all_gather_rows(flat) if G > 1 else flat).cpu().numpy()
+        off = 0
+        for name, kind in items:
+            shape = tuple(getattr(rb, name).shape)
+            size = int(np.prod(shape))
+            parts = [rows[g, off:off + size].reshape(shape) for g in range(G)]
+            h[name] = SP.merge_rows(parts, Ng, G, N, kind)
+            off += size
+    h["rho0"] = rb.rho0.cpu().numpy()
+    h["counts0"] = rb.counts0.cpu().numpy()
+    _raise_first_error(h, N, K, 1)
+    trace = _build_trace(h, None, dataclasses.replace(cfg, retain_snapshots=False), plan, times, K, 1,
+                         _StageTimer(False), None)
+    own_b = SP.owned_boundaries(R, Ng, G, N)
+    if cfg.retain_snapshots:
+        trace.snapshots = [[ParticleEnsemble._wrap(rb.snap[k, n]) for n in own_b] for k in range(K + 1)]
+    trace.timings = timer.resolve()
+    trace.timings["slice_offset"] = own_b.start
+    trace.timings["slices_per_rank"] = Ng
+    trace.d2h_bytes = int(sum(v.nbytes for v in h.values()))
+    return trace
+
+
 def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: NoisePlan, comm=None,
                             backend=None, reuse_converged_coarse: bool = True,
                             record_timings: bool = True) -> PararealTrace:
     """mM-Parareal over ``comm.world`` ranks; every rank returns the full
     macro/micro trace, snapshots hold the rank's own slices only
-    (``trace.snapshots[k][m]`` is global slice boundary ``offset + m``)."""
+    (``trace.snapshots[k][m]`` is global slice boundary ``offset + m``).
+
+    Configurations the iteration pipeline covers run it on every GPU
+    (cross-rank dependencies through peer memory, one gather at the end);
+    the rest run the per-iteration kernels with NCCL collectives."""
     comm = comm if comm is not None else TorchComm()
     reuse_converged_coarse = reuse_converged_coarse and not plan.fresh  # see engine.run_micro_macro
     be = backend if backend is not None else GpuBackend(model, coarse, cfg)
+    if _pipeline_sharded_ok(be, cfg, plan, comm):
+        st = _pipeline_state(be, cfg, comm)
+        if st is not None:
+            last_run_info["pipeline"] = True
+            return _run_pipeline_sharded(be, initial, cfg, plan, comm, reuse_converged_coarse, record_timings, st)
+    last_run_info["pipeline"] = False
     R, G = comm.rank, comm.world
     N, K, P, S, I = cfg.n_slices, cfg.iterations, cfg.particles, cfg.step.steps_per_slice, cfg.partition.n_regions
     if N % G:

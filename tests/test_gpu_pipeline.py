@@ -150,3 +150,96 @@ def test_pipeline_full_config4(mm, monkeypatch):
     a = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
     b = _run(mm, monkeypatch, False, model, ode, init, cfg, plan)
     _same(a, b)
+
+
+def _emulated_ranks(mm, G, model, ode, init, cfg, plan, epochs=1):
+    """The multi-rank pipeline over G ranks on one GPU: per-rank buffers and
+    prologues, ONE launch over every rank's units (ranks reading each other's
+    exchange arrays), merged like the multi-GPU driver does."""
+    import torch
+    from paper_2310_11365_b200 import sharded_pipeline as SP
+    from paper_2310_11365_b200.models import device_model
+    from paper_2310_11365_b200.moments import device_ode
+    from paper_2310_11365_b200.rk54 import integrator_descriptor
+    N, K, P, S = cfg.n_slices, cfg.iterations, cfg.particles, cfg.step.steps_per_slice
+    model_d = device_model(model)
+    ode_d, odm = device_ode(ode)
+    integ_d = integrator_descriptor(cfg.integrator)
+    times = torch.tensor([cfg.t_start + n * cfg.slice_length for n in range(N + 1)], dtype=torch.float64,
+                         device="cuda")
+    x0 = mm.sample_initial(init, plan, P).device_positions
+    ranks = [SP.RankBuffers(r, G, N, K, P, S, cfg.retain_snapshots) for r in range(G)]
+    for epoch in range(1, epochs + 1):
+        for rb in ranks:
+            rb.prologue(ode_d, odm, integ_d, times, x0, plan.master_seed)
+        ios = [rb.io(times) for rb in ranks]
+        SP.launch(model_d, ode_d, odm, integ_d, cfg.step.dt, S, True, ios, 0, G, epoch, epochs == 1, False, N, K, P)
+    torch.cuda.synchronize()
+    Ng = N // G
+    out = {}
+    for name, kind in (("macro", "boundary"), ("micro", "boundary"), ("micro_counts", "boundary"),
+                       ("fine_stats", "slice"), ("fine_counts", "slice"), ("bad", "slice"), ("raw", "shifted"),
+                       ("cache", "shifted"), ("coarse_status", "shifted"), ("match_status", "shifted")):
+        out[name] = SP.merge_rows([getattr(rb, name).cpu().numpy() for rb in ranks], Ng, G, N, kind)
+    rows = ranks[0].snap.shape[0]
+    snap = np.stack([ranks[SP.owner(n, Ng, G)].snap[:, n].cpu().numpy() for n in range(N + 1)], axis=1)
+    out["snap"] = snap[:rows]
+    return out
+
+
+@pytest.mark.parametrize("G,N,K", [(2, 8, 4), (4, 16, 5), (8, 16, 3), (3, 9, 9)])
+def test_multi_rank_pipeline_emulated_on_one_gpu(mm, monkeypatch, G, N, K):
+    """Ranks exchange only through each other's exchange arrays and flags;
+    the merged result equals the single-rank pipeline bit for bit."""
+    model, ode, init, cfg = _ou_case(mm, N, K, 12)
+    plan = mm.NoisePlan(0)
+    ref = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
+    emu = _emulated_ranks(mm, G, model, ode, init, cfg, plan)
+    assert np.array_equal(emu["macro"], ref["macro"])
+    assert np.array_equal(emu["micro"], ref["micro"])
+    assert np.array_equal(emu["snap"], ref["snap"])
+    for name in ("bad", "coarse_status", "match_status"):
+        assert (emu[name] == mm._lib.STAT_OK).all(), name
+
+
+def test_multi_rank_pipeline_epochs(mm, monkeypatch):
+    """Flags accumulate across runs (no reset between them): the second run,
+    waiting for epoch 2, reproduces the first."""
+    model, ode, init, cfg = _ou_case(mm, 8, 3, 10, retain=False)
+    plan = mm.NoisePlan(0)
+    one = _emulated_ranks(mm, 4, model, ode, init, cfg, plan, epochs=1)
+    two = _emulated_ranks(mm, 4, model, ode, init, cfg, plan, epochs=2)
+    for key in one:
+        assert np.array_equal(one[key], two[key]), key
+    ref = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
+    assert np.array_equal(one["macro"], ref["macro"])
+
+
+def test_sharded_driver_takes_the_pipeline_over_nccl_world_one(mm, monkeypatch):
+    """run_micro_macro_sharded with its real communicator (NCCL, one rank)
+    runs the multi-GPU pipeline path (rank buffers, epoch-tagged flags, the
+    ownership merge) and equals the single-GPU engine bit for bit, run after
+    run (flags accumulate across epochs)."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2310_11365_b200 import distributed as D
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        model, ode, init, cfg = _ou_case(mm, 8, 4, 16)
+        plan = mm.NoisePlan(0)
+        ref = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
+        for _ in range(3):
+            tr = D.run_micro_macro_sharded(model, ode, init, cfg, plan, comm=D.TorchComm())
+            assert D.last_run_info["pipeline"]
+            assert np.array_equal(_packed(tr, "macro"), ref["macro"])
+            assert np.array_equal(_packed(tr, "micro_stats"), ref["micro"])
+            assert np.array_equal(np.array([[e.positions for e in row] for row in tr.snapshots]), ref["snap"])
+            assert np.array_equal(np.array(tr.fraction_gaps, dtype=float), ref["gaps"])
+    finally:
+        dist.destroy_process_group()
