@@ -243,3 +243,62 @@ def test_sharded_driver_takes_the_pipeline_over_nccl_world_one(mm, monkeypatch):
             assert np.array_equal(np.array(tr.fraction_gaps, dtype=float), ref["gaps"])
     finally:
         dist.destroy_process_group()
+
+
+def _ipc_worker(rank, port, result_path):
+    """One of two processes on GPU 0: export an exchange block, open the
+    other rank's through CUDA IPC, read its macro array (no kernel waits on
+    the other process)."""
+    import ctypes
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2310_11365_b200 as mm
+        from paper_2310_11365_b200 import _lib, sharded_pipeline as SP
+        from paper_2310_11365_b200.distributed import TorchComm
+        comm = TorchComm()
+        rb = SP.RankBuffers(rank, 2, 8, 2, 100_000, 4, False, raw_exchange=True)
+        rb.macro.copy_(torch.full_like(rb.macro, 10.0 + rank))
+        torch.cuda.synchronize()
+        handle = (ctypes.c_ubyte * 64)()
+        _lib.call("mmpr_ipc_handle", ctypes.c_void_p(rb.block.ptr), handle)
+        handles = comm.all_gather_bytes(bytes(handle))
+        other = 1 - rank
+        ptr = ctypes.c_void_p()
+        _lib.call("mmpr_ipc_open", (ctypes.c_ubyte * 64).from_buffer_copy(handles[other]), ctypes.byref(ptr))
+        io = rb.peer_io(int(ptr.value), rb.io(torch.zeros(9, dtype=torch.float64, device="cuda")))
+
+        class _View:
+            pass
+        v = _View()
+        v.__cuda_array_interface__ = {"shape": (rb.macro.numel(),), "typestr": "<f8", "data": (io.macro, False),
+                                      "version": 2}
+        seen = torch.as_tensor(v, device="cuda").clone()
+        torch.cuda.synchronize()
+        ok = bool((seen == 10.0 + other).all())
+        dist.barrier()  # the peer keeps its block alive until both have read
+        _lib.call("mmpr_ipc_close", ptr)
+        rb.free()
+        with open(f"{result_path}.{rank}", "w") as fh:
+            fh.write("ok" if ok else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exchange_block_ipc_roundtrip(tmp_path):
+    """The multi-GPU pipeline's plumbing: an exchange block exported by one
+    process is mapped by another (cudaIpcOpenMemHandle) at the exchange-layout
+    offsets peer_io computes."""
+    import socket
+    import torch.multiprocessing as tmp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    path = str(tmp_path / "ipc")
+    tmp.spawn(_ipc_worker, args=(port, path), nprocs=2, join=True)
+    assert open(path + ".0").read() == "ok"
+    assert open(path + ".1").read() == "ok"
