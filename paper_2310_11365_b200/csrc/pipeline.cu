@@ -88,13 +88,15 @@ __device__ __forceinline__ void pl_publish(int *p, int v, bool sys, bool fence =
 }
 
 // Spin until *p >= target.  A dependency that never arrives is a bug; the
-// watchdog (~9 s) turns it into a kernel fault instead of a hung device.
+// watchdog turns it into a kernel fault instead of a hung device (~9 s on one
+// GPU; ~70 s for a peer GPU's flag, whose kernel a slow host may launch late).
 __device__ __forceinline__ void pl_wait(const int *p, int target, bool sys) {
   if (pl_ld_acquire(p, sys) >= target) return;
   const long long t0 = clock64();
+  const long long limit = sys ? (1LL << 37) : (1LL << 34);
   while (pl_ld_acquire(p, sys) < target) {
     __nanosleep(64);
-    if (clock64() - t0 > (1LL << 34)) __trap();
+    if (clock64() - t0 > limit) __trap();
   }
 }
 

@@ -186,21 +186,19 @@ def launch(model_d, ode_d, ode_model_d, integ_d, dt: float, S: int, reuse: bool,
 # ---- merge of the per-rank results (host, numpy) ---------------------------------------
 def merge_rows(parts: list, Ng: int, G: int, N: int, kind: str) -> np.ndarray:
     """Assemble global arrays from per-rank copies (each written only at its
-    owned entries).  kind: "boundary" (index n in [0, N]: macro, micro, the
-    owner is owner(n) with boundary 0 from rank 0 and N from the last), or
-    "slice" (fine_stats/fine_counts/bad at slice n, owner(n)), or
-    "shifted" (cache/raw/coarse_status/match_status at n-1 for the match
-    unit of boundary n: index m is owned by owner(m + 1))."""
-    out = parts[0].copy()
-    length = out.shape[1]
-    for idx in range(length):
-        if kind == "boundary":
-            src = owner(idx, Ng, G)
-        elif kind == "slice":
-            src = owner(idx, Ng, G)
-        elif kind == "shifted":
-            src = owner(idx + 1, Ng, G)
-        else:
-            raise ValueError(kind)
-        out[:, idx] = parts[src][:, idx]
-    return out
+    owned entries; axis 1 indexes slices/boundaries).  kind: "boundary"
+    (index n in [0, N]: macro, micro; owner(n), boundary 0 from rank 0 and N
+    from the last), "slice" (fine_stats/fine_counts/bad at slice n,
+    owner(n)), or "shifted" (cache/raw/coarse_status/match_status at n-1 for
+    the match unit of boundary n: index m is owned by owner(m + 1))."""
+    stacked = np.stack(parts)  # (G, rows, length, ...)
+    length = stacked.shape[2]
+    idx = np.arange(length)
+    if kind in ("boundary", "slice"):
+        src = np.minimum(idx // Ng, G - 1)
+    elif kind == "shifted":
+        src = np.minimum((idx + 1) // Ng, G - 1)
+    else:
+        raise ValueError(kind)
+    picked = stacked[src, :, idx]  # (length, rows, ...)
+    return np.moveaxis(picked, 0, 1).copy()
