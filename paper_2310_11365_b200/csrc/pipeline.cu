@@ -31,6 +31,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <limits.h>
 
 #include <type_traits>
 
@@ -60,6 +61,8 @@ struct PipeParams {
   int lo_n;         // first boundary index of the launch's units
   int row_units;    // units per row for this launch
   int units;
+  int rank_tickets;  // one-GPU emulation of multi-GPU scheduling: cluster c serves rank r0 + c % nranks
+  int nranks;        // ranks of this launch
   int reuse;  // cached predictions for converged slices (engine skip_until)
   int retain;
   int epoch;
@@ -87,6 +90,18 @@ __device__ __forceinline__ void pl_publish(int *p, int v, bool sys, bool fence =
   }
 }
 
+// Publish a value (idempotent: several threads may publish the same chain
+// step with the same value) after this thread's stores.
+__device__ __forceinline__ void pl_publish_value(int *p, int v, bool sys) {
+  if (sys) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  } else {
+    __threadfence();
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  }
+}
+
 // Spin until *p >= target.  A dependency that never arrives is a bug; the
 // watchdog turns it into a kernel fault instead of a hung device (~9 s on one
 // GPU; ~70 s for a peer GPU's flag, whose kernel a slow host may launch late).
@@ -106,7 +121,8 @@ __device__ __forceinline__ int64_t pl_ld64(const int64_t *p, bool remote) {
   return remote ? (int64_t)__ldcv((const long long *)p) : (int64_t)__ldcg((const long long *)p);
 }
 
-// flag words of one rank: [0] ticket, then fine_done[K][N], chain_done[K+1][N+1], consumed[K+1][N+1]
+// flag words of one rank: [0] ticket, then fine_done[K][N], chain_done[K+1][N+1], consumed[K+1][N+1],
+// chain_front[K+1]
 struct PlFlags {
   int *base;
   int N, K;
@@ -117,9 +133,111 @@ struct PlFlags {
   __device__ int *consumed(int k, int n) const {
     return base + 1 + (int64_t)K * N + (int64_t)(K + 1) * (N + 1) + (int64_t)k * (N + 1) + n;
   }
+  // hint: epoch * (N + 2) + first boundary of row k whose chain step this
+  // rank has not yet published (atomicMax, monotone across epochs)
+  __device__ int *chain_front(int k) const { return base + 1 + (int64_t)K * N + 2 * (int64_t)(K + 1) * (N + 1) + k; }
 };
 
 enum { PL_KEEP = 0, PL_SET = 1, PL_AFFINE = 2 };
+
+__device__ __forceinline__ int pl_owner(const PipeParams &pp, int m) {
+  const int o = m / pp.Ng;
+  return o < pp.G ? o : pp.G - 1;
+}
+
+// One step of the serial correction (engine.py:210-236): boundary m of row
+// k from macro[k][m-1] (rho0 for m = 1), R(F^{k-1}_{m-1}) and the previous
+// row's prediction cache[k-1][m-1] (reused as the prediction itself for a
+// converged slice, m-1 < k).  io: the rank owning boundary m; iop: the owner
+// of slice m-1 (another rank's exchange arrays for a rank's first boundary).
+// STORE: write macro[k][m], cache[k][m-1], raw[k-1][m-1],
+// coarse_status[k][m-1] and publish chain_done(k, m); the corrected state
+// also goes to s_chain for the calling CTA.
+template <int OK, int MK, bool STORE = true>
+__device__ __forceinline__ void pl_chain_step(const PipeParams &pp, const mmpr_pipeline_io &io,
+                                              const mmpr_pipeline_io &iop, const PlFlags &fl, int k, int m,
+                                              bool remote, double *s_out = nullptr) {
+  const int N = pp.N;
+  const double *fs = iop.fine_stats + ((int64_t)(k - 1) * N + (m - 1)) * 3;
+  const double *cin = io.cache + ((int64_t)(k - 1) * N + (m - 1)) * 3;
+  double cur[3], f[3], c[3], pred[3], raw[3];
+#pragma unroll
+  for (int v = 0; v < 3; ++v) {
+    cur[v] = (m - 1 == 0) ? io.rho0[v] : pl_ld(iop.macro + ((int64_t)k * (N + 1) + (m - 1)) * 3 + v, remote);
+    f[v] = pl_ld(fs + v, remote);
+    c[v] = __ldcg(cin + v);
+  }
+  int st = MMPR_STAT_OK;
+  if (pp.reuse && m - 1 < k) {
+#pragma unroll
+    for (int v = 0; v < 3; ++v) pred[v] = c[v];
+  } else {
+#pragma unroll
+    for (int v = 0; v < 3; ++v) pred[v] = cur[v];
+    long long steps;
+    double h;
+    const double t0 = __ldg(io.times + m - 1);
+    euler_grid(pp.integ.dt, t0, __ldg(io.times + m), &steps, &h);
+    st = integrate_euler_n<3, OK, MK>(pp.ode, pp.ode_model, steps, h, t0, pred);
+  }
+#pragma unroll
+  for (int v = 0; v < 3; ++v) raw[v] = add(f[v], sub(pred[v], c[v]));
+  const bool neg = raw[1] < 0.0;
+  const double nxt[3] = {raw[0], (neg && raw[1] < 0.0) ? 0.0 : raw[1], f[2]};
+  if (s_out) {
+#pragma unroll
+    for (int v = 0; v < 3; ++v) s_out[v] = nxt[v];
+  }
+  if (STORE) {
+    const int64_t e = (int64_t)(k - 1) * N + (m - 1);
+    io.coarse_status[(int64_t)k * N + (m - 1)] = st;
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+      io.cache[((int64_t)k * N + (m - 1)) * 3 + v] = pred[v];
+      io.raw[e * 3 + v] = raw[v];
+      io.macro[((int64_t)k * (N + 1) + m) * 3 + v] = nxt[v];
+    }
+    pl_publish_value(fl.chain_done(k, m), pp.epoch, pp.sys != 0);
+  }
+}
+
+// Several ranks: advance rank r's chain of row k over its boundaries from
+// the published frontier -- waiting for the inputs of boundaries up to
+// n_must, stopping at the first boundary beyond it whose inputs are not yet
+// there.  Called by the first CTA of every unit that needs a boundary, so a
+// rank hands its last chain value to the next rank soon after its previous
+// row is done instead of only when its last unit of the row starts.
+// Steps evaluated twice (by two units racing) are identical and publish the
+// same value.
+template <int OK, int MK>
+__device__ __forceinline__ void pl_advance_chain(const PipeParams &pp, int k, int r, int n_must) {
+  const int N = pp.N, K = pp.K, ep = pp.epoch, cdone = pp.epoch * pp.f.ctas;
+  const bool sys = pp.sys != 0;
+  const mmpr_pipeline_io &io = pp.io[r];
+  const PlFlags fl{io.flags, N, K};
+  const int hi = (r == pp.G - 1) ? N : (r + 1) * pp.Ng - 1;
+  const int lo = r * pp.Ng > 1 ? r * pp.Ng : 1;
+  const int fr = *(volatile int *)fl.chain_front(k) - ep * (N + 2);
+  for (int m = fr > lo ? fr : lo; m <= hi; ++m) {
+    if (pl_ld_acquire(fl.chain_done(k, m), false) >= ep) continue;
+    const int om = pl_owner(pp, m - 1);
+    const mmpr_pipeline_io &iom = pp.io[om];
+    const PlFlags flm{iom.flags, N, K};
+    const bool rem = om != r;
+    const bool msys = sys && rem;
+    if (m > n_must) {
+      if (pl_ld_acquire(flm.fine_done(k - 1, m - 1), msys) < cdone) return;
+      if (m - 1 >= 1 && pl_ld_acquire(flm.chain_done(k, m - 1), msys) < ep) return;
+      if (k - 1 >= 1 && pl_ld_acquire(fl.chain_done(k - 1, m), false) < ep) return;
+    } else {
+      pl_wait(flm.fine_done(k - 1, m - 1), cdone, msys);
+      if (m - 1 >= 1) pl_wait(flm.chain_done(k, m - 1), ep, msys);
+      if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, m), ep, false);
+    }
+    pl_chain_step<OK, MK>(pp, io, iom, fl, k, m, rem);
+    atomicMax(fl.chain_front(k), ep * (N + 2) + m + 1);
+  }
+}
 
 // MULTI = false: one rank (the single-GPU engine); the rank table collapses
 // to io[0] at compile time and the step loop keeps every value in registers.
@@ -136,6 +254,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
   __shared__ __align__(8) uint64_t s_red_bar[2];
   __shared__ int s_ticket[2];
   __shared__ double s_match[3];  // mu, scale, mc
+  __shared__ double s_chain[3];  // this CTA's evaluation of the corrected state (one rank)
   __shared__ int s_mode;
   __shared__ const double *s_xi_base;  // this CTA's increments of the unit's slice, step 0
   __shared__ uint32_t s_stage_bytes;
@@ -299,7 +418,17 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
   for (int it = 0;; ++it) {
     // ---- next ticket, broadcast to the cluster ---------------------------------
     if (rank == 0 && tid == 0) {
-      const int t = atomicAdd(pp.io[pp.r0].flags, 1);
+      int t;
+      if (MULTI && pp.rank_tickets) {
+        // rank rr's own units in (k, n) order, encoded as k * (N + 1) + n
+        const int rr = pp.r0 + (int)(blockIdx.x / p.ctas) % pp.nranks;
+        const int lo = rr * pp.Ng, hi = (rr == pp.G - 1) ? N : (rr + 1) * pp.Ng - 1;
+        const int ru = hi - lo + 1;
+        const int q = atomicAdd(pp.io[rr].flags, 1);
+        t = q >= (K + 1) * ru ? INT_MAX : (q / ru) * (N + 1) + lo + q % ru;
+      } else {
+        t = atomicAdd(pp.io[pp.r0].flags, 1);
+      }
       if (p.ctas > 1) {
         for (int c = 0; c < p.ctas; ++c) st_cluster_u32(mapa_shared(smem_addr(&s_ticket[it & 1]), (uint32_t)c), t);
       } else {
@@ -309,8 +438,9 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
     if (p.ctas > 1) cluster_sync_all();
     else __syncthreads();
     const int t = s_ticket[it & 1];
-    if (t >= pp.units) break;
-    const int k = t / pp.row_units, n = pp.lo_n + t % pp.row_units;
+    if (MULTI && pp.rank_tickets ? t == INT_MAX : t >= pp.units) break;
+    const int k = (MULTI && pp.rank_tickets) ? t / (N + 1) : t / pp.row_units;
+    const int n = (MULTI && pp.rank_tickets) ? t % (N + 1) : pp.lo_n + t % pp.row_units;
     const int r = owner(n);
     const mmpr_pipeline_io &io = pp.io[r];
     const PlFlags fl{io.flags, N, K};
@@ -344,47 +474,28 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       const bool rsys = sys && remote;
       // ---- serial correction of boundary n, then the match parameters ---------
       if (tid == 0) {
+        if constexpr (MULTI) {
+          // the chain of row k advances independently of unit order
+          // (pl_advance_chain); other CTAs only wait for boundary n
+          if (rank == 0) pl_advance_chain<OK, MK>(pp, k, r, n);
+          else pl_wait(fl.chain_done(k, n), ep, false);
+        } else {
+          // one rank: the chain follows the ticket order; every CTA evaluates
+          // the step (identically) and the first CTA publishes it
+          pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys);
+          if (n - 1 >= 1) pl_wait(flp.chain_done(k, n - 1), ep, rsys);
+          if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, n), ep, false);
+          if (rank == 0) pl_chain_step<OK, MK>(pp, io, iop, fl, k, n, remote, s_chain);
+          else pl_chain_step<OK, MK, false>(pp, io, iop, fl, k, n, remote, s_chain);
+        }
         pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys);
-        if (n - 1 >= 1) pl_wait(flp.chain_done(k, n - 1), ep, rsys);
-        if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, n), ep, false);
         // row 0's reader of this snapshot slot (units (0, n < N) read it)
         if (!pp.retain && k == 2 && n < N) pl_wait(fl.consumed(0, n), cdone, false);
-        const double *fs = iop.fine_stats + ((int64_t)(k - 1) * N + (n - 1)) * 3;
-        const double *cin = io.cache + ((int64_t)(k - 1) * N + (n - 1)) * 3;
-        double cur[3], f[3], c[3], pred[3], raw[3];
+        double nxt[3], f[3];
 #pragma unroll
         for (int v = 0; v < 3; ++v) {
-          cur[v] = (n - 1 == 0) ? io.rho0[v] : pl_ld(iop.macro + ((int64_t)k * (N + 1) + (n - 1)) * 3 + v, remote);
-          f[v] = pl_ld(fs + v, remote);
-          c[v] = __ldcg(cin + v);
-        }
-        int st = MMPR_STAT_OK;
-        if (pp.reuse && n - 1 < k) {
-#pragma unroll
-          for (int v = 0; v < 3; ++v) pred[v] = c[v];
-        } else {
-#pragma unroll
-          for (int v = 0; v < 3; ++v) pred[v] = cur[v];
-          long long steps;
-          double h;
-          const double t0 = __ldg(io.times + n - 1);
-          euler_grid(pp.integ.dt, t0, __ldg(io.times + n), &steps, &h);
-          st = integrate_euler_n<3, OK, MK>(pp.ode, pp.ode_model, steps, h, t0, pred);
-        }
-#pragma unroll
-        for (int v = 0; v < 3; ++v) raw[v] = add(f[v], sub(pred[v], c[v]));
-        const bool neg = raw[1] < 0.0;
-        double nxt[3] = {raw[0], (neg && raw[1] < 0.0) ? 0.0 : raw[1], f[2]};
-        if (rank == 0) {
-          const int64_t e = (int64_t)(k - 1) * N + (n - 1);
-          io.coarse_status[(int64_t)k * N + (n - 1)] = st;
-#pragma unroll
-          for (int v = 0; v < 3; ++v) {
-            io.cache[((int64_t)k * N + (n - 1)) * 3 + v] = pred[v];
-            io.raw[e * 3 + v] = raw[v];
-            io.macro[((int64_t)k * (N + 1) + n) * 3 + v] = nxt[v];
-          }
-          pl_publish(fl.chain_done(k, n), 1, sys);
+          nxt[v] = MULTI ? __ldcg(io.macro + ((int64_t)k * (N + 1) + n) * 3 + v) : s_chain[v];
+          f[v] = pl_ld(iop.fine_stats + ((int64_t)(k - 1) * N + (n - 1)) * 3 + v, remote);
         }
         // match(corrected, F^{k-1}_{n-1}), raise policy (coupling.py:32-95)
         const int64_t cn = pl_ld64(iop.fine_counts + (int64_t)(k - 1) * N + (n - 1), remote);
@@ -520,7 +631,8 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       // the unit's coordinates again from shared memory (not held in
       // registers across the step loop)
       const int tt = *(volatile int *)&s_ticket[it & 1];
-      const int k = tt / pp.row_units, n = pp.lo_n + tt % pp.row_units;
+      const int k = (MULTI && pp.rank_tickets) ? tt / (N + 1) : tt / pp.row_units;
+      const int n = (MULTI && pp.rank_tickets) ? tt % (N + 1) : pp.lo_n + tt % pp.row_units;
       const int r = owner(n);
       const mmpr_pipeline_io &io = pp.io[r];
       const PlFlags fl{io.flags, N, K};
@@ -691,7 +803,7 @@ using namespace mmpr;
 extern "C" int64_t mmpr_pipeline_flags_size(int32_t n_slices, int32_t iterations) {
   if (n_slices < 1 || iterations < 0) return 0;
   const int64_t N = n_slices, K = iterations;
-  return 1 + K * N + 2 * (K + 1) * (N + 1);
+  return 1 + K * N + 2 * (K + 1) * (N + 1) + (K + 1);
 }
 
 extern "C" int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_moment_ode *ode,
@@ -805,6 +917,14 @@ extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_
   pp.retain = retain;
   pp.epoch = epoch;
   pp.sys = multi_gpu ? 1 : 0;
+  pp.nranks = launch_ranks;
+  // one launch over several ranks normally takes one global ticket order;
+  // MMPR_PIPELINE_RANK_TICKETS=1 gives every rank its own clusters and
+  // ticket counter instead, the scheduling of one launch per GPU (the
+  // clusters of a launch are co-resident, so every rank keeps at least one)
+  pp.rank_tickets = 0;
+  if (const char *env = getenv("MMPR_PIPELINE_RANK_TICKETS"))
+    pp.rank_tickets = (atoi(env) == 1 && launch_ranks > 1) ? 1 : 0;
   return dispatch_pipe(*model, *ode, *ode_model, &pp, g, s);
 }
 

@@ -147,6 +147,10 @@ def _pipeline_sharded_ok(be, cfg: PararealConfig, plan: NoisePlan, comm) -> bool
     if (not isinstance(be, GpuBackend) or os.environ.get("MMPR_PIPELINE", "1") == "0"
             or not hasattr(comm, "all_min_int")):
         return False
+    # opt-in above one rank: the cross-GPU form is verified by the one-GPU
+    # emulation of its scheduling only (Multi-GPU)
+    if comm.world > 1 and os.environ.get("MMPR_SHARDED_PIPELINE", "0") != "1":
+        return False
     G = comm.world
     ok = (G <= 8 and cfg.n_slices % G == 0 and cfg.iterations >= 1 and not plan.fresh
           and cfg.stop_wasserstein_tol is None
@@ -264,9 +268,10 @@ def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: N
     macro/micro trace, snapshots hold the rank's own slices only
     (``trace.snapshots[k][m]`` is global slice boundary ``offset + m``).
 
-    Configurations the iteration pipeline covers run it on every GPU
+    With MMPR_SHARDED_PIPELINE=1 (and always at world size 1),
+    configurations the iteration pipeline covers run it on every GPU
     (cross-rank dependencies through peer memory, one gather at the end);
-    the rest run the per-iteration kernels with NCCL collectives."""
+    otherwise the per-iteration kernels run with NCCL collectives."""
     comm = comm if comm is not None else TorchComm()
     reuse_converged_coarse = reuse_converged_coarse and not plan.fresh  # see engine.run_micro_macro
     be = backend if backend is not None else GpuBackend(model, coarse, cfg)

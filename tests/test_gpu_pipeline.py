@@ -187,10 +187,15 @@ def _emulated_ranks(mm, G, model, ode, init, cfg, plan, epochs=1):
     return out
 
 
-@pytest.mark.parametrize("G,N,K", [(2, 8, 4), (4, 16, 5), (8, 16, 3), (3, 9, 9)])
-def test_multi_rank_pipeline_emulated_on_one_gpu(mm, monkeypatch, G, N, K):
+@pytest.mark.parametrize("G,N,K,rank_tickets", [(2, 8, 4, 0), (4, 16, 5, 0), (8, 16, 3, 0), (3, 9, 9, 0),
+                                                (2, 16, 4, 1), (4, 16, 5, 1), (8, 32, 3, 1)])
+def test_multi_rank_pipeline_emulated_on_one_gpu(mm, monkeypatch, G, N, K, rank_tickets):
     """Ranks exchange only through each other's exchange arrays and flags;
-    the merged result equals the single-rank pipeline bit for bit."""
+    the merged result equals the single-rank pipeline bit for bit -- with one
+    global unit order, and with every rank taking only its own units on its
+    own clusters (MMPR_PIPELINE_RANK_TICKETS=1: the multi-GPU schedule, in
+    which ranks wait on their predecessor's coarse chain)."""
+    monkeypatch.setenv("MMPR_PIPELINE_RANK_TICKETS", str(rank_tickets))
     model, ode, init, cfg = _ou_case(mm, N, K, 12)
     plan = mm.NoisePlan(0)
     ref = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
@@ -230,6 +235,7 @@ def test_sharded_driver_takes_the_pipeline_over_nccl_world_one(mm, monkeypatch):
         port = s.getsockname()[1]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    monkeypatch.setenv("MMPR_SHARDED_PIPELINE", "1")
     try:
         model, ode, init, cfg = _ou_case(mm, 8, 4, 16)
         plan = mm.NoisePlan(0)

@@ -61,7 +61,7 @@ def test_pipeline_support_query_without_a_gpu():
     dwm = mm.make_double_well(dw)
     ode_m, odm_m = moments.device_ode(mm.multimodal_rhs(dwm, dw.default_partition(), dw.potential, dw.sigma))
     assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 100_000)  # two regions
-    assert kernels.pipeline_flags_size(64, 5) == 1 + 5 * 64 + 2 * 6 * 65
+    assert kernels.pipeline_flags_size(64, 5) == 1 + 5 * 64 + 2 * 6 * 65 + 6
     lib = _lib.load()
     assert lib.mmpr_pipeline_supported(None, None, None, None, 100_000) == 1
     assert lib.mmpr_parareal_pipeline(None, None, None, None, 4, 2, 100_000, 10, 1e-3, 0.03, 1, None, None) == 1
