@@ -271,7 +271,6 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
   const int64_t slot = (int64_t)rank * p.slots_per_cta + warp * 4 + (lane >> 3);
   const int j8 = lane & 7;
   int off, cnt, tail, tail_off, lo;
-  int last_idx;
   {
     int64_t o64 = 0, l64 = 0, lo64, hi64, o2, l2;
     pw_leaf(p.P, p.D, slot, &o64, &l64);
@@ -283,7 +282,6 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
     tail = (int)(l64 & 7);
     tail_off = (int)(o64 + (l64 & ~int64_t(7)));
     lo = (int)lo64;
-    last_idx = (int)(hi64 - lo64) - 1;
     if (tid == 0) s_stage_bytes = (uint32_t)((((hi64 - lo64) * 8) + 15) & ~int64_t(15));
   }
   const int my_idx = off - lo + j8;
@@ -597,14 +595,10 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
           if (m < LO) {
             x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
           } else {
-#ifdef PL_CLAMP
-            const double nx = em_update<KIND>(p, x[m], s, xb[max(0, min(my_idx + 8 * m, last_idx))]);
-#else
             // past a 12-element leaf this reads up to 8 doubles beyond the
             // CTA's range (into the next stage or the 64-byte pad after the
             // last): the value is discarded, so no clamp is needed
             const double nx = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
-#endif
             x[m] = (m < cnt) ? nx : x[m];
           }
         }

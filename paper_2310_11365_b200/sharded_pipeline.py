@@ -115,7 +115,6 @@ class RankBuffers:
         self.x0 = torch.empty((1, P), dtype=f64, device=dev)
         self.rho0 = torch.empty((1, 3), dtype=f64, device=dev)
         self.counts0 = torch.empty((1, 1), dtype=i64, device=dev)
-        self.lift_status = torch.full((1,), _lib.STAT_OK, dtype=i32, device=dev)
         self.epoch = 0
 
     def free(self):
