@@ -308,3 +308,24 @@ def test_exchange_block_ipc_roundtrip(tmp_path):
     tmp.spawn(_ipc_worker, args=(port, path), nprocs=2, join=True)
     assert open(path + ".0").read() == "ok"
     assert open(path + ".1").read() == "ok"
+
+
+@pytest.mark.parametrize("case", ["perturbed_ou_closure", "linear", "cubic_unimodal"])
+def test_pipeline_other_instantiations_equal_per_iteration(mm, monkeypatch, case):
+    """Every (model, closure) pair with a pipeline instantiation, against the
+    per-iteration kernels, bit for bit (linear: multiplicative noise b(x))."""
+    if case == "perturbed_ou_closure":
+        spec = mm.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5)
+        model, ode = mm.make_perturbed_ou(spec), mm.perturbed_ou_rhs(spec)
+    elif case == "linear":
+        model = mm.make_linear(mm.LinearMcKVSpec(A=-1.0, A_E=0.3, A_0=0.1, B=0.05, B_E=0.0, B_0=0.4))
+        ode = mm.unimodal_rhs(model)
+    else:
+        model = mm.make_cubic_meanfield(mm.CubicMeanFieldSpec(1.0, 1.0, 1.0, 0.4))
+        ode = mm.unimodal_rhs(model)
+    cfg = mm.PararealConfig(n_slices=6, iterations=3, slice_length=0.02, particles=100_000,
+                            step=mm.StepConfig(1e-3, 20), integrator=mm.EulerConfig(1e-2))
+    args = (model, ode, mm.InitialDistribution.normal(0.8, 0.04), cfg, mm.NoisePlan(5))
+    a = _run(mm, monkeypatch, True, *args)
+    b = _run(mm, monkeypatch, False, *args)
+    _same(a, b)
