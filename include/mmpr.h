@@ -274,6 +274,22 @@ int mmpr_match_restrict(int32_t n_ens, int64_t particles, const double *targets,
                         int32_t *status, int32_t *clamped, double *stats, int64_t *counts,
                         void *stream);
 
+/* mmpr_match (any partition) and the per-region restriction of the
+ * matched ensembles in one pass, one thread-block cluster per ensemble:
+ * regions of the matched positions, their members compacted in index order
+ * into scratch (double[n_ens][I][particles]), each region's pairwise tree
+ * over its compacted members -> stats[e][3I], counts[e][I] (as
+ * mmpr_restrict).  Beyond one cluster the two separate calls run.  The
+ * multi-region mmpr_restrict uses the same cluster kernel when it fits. */
+int mmpr_match_restrict_regions(const mmpr_partition *part, int32_t n_ens, int64_t particles,
+                                const double *targets, int64_t tgt_stride,
+                                const double *cur_stats, int64_t cur_stride,
+                                const int64_t *cur_counts, int64_t cnt_stride,
+                                const double *x_src, int64_t src_pitch, double *x_out,
+                                int64_t out_pitch, int32_t policy, int32_t *status,
+                                int32_t *clamped, double *stats, int64_t *counts,
+                                double *scratch, void *stream);
+
 /* ------------------------------------------------------------------ */
 /* Coarse propagator and Parareal correction (moments.py:195-203,      */
 /* engine.py:170-236), one warp, no host round-trip                    */

@@ -111,6 +111,8 @@ SIGNATURES = {
                                    _I64, _I32, _P, _P, _P]),
     "mmpr_match_restrict": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _I32,
                                             _P, _P, _P, _P, _P]),
+    "mmpr_match_restrict_regions": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64,
+                                                    _I32, _P, _P, _P, _P, _P, _P]),
     "mmpr_coarse_row": (ctypes.c_int, [_P, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
                                         _I32, _P]),
     "mmpr_integrate_macro": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),
@@ -163,7 +165,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
 
 # entry points that launch exactly one kernel each (bench.py counts them)
 LAUNCHING = frozenset({"mmpr_noise_keys", "mmpr_entropy_key", "mmpr_normals_fill", "mmpr_fine_sweep",
-                       "mmpr_fine_sweep_restrict", "mmpr_match_restrict",
+                       "mmpr_fine_sweep_restrict", "mmpr_match_restrict", "mmpr_match_restrict_regions",
                        "mmpr_restrict", "mmpr_match", "mmpr_coarse_row", "mmpr_integrate_macro",
                        "mmpr_mean_abs_diff", "mmpr_parareal_pipeline", "mmpr_parareal_pipeline_ranks"})
 launch_count = {"total": 0}

@@ -14,11 +14,13 @@
 // makes match(restrict(u), u) the bitwise identity exactly as in the
 // reference (coupling.py:82-83).
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <stdint.h>
 
 #include "mmpr_device.cuh"
 #include "capi_internal.h"
 #include "fine_common.cuh"
+#include "regions.cuh"
 
 namespace mmpr {
 
@@ -510,6 +512,21 @@ extern "C" int mmpr_restrict(const mmpr_partition *part, int32_t n_ens, int64_t 
   if (n_ens == 0) return MMPR_OK;
   if (part->n_regions == 1) {
     const int st = restrict_single_region(n_ens, particles, x, pitch, stats, counts, (cudaStream_t)stream);
+    if (st != MMPR_ERR_UNSUPPORTED) return st;
+  }
+  // one cluster per ensemble (restrict_regions.cu) only on request: the
+  // multi-kernel passes below are faster on the BASELINE bimodal shapes
+  const char *cl_env = getenv("MMPR_RESTRICT_CLUSTER");
+  if (part->n_regions > 1 && counts && cl_env && atoi(cl_env) == 1) {
+    RegionsParams rp = {};
+    rp.part = *part;
+    rp.P = particles;
+    rp.x = x;
+    rp.pitch = pitch;
+    rp.stats = stats;
+    rp.counts = counts;
+    rp.scratch = scratch;  // [n_ens][I][P] leads the multi-kernel scratch layout
+    const int st = restrict_regions(rp, n_ens, false, (cudaStream_t)stream);
     if (st != MMPR_ERR_UNSUPPORTED) return st;
   }
   if (part->n_regions > 1 && counts && rm_chunks(particles) <= 65535 && rm_subtrees(particles) <= 65535)

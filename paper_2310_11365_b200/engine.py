@@ -232,6 +232,11 @@ class _RunPlan:
         self.ws = _Workspace(K, N, P, S, I, cfg.retain_snapshots, noise_slices=N if injected else None)
         # single-region restriction of the fine outputs fused into the sweep
         self.fused_restrict = I == 1 and model_d.stat_kind == _lib.STAT_MEAN_OF_F
+        # several regions: match and micro restriction in one cluster pass
+        # (kernels.match_restrict_regions) only with MMPR_RESTRICT_CLUSTER=1 --
+        # measured slower than the separate passes on config 3 (12.2-12.5 vs
+        # 11.3-11.8 ms per run: 14 clusters at a time, latency-bound phases)
+        self.regions_fused = I > 1 and os.environ.get("MMPR_RESTRICT_CLUSTER", "0") == "1"
         # snapshot rows streamed to pinned host memory on a side stream while
         # the next iteration computes (harness artefacts need them on the host)
         self.host_snap = None
@@ -275,11 +280,16 @@ class _RunPlan:
                                    ws.match_status[0], ws.micro[0, 1:], ws.micro_counts[0, 1:])
             ws.micro[0, 0].copy_(ws.rho0[0])
             ws.micro_counts[0, 0].copy_(ws.counts0[0])
+        elif self.regions_fused:  # per-region lift and restriction in one pass
+            kernels.match_restrict_regions(part_d, ws.macro[0, 1:], ws.rho0, ws.counts0, ws.x0, self.snap(0)[1:], 1,
+                                           ws.match_status[0], ws.micro[0, 1:], ws.micro_counts[0, 1:], ws.scratch)
+            ws.micro[0, 0].copy_(ws.rho0[0])
+            ws.micro_counts[0, 0].copy_(ws.counts0[0])
         else:
             kernels.match(part_d, ws.macro[0, 1:], ws.rho0, ws.counts0, ws.x0, self.snap(0)[1:], 1,
                           ws.match_status[0])
         timer.stop("match", ev)
-        if not self.fused_restrict:
+        if not self.fused_restrict and not self.regions_fused:
             kernels.restrict(part_d, self.snap(0), ws.micro[0], ws.micro_counts[0], ws.scratch)
         if not injected and not self.plan.fresh and self.batch == N:
             ev = timer.start()
@@ -319,12 +329,18 @@ class _RunPlan:
                                    ws.match_status[k + 1], ws.micro[k + 1, 1:], ws.micro_counts[k + 1, 1:])
             ws.micro[k + 1, 0].copy_(ws.rho0[0])
             ws.micro_counts[k + 1, 0].copy_(ws.counts0[0])
+        elif self.regions_fused:  # per-region match and micro restriction in one pass
+            kernels.match_restrict_regions(part_d, ws.macro[k + 1, 1:], ws.fine_stats[k], ws.fine_counts[k], ws.fine,
+                                           nxt[1:], 0, ws.match_status[k + 1], ws.micro[k + 1, 1:],
+                                           ws.micro_counts[k + 1, 1:], ws.scratch)
+            ws.micro[k + 1, 0].copy_(ws.rho0[0])
+            ws.micro_counts[k + 1, 0].copy_(ws.counts0[0])
         else:
             kernels.match(part_d, ws.macro[k + 1, 1:], ws.fine_stats[k], ws.fine_counts[k], ws.fine, nxt[1:], 0,
                           ws.match_status[k + 1])
         nxt[0].copy_(ws.x0[0])
         timer.stop("match", ev)
-        if not self.fused_restrict:
+        if not self.fused_restrict and not self.regions_fused:
             kernels.restrict(part_d, nxt, ws.micro[k + 1], ws.micro_counts[k + 1], ws.scratch)
 
     def issue_pipeline(self, timer):

@@ -132,6 +132,43 @@ def match(part: _lib.Partition, targets, cur_stats, cur_counts, x_src, x_out, po
               _lib.ptr(clamped), _lib.stream_handle(stream))
 
 
+def match_restrict_regions(part: _lib.Partition, targets, cur_stats, cur_counts, x_src, x_out, policy: int, status,
+                           stats, counts, scratch, clamped=None, stream=None) -> None:
+    """Per-region match of E ensembles and the per-region restriction of the
+    matched ensembles in one pass (one cluster per ensemble; the separate
+    passes beyond one cluster).  stats (E, 3I), counts (E, I) int64,
+    scratch: >= E*I*P doubles."""
+    require_cuda()
+    E, P = x_out.shape
+    out_pitch = _rows(x_out, "x_out")
+    src_pitch = _rows(x_src, "x_src") if x_src.shape[0] > 1 else 0
+    if x_src.shape[1] != P or x_src.shape[0] not in (1, E):
+        raise ValueError("x_src must be (1 or E, P)")
+    I = part.n_regions
+    for t, name in ((targets, "targets"), (cur_stats, "cur_stats")):
+        _f64(t, name)
+        if t.dim() != 2 or t.shape[1] != 3 * I or t.stride(1) != 1 or t.shape[0] not in (1, E):
+            raise ValueError(f"{name} must be (1 or E, 3I)")
+    tgt_stride = targets.stride(0) if targets.shape[0] > 1 else 0
+    cur_stride = cur_stats.stride(0) if cur_stats.shape[0] > 1 else 0
+    if cur_counts.dtype != torch.int64 or cur_counts.shape[1] != I or cur_counts.shape[0] not in (1, E):
+        raise ValueError("cur_counts must be int64 (1 or E, I)")
+    cnt_stride = cur_counts.stride(0) if cur_counts.shape[0] > 1 else 0
+    if status.dtype != torch.int32 or status.numel() < E:
+        raise ValueError("status must be int32 (E,)")
+    _f64(stats, "stats")
+    if stats.shape != (E, 3 * I) or not stats.is_contiguous():
+        raise ValueError("stats must be contiguous float64 (E, 3I)")
+    if counts.dtype != torch.int64 or tuple(counts.shape) != (E, I) or not counts.is_contiguous():
+        raise ValueError("counts must be contiguous int64 (E, I)")
+    if scratch is None or scratch.numel() < E * I * P:
+        raise ValueError("scratch must hold E*I*P doubles")
+    _lib.call("mmpr_match_restrict_regions", ctypes.byref(part), int(E), int(P), targets.data_ptr(), int(tgt_stride),
+              cur_stats.data_ptr(), int(cur_stride), cur_counts.data_ptr(), int(cnt_stride), x_src.data_ptr(),
+              int(src_pitch), x_out.data_ptr(), int(out_pitch), int(policy), status.data_ptr(), _lib.ptr(clamped),
+              stats.data_ptr(), counts.data_ptr(), scratch.data_ptr(), _lib.stream_handle(stream))
+
+
 def match_restrict(targets, cur_stats, cur_counts, x_src, x_out, policy: int, status, stats, counts=None,
                    clamped=None, stream=None) -> None:
     """Single-region match of E ensembles and the restriction of the matched
