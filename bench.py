@@ -281,6 +281,7 @@ def our_arm(args):
         barrier()
         e2e_times.append(time.perf_counter() - t)
     e2e_s = sum(e2e_times) / len(e2e_times)
+    print("e2e ms per step: " + " ".join(f"{1e3 * t:.2f}" for t in e2e_times), file=sys.stderr, flush=True)
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
