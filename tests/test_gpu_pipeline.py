@@ -152,7 +152,7 @@ def test_pipeline_full_config4(mm, monkeypatch):
     _same(a, b)
 
 
-def _emulated_ranks(mm, G, model, ode, init, cfg, plan, epochs=1):
+def _emulated_ranks(mm, G, model, ode, init, cfg, plan, epochs=1, sys_scope=False):
     """The multi-rank pipeline over G ranks on one GPU: per-rank buffers and
     prologues, ONE launch over every rank's units (ranks reading each other's
     exchange arrays), merged like the multi-GPU driver does."""
@@ -173,7 +173,8 @@ def _emulated_ranks(mm, G, model, ode, init, cfg, plan, epochs=1):
         for rb in ranks:
             rb.prologue(ode_d, odm, integ_d, times, x0, plan.master_seed)
         ios = [rb.io(times) for rb in ranks]
-        SP.launch(model_d, ode_d, odm, integ_d, cfg.step.dt, S, True, ios, 0, G, epoch, epochs == 1, False, N, K, P)
+        SP.launch(model_d, ode_d, odm, integ_d, cfg.step.dt, S, True, ios, 0, G, epoch, epochs == 1, sys_scope, N, K,
+                  P)
     torch.cuda.synchronize()
     Ng = N // G
     out = {}
@@ -205,6 +206,19 @@ def test_multi_rank_pipeline_emulated_on_one_gpu(mm, monkeypatch, G, N, K, rank_
     assert np.array_equal(emu["snap"], ref["snap"])
     for name in ("bad", "coarse_status", "match_status"):
         assert (emu[name] == mm._lib.STAT_OK).all(), name
+
+
+def test_multi_rank_pipeline_system_scope(mm, monkeypatch):
+    """The multi-GPU instruction paths (ld.acquire.sys / st.release.sys /
+    red.release.sys, uncached loads of a peer's outputs) executed on one
+    GPU under the per-rank schedule: same bits."""
+    monkeypatch.setenv("MMPR_PIPELINE_RANK_TICKETS", "1")
+    model, ode, init, cfg = _ou_case(mm, 16, 4, 10)
+    plan = mm.NoisePlan(0)
+    ref = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
+    emu = _emulated_ranks(mm, 4, model, ode, init, cfg, plan, sys_scope=True)
+    assert np.array_equal(emu["macro"], ref["macro"])
+    assert np.array_equal(emu["snap"], ref["snap"])
 
 
 def test_multi_rank_pipeline_epochs(mm, monkeypatch):
