@@ -165,15 +165,16 @@ __device__ int integrate_euler_n(const mmpr_moment_ode &ode, const mmpr_model &m
     y[1] = v;
     y[2] = add(y[2], z);
     return all_finite<NV>(y) ? MMPR_STAT_OK : 1;
-  }
-  double k[NV];
-  for (long long i = 0; i < n; ++i) {
-    const double t = add(t0, mul((double)i, h));
-    if (ode_rhs<NV, OK, MK>(ode, model, t, y, k)) return MMPR_COARSE_SINGULAR;
+  } else {
+    double k[NV];
+    for (long long i = 0; i < n; ++i) {
+      const double t = add(t0, mul((double)i, h));
+      if (ode_rhs<NV, OK, MK>(ode, model, t, y, k)) return MMPR_COARSE_SINGULAR;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) y[v] = add(y[v], mul(h, k[v]));
+      for (int v = 0; v < NV; ++v) y[v] = add(y[v], mul(h, k[v]));
+    }
+    return all_finite<NV>(y) ? MMPR_STAT_OK : 1;
   }
-  return all_finite<NV>(y) ? MMPR_STAT_OK : 1;
 }
 
 }  // namespace mmpr
