@@ -245,6 +245,7 @@ class _RunPlan:
             self.host_snap = torch.empty((K + 1, N + 1, P), dtype=torch.float64, pin_memory=True)
             self.copy_stream = torch.cuda.Stream()
         self.batch = self.ws.noise_slices
+        self.side_stream = None
         self.graph = None
         self.launches_per_run = 0
         # iterations 1..K as one persistent kernel (mmpr_parareal_pipeline)
@@ -262,11 +263,33 @@ class _RunPlan:
 
     def issue_prologue(self, timer, injected=False):
         """Iteration 0 (coarse cascade + lift) and, for frozen noise, the
-        increments of every slice."""
-        ws, cfg, part_d = self.ws, self.cfg, self.part_d
+        increments of every slice.  In front of the iteration pipeline the
+        increments go first and iteration 0 runs on a side stream, in the
+        SMs the noise kernel's last wave leaves free (untimed runs)."""
+        ws = self.ws
         N, P, S = self.N, self.P, self.S
         ws.reset_status()
         self.snap(0)[0].copy_(ws.x0[0])
+        noise_here = not injected and not self.plan.fresh and self.batch == N
+        if noise_here and self.pipeline and not timer.enabled:
+            main = torch.cuda.current_stream()
+            if self.side_stream is None:
+                self.side_stream = torch.cuda.Stream()
+            self.side_stream.wait_stream(main)
+            slice_noise(self.plan.master_seed, 0, N, S, P, 0, False, out=ws.xi)
+            with torch.cuda.stream(self.side_stream):
+                self._iteration_zero(timer)
+            main.wait_stream(self.side_stream)
+            return
+        self._iteration_zero(timer)
+        if noise_here:
+            ev = timer.start()
+            slice_noise(self.plan.master_seed, 0, N, S, P, 0, False, out=ws.xi)
+            timer.stop("noise", ev)
+
+    def _iteration_zero(self, timer):
+        """rho0 = R(ens0), the coarse cascade, the lift (engine.py:153-195)."""
+        ws, part_d = self.ws, self.part_d
         ev = timer.start()
         kernels.restrict(part_d, ws.x0, ws.rho0, ws.counts0, ws.scratch)
         timer.stop("restrict", ev)
@@ -291,10 +314,6 @@ class _RunPlan:
         timer.stop("match", ev)
         if not self.fused_restrict and not self.regions_fused:
             kernels.restrict(part_d, self.snap(0), ws.micro[0], ws.micro_counts[0], ws.scratch)
-        if not injected and not self.plan.fresh and self.batch == N:
-            ev = timer.start()
-            slice_noise(self.plan.master_seed, 0, N, S, P, 0, False, out=ws.xi)
-            timer.stop("noise", ev)
 
     def issue_iteration(self, k, timer, injected=False):
         ws, part_d, N, S, B = self.ws, self.part_d, self.N, self.S, self.batch
