@@ -470,6 +470,14 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       const PlFlags flp{iop.flags, N, K};
       const bool remote = rp != r;
       const bool rsys = sys && remote;
+      // F^{k-1}_{n-1} complete: its loads go out first and land while thread 0
+      // evaluates the serial correction
+      if (tid == 0) pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys);
+      __syncthreads();
+      const double *src = iop.fine + ((int64_t)((k - 1) & 1) * N + (n - 1)) * iop.fine_pitch;
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? pl_ld(src + off + j8 + 8 * m, remote) : 0.0;
+      if (HAS_TAIL && j8 < tail) xt = pl_ld(src + tail_off + j8, remote);
       // ---- serial correction of boundary n, then the match parameters ---------
       if (tid == 0) {
         if constexpr (MULTI) {
@@ -480,13 +488,11 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
         } else {
           // one rank: the chain follows the ticket order; every CTA evaluates
           // the step (identically) and the first CTA publishes it
-          pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys);
           if (n - 1 >= 1) pl_wait(flp.chain_done(k, n - 1), ep, rsys);
           if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, n), ep, false);
           if (rank == 0) pl_chain_step<OK, MK>(pp, io, iop, fl, k, n, remote, s_chain);
           else pl_chain_step<OK, MK, false>(pp, io, iop, fl, k, n, remote, s_chain);
         }
-        pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys);
         // row 0's reader of this snapshot slot (units (0, n < N) read it)
         if (!pp.retain && k == 2 && n < N) pl_wait(fl.consumed(0, n), cdone, false);
         double nxt[3], f[3];
@@ -522,10 +528,6 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       __syncthreads();
       const double mu = s_match[0], scale = s_match[1], mc = s_match[2];
       const int mode = s_mode;
-      const double *src = iop.fine + ((int64_t)((k - 1) & 1) * N + (n - 1)) * iop.fine_pitch;
-#pragma unroll
-      for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? pl_ld(src + off + j8 + 8 * m, remote) : 0.0;
-      if (HAS_TAIL && j8 < tail) xt = pl_ld(src + tail_off + j8, remote);
       auto apply = [&](double v) {
         return mode == PL_SET ? mu : (mode == PL_AFFINE ? add(mul(scale, sub(v, mc)), mu) : v);
       };
