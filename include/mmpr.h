@@ -179,6 +179,17 @@ int mmpr_normals_fill(const uint64_t *keys, int32_t n_streams, int64_t count,
                       double *out, int64_t pitch, int32_t affine, double loc,
                       double scale, void *stream);
 
+/* Wedge tests of the ziggurat (numpy's `... < exp(-x*x/2)`) whose outcome
+ * lay inside the band where CUDA's exp and the host libm's exp could
+ * disagree (relative 2^-50 around the value); 0 means every accept/reject
+ * decision equals numpy's.  reset != 0 zeroes the device counter. */
+int mmpr_noise_exp_ambiguous(uint64_t *count, int32_t reset);
+
+/* out[i] = log1p(x[i]) as the host C library computes it (glibc 2.39 FMA
+ * build, restated bit for bit; numpy's tail draws call it through
+ * npy_log1p).  Exposed for the parity tests of the tail path. */
+int mmpr_log1p_libm(const double *x, double *out, int64_t n, void *stream);
+
 /* ------------------------------------------------------------------ */
 /* Fine propagator (particles.py:119-159, engine.py:110-124)           */
 /* ------------------------------------------------------------------ */

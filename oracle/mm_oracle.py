@@ -529,11 +529,24 @@ class Trace:
     lift_collapses: list = field(default_factory=list)
 
 
+def _fine_task(model, x, n, t0, dt, steps, seed, k, fresh):
+    """One slice's F(u_n^k) with its addressed noise (a process-pool task:
+    the reference's _fine_sweep map, engine.py:110-124, over processes)."""
+    x = np.array(x, dtype=float, copy=True)
+    for j in range(steps):  # one step's normals at a time (P = 2^20 slices)
+        x = em_step_raw(model, x, t0 + j * dt, dt, step_normals(seed, n, j, x.size, k, fresh))
+        if not np.all(np.isfinite(x)):
+            raise OracleBlowup(n, j)
+    return x
+
+
 def run_micro_macro(model: Model, ode: Ode, ens0, n_slices, iterations, slice_length, dt, steps,
                     seed, part: Partition = SINGLE, integ=None, t_start=0.0, fresh=False,
-                    noise=None, retain_snapshots=True):
+                    noise=None, retain_snapshots=True, pool=None):
     """noise: optional callable (n, k) -> (steps, P) array (injected mode);
-    default draws the reference's addressed numpy streams."""
+    default draws the reference's addressed numpy streams.  pool: optional
+    multiprocessing pool the fine sweep's slices are mapped over (results are
+    identical: every slice's noise is addressed by (n, j[, k]))."""
     integ = integ if integ is not None else DP54()
     ens0 = np.asarray(ens0, dtype=float)
     P = ens0.size
@@ -578,8 +591,12 @@ def run_micro_macro(model: Model, ode: Ode, ens0, n_slices, iterations, slice_le
 
     prev = ens_row
     for k in range(iterations):
-        fine_out = [propagate_fine(model, prev[n], n, times[n], dt, steps, xi(n, k))
-                    for n in range(n_slices)]
+        if pool is not None and noise is None:
+            fine_out = pool.starmap(_fine_task, [(model, prev[n], n, times[n], dt, steps, seed, k, fresh)
+                                                 for n in range(n_slices)])
+        else:
+            fine_out = [propagate_fine(model, prev[n], n, times[n], dt, steps, xi(n, k))
+                        for n in range(n_slices)]
         fine_stats = [restrict(f, part)[0] for f in fine_out]
         new_row = [rho0]
         new_ens = [ens0]

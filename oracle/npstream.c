@@ -158,3 +158,95 @@ uint64_t nps_standard_normal_fill_key(const uint64_t key[2], int64_t count, doub
   for (int64_t i = 0; i < count; ++i) out[i] = standard_normal(&s);
   return s.pos;
 }
+
+/* ---- 4. the host libm's log1p (numpy's tail draws call it) ---------------- */
+/* nps_libm_log1p_fill: out[i] = log1p(x[i]) from the C library itself (what
+ * numpy's npy_log1p resolves to).  nps_log1p_restated_fill: the restatement
+ * of glibc 2.39's FMA build of s_log1p.c (fdlibm algorithm, parallel
+ * polynomial) that the device uses (npstream.cuh np::glibc_log1p), compiled
+ * with -ffp-contract=off and explicit fma() where the FMA build fuses.
+ * tests/test_oracle_npstream.py pins the two against each other here and
+ * tests/test_gpu_noise.py pins the device against nps_libm_log1p_fill. */
+void nps_libm_log1p_fill(const double *x, int64_t n, double *out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = log1p(x[i]);
+}
+
+static int32_t hiword(double x) {
+  uint64_t u;
+  memcpy(&u, &x, 8);
+  return (int32_t)(u >> 32);
+}
+
+static double with_hiword(double x, int32_t h) {
+  uint64_t u;
+  memcpy(&u, &x, 8);
+  u = (u & 0xffffffffULL) | ((uint64_t)(uint32_t)h << 32);
+  memcpy(&x, &u, 8);
+  return x;
+}
+
+static double log1p_restated(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01, Lp3 = 2.857142874366239149e-01,
+               Lp4 = 2.222219843214978396e-01, Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+               Lp7 = 1.479819860511658591e-01;
+  const int32_t hx = hiword(x), ax = hx & 0x7fffffff;
+  int32_t k = 1, hu = 0;
+  double f = 0.0, c = 0.0;
+  if (hx < 0x3FDA827A) {
+    if (ax >= 0x3ff00000) return x == -1.0 ? -INFINITY : NAN;
+    if (ax < 0x3e200000) return ax < 0x3c900000 ? x : fma(-(x * x), 0.5, x);
+    if (hx > 0 || hx <= (int32_t)0xbfd2bec3) {
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  } else if (hx >= 0x7ff00000) {
+    return x + x;
+  }
+  if (k != 0) {
+    double u;
+    if (hx < 0x43400000) {
+      u = 1.0 + x;
+      hu = hiword(u);
+      k = (hu >> 20) - 1023;
+      c = (k > 0) ? 1.0 - (u - x) : x - (u - 1.0);
+      c /= u;
+    } else {
+      u = x;
+      hu = hiword(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = with_hiword(u, hu | 0x3ff00000);
+    } else {
+      k += 1;
+      u = with_hiword(u, hu | 0x3fe00000);
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = u - 1.0;
+  }
+  const double dk = (double)k, hfsq = (0.5 * f) * f;
+  if (hu == 0) {
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      c = fma(dk, ln2_lo, c);
+      return fma(dk, ln2_hi, c);
+    }
+    const double R = hfsq * fma(-0.66666666666666666, f, 1.0);
+    if (k == 0) return f - R;
+    return fma(dk, ln2_hi, -((R - fma(dk, ln2_lo, c)) - f));
+  }
+  const double s = f / (2.0 + f), z = s * s;
+  const double z2 = z * z, z4 = z2 * z2, z6 = z4 * z2;
+  const double R = fma(z6, fma(z, Lp7, Lp6), fma(z4, fma(z, Lp5, Lp4), fma(z, Lp1, z2 * fma(z, Lp3, Lp2))));
+  const double sR = s * (hfsq + R);
+  if (k == 0) return f - (hfsq - sR);
+  return fma(dk, ln2_hi, -((hfsq - (sR + fma(dk, ln2_lo, c))) - f));
+}
+
+void nps_log1p_restated_fill(const double *x, int64_t n, double *out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = log1p_restated(x[i]);
+}

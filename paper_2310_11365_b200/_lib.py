@@ -103,6 +103,8 @@ SIGNATURES = {
     "mmpr_noise_keys": (ctypes.c_int, [_U64, _I32, _I32, _I32, _I32, _I32, _P, _P]),
     "mmpr_entropy_key": (ctypes.c_int, [_P, _I32, _P, _P]),
     "mmpr_normals_fill": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _I32, _D, _D, _P]),
+    "mmpr_noise_exp_ambiguous": (ctypes.c_int, [_P, _I32]),
+    "mmpr_log1p_libm": (ctypes.c_int, [_P, _P, _I64, _P]),
     "mmpr_fine_sweep": (ctypes.c_int, [_P, _I32, _I64, _I32, _D, _D, _P, _P, _I64, _P, _I64,
                                         _P, _I64, _I64, _P, _P, _P]),
     "mmpr_restrict": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _P, _P, _P, _P]),

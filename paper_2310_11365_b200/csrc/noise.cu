@@ -4,8 +4,10 @@
 // (/root/reference/pkg/src/mcparareal/particles.py:49-65): every (slice,
 // step[, iteration]) address is its own numpy stream
 //   Generator(Philox(SeedSequence((seed, domain, n, j[, k])))).standard_normal(P)
-// and this file reproduces those streams bit-for-bit (libm-ulp caveat on the
-// ~2.6e-4 tail draws: log1p is CUDA's, not glibc's).
+// and this file reproduces those streams bit-for-bit: the Marsaglia tail
+// uses the host libm's log1p restated (np::glibc_log1p), and a wedge test
+// whose outcome CUDA's exp cannot decide the way glibc's would is counted
+// (mmpr_noise_exp_ambiguous; tests assert the count stays 0).
 //
 // One CTA materialises one stream.  The stream is a variable-length parse of
 // Philox words (a fast-accept word yields one normal; a wedge word consumes
@@ -30,6 +32,9 @@ namespace mmpr {
 __constant__ uint64_t c_zig_ki[256] = {NPZ_KI_VALUES};
 __constant__ double c_zig_wi[256] = {NPZ_WI_VALUES};
 __constant__ double c_zig_fi[256] = {NPZ_FI_VALUES};
+
+// wedge tests decided inside the exp ambiguity band (see wedge_accepts)
+__device__ unsigned long long g_exp_ambiguous = 0;
 
 #define NF_THREADS 256
 // streams at or above which one warp (not one CTA) materialises a stream
@@ -154,8 +159,8 @@ __device__ __noinline__ double tail_token(uint64_t wi, uint64_t mant, uint64_t k
   for (;;) {
     const uint64_t a = np::philox_word(i++, k0, k1);
     const uint64_t b = np::philox_word(i++, k0, k1);
-    const double xx = mul(-NPZ_INV_R, log1p(-np::unit_double(a)));
-    const double yy = -log1p(-np::unit_double(b));
+    const double xx = mul(-NPZ_INV_R, np::glibc_log1p(-np::unit_double(a)));
+    const double yy = -np::glibc_log1p(-np::unit_double(b));
     if (add(yy, yy) > mul(xx, xx)) {
       const uint64_t L = i - wi;
       *len = (int)(L < 0xffffu ? L : 0xffffu);
@@ -177,7 +182,12 @@ __device__ __forceinline__ bool wedge_accepts(int layer, double x, uint64_t next
   const double ef = (double)expf((float)q);
   if (lhs < ef * (1.0 - 0x1.0p-18)) return true;
   if (lhs > ef * (1.0 + 0x1.0p-18)) return false;
-  return lhs < exp(q);
+  // glibc's exp is within 0.52 ulp of exp(q) and CUDA's within 1 ulp, so
+  // outside a 2^-50 relative band around CUDA's value both give the same
+  // comparison; inside it (never observed) the draw is counted
+  const double e = exp(q);
+  if (fabs(sub(lhs, e)) <= mul(e, 0x1.0p-50)) atomicAdd(&g_exp_ambiguous, 1ULL);
+  return lhs < e;
 }
 
 // ---------------------------------------------------------------------------
@@ -620,4 +630,32 @@ extern "C" int mmpr_normals_fill(const uint64_t *keys, int32_t n_streams, int64_
   normals_fill_kernel<<<n_streams, NF_THREADS, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, affine, loc,
                                                                           scale);
   return mmpr_check_launch("normals_fill_kernel");
+}
+
+namespace mmpr {
+__global__ void log1p_kernel(const double *__restrict__ x, double *__restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = np::glibc_log1p(x[i]);
+}
+}  // namespace mmpr
+
+extern "C" int mmpr_noise_exp_ambiguous(uint64_t *count, int32_t reset) {
+  if (!count) return MMPR_ERR_ARG;
+  unsigned long long v = 0;
+  int st = mmpr_check(cudaMemcpyFromSymbol(&v, g_exp_ambiguous, sizeof v), "exp ambiguity counter");
+  if (st != MMPR_OK) return st;
+  *count = (uint64_t)v;
+  if (reset) {
+    v = 0;
+    st = mmpr_check(cudaMemcpyToSymbol(g_exp_ambiguous, &v, sizeof v), "exp ambiguity counter");
+  }
+  return st;
+}
+
+extern "C" int mmpr_log1p_libm(const double *x, double *out, int64_t n, void *stream) {
+  if (n < 0 || (n > 0 && (!x || !out))) return MMPR_ERR_ARG;
+  if (n == 0) return MMPR_OK;
+  const int64_t blocks = (n + 255) / 256;
+  log1p_kernel<<<(unsigned)(blocks < 4736 ? blocks : 4736), 256, 0, (cudaStream_t)stream>>>(x, out, n);
+  return mmpr_check_launch("log1p_kernel");
 }

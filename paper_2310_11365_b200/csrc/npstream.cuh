@@ -106,5 +106,81 @@ __device__ __forceinline__ uint64_t philox_word(uint64_t i, uint64_t k0, uint64_
 // next_double(): (w >> 11) * 2^-53
 __device__ __forceinline__ double unit_double(uint64_t w) { return (double)(w >> 11) * 0x1.0p-53; }
 
+
+// ---- libm log1p of the host numpy links against ----------------------------
+// numpy's Marsaglia tail (random_standard_normal, the idx == 0 branch) calls
+// npy_log1p = the C library's log1p.  On x86-64 glibc 2.39 resolves log1p
+// through an ifunc to the FMA build of the fdlibm-derived s_log1p.c (parallel
+// polynomial evaluation); this is that function with gcc's contraction
+// pattern spelled out (__fma_rn where the FMA build fuses, _rn elsewhere).
+// The same restatement in C (oracle/npstream.c log1p_restated) is pinned to
+// the host libm in tests/test_oracle_npstream.py; this device function is
+// pinned to the host libm in tests/test_gpu_noise.py.
+__device__ __forceinline__ double glibc_log1p(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01, Lp3 = 2.857142874366239149e-01,
+               Lp4 = 2.222219843214978396e-01, Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+               Lp7 = 1.479819860511658591e-01;
+  const int32_t hx = __double2hiint(x);
+  const int32_t ax = hx & 0x7fffffff;
+  int32_t k = 1, hu = 0;
+  double f = 0.0, c = 0.0;
+  if (hx < 0x3FDA827A) {
+    if (ax >= 0x3ff00000) return x == -1.0 ? -__longlong_as_double(0x7ff0000000000000LL) : __longlong_as_double(0x7ff8000000000000LL);
+    if (ax < 0x3e200000) return ax < 0x3c900000 ? x : __fma_rn(-__dmul_rn(x, x), 0.5, x);
+    if (hx > 0 || hx <= (int32_t)0xbfd2bec3) {
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  } else if (hx >= 0x7ff00000) {
+    return __dadd_rn(x, x);
+  }
+  if (k != 0) {
+    double u;
+    if (hx < 0x43400000) {
+      u = __dadd_rn(1.0, x);
+      hu = __double2hiint(u);
+      k = (hu >> 20) - 1023;
+      c = (k > 0) ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+      c = __ddiv_rn(c, u);
+    } else {
+      u = x;
+      hu = __double2hiint(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = __hiloint2double(hu | 0x3ff00000, __double2loint(u));
+    } else {
+      k += 1;
+      u = __hiloint2double(hu | 0x3fe00000, __double2loint(u));
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  const double dk = (double)k;
+  const double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
+  if (hu == 0) {
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      c = __fma_rn(dk, ln2_lo, c);
+      return __fma_rn(dk, ln2_hi, c);
+    }
+    const double R = __dmul_rn(hfsq, __fma_rn(-0.66666666666666666, f, 1.0));
+    if (k == 0) return __dsub_rn(f, R);
+    return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(R, __fma_rn(dk, ln2_lo, c)), f));
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
+  const double z = __dmul_rn(s, s);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z4, z2);
+  const double R2 = __fma_rn(z, Lp3, Lp2), R3 = __fma_rn(z, Lp5, Lp4), R4 = __fma_rn(z, Lp7, Lp6);
+  const double R = __fma_rn(z6, R4, __fma_rn(z4, R3, __fma_rn(z, Lp1, __dmul_rn(z2, R2))));
+  const double sR = __dmul_rn(s, __dadd_rn(hfsq, R));
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, sR));
+  return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(hfsq, __dadd_rn(sR, __fma_rn(dk, ln2_lo, c))), f));
+}
+
 }  // namespace np
 }  // namespace mmpr

@@ -67,6 +67,7 @@ struct PipeParams {
   int retain;
   int epoch;
   int sys;  // ranks on several GPUs: system-scope ordering
+  long long watchdog;  // pl_wait limit in cycles (see pl_wait)
 };
 
 __device__ __forceinline__ int pl_ld_acquire(const int *p, bool sys) {
@@ -103,12 +104,16 @@ __device__ __forceinline__ void pl_publish_value(int *p, int v, bool sys) {
 }
 
 // Spin until *p >= target.  A dependency that never arrives is a bug; the
-// watchdog turns it into a kernel fault instead of a hung device (~9 s on one
-// GPU; ~70 s for a peer GPU's flag, whose kernel a slow host may launch late).
-__device__ __forceinline__ void pl_wait(const int *p, int target, bool sys) {
+// watchdog turns it into a kernel fault instead of a hung device.  Its limit
+// (PipeParams::watchdog, set by the host) scales with the launch's work --
+// at least 2^34 cycles (~9 s), else one cycle per particle-step of the whole
+// launch (~300x the launch's expected duration), 8x that for a peer GPU's
+// flag, whose kernel a slow host may launch late -- so a legitimate wait on
+// a long-slice configuration never trips it.
+__device__ __forceinline__ void pl_wait(const int *p, int target, bool sys, long long watchdog) {
   if (pl_ld_acquire(p, sys) >= target) return;
   const long long t0 = clock64();
-  const long long limit = sys ? (1LL << 37) : (1LL << 34);
+  const long long limit = sys ? 8 * watchdog : watchdog;
   while (pl_ld_acquire(p, sys) < target) {
     __nanosleep(64);
     if (clock64() - t0 > limit) __trap();
@@ -230,9 +235,9 @@ __device__ __forceinline__ void pl_advance_chain(const PipeParams &pp, int k, in
       if (m - 1 >= 1 && pl_ld_acquire(flm.chain_done(k, m - 1), msys) < ep) return;
       if (k - 1 >= 1 && pl_ld_acquire(fl.chain_done(k - 1, m), false) < ep) return;
     } else {
-      pl_wait(flm.fine_done(k - 1, m - 1), cdone, msys);
-      if (m - 1 >= 1) pl_wait(flm.chain_done(k, m - 1), ep, msys);
-      if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, m), ep, false);
+      pl_wait(flm.fine_done(k - 1, m - 1), cdone, msys, pp.watchdog);
+      if (m - 1 >= 1) pl_wait(flm.chain_done(k, m - 1), ep, msys, pp.watchdog);
+      if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, m), ep, false, pp.watchdog);
     }
     pl_chain_step<OK, MK>(pp, io, iom, fl, k, m, rem);
     atomicMax(fl.chain_front(k), ep * (N + 2) + m + 1);
@@ -472,7 +477,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       const bool rsys = sys && remote;
       // F^{k-1}_{n-1} complete: its loads go out first and land while thread 0
       // evaluates the serial correction
-      if (tid == 0) pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys);
+      if (tid == 0) pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys, pp.watchdog);
       __syncthreads();
       const double *src = iop.fine + ((int64_t)((k - 1) & 1) * N + (n - 1)) * iop.fine_pitch;
 #pragma unroll
@@ -484,17 +489,17 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
           // the chain of row k advances independently of unit order
           // (pl_advance_chain); other CTAs only wait for boundary n
           if (rank == 0) pl_advance_chain<OK, MK>(pp, k, r, n);
-          else pl_wait(fl.chain_done(k, n), ep, false);
+          else pl_wait(fl.chain_done(k, n), ep, false, pp.watchdog);
         } else {
           // one rank: the chain follows the ticket order; every CTA evaluates
           // the step (identically) and the first CTA publishes it
-          if (n - 1 >= 1) pl_wait(flp.chain_done(k, n - 1), ep, rsys);
-          if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, n), ep, false);
+          if (n - 1 >= 1) pl_wait(flp.chain_done(k, n - 1), ep, rsys, pp.watchdog);
+          if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, n), ep, false, pp.watchdog);
           if (rank == 0) pl_chain_step<OK, MK>(pp, io, iop, fl, k, n, remote, s_chain);
           else pl_chain_step<OK, MK, false>(pp, io, iop, fl, k, n, remote, s_chain);
         }
         // row 0's reader of this snapshot slot (units (0, n < N) read it)
-        if (!pp.retain && k == 2 && n < N) pl_wait(fl.consumed(0, n), cdone, false);
+        if (!pp.retain && k == 2 && n < N) pl_wait(fl.consumed(0, n), cdone, false, pp.watchdog);
         double nxt[3], f[3];
 #pragma unroll
         for (int v = 0; v < 3; ++v) {
@@ -636,7 +641,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       // ---- write F^k_n into the parity buffer, restriction, publish -------------
       if (k >= 2) {
         // the reader of F^{k-2}_n (unit (k-1, n+1), owner of slice n+1) is done
-        if (tid == 0) pl_wait(fl.consumed(k - 1, n + 1), cdone, sys && owner(n + 1) != r);
+        if (tid == 0) pl_wait(fl.consumed(k - 1, n + 1), cdone, sys && owner(n + 1) != r, pp.watchdog);
         __syncthreads();
       }
       double *xo = io.fine + ((int64_t)(k & 1) * N + n) * io.fine_pitch;
@@ -913,6 +918,10 @@ extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_
   pp.retain = retain;
   pp.epoch = epoch;
   pp.sys = multi_gpu ? 1 : 0;
+  {
+    const long long work = (long long)iterations * n_slices * (long long)steps * (long long)particles;
+    pp.watchdog = work > (1LL << 34) ? work : (1LL << 34);
+  }
   pp.nranks = launch_ranks;
   // one launch over several ranks normally takes one global ticket order;
   // MMPR_PIPELINE_RANK_TICKETS=1 gives every rank its own clusters and

@@ -20,6 +20,7 @@ from __future__ import annotations
 import logging
 import os
 import time
+import weakref
 from collections.abc import Sequence
 from dataclasses import dataclass, field
 
@@ -100,6 +101,15 @@ class PararealTrace:
     @property
     def n_slices(self) -> int:
         return len(self.times) - 1
+
+    def _detach(self) -> None:
+        """Give this trace private copies of the cached run buffers its
+        snapshots view (called before the next run of the same
+        configuration overwrites them: ensembles stay immutable)."""
+        if isinstance(self.snapshots, _SnapshotRows):
+            self.snapshots.detach()
+        if self.snapshot_positions is not None:
+            self.snapshot_positions = self.snapshot_positions.copy()
 
     @property
     def iterations(self) -> int:
@@ -220,7 +230,7 @@ class _RunPlan:
     (replayed from a CUDA graph when the configuration repeats)."""
 
     def __init__(self, model_d, ode_d, ode_model_d, integ_d, part_d, cfg: PararealConfig, plan: NoisePlan,
-                 reuse: bool, injected: bool = False, host_snapshots: bool = False):
+                 reuse: bool, injected: bool = False, host_snapshots: bool = False, allow_pipeline: bool = True):
         self.model_d, self.ode_d, self.ode_model_d, self.integ_d, self.part_d = \
             model_d, ode_d, ode_model_d, integ_d, part_d
         self.cfg, self.plan, self.reuse = cfg, plan, reuse
@@ -250,8 +260,11 @@ class _RunPlan:
         self.launches_per_run = 0
         # iterations 1..K as one persistent kernel (mmpr_parareal_pipeline)
         # when the configuration has an instantiation; every iterate is
-        # bitwise the one of the per-iteration kernel sequence
-        self.pipeline = (K >= 1 and self.fused_restrict and not plan.fresh and self.batch == N
+        # bitwise the one of the per-iteration kernel sequence.  Not with the
+        # Wasserstein stop criterion (a host decision after every iteration)
+        # or per-iteration increment callables (allow_pipeline=False).
+        self.prev_trace = None  # weakref to the last trace built on this plan's buffers
+        self.pipeline = (allow_pipeline and K >= 1 and self.fused_restrict and not plan.fresh and self.batch == N
                          and not host_snapshots and os.environ.get("MMPR_PIPELINE", "1") != "0"
                          and kernels.pipeline_supported(model_d, ode_d, ode_model_d, integ_d, P))
         if self.pipeline:
@@ -426,7 +439,8 @@ def _plan_key(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse):
     return (bytes(model_d), bytes(ode_d), bytes(ode_model_d), bytes(integ_d), bytes(part_d), cfg.n_slices,
             cfg.iterations, cfg.particles, cfg.step.dt, cfg.step.steps_per_slice, cfg.slice_length, cfg.t_start,
             cfg.retain_snapshots, plan.master_seed, plan.mode, reuse, torch.cuda.current_device(),
-            os.environ.get("MMPR_NOISE_SLICES"))
+            os.environ.get("MMPR_NOISE_SLICES"), os.environ.get("MMPR_PIPELINE", "1"),
+            os.environ.get("MMPR_RESTRICT_CLUSTER", "0"))
 
 
 def _wasserstein_delta(a, b) -> float:
@@ -453,8 +467,10 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
     ``use_graph`` replays the run's launch sequence as one CUDA graph, cached
     per configuration (eager launches when timings are recorded, increments
     are injected or the Wasserstein stop criterion is active).
-    Snapshots of a graph-replayed run live in the cached workspace and are
-    overwritten by the next run of the same configuration.
+    Snapshots of a graph-replayed run view the cached workspace; when the
+    same configuration runs again while an earlier trace is still
+    referenced, that trace first receives its own copy (copy on reuse), so
+    ensembles never change under the caller.
     """
     require_cuda()
     if coarse.n_regions != cfg.partition.n_regions:
@@ -474,7 +490,8 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
         raise ConfigError("snapshots_to_host needs retain_snapshots=True")
     if eager:
         rp = _RunPlan(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse,
-                      injected=increments is not None, host_snapshots=snapshots_to_host)
+                      injected=increments is not None, host_snapshots=snapshots_to_host,
+                      allow_pipeline=cfg.stop_wasserstein_tol is None and not callable(increments))
     else:
         key = _plan_key(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse) + \
             (snapshots_to_host,)
@@ -485,6 +502,11 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
             rp = _RunPlan(model_d, ode_d, ode_model_d, integ_d, part_d, cfg, plan, reuse_converged_coarse,
                           host_snapshots=snapshots_to_host)
             _PLANS[key] = rp
+        # the cached workspace is about to be overwritten: a trace of an
+        # earlier run that is still referenced gets its own copy first
+        prev = rp.prev_trace() if rp.prev_trace is not None else None
+        if prev is not None:
+            prev._detach()
     ws = rp.ws
     last_run_info["pipeline"] = rp.pipeline
     ws.x0.copy_(ens0.device_positions.reshape(1, -1))
@@ -529,6 +551,8 @@ def run_micro_macro(model: McKeanVlasovModel, coarse: MomentODE, initial: Initia
     if rp.host_snap is not None:
         trace.snapshot_positions = rp.host_snap.numpy()[:Kd + 1]
         trace.d2h_bytes += int(rp.host_snap[:Kd + 1].numel()) * 8
+    if not eager:
+        rp.prev_trace = weakref.ref(trace)
     return trace
 
 
@@ -586,6 +610,24 @@ class _LazyRows(Sequence):
         return f"<{self._n} trace rows>"
 
 
+class _SnapshotRows(_LazyRows):
+    """trace.snapshots: rows of ensembles viewing the run's snapshot buffer."""
+
+    def __init__(self, K: int, N: int, buf):
+        self.buf, self.N = buf, N
+        super().__init__(K + 1, self._row)
+
+    def _row(self, k):
+        return [ParticleEnsemble._wrap(self.buf[k, n]) for n in range(self.N + 1)]
+
+    def detach(self) -> None:
+        new = self.buf[:self._n].clone()
+        for k, row in self._rows.items():
+            for n, e in enumerate(row):
+                e._dev = new[k, n]
+        self.buf = new
+
+
 def _build_trace(h, ws, cfg, plan, times, K, I, timer, stopped_at) -> PararealTrace:
     N = cfg.n_slices
     macro, micro, mcounts = h["macro"], h["micro"], h["micro_counts"]
@@ -600,8 +642,7 @@ def _build_trace(h, ws, cfg, plan, times, K, I, timer, stopped_at) -> PararealTr
 
     snapshots = None
     if cfg.retain_snapshots and ws is not None:
-        snap = ws.snap
-        snapshots = _LazyRows(K + 1, lambda k: [ParticleEnsemble._wrap(snap[k, n]) for n in range(N + 1)])
+        snapshots = _SnapshotRows(K, N, ws.snap)
     trace = PararealTrace(times=times, macro=_LazyRows(K + 1, macro_row), micro_stats=_LazyRows(K + 1, micro_row),
                           snapshots=snapshots, noise_mode=plan.mode.value, master_seed=plan.master_seed,
                           stopped_at=stopped_at)

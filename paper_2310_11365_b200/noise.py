@@ -105,3 +105,23 @@ def initial_normal(seed: int, mean: float, sd: float, count: int, stream=None):
     out = torch.empty(count, dtype=torch.float64, device=device())
     fill_normals(key, count, out, count, loc=mean, scale=sd, stream=stream)
     return out
+
+
+def exp_ambiguous(reset: bool = False) -> int:
+    """Wedge tests decided inside the band where CUDA's exp and the host
+    libm's exp could disagree (0: every ziggurat decision equals numpy's)."""
+    import ctypes
+    require_cuda()
+    torch.cuda.synchronize()
+    out = ctypes.c_uint64(0)
+    _lib.call("mmpr_noise_exp_ambiguous", ctypes.addressof(out), int(bool(reset)))
+    return int(out.value)
+
+
+def log1p_libm(x):
+    """Device log1p equal to the host C library's (numpy's tail draws)."""
+    require_cuda()
+    x = torch.as_tensor(x, dtype=torch.float64, device=device()).contiguous()
+    out = torch.empty_like(x)
+    _lib.call("mmpr_log1p_libm", x.data_ptr(), out.data_ptr(), int(x.numel()), _lib.stream_handle())
+    return out

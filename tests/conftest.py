@@ -46,4 +46,6 @@ def npstream_lib():
     lib.nps_standard_normal_fill_key.restype = ctypes.c_uint64
     lib.nps_word.argtypes = [P, ctypes.c_uint64]
     lib.nps_word.restype = ctypes.c_uint64
+    lib.nps_libm_log1p_fill.argtypes = [P, ctypes.c_int64, P]
+    lib.nps_log1p_restated_fill.argtypes = [P, ctypes.c_int64, P]
     return lib

@@ -69,12 +69,12 @@ def test_pipeline_ou_matches_oracle_bitwise(mm, monkeypatch):
     om = O.model_ou(-1.0, 0.5, 0.5)
     ens0 = O.sample_normal_initial(0, 1.0, 0.01, P)
     ref = O.run_micro_macro(om, O.ode_unimodal(om), ens0, N, K, S * 1e-3, 1e-3, S, 0, integ=O.Euler(1e-2))
-    # the device's Marsaglia-tail draws may differ from numpy's by one ulp
-    # (log1p), so trajectories are held to the acceptance-1 metric
+    # numpy-exact noise (tail draws included) and numpy-order arithmetic:
+    # every snapshot and macro state equals the reference's bit for bit
     ref_snap = np.array([[e for e in row] for row in ref.snapshots])
-    assert np.max(np.abs(a["snap"] - ref_snap)) / max(1.0, np.max(np.abs(ref_snap))) <= 1e-12
-    ref_macro = np.asarray(ref.macro)
-    assert np.max(np.abs(a["macro"] - ref_macro)) / max(1.0, np.max(np.abs(ref_macro))) <= 1e-10
+    assert np.array_equal(a["snap"], ref_snap)
+    assert np.array_equal(a["macro"], np.asarray(ref.macro))
+    assert np.array_equal(a["micro"], np.asarray(ref.micro))
 
 
 def test_pipeline_without_retained_snapshots(mm, monkeypatch):

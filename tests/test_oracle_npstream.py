@@ -56,3 +56,30 @@ def test_golden_noise_vectors(npstream_lib, golden):
         ent = (seed, 2, n, j, k) if fresh else (seed, 1, n, j)
         got, _ = _fill(npstream_lib, ent, P)
         assert np.array_equal(got, g[f"case{c}_normals"]), c
+
+
+def _log1p_inputs(n, seed=3):
+    """-u for numpy's unit doubles u (the tail draws' arguments), plus
+    tiny/near-one/edge values that reach every branch of log1p."""
+    rng = np.random.default_rng(seed)
+    u = (rng.integers(0, 2 ** 53, n, dtype=np.uint64) * 2.0 ** -53)
+    extra = np.concatenate([u[: n // 8] * 1e-9, 1.0 - u[: n // 8] * 1e-7, u[: n // 16] * 2.0 ** -60,
+                            -u[: n // 16] * 10, [0.0, -0.0, -1.0, 2.0 ** -54, -2.0 ** -29, 1e300, -0.2929,
+                                                  0.41422, 3.0, 1e17]])
+    return np.ascontiguousarray(np.concatenate([-u, extra]))
+
+
+def test_log1p_restatement_matches_host_libm(npstream_lib):
+    """numpy's Marsaglia tail calls the C library's log1p; the device restates
+    glibc's FMA build of it (npstream.cuh np::glibc_log1p).  The same
+    restatement in C must equal this host's libm bit for bit."""
+    import platform
+    x = _log1p_inputs(4_000_000)
+    libm = np.empty_like(x)
+    mine = np.empty_like(x)
+    npstream_lib.nps_libm_log1p_fill(x.ctypes.data, len(x), libm.ctypes.data)
+    npstream_lib.nps_log1p_restated_fill(x.ctypes.data, len(x), mine.ctypes.data)
+    if platform.machine() != "x86_64":
+        pytest.skip("restatement is of the x86-64 glibc FMA build")
+    same = (mine.view(np.uint64) == libm.view(np.uint64)) | (np.isnan(mine) & np.isnan(libm))
+    assert same.all(), f"{(~same).sum()} mismatches, first at {x[~same][:3]}"
