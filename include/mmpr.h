@@ -136,6 +136,9 @@ typedef struct {
  * MMPR_STAT_INTEG_FAILED (IntegrationFailure) / MMPR_STAT_SINGULAR
  * (SingularityError). */
 #define MMPR_STAT_OK (-1)
+/* the iteration pipeline's watchdog expired (a dependency never arrived):
+ * written to every bad/match status of the units that ran after it */
+#define MMPR_STAT_WATCHDOG (-2)
 #define MMPR_STAT_INTEG_FAILED 1
 #define MMPR_STAT_SINGULAR 2
 

@@ -44,6 +44,7 @@ INTEG_EULER = 1
 INTEG_DP54 = 2
 
 STAT_OK = -1
+STAT_WATCHDOG = -2
 STAT_INTEG_FAILED = 1
 STAT_SINGULAR = 2
 

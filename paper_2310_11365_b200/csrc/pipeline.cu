@@ -68,6 +68,7 @@ struct PipeParams {
   int epoch;
   int sys;  // ranks on several GPUs: system-scope ordering
   long long watchdog;  // pl_wait limit in cycles (see pl_wait)
+  int *abort;          // this launch's abort word (last flag word of rank r0)
 };
 
 __device__ __forceinline__ int pl_ld_acquire(const int *p, bool sys) {
@@ -110,13 +111,22 @@ __device__ __forceinline__ void pl_publish_value(int *p, int v, bool sys) {
 // launch (~300x the launch's expected duration), 8x that for a peer GPU's
 // flag, whose kernel a slow host may launch late -- so a legitimate wait on
 // a long-slice configuration never trips it.
-__device__ __forceinline__ void pl_wait(const int *p, int target, bool sys, long long watchdog) {
+// On expiry the wait sets the launch's abort word and returns: every later
+// wait returns at once, the units run to completion on whatever data is
+// there, and every status they write is MMPR_STAT_WATCHDOG, so the host
+// raises an error instead of the context dying on a sticky trap (and a
+// multi-GPU driver can fall back collectively).
+__device__ __forceinline__ void pl_wait(const int *p, int target, bool sys, long long watchdog, int *abort) {
   if (pl_ld_acquire(p, sys) >= target) return;
   const long long t0 = clock64();
   const long long limit = sys ? 8 * watchdog : watchdog;
   while (pl_ld_acquire(p, sys) < target) {
+    if (*(volatile int *)abort) return;
     __nanosleep(64);
-    if (clock64() - t0 > limit) __trap();
+    if (clock64() - t0 > limit) {
+      atomicExch(abort, 1);
+      return;
+    }
   }
 }
 
@@ -235,9 +245,9 @@ __device__ __forceinline__ void pl_advance_chain(const PipeParams &pp, int k, in
       if (m - 1 >= 1 && pl_ld_acquire(flm.chain_done(k, m - 1), msys) < ep) return;
       if (k - 1 >= 1 && pl_ld_acquire(fl.chain_done(k - 1, m), false) < ep) return;
     } else {
-      pl_wait(flm.fine_done(k - 1, m - 1), cdone, msys, pp.watchdog);
-      if (m - 1 >= 1) pl_wait(flm.chain_done(k, m - 1), ep, msys, pp.watchdog);
-      if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, m), ep, false, pp.watchdog);
+      pl_wait(flm.fine_done(k - 1, m - 1), cdone, msys, pp.watchdog, pp.abort);
+      if (m - 1 >= 1) pl_wait(flm.chain_done(k, m - 1), ep, msys, pp.watchdog, pp.abort);
+      if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, m), ep, false, pp.watchdog, pp.abort);
     }
     pl_chain_step<OK, MK>(pp, io, iom, fl, k, m, rem);
     atomicMax(fl.chain_front(k), ep * (N + 2) + m + 1);
@@ -477,7 +487,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       const bool rsys = sys && remote;
       // F^{k-1}_{n-1} complete: its loads go out first and land while thread 0
       // evaluates the serial correction
-      if (tid == 0) pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys, pp.watchdog);
+      if (tid == 0) pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys, pp.watchdog, pp.abort);
       __syncthreads();
       const double *src = iop.fine + ((int64_t)((k - 1) & 1) * N + (n - 1)) * iop.fine_pitch;
 #pragma unroll
@@ -489,17 +499,17 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
           // the chain of row k advances independently of unit order
           // (pl_advance_chain); other CTAs only wait for boundary n
           if (rank == 0) pl_advance_chain<OK, MK>(pp, k, r, n);
-          else pl_wait(fl.chain_done(k, n), ep, false, pp.watchdog);
+          else pl_wait(fl.chain_done(k, n), ep, false, pp.watchdog, pp.abort);
         } else {
           // one rank: the chain follows the ticket order; every CTA evaluates
           // the step (identically) and the first CTA publishes it
-          if (n - 1 >= 1) pl_wait(flp.chain_done(k, n - 1), ep, rsys, pp.watchdog);
-          if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, n), ep, false, pp.watchdog);
+          if (n - 1 >= 1) pl_wait(flp.chain_done(k, n - 1), ep, rsys, pp.watchdog, pp.abort);
+          if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, n), ep, false, pp.watchdog, pp.abort);
           if (rank == 0) pl_chain_step<OK, MK>(pp, io, iop, fl, k, n, remote, s_chain);
           else pl_chain_step<OK, MK, false>(pp, io, iop, fl, k, n, remote, s_chain);
         }
         // row 0's reader of this snapshot slot (units (0, n < N) read it)
-        if (!pp.retain && k == 2 && n < N) pl_wait(fl.consumed(0, n), cdone, false, pp.watchdog);
+        if (!pp.retain && k == 2 && n < N) pl_wait(fl.consumed(0, n), cdone, false, pp.watchdog, pp.abort);
         double nxt[3], f[3];
 #pragma unroll
         for (int v = 0; v < 3; ++v) {
@@ -524,7 +534,8 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
             if (!(scale == 1.0 && mu == mc)) mode = PL_AFFINE;
           }
         }
-        if (rank == 0) io.match_status[(int64_t)k * N + (n - 1)] = status;
+        if (rank == 0)
+          io.match_status[(int64_t)k * N + (n - 1)] = *(volatile int *)pp.abort ? MMPR_STAT_WATCHDOG : status;
         s_match[0] = mu;
         s_match[1] = scale;
         s_match[2] = mc;
@@ -641,7 +652,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       // ---- write F^k_n into the parity buffer, restriction, publish -------------
       if (k >= 2) {
         // the reader of F^{k-2}_n (unit (k-1, n+1), owner of slice n+1) is done
-        if (tid == 0) pl_wait(fl.consumed(k - 1, n + 1), cdone, sys && owner(n + 1) != r, pp.watchdog);
+        if (tid == 0) pl_wait(fl.consumed(k - 1, n + 1), cdone, sys && owner(n + 1) != r, pp.watchdog, pp.abort);
         __syncthreads();
       }
       double *xo = io.fine + ((int64_t)(k & 1) * N + n) * io.fine_pitch;
@@ -657,7 +668,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       }
       if (rank == 0 && tid == 0) {
         const int64_t e = (int64_t)k * N + n;
-        io.bad[e] = first_bad;
+        io.bad[e] = *(volatile int *)pp.abort ? MMPR_STAT_WATCHDOG : first_bad;
         if (ok) {
           io.fine_stats[e * 3 + 0] = s;
           io.fine_stats[e * 3 + 1] = var;
@@ -804,7 +815,7 @@ using namespace mmpr;
 extern "C" int64_t mmpr_pipeline_flags_size(int32_t n_slices, int32_t iterations) {
   if (n_slices < 1 || iterations < 0) return 0;
   const int64_t N = n_slices, K = iterations;
-  return 1 + K * N + 2 * (K + 1) * (N + 1) + (K + 1);
+  return 1 + K * N + 2 * (K + 1) * (N + 1) + (K + 1) + 1;  // ..., abort word
 }
 
 extern "C" int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_moment_ode *ode,
@@ -870,6 +881,8 @@ extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_
     const size_t bytes = reset_flags ? (size_t)nflags * sizeof(int32_t) : sizeof(int32_t);
     cudaError_t err = cudaMemsetAsync(ios[r].flags, 0, bytes, s);
     if (err != cudaSuccess) return mmpr_check(err, "pipeline: flag reset");
+    err = cudaMemsetAsync(ios[r].flags + nflags - 1, 0, sizeof(int32_t), s);  // abort word, every launch
+    if (err != cudaSuccess) return mmpr_check(err, "pipeline: abort reset");
   }
 
   PipeParams pp = {};
@@ -921,7 +934,9 @@ extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_
   {
     const long long work = (long long)iterations * n_slices * (long long)steps * (long long)particles;
     pp.watchdog = work > (1LL << 34) ? work : (1LL << 34);
+    if (const char *env = getenv("MMPR_PIPELINE_WATCHDOG")) pp.watchdog = atoll(env);  // tests
   }
+  pp.abort = ios[first_rank].flags + nflags - 1;
   pp.nranks = launch_ranks;
   // one launch over several ranks normally takes one global ticket order;
   // MMPR_PIPELINE_RANK_TICKETS=1 gives every rank its own clusters and

@@ -563,6 +563,9 @@ def _coarse_error(status: int, n: int, k: int):
 
 
 def _raise_first_error(h, N: int, K: int, I: int) -> None:
+    if (h["bad"] == _lib.STAT_WATCHDOG).any() or (h["match_status"] == _lib.STAT_WATCHDOG).any():
+        raise _lib.MmprError("iteration pipeline watchdog expired: a dependency between (k, n) units never "
+                             "arrived; the run's results were discarded")
     for n in range(N):
         if h["coarse_status"][0, n] != _lib.STAT_OK:
             raise _coarse_error(int(h["coarse_status"][0, n]), n, 0)

@@ -343,3 +343,18 @@ def test_pipeline_other_instantiations_equal_per_iteration(mm, monkeypatch, case
     a = _run(mm, monkeypatch, True, *args)
     b = _run(mm, monkeypatch, False, *args)
     _same(a, b)
+
+
+def test_pipeline_watchdog_is_recoverable(mm, monkeypatch):
+    """An expired dependency wait (forced with a tiny watchdog) ends the
+    launch cleanly with MMPR_STAT_WATCHDOG statuses -> MmprError, and the
+    CUDA context stays usable (no sticky trap)."""
+    model, ode, init, cfg = _ou_case(mm, 8, 4, 20)
+    plan = mm.NoisePlan(0)
+    monkeypatch.setenv("MMPR_PIPELINE_WATCHDOG", "1")
+    with pytest.raises(mm._lib.MmprError, match="watchdog"):
+        mm.run_micro_macro(model, ode, init, cfg, plan, use_graph=False)
+    monkeypatch.delenv("MMPR_PIPELINE_WATCHDOG")
+    a = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
+    b = _run(mm, monkeypatch, False, model, ode, init, cfg, plan)
+    _same(a, b)
