@@ -12,8 +12,12 @@ iteration 0, K iterations), so value = K*N*P*S / run time (all GPUs).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 is launched by torchrun (one process per GPU, NCCL).  Prints ONE JSON
-line on rank 0.
+N > 1 runs one process per GPU over NCCL: under torchrun as launched by the
+driver, or relaunched through torch.distributed.run by this script when
+started without one.  Both multi-GPU drivers run (per-iteration kernels with
+NCCL collectives; the iteration pipeline with peer-memory hand-offs), their
+traces are compared bit for bit and the faster verified one is `value`.
+Prints ONE JSON line on rank 0.
 """
 
 from __future__ import annotations
@@ -142,11 +146,37 @@ def pipeline_bytes(N, K):
 
 
 # ---------------------------------------------------------------------------
-# CPU legs (oracle port: the checker restated from the reference)
+# CPU legs: the unmodified reference (baseline/_ref, pip-installed from
+# /root/reference) when it is present, else the oracle's restatement of it
 # ---------------------------------------------------------------------------
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_kind() -> str:
+    """'reference' when the unmodified mcparareal package is importable from
+    baseline/_ref, else 'port' (oracle/mm_oracle.py)."""
+    if os.path.isdir(os.path.join(REF_PATH, "mcparareal")):
+        if REF_PATH not in sys.path:
+            sys.path.insert(0, REF_PATH)
+        try:
+            import mcparareal  # noqa: F401
+            return "reference"
+        except Exception:  # noqa: BLE001 -- a broken install falls back to the port
+            return "port"
+    return "port"
+
+
 def _cpu_slice(args):
-    n, seconds_hint = args
-    import numpy as np
+    """propagate_fine of slice n of config 4 (noise included), seconds."""
+    n, kind = args
+    if kind == "reference":
+        import mcparareal as R
+        model = R.make_perturbed_ou(R.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5))
+        plan = R.NoisePlan(SEED)
+        ens = R.sample_initial(R.InitialDistribution.normal(1.0, 0.01), plan, P)
+        t = time.perf_counter()
+        R.propagate_fine(model, ens, n, n * S * DT, R.StepConfig(DT, S), plan)
+        return time.perf_counter() - t
     from oracle import mm_oracle as O
     m = O.model_ou(-1.0, 0.5, 0.5)
     x0 = O.sample_normal_initial(SEED, 1.0, 0.01, P)
@@ -156,17 +186,43 @@ def _cpu_slice(args):
     return time.perf_counter() - t
 
 
+def _what(kind):
+    return ("the unmodified reference's mcparareal.propagate_fine (baseline/_ref)" if kind == "reference"
+            else "the oracle's numpy restatement of propagate_fine")
+
+
 def cpu_baseline(seconds: float) -> dict:
-    """Single-core numpy restatement of propagate_fine (noise included) on
-    slices of the workload until ~`seconds` of CPU work."""
+    """Single-core propagate_fine (noise included) on slices of the workload
+    until ~`seconds` of CPU work."""
+    kind = reference_kind()
     done, elapsed = 0, 0.0
     while elapsed < seconds and done < SLICES_PER_GPU:
-        elapsed += _cpu_slice((done, seconds))
+        elapsed += _cpu_slice((done, kind))
         done += 1
     value = done * P * S / elapsed
-    return {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{done} slice(s) x {S} EM steps x {P} particles of config 4 through the oracle's numpy "
-                      f"restatement of propagate_fine (numpy Philox/ziggurat noise included), {elapsed:.1f} s"}
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{done} slice(s) x {S} EM steps x {P} particles of config 4 through {_what(kind)} "
+                      f"(numpy Philox/ziggurat noise included), one core, {elapsed:.1f} s"}
+
+
+def reference_loop(cores: int) -> dict:
+    """The reference's own loop (engine.py:127-259), unmodified, on config 4
+    with K = 1 (iteration 0 + one Parareal iteration) and its default DP5(4)
+    coarse (the reference has no forward-Euler integrator), workers = 1 and
+    workers = cores (its GIL-bound thread pool), retain_snapshots=False."""
+    import mcparareal as R
+    model = R.make_perturbed_ou(R.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5))
+    out = {"config": "config 4 (N=64, P=1e5, S=100), K=1, reference default DP5(4) coarse, retain_snapshots=False"}
+    for workers in (1, cores):
+        cfg = R.PararealConfig(n_slices=SLICES_PER_GPU, iterations=1, slice_length=S * DT, particles=P,
+                               step=R.StepConfig(DT, S), workers=workers, retain_snapshots=False)
+        t = time.perf_counter()
+        R.run_micro_macro(model, R.unimodal_rhs(model), R.InitialDistribution.normal(1.0, 0.01), cfg,
+                          R.NoisePlan(SEED))
+        el = time.perf_counter() - t
+        out[f"run_micro_macro_workers{workers}_s"] = el
+        out[f"workers{workers}_particle_steps_per_s"] = SLICES_PER_GPU * P * S / el
+    return out
 
 
 def reference_arm(args):
@@ -175,23 +231,26 @@ def reference_arm(args):
         return 0
     import multiprocessing as mp
     cores = len(os.sched_getaffinity(0))
+    kind = reference_kind()
     G = args.gpus
     with mp.get_context("fork").Pool(cores) as pool:
         for _ in range(args.warmup):
-            pool.map(_cpu_slice, [(n, 0) for n in range(cores)])
+            pool.map(_cpu_slice, [(n, kind) for n in range(cores)])
         t = time.perf_counter()
         for _ in range(args.steps):
-            pool.map(_cpu_slice, [(n, 0) for n in range(cores)])
+            pool.map(_cpu_slice, [(n, kind) for n in range(cores)])
         elapsed = time.perf_counter() - t
     value = args.steps * cores * P * S / elapsed
     sample = (f"per step: {cores} slices of config 4 ({S} steps x {P} particles each) propagated in parallel by "
-              f"{cores} processes running the oracle's numpy restatement of propagate_fine (noise included)")
+              f"{cores} processes running {_what(kind)} (noise included; BASELINE.md section 3, driver 3)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": G,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload(G),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if kind == "reference" and not args.no_reference_loop:
+        line["reference_loop"] = reference_loop(cores)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -199,6 +258,13 @@ def reference_arm(args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def _trace_arrays(tr):
+    """Per-run trace arrays the drivers must agree on bit for bit."""
+    import numpy as np
+    return (np.array([[st.packed() for st in row] for row in tr.macro]),
+            np.array([[st.packed() for st in row] for row in tr.micro_stats]))
+
+
 def our_arm(args):
     import numpy as np
     import torch
@@ -206,14 +272,16 @@ def our_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch N > 1 through torchrun "
+                         "or let bench.py relaunch itself)")
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     G = world
     import paper_2310_11365_b200 as mm
-    from paper_2310_11365_b200 import _lib
-    from paper_2310_11365_b200.distributed import run_micro_macro_sharded
+    from paper_2310_11365_b200 import _lib, distributed
 
     N = SLICES_PER_GPU * G
     spec = mm.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5)
@@ -228,7 +296,7 @@ def our_arm(args):
 
     def run(ens, timings=False):
         if world > 1:
-            return run_micro_macro_sharded(model, ode, ens, cfg, plan, record_timings=timings)
+            return distributed.run_micro_macro_sharded(model, ode, ens, cfg, plan, record_timings=timings)
         return mm.run_micro_macro(model, ode, ens, cfg, plan, record_timings=timings)
 
     def barrier():
@@ -236,22 +304,66 @@ def our_arm(args):
         if world > 1:
             torch.distributed.barrier()
 
-    for _ in range(max(args.warmup, 0)):
-        run(ens0_dev)
-    barrier()
+    def all_max(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
 
-    # ---- device-resident timing ------------------------------------------------
-    launches0 = _lib.launch_count["total"]
-    with ClockSampler(local) as clocks:
+    def measure():
+        """W warm-up runs, then K timed runs between barriers (CUDA events,
+        max over ranks); returns (ms per run, launches, clocks, last trace)."""
+        for _ in range(max(args.warmup, 0)):
+            run(ens0_dev)
         barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
-            tr = run(ens0_dev)
-        e1.record()
-        barrier()
-    launches = _lib.launch_count["total"] - launches0
+        launches0 = _lib.launch_count["total"]
+        with ClockSampler(local) as clocks:
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                tr = run(ens0_dev)
+            e1.record()
+            barrier()
+        return all_max(e0.elapsed_time(e1) / args.steps), _lib.launch_count["total"] - launches0, \
+            clocks.summary(), tr
+
+    # ---- device-resident timing, per multi-GPU driver --------------------------
+    # G > 1: the per-iteration kernels with NCCL collectives, and the
+    # iteration pipeline on every GPU with the rank hand-offs through peer
+    # memory (MMPR_SHARDED_PIPELINE=1).  Both run the same inputs; their
+    # traces must agree bit for bit, and the faster verified one is `value`.
+    drivers = {}
+    if G == 1:
+        drivers["engine"] = measure()
+    else:
+        os.environ["MMPR_SHARDED_PIPELINE"] = "0"
+        drivers["nccl_per_iteration"] = measure()
+        os.environ["MMPR_SHARDED_PIPELINE"] = "1"
+        try:
+            res = measure()
+            ok = 1 if distributed.last_run_info.get("pipeline") else 0
+        except Exception as exc:  # noqa: BLE001 -- collective decision below
+            print(f"rank {rank}: peer-memory pipeline failed: {exc}", file=sys.stderr, flush=True)
+            res, ok = None, 0
+        t = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+        if int(t.item()) == 1:
+            ref_arrays = _trace_arrays(drivers["nccl_per_iteration"][3])
+            same = all(np.array_equal(a, b) for a, b in zip(ref_arrays, _trace_arrays(res[3])))
+            t = torch.tensor([1 if same else 0], dtype=torch.int32, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+            if int(t.item()) == 1:
+                drivers["peer_pipeline"] = res
+            else:
+                print("peer-memory pipeline trace differs from the NCCL driver's: not reported",
+                      file=sys.stderr, flush=True)
+    best = min(drivers, key=lambda d: drivers[d][0])
+    if G > 1:
+        os.environ["MMPR_SHARDED_PIPELINE"] = "1" if best == "peer_pipeline" else "0"
+    ms_all, launches, clock_summary, _ = drivers[best]
     # per-launch kernel durations (CUDA events on the launching stream) from
     # two eager runs of the same configuration, for the roofline
     stage_ms = {}
@@ -261,12 +373,6 @@ def our_arm(args):
             if isinstance(vals, list):
                 stage_ms.setdefault(key, []).extend(1e3 * v for v in vals)
     fine_ms = stage_ms.get("fine", [])
-    ms = e0.elapsed_time(e1) / args.steps
-    ms_all = ms
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_all = float(t.item())
     psteps = K_ITER * N * P * S
     value = psteps / (ms_all / 1e3)
 
@@ -280,12 +386,8 @@ def our_arm(args):
         tr = run(ens)  # returns after the trace arrays reached host memory
         barrier()
         e2e_times.append(time.perf_counter() - t)
-    e2e_s = sum(e2e_times) / len(e2e_times)
+    e2e_s = all_max(sum(e2e_times) / len(e2e_times))
     print("e2e ms per step: " + " ".join(f"{1e3 * t:.2f}" for t in e2e_times), file=sys.stderr, flush=True)
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
     d2h = int(getattr(tr, "d2h_bytes", 0))
     h2d = 8 * P + 8 * (N + 1)  # ens0 from pinned memory + the slice start times
 
@@ -320,16 +422,33 @@ def our_arm(args):
                      "avg_launch_ms": kern_ms, "bytes_model": roof["bytes_model"]},
         "e2e": {"value": psteps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
-        "clocks": clocks.summary(),
-        "fp64_canonical": fp64_canonical(value / G, clocks.summary().get("sm_mhz") or 1965.0),
+        "clocks": clock_summary,
+        "fp64_canonical": fp64_canonical(value / G, clock_summary.get("sm_mhz") or 1965.0),
         "stage_ms_per_run": {k: round(sum(v) / 2, 4) for k, v in stage_ms.items() if v},
     }
+    if G > 1:
+        line["driver"] = best
+        line["drivers"] = {d: {"ms_per_step": r[0], "value": psteps / (r[0] / 1e3), "gpu_launches": r[1]}
+                           for d, r in drivers.items()}
+        line["drivers_bitwise_equal"] = len(drivers) == 2
     if G == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def relaunch(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: run this script
+    as N NCCL ranks, one per GPU (torch.distributed.run, 127.0.0.1)."""
+    import socket
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -340,9 +459,13 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-reference-loop", action="store_true",
+                    help="reference arm: skip the one-off timing of the reference's own run_micro_macro")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     return our_arm(args)
 
 

@@ -139,6 +139,20 @@ typedef struct {
 /* the iteration pipeline's watchdog expired (a dependency never arrived):
  * written to every bad/match status of the units that ran after it */
 #define MMPR_STAT_WATCHDOG (-2)
+
+/* Counter-based Philox noise (NoiseMode.PHILOX / PHILOX_FRESH): the
+ * increment of particle p at step j of global slice n is numpy's ziggurat
+ * transform over Philox4x32-10(counter = (p, j, n, kfield + (draw << 24)),
+ * key), generated in registers by the fine kernels -- no increment buffer
+ * (paper_2310_11365_b200/csrc/counter_noise.cuh).  Replaces the
+ * materialised NoisePlan.normals rows (particles.py:49-61) where the
+ * north star's in-register noise is wanted; statistically, not bitwise,
+ * equivalent to the reference's numpy streams. */
+typedef struct mmpr_counter_noise {
+  uint32_t key[2];       /* SeedSequence((seed, 4)).generate_state(2, uint32) */
+  uint32_t kfield;       /* 0 = frozen, iteration + 1 = fresh (< 2^24) */
+  int32_t slice_offset;  /* global index of local slice 0 */
+} mmpr_counter_noise;
 #define MMPR_STAT_INTEG_FAILED 1
 #define MMPR_STAT_SINGULAR 2
 
@@ -151,6 +165,20 @@ const char *mmpr_version(void);
 
 /* Last CUDA error string recorded by a failing call on this thread. */
 const char *mmpr_last_error(void);
+
+/* mmpr_fine_sweep / mmpr_fine_sweep_restrict with counter-based Philox
+ * increments generated in registers (no xi buffer).  stats/counts may be
+ * NULL (no fused restriction). */
+int mmpr_fine_sweep_counter(const mmpr_model *model, int32_t n_slices, int64_t particles, int32_t steps,
+                            double dt, double sqrt_dt, const double *t0, const double *x_in,
+                            int64_t in_pitch, double *x_out, int64_t out_pitch,
+                            const mmpr_counter_noise *noise, int32_t *bad_step, double *stats,
+                            int64_t *counts, void *stream);
+
+/* Counter-mode increments written out (parity tests): out[r*pitch + i] =
+ * increment of particle p0 + i at step j0 + r of global slice n. */
+int mmpr_counter_normals_fill(const mmpr_counter_noise *noise, int32_t n, int32_t j0, int32_t rows,
+                              int64_t p0, int64_t count, double *out, int64_t pitch, void *stream);
 
 /* Max concurrently resident clusters of the fine-sweep kernel for P
  * particles per slice (cudaOccupancyMaxActiveClusters). */
@@ -192,6 +220,7 @@ int mmpr_noise_exp_ambiguous(uint64_t *count, int32_t reset);
  * build, restated bit for bit; numpy's tail draws call it through
  * npy_log1p).  Exposed for the parity tests of the tail path. */
 int mmpr_log1p_libm(const double *x, double *out, int64_t n, void *stream);
+
 
 /* ------------------------------------------------------------------ */
 /* Fine propagator (particles.py:119-159, engine.py:110-124)           */
@@ -371,6 +400,10 @@ typedef struct mmpr_pipeline_io {
   int32_t *coarse_status;     /* [K+1][N] */
   int32_t *match_status;      /* [K+1][N] */
   int32_t *flags;             /* [mmpr_pipeline_flags_size(N, K)] scratch, reset by the call */
+  int32_t counter_noise;      /* 1: increments from counter-based Philox (xi unused; see
+                                 mmpr_counter_noise), 0: from xi */
+  uint32_t counter_key[2];
+  uint32_t counter_kfield;    /* 0: frozen (the pipeline runs frozen noise only) */
 } mmpr_pipeline_io;
 
 /* int32 scratch words the pipeline needs for (n_slices, iterations). */

@@ -91,6 +91,45 @@ def slice_noise(seed, slice_index, steps, count, iteration=0, fresh=False):
                      for j in range(steps)])
 
 
+# counter-based Philox mode (NoiseMode.PHILOX*: the device's in-register
+# generator, no reference counterpart) -- restated in C in npstream.c
+_NPS = None
+
+
+def _nps():
+    global _NPS
+    if _NPS is None:
+        import ctypes
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnpstream.so")
+        lib = ctypes.CDLL(path)
+        P = ctypes.c_void_p
+        lib.nps_counter_normals.argtypes = [P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                            ctypes.c_int64, P]
+        lib.nps_philox4x32_10.argtypes = [P, P, P]
+        _NPS = lib
+    return _NPS
+
+
+def counter_key(seed):
+    """SeedSequence((seed, 4)).generate_state(2, uint32) (noise.counter_key)."""
+    return np.random.SeedSequence((int(seed), 4)).generate_state(2, np.uint32)
+
+
+def counter_normals(seed, slice_index, step_index, count, iteration=0, fresh=False, first_particle=0):
+    key = np.ascontiguousarray(counter_key(seed))
+    out = np.empty(count)
+    kf = (int(iteration) + 1) if fresh else 0
+    _nps().nps_counter_normals(key.ctypes.data, kf, int(slice_index), int(step_index), int(first_particle),
+                               int(count), out.ctypes.data)
+    return out
+
+
+def counter_slice_noise(seed, slice_index, steps, count, iteration=0, fresh=False):
+    """(steps, P) increments of one slice in the counter-based mode."""
+    return np.stack([counter_normals(seed, slice_index, j, count, iteration, fresh) for j in range(steps)])
+
+
 # ---------------------------------------------------------------------------
 # models (descriptor = (kind, params)); factory closures' op order
 # ---------------------------------------------------------------------------

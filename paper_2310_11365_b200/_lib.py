@@ -87,7 +87,13 @@ class PipelineIO(ctypes.Structure):
                 ("micro_counts", ctypes.c_void_p), ("fine_stats", ctypes.c_void_p),
                 ("fine_counts", ctypes.c_void_p), ("raw", ctypes.c_void_p), ("cache", ctypes.c_void_p),
                 ("bad", ctypes.c_void_p), ("coarse_status", ctypes.c_void_p), ("match_status", ctypes.c_void_p),
-                ("flags", ctypes.c_void_p)]
+                ("flags", ctypes.c_void_p), ("counter_noise", ctypes.c_int32),
+                ("counter_key", ctypes.c_uint32 * 2), ("counter_kfield", ctypes.c_uint32)]
+
+
+class CounterNoise(ctypes.Structure):
+    """mmpr_counter_noise: counter-based Philox increments (NoiseMode.PHILOX*)."""
+    _fields_ = [("key", ctypes.c_uint32 * 2), ("kfield", ctypes.c_uint32), ("slice_offset", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -105,6 +111,9 @@ SIGNATURES = {
     "mmpr_entropy_key": (ctypes.c_int, [_P, _I32, _P, _P]),
     "mmpr_normals_fill": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _I32, _D, _D, _P]),
     "mmpr_noise_exp_ambiguous": (ctypes.c_int, [_P, _I32]),
+    "mmpr_fine_sweep_counter": (ctypes.c_int, [_P, _I32, _I64, _I32, _D, _D, _P, _P, _I64, _P, _I64, _P, _P, _P,
+                                                _P, _P]),
+    "mmpr_counter_normals_fill": (ctypes.c_int, [_P, _I32, _I32, _I32, _I64, _I64, _P, _I64, _P]),
     "mmpr_log1p_libm": (ctypes.c_int, [_P, _P, _I64, _P]),
     "mmpr_fine_sweep": (ctypes.c_int, [_P, _I32, _I64, _I32, _D, _D, _P, _P, _I64, _P, _I64,
                                         _P, _I64, _I64, _P, _P, _P]),
@@ -168,6 +177,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
 
 # entry points that launch exactly one kernel each (bench.py counts them)
 LAUNCHING = frozenset({"mmpr_noise_keys", "mmpr_entropy_key", "mmpr_normals_fill", "mmpr_fine_sweep",
+                       "mmpr_fine_sweep_counter", "mmpr_counter_normals_fill",
                        "mmpr_fine_sweep_restrict", "mmpr_match_restrict", "mmpr_match_restrict_regions",
                        "mmpr_restrict", "mmpr_match", "mmpr_coarse_row", "mmpr_integrate_macro",
                        "mmpr_mean_abs_diff", "mmpr_parareal_pipeline", "mmpr_parareal_pipeline_ranks"})

@@ -60,7 +60,10 @@ __device__ __forceinline__ void group_sync(int grp, int nthreads) {
 // LO >= 0: every populated leaf has at least LO accumulator elements per
 // lane (compile-time, so only elements LO..PPT-1 carry a predicate);
 // LO < 0: the bound comes from p.cnt_min at run time.
-template <int KIND, int PPT, bool HAS_TAIL, bool PADDED, int MAXT, int GROUPS, int LO = -1>
+// PHX: increments generated in registers by counter-based Philox
+// (counter_noise.cuh) instead of read from HBM; the dynamic shared memory
+// then holds the ziggurat tables and no copy pipeline runs.
+template <int KIND, int PPT, bool HAS_TAIL, bool PADDED, int MAXT, int GROUPS, int LO = -1, bool PHX = false>
 __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const FineParams p) {
   using PartT = Part<PADDED>;
   extern __shared__ __align__(128) double s_dyn[];  // [GROUPS][nstages][stage_elems]
@@ -83,6 +86,9 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
 
   const int ns = p.nstages;
   double *s_stage = s_dyn + (size_t)grp * ns * p.stage_elems;
+  const cn::ZigTables *zt = reinterpret_cast<const cn::ZigTables *>(s_dyn);
+  const uint32_t nglob = (uint32_t)(p.cn.n_base + slice);
+  if constexpr (PHX) cn::load_zig(reinterpret_cast<cn::ZigTables *>(s_dyn), (int)threadIdx.x, (int)blockDim.x);
   PartT(*s_wp)[32] = s_wp_all[grp];
   ClusterSlot(*s_slot)[FS_MAX_CLUSTER] = s_slot_all[grp];
   int *s_bad = s_bad_all[grp];
@@ -133,7 +139,7 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
   // every CTA's barriers must be initialised before any peer sends to them
   if (p.ctas > 1) cluster_sync_all();
   else __syncthreads();
-  if (tid == 0 && active) {
+  if (!PHX && tid == 0 && active) {
     for (int j = 0; j < ns && j < p.S; ++j) {
       mbar_arrive_expect_tx(&s_bar[j], stage_bytes);
       bulk_g2s(s_stage + j * p.stage_elems, xi_slice + j * p.xi_row_pitch + lo, stage_bytes, &s_bar[j]);
@@ -141,7 +147,7 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
     for (int j = ns; j < ns + p.l2_ahead && j < p.S; ++j)
       prefetch_l2(xi_slice + (int64_t)j * p.xi_row_pitch + lo, stage_bytes);
   }
-  int issued = (p.S < ns) ? p.S : ns;
+  int issued = PHX ? 0 : ((p.S < ns) ? p.S : ns);
 
   // ---- sum(x) in numpy's pairwise order + non-finite flag --------------------
   // One group barrier per call (B1) and, in a cluster, one mbarrier wait for
@@ -264,14 +270,19 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
     for (int j = 0; j < p.S; ++j) {
       const int stage = j % ns;
       PROF_MARK(tw0);
-      mbar_wait_parity(&s_bar[stage], (uint32_t)((j / ns) & 1));
+      if constexpr (!PHX) mbar_wait_parity(&s_bar[stage], (uint32_t)((j / ns) & 1));
       PROF_MARK(tw1);
       PROF_ADD(0, tw0, tw1);
       const double *xb = s_stage + stage * p.stage_elems;
 #pragma unroll
       for (int m = 0; m < PPT; ++m) {
         if (m < cmin) {
-          x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
+          const double z = PHX ? cn::normal(p.cn, (uint32_t)(off + j8 + 8 * m), (uint32_t)j, nglob, zt)
+                               : xb[my_idx + 8 * m];
+          x[m] = em_update<KIND>(p, x[m], s, z);
+        } else if (PHX) {
+          if (m < cnt) x[m] = em_update<KIND>(p, x[m], s, cn::normal(p.cn, (uint32_t)(off + j8 + 8 * m),
+                                                                      (uint32_t)j, nglob, zt));
         } else {
           // past some lanes' leaves: clamped index, value kept only when live
           const int idx = max(0, min(my_idx + 8 * m, last_idx));
@@ -279,11 +290,13 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
           x[m] = (m < cnt) ? nx : x[m];
         }
       }
-      if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
+      if (HAS_TAIL && j8 < tail)
+        xt = em_update<KIND>(p, xt, s, PHX ? cn::normal(p.cn, (uint32_t)(tail_off + j8), (uint32_t)j, nglob, zt)
+                                           : xb[(int)(tail_off - lo) + j8]);
       PROF_MARK(tu1);
       PROF_ADD(1, tw1, tu1);
       // B1 inside reduce() orders every read of this stage before its refill
-      reduce(j + 1, (j + ns < p.S) ? j + ns : -1, s, bad);
+      reduce(j + 1, (!PHX && j + ns < p.S) ? j + ns : -1, s, bad);
       if (bad) {
         first_bad = j;
         break;
@@ -428,7 +441,17 @@ template <void (*KERN)(const FineParams)>
 static int launch_fine_t(const FineParams &p, const FineGeometry &g, cudaStream_t stream);
 
 template <int KIND, int PPT, bool HAS_TAIL>
-static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t stream) {
+static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t stream, bool phx) {
+  if (phx) {
+    if (g.groups != 1) return MMPR_ERR_UNSUPPORTED;
+    if (!g.padded && g.ppt == PPT && g.cnt_min >= PPT - 1) {
+      if (g.threads <= 512)
+        return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 512, 1, PPT - 1, true>>(p, g, stream);
+      return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 1024, 1, PPT - 1, true>>(p, g, stream);
+    }
+    if (g.padded) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 1024, 1, -1, true>>(p, g, stream);
+    return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 1024, 1, -1, true>>(p, g, stream);
+  }
 #ifdef MMPR_FINE_TWO_GROUPS
   if (g.groups == 2) {
     if (g.padded) return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, true, 1024, 2>>(p, g, stream);
@@ -487,21 +510,21 @@ static int launch_fine_t(const FineParams &p, const FineGeometry &g, cudaStream_
 }
 
 template <int PPT, bool HAS_TAIL>
-static int dispatch_kind(const FineParams &p, const FineGeometry &g, cudaStream_t s) {
+static int dispatch_kind(const FineParams &p, const FineGeometry &g, cudaStream_t s, bool phx) {
   switch (p.model.kind) {
-    case MMPR_MODEL_OU: return launch_fine<MMPR_MODEL_OU, PPT, HAS_TAIL>(p, g, s);
-    case MMPR_MODEL_LINEAR: return launch_fine<MMPR_MODEL_LINEAR, PPT, HAS_TAIL>(p, g, s);
-    case MMPR_MODEL_DOUBLE_WELL: return launch_fine<MMPR_MODEL_DOUBLE_WELL, PPT, HAS_TAIL>(p, g, s);
-    case MMPR_MODEL_CUBIC_MF: return launch_fine<MMPR_MODEL_CUBIC_MF, PPT, HAS_TAIL>(p, g, s);
-    case MMPR_MODEL_DW_MULT: return launch_fine<MMPR_MODEL_DW_MULT, PPT, HAS_TAIL>(p, g, s);
+    case MMPR_MODEL_OU: return launch_fine<MMPR_MODEL_OU, PPT, HAS_TAIL>(p, g, s, phx);
+    case MMPR_MODEL_LINEAR: return launch_fine<MMPR_MODEL_LINEAR, PPT, HAS_TAIL>(p, g, s, phx);
+    case MMPR_MODEL_DOUBLE_WELL: return launch_fine<MMPR_MODEL_DOUBLE_WELL, PPT, HAS_TAIL>(p, g, s, phx);
+    case MMPR_MODEL_CUBIC_MF: return launch_fine<MMPR_MODEL_CUBIC_MF, PPT, HAS_TAIL>(p, g, s, phx);
+    case MMPR_MODEL_DW_MULT: return launch_fine<MMPR_MODEL_DW_MULT, PPT, HAS_TAIL>(p, g, s, phx);
     default: return MMPR_ERR_UNSUPPORTED;
   }
 }
 
 template <int PPT>
-static int dispatch_tail(const FineParams &p, const FineGeometry &g, cudaStream_t s) {
-  if (p.P % 8) return dispatch_kind<PPT, true>(p, g, s);
-  return dispatch_kind<PPT, false>(p, g, s);
+static int dispatch_tail(const FineParams &p, const FineGeometry &g, cudaStream_t s, bool phx) {
+  if (p.P % 8) return dispatch_kind<PPT, true>(p, g, s, phx);
+  return dispatch_kind<PPT, false>(p, g, s, phx);
 }
 
 }  // namespace mmpr
@@ -512,11 +535,14 @@ static int fine_sweep_impl(const mmpr_model *model, int32_t n_slices, int64_t pa
                            double dt, double sqrt_dt, const double *t0, const double *x_in, int64_t in_pitch,
                            double *x_out, int64_t out_pitch, const double *xi, int64_t xi_slice_pitch,
                            int64_t xi_row_pitch, int32_t *bad_step, double *final_mean, double *stats,
-                           int64_t *counts, void *stream) {
+                           int64_t *counts, void *stream, const mmpr_counter_noise *cnoise = nullptr) {
   if (!model || n_slices < 0 || particles < 1 || steps < 0 || !x_in || !x_out || !bad_step || !t0)
     return MMPR_ERR_ARG;
   if (n_slices == 0) return MMPR_OK;
-  if (steps > 0 && (!xi || (xi_row_pitch & 1) || xi_row_pitch < particles ||
+  const bool phx = cnoise != nullptr;
+  if (phx && (particles > UINT32_MAX || cnoise->slice_offset < 0 || cnoise->kfield >= (1u << 24)))
+    return MMPR_ERR_ARG;
+  if (!phx && steps > 0 && (!xi || (xi_row_pitch & 1) || xi_row_pitch < particles ||
                     (reinterpret_cast<uintptr_t>(xi) & 15) || (steps > 1 && xi_slice_pitch < steps * xi_row_pitch)))
     return MMPR_ERR_ARG;
   if (model->stat_kind != 0) return MMPR_ERR_UNSUPPORTED;
@@ -552,8 +578,10 @@ static int fine_sweep_impl(const mmpr_model *model, int32_t n_slices, int64_t pa
   p.final_mean = final_mean;
   p.stats = stats;
   p.counts = counts;
+  p.cn = cn::CounterNoise{0u, 0u, 0u, 0};
+  if (phx) p.cn = cn::CounterNoise{cnoise->key[0], cnoise->key[1], cnoise->kfield, cnoise->slice_offset};
   cudaStream_t s = (cudaStream_t)stream;
-  if (use_grid) return fine_grid_sweep(p, s);
+  if (use_grid) return fine_grid_sweep(p, s, phx);
   p.D = g.D;
   p.slots_per_cta = g.slots_per_cta;
   p.ctas = g.ctas;
@@ -562,9 +590,14 @@ static int fine_sweep_impl(const mmpr_model *model, int32_t n_slices, int64_t pa
   p.cnt_min = g.cnt_min;
   p.l2_ahead = 3;
   if (const char *env = getenv("MMPR_FINE_L2_AHEAD")) p.l2_ahead = max(0, min(16, atoi(env)));
-  if (g.ppt <= 8) return dispatch_tail<8>(p, g, s);
-  if (g.ppt <= 13) return dispatch_tail<13>(p, g, s);
-  return dispatch_tail<16>(p, g, s);
+  if (phx) {
+    g.smem_bytes = MMPR_PHX_SMEM;
+    p.nstages = 2;
+    p.l2_ahead = 0;
+  }
+  if (g.ppt <= 8) return dispatch_tail<8>(p, g, s, phx);
+  if (g.ppt <= 13) return dispatch_tail<13>(p, g, s, phx);
+  return dispatch_tail<16>(p, g, s, phx);
 }
 
 extern "C" int mmpr_fine_sweep(const mmpr_model *model, int32_t n_slices, int64_t particles, int32_t steps,
@@ -584,6 +617,16 @@ extern "C" int mmpr_fine_sweep_restrict(const mmpr_model *model, int32_t n_slice
   if (!stats) return MMPR_ERR_ARG;
   return fine_sweep_impl(model, n_slices, particles, steps, dt, sqrt_dt, t0, x_in, in_pitch, x_out, out_pitch, xi,
                          xi_slice_pitch, xi_row_pitch, bad_step, nullptr, stats, counts, stream);
+}
+
+extern "C" int mmpr_fine_sweep_counter(const mmpr_model *model, int32_t n_slices, int64_t particles, int32_t steps,
+                                       double dt, double sqrt_dt, const double *t0, const double *x_in,
+                                       int64_t in_pitch, double *x_out, int64_t out_pitch,
+                                       const mmpr_counter_noise *noise, int32_t *bad_step, double *stats,
+                                       int64_t *counts, void *stream) {
+  if (!noise) return MMPR_ERR_ARG;
+  return fine_sweep_impl(model, n_slices, particles, steps, dt, sqrt_dt, t0, x_in, in_pitch, x_out, out_pitch,
+                         nullptr, 0, 0, bad_step, nullptr, stats, counts, stream, noise);
 }
 
 extern "C" int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_out, int32_t *ctas_out) {

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "mmpr_device.cuh"
+#include "counter_noise.cuh"
 
 namespace mmpr {
 
@@ -36,7 +37,11 @@ struct FineParams {
   int nstages;        // increment stages in shared memory (2..FS_MAX_STAGES)
   int cnt_min;        // min elements per lane over populated slots
   int l2_ahead;       // steps of increments prefetched into L2 beyond the smem stages
+  cn::CounterNoise cn;  // PHX kernels: increments from counter-based Philox (xi unused)
 };
+
+// dynamic shared memory of a PHX kernel: the ziggurat tables
+#define MMPR_PHX_SMEM ((size_t)sizeof(cn::ZigTables))
 
 struct __align__(16) ClusterSlot {
   double v;
@@ -96,7 +101,7 @@ struct Part<false> {
 };
 
 // Grid (multi-team) variant for ensembles beyond one cluster, fine_grid.cu.
-int fine_grid_sweep(FineParams p, cudaStream_t stream);
+int fine_grid_sweep(FineParams p, cudaStream_t stream, bool phx = false);
 int fine_grid_shape(int64_t P, int n_slices, int *teams_out, int *ctas_out);
 
 // Single-region restriction with one cluster per ensemble, restrict1.cu

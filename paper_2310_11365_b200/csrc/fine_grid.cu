@@ -96,7 +96,9 @@ __device__ __forceinline__ void chunk_range(int64_t len, int h, int64_t *a, int6
 
 // LO: compile-time lower bound on the accumulator elements per lane of every
 // populated leaf (elements LO..PPT-1 carry a predicate); -1 = p.cnt_min.
-template <int KIND, int PPT, bool HAS_TAIL, bool PADDED, int H, int LO>
+// PHX: increments from counter-based Philox in registers (counter_noise.cuh);
+// the dynamic shared memory holds the ziggurat tables, no copies run.
+template <int KIND, int PPT, bool HAS_TAIL, bool PADDED, int H, int LO, bool PHX = false>
 __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, const GridExtra e) {
   using PartT = Part<PADDED>;
   constexpr int MH = PPT / H;  // accumulator elements of chunk 0 (chunk H-1 takes the rest)
@@ -145,6 +147,8 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
   const int my_base = li * LS + j8;
   const int tail_idx = li * LS + (int)(8 * cnt - 8 * (H - 1) * MH) + j8;  // tail sits in chunk H-1
 
+  const cn::ZigTables *zt = reinterpret_cast<const cn::ZigTables *>(s_buf);
+  if constexpr (PHX) cn::load_zig(reinterpret_cast<cn::ZigTables *>(s_buf), tid, (int)blockDim.x);
   if (tid == 0) {
     for (int q = 0; q < NB; ++q) mbar_init(&s_bar[q], 1);
     mbar_init(&s_red_bar[0], 1);
@@ -197,9 +201,10 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
   for (int slice = team; slice < p.n_slices; slice += e.teams) {
     const int total_chunks = p.S * H;
     const double *xi_slice = p.xi + (int64_t)slice * p.xi_slice_pitch;
-    if (issuer) {
+    if (!PHX && issuer) {
       for (int c = 0; c < NB && c < total_chunks; ++c) issue(xi_slice, c);
     }
+    const uint32_t nglob = (uint32_t)(p.cn.n_base + slice);
     double x[PPT];
     double xt = 0.0;
     const double *xin = p.x_in + (int64_t)slice * p.in_pitch;
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
       GPROF_ADD(1, pb0, pb1);
       // B1 orders every read of the consumed buffers before their refill; the
       // copies overlap the team exchange below
-      if (issuer && refill_step >= 0) {
+      if (!PHX && issuer && refill_step >= 0) {
         for (int h = 0; h < H; ++h) {
           const int c = refill_step * H + h + NB;
           if (c < total_chunks) issue(xi_slice, c);
@@ -368,10 +373,22 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
     double s = 0.0;
     int bad = 0;
     int first_bad = MMPR_STAT_OK;
-    int issued = min(NB, total_chunks);
+    int issued = PHX ? 0 : min(NB, total_chunks);
     reduce(-1, s, bad);
     for (int j = 0; j < p.S; ++j) {
       GPROF_MARK(pu0);
+      if constexpr (PHX) {
+#pragma unroll
+        for (int m = 0; m < PPT; ++m) {
+          if (m < cmin) {
+            x[m] = em_update<KIND>(p, x[m], s, cn::normal(p.cn, (uint32_t)(off + j8 + 8 * m), (uint32_t)j, nglob, zt));
+          } else if (m < cnt) {
+            x[m] = em_update<KIND>(p, x[m], s, cn::normal(p.cn, (uint32_t)(off + j8 + 8 * m), (uint32_t)j, nglob, zt));
+          }
+        }
+        if (HAS_TAIL && j8 < tail)
+          xt = em_update<KIND>(p, xt, s, cn::normal(p.cn, (uint32_t)(off + 8 * cnt + j8), (uint32_t)j, nglob, zt));
+      } else {
 #pragma unroll
           for (int h = 0; h < H; ++h) {
             const uint32_t q = qbase + (uint32_t)(j * H + h);
@@ -392,12 +409,13 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
             }
             if (h == H - 1 && HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[tail_idx]);
           }
+      }
       GPROF_MARK(pu1);
       GPROF_ADD(0, pu0, pu1);
       reduce(j, s, bad);  // refills the buffers step j consumed
       GPROF_MARK(pu2);
       GPROF_ADD(6, pu1, pu2);
-      issued = min(total_chunks, NB + (j + 1) * H);
+      if (!PHX) issued = min(total_chunks, NB + (j + 1) * H);
       if (bad) {
         first_bad = j;
         break;
@@ -613,9 +631,14 @@ static int launch_grid_t(const FineParams &p, const GridGeometry &g, cudaStream_
 }
 
 template <int KIND, bool HAS_TAIL>
-static int grid_dispatch_shape(const FineParams &p, const GridGeometry &g, cudaStream_t s) {
+static int grid_dispatch_shape(const FineParams &p, const GridGeometry &g, cudaStream_t s, bool phx) {
   // P = 2^20: every leaf holds 128 elements, no predicated accumulator element
   const bool full = !g.padded && g.cnt_min >= 16;
+  if (phx) {  // no chunking: one PHX instantiation per leaf shape
+    if (full) return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, false, 1, 16, true>>(p, g, s);
+    if (g.padded) return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, true, 1, -1, true>>(p, g, s);
+    return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, false, 1, -1, true>>(p, g, s);
+  }
   if (g.H == 1) {
     if (full) return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, false, 1, 16>>(p, g, s);
     if (g.padded) return launch_grid_t<fine_grid_kernel<KIND, 16, HAS_TAIL, true, 1, -1>>(p, g, s);
@@ -627,13 +650,13 @@ static int grid_dispatch_shape(const FineParams &p, const GridGeometry &g, cudaS
 }
 
 template <bool HAS_TAIL>
-static int grid_dispatch_kind(const FineParams &p, const GridGeometry &g, cudaStream_t s) {
+static int grid_dispatch_kind(const FineParams &p, const GridGeometry &g, cudaStream_t s, bool phx) {
   switch (p.model.kind) {
-    case MMPR_MODEL_OU: return grid_dispatch_shape<MMPR_MODEL_OU, HAS_TAIL>(p, g, s);
-    case MMPR_MODEL_LINEAR: return grid_dispatch_shape<MMPR_MODEL_LINEAR, HAS_TAIL>(p, g, s);
-    case MMPR_MODEL_DOUBLE_WELL: return grid_dispatch_shape<MMPR_MODEL_DOUBLE_WELL, HAS_TAIL>(p, g, s);
-    case MMPR_MODEL_CUBIC_MF: return grid_dispatch_shape<MMPR_MODEL_CUBIC_MF, HAS_TAIL>(p, g, s);
-    case MMPR_MODEL_DW_MULT: return grid_dispatch_shape<MMPR_MODEL_DW_MULT, HAS_TAIL>(p, g, s);
+    case MMPR_MODEL_OU: return grid_dispatch_shape<MMPR_MODEL_OU, HAS_TAIL>(p, g, s, phx);
+    case MMPR_MODEL_LINEAR: return grid_dispatch_shape<MMPR_MODEL_LINEAR, HAS_TAIL>(p, g, s, phx);
+    case MMPR_MODEL_DOUBLE_WELL: return grid_dispatch_shape<MMPR_MODEL_DOUBLE_WELL, HAS_TAIL>(p, g, s, phx);
+    case MMPR_MODEL_CUBIC_MF: return grid_dispatch_shape<MMPR_MODEL_CUBIC_MF, HAS_TAIL>(p, g, s, phx);
+    case MMPR_MODEL_DW_MULT: return grid_dispatch_shape<MMPR_MODEL_DW_MULT, HAS_TAIL>(p, g, s, phx);
     default: return MMPR_ERR_UNSUPPORTED;
   }
 }
@@ -647,18 +670,22 @@ int fine_grid_shape(int64_t P, int n_slices, int *teams_out, int *ctas_out) {
   return MMPR_OK;
 }
 
-int fine_grid_sweep(FineParams p, cudaStream_t stream) {
+int fine_grid_sweep(FineParams p, cudaStream_t stream, bool phx) {
   GridGeometry g;
   int st = grid_geometry(p.P, p.n_slices, &g);
   if (st != MMPR_OK) return st;
+  if (phx) {
+    g.smem = MMPR_PHX_SMEM;
+    g.H = 1;
+  }
   p.D = g.D;
   p.slots_per_cta = g.spc;
   p.ctas = g.C;
   p.cnt_min = g.cnt_min;
   p.stage_elems = g.chunk_elems;
   p.nstages = g.nbuf;
-  if (p.P % 8) return grid_dispatch_kind<true>(p, g, stream);
-  return grid_dispatch_kind<false>(p, g, stream);
+  if (p.P % 8) return grid_dispatch_kind<true>(p, g, stream, phx);
+  return grid_dispatch_kind<false>(p, g, stream, phx);
 }
 
 }  // namespace mmpr

@@ -25,6 +25,7 @@
 
 #include "mmpr_device.cuh"
 #include "npstream.cuh"
+#include "counter_noise.cuh"
 #include "capi_internal.h"
 
 namespace mmpr {
@@ -658,4 +659,34 @@ extern "C" int mmpr_log1p_libm(const double *x, double *out, int64_t n, void *st
   const int64_t blocks = (n + 255) / 256;
   log1p_kernel<<<(unsigned)(blocks < 4736 ? blocks : 4736), 256, 0, (cudaStream_t)stream>>>(x, out, n);
   return mmpr_check_launch("log1p_kernel");
+}
+
+namespace mmpr {
+__global__ void counter_normals_kernel(const cn::CounterNoise c, uint32_t n, uint32_t j0, int rows, int64_t p0,
+                                       int64_t count, double *__restrict__ out, int64_t pitch) {
+  __shared__ cn::ZigTables z;
+  cn::load_zig(&z, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int64_t total = (int64_t)rows * count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / count);
+    const int64_t q = i - (int64_t)r * count;
+    out[r * pitch + q] = cn::normal(c, (uint32_t)(p0 + q), j0 + (uint32_t)r, n, &z);
+  }
+}
+}  // namespace mmpr
+
+extern "C" int mmpr_counter_normals_fill(const mmpr_counter_noise *noise, int32_t n, int32_t j0, int32_t rows,
+                                         int64_t p0, int64_t count, double *out, int64_t pitch, void *stream) {
+  if (!noise || n < 0 || j0 < 0 || rows < 0 || p0 < 0 || count < 0 || p0 + count > (int64_t)UINT32_MAX ||
+      (rows > 1 && pitch < count) || noise->kfield >= (1u << 24))
+    return MMPR_ERR_ARG;
+  if (rows == 0 || count == 0) return MMPR_OK;
+  if (!out) return MMPR_ERR_ARG;
+  const cn::CounterNoise c{noise->key[0], noise->key[1], noise->kfield, noise->slice_offset};
+  const int64_t total = (int64_t)rows * count;
+  const int64_t blocks = (total + 255) / 256;
+  counter_normals_kernel<<<(unsigned)(blocks < 4736 ? blocks : 4736), 256, 0, (cudaStream_t)stream>>>(
+      c, (uint32_t)n, (uint32_t)j0, rows, p0, count, out, pitch);
+  return mmpr_check_launch("counter_normals_kernel");
 }

@@ -69,6 +69,7 @@ struct PipeParams {
   int sys;  // ranks on several GPUs: system-scope ordering
   long long watchdog;  // pl_wait limit in cycles (see pl_wait)
   int *abort;          // this launch's abort word (last flag word of rank r0)
+  int phx;             // increments from counter-based Philox (f.cn) instead of io.xi
 };
 
 __device__ __forceinline__ int pl_ld_acquire(const int *p, bool sys) {
@@ -256,7 +257,10 @@ __device__ __forceinline__ void pl_advance_chain(const PipeParams &pp, int k, in
 
 // MULTI = false: one rank (the single-GPU engine); the rank table collapses
 // to io[0] at compile time and the step loop keeps every value in registers.
-template <int KIND, int PPT, bool HAS_TAIL, int OK, int MK, bool MULTI>
+// PHX: every unit's increments come from counter-based Philox in registers
+// (counter_noise.cuh) -- the dynamic shared memory holds the ziggurat tables
+// and the increment copies, their mbarriers and the L2 prefetch disappear.
+template <int KIND, int PPT, bool HAS_TAIL, int OK, int MK, bool MULTI, bool PHX = false>
 __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
   constexpr int LO = PPT - 1;  // every leaf has PPT-1 or PPT accumulator elements per lane
   using PartT = Part<false>;
@@ -301,6 +305,8 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
   }
   const int my_idx = off - lo + j8;
   const int ns = p.nstages;
+  const cn::ZigTables *zt = reinterpret_cast<const cn::ZigTables *>(s_stage);
+  if constexpr (PHX) cn::load_zig(reinterpret_cast<cn::ZigTables *>(s_stage), tid, gthreads);
 
   if (tid == 0) {
     for (int q = 0; q < ns; ++q) mbar_init(&s_bar[q], 1);
@@ -463,7 +469,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
     double *snap_kn = io.snap + srow * io.snap_iter_stride + (int64_t)n * io.snap_slice_pitch;
 
     // the increments do not depend on anything: start their copies first
-    if (has_fine && tid == 0) {
+    if (!PHX && has_fine && tid == 0) {
       const double *base = io.xi + (int64_t)(n - r * pp.Ng) * io.xi_slice_pitch + lo;
       const uint32_t bytes = s_stage_bytes;
       s_xi_base = base;  // read by the refill thread after the next block barrier
@@ -603,25 +609,36 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       int bad = 0;
       if (!mean_known) reduce(Plain{}, 0.0, -1, s, bad);
       int first_bad = MMPR_STAT_OK;
+      const uint32_t nglob = (uint32_t)n;
       for (int j = 0; j < p.S; ++j) {
         const uint32_t lj = ld + (uint32_t)j;
         const int stage = (int)(lj % (uint32_t)ns);
-        mbar_wait_parity(&s_bar[stage], (lj / (uint32_t)ns) & 1u);
-        const double *xb = s_stage + stage * p.stage_elems;
+        if constexpr (PHX) {
 #pragma unroll
-        for (int m = 0; m < PPT; ++m) {
-          if (m < LO) {
-            x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
-          } else {
-            // past a 12-element leaf this reads up to 8 doubles beyond the
-            // CTA's range (into the next stage or the 64-byte pad after the
-            // last): the value is discarded, so no clamp is needed
-            const double nx = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
-            x[m] = (m < cnt) ? nx : x[m];
+          for (int m = 0; m < PPT; ++m) {
+            if (m < LO || m < cnt)
+              x[m] = em_update<KIND>(p, x[m], s, cn::normal(p.cn, (uint32_t)(off + j8 + 8 * m), (uint32_t)j, nglob, zt));
           }
+          if (HAS_TAIL && j8 < tail)
+            xt = em_update<KIND>(p, xt, s, cn::normal(p.cn, (uint32_t)(tail_off + j8), (uint32_t)j, nglob, zt));
+        } else {
+          mbar_wait_parity(&s_bar[stage], (lj / (uint32_t)ns) & 1u);
+          const double *xb = s_stage + stage * p.stage_elems;
+#pragma unroll
+          for (int m = 0; m < PPT; ++m) {
+            if (m < LO) {
+              x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
+            } else {
+              // past a 12-element leaf this reads up to 8 doubles beyond the
+              // CTA's range (into the next stage or the 64-byte pad after the
+              // last): the value is discarded, so no clamp is needed
+              const double nx = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
+              x[m] = (m < cnt) ? nx : x[m];
+            }
+          }
+          if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
         }
-        if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
-        reduce(Plain{}, 0.0, (j + ns < p.S) ? j + ns : -1, s, bad);
+        reduce(Plain{}, 0.0, (!PHX && j + ns < p.S) ? j + ns : -1, s, bad);
         if (bad) {
           first_bad = j;
           break;
@@ -629,9 +646,9 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       }
       // loads issued for this unit: the first min(ns, S) plus one refill per
       // completed step while j + ns < S
-      const int init = ns < p.S ? ns : p.S;
+      const int init = PHX ? 0 : (ns < p.S ? ns : p.S);
       const int done_steps = first_bad == MMPR_STAT_OK ? p.S : first_bad + 1;
-      const int refills = max(0, min(done_steps, p.S - ns));
+      const int refills = PHX ? 0 : max(0, min(done_steps, p.S - ns));
       const int issued = init + refills;
       if (tid == gthreads - 32 && first_bad != MMPR_STAT_OK) {
         for (int j = first_bad + 1; j < issued; ++j) {
@@ -780,6 +797,16 @@ static int launch_pipe(const PipeParams &pp, const PipeGeometry &g, cudaStream_t
 
 template <int KIND, int OK, int MK>
 static int dispatch_pipe_tail(const PipeParams &pp, const PipeGeometry &g, cudaStream_t s) {
+  if (pp.phx) {
+    PipeGeometry gp = g;
+    gp.smem = MMPR_PHX_SMEM;
+    if (pp.G > 1) {
+      if (g.tail) return launch_pipe<pipeline_kernel<KIND, 13, true, OK, MK, true, true>>(pp, gp, s);
+      return launch_pipe<pipeline_kernel<KIND, 13, false, OK, MK, true, true>>(pp, gp, s);
+    }
+    if (g.tail) return launch_pipe<pipeline_kernel<KIND, 13, true, OK, MK, false, true>>(pp, gp, s);
+    return launch_pipe<pipeline_kernel<KIND, 13, false, OK, MK, false, true>>(pp, gp, s);
+  }
   if (pp.G > 1) {
     if (g.tail) return launch_pipe<pipeline_kernel<KIND, 13, true, OK, MK, true>>(pp, g, s);
     return launch_pipe<pipeline_kernel<KIND, 13, false, OK, MK, true>>(pp, g, s);
@@ -840,7 +867,8 @@ static int check_io(const mmpr_pipeline_io *io, int32_t n_slices, int32_t iterat
   if (io->fine_pitch < particles || io->snap_slice_pitch < particles ||
       io->snap_iter_stride < (int64_t)(n_slices + 1) * io->snap_slice_pitch)
     return MMPR_ERR_ARG;
-  if (steps > 0 && (!io->xi || (io->xi_row_pitch & 1) || io->xi_row_pitch < particles ||
+  if (io->counter_noise && io->counter_kfield >= (1u << 24)) return MMPR_ERR_ARG;
+  if (steps > 0 && !io->counter_noise && (!io->xi || (io->xi_row_pitch & 1) || io->xi_row_pitch < particles ||
                     (reinterpret_cast<uintptr_t>(io->xi) & 15) ||
                     (steps > 1 && io->xi_slice_pitch < steps * io->xi_row_pitch)))
     return MMPR_ERR_ARG;
@@ -937,6 +965,9 @@ extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_
     if (const char *env = getenv("MMPR_PIPELINE_WATCHDOG")) pp.watchdog = atoll(env);  // tests
   }
   pp.abort = ios[first_rank].flags + nflags - 1;
+  pp.phx = ios[first_rank].counter_noise ? 1 : 0;
+  p.cn = cn::CounterNoise{ios[first_rank].counter_key[0], ios[first_rank].counter_key[1],
+                          ios[first_rank].counter_kfield, 0};
   pp.nranks = launch_ranks;
   // one launch over several ranks normally takes one global ticket order;
   // MMPR_PIPELINE_RANK_TICKETS=1 gives every rank its own clusters and

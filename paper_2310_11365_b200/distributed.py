@@ -53,14 +53,23 @@ class GpuBackend:
     def noise(self, seed, n_offset, n_slices, steps, P, iteration, fresh, out):
         slice_noise(seed, n_offset, n_slices, steps, P, iteration, fresh, out=out)
 
+    @staticmethod
+    def _noise_args(xi):
+        """xi is an increment buffer, or a CounterNoise (NoiseMode.PHILOX*:
+        increments generated in registers)."""
+        return (None, xi) if isinstance(xi, _lib.CounterNoise) else (xi, None)
+
     def fine(self, x_in, x_out, t0, steps, dt, xi, bad):
-        kernels.fine_sweep(self.model_d, x_in, x_out, t0, steps, dt, xi, bad)
+        xi, counter = self._noise_args(xi)
+        kernels.fine_sweep(self.model_d, x_in, x_out, t0, steps, dt, xi, bad, counter=counter)
 
     def fine_restrict(self, x_in, x_out, t0, steps, dt, xi, bad, stats, counts):
         """Sweep plus the single-region restriction of its outputs, fused
         (MEAN_OF_F models; the restriction kernel otherwise)."""
         if self.model_d.stat_kind == _lib.STAT_MEAN_OF_F:
-            kernels.fine_sweep(self.model_d, x_in, x_out, t0, steps, dt, xi, bad, stats=stats, counts=counts)
+            xi, counter = self._noise_args(xi)
+            kernels.fine_sweep(self.model_d, x_in, x_out, t0, steps, dt, xi, bad, stats=stats, counts=counts,
+                               counter=counter)
         else:
             kernels.fine_sweep(self.model_d, x_in, x_out, t0, steps, dt, xi, bad)
             kernels.restrict(SINGLE_REGION.descriptor(), x_out, stats, counts)
@@ -152,7 +161,7 @@ def _pipeline_sharded_ok(be, cfg: PararealConfig, plan: NoisePlan, comm) -> bool
     if comm.world > 1 and os.environ.get("MMPR_SHARDED_PIPELINE", "0") != "1":
         return False
     G = comm.world
-    ok = (G <= 8 and cfg.n_slices % G == 0 and cfg.iterations >= 1 and not plan.fresh
+    ok = (G <= 8 and cfg.n_slices % G == 0 and cfg.iterations >= 1 and not plan.fresh and not plan.counter_based
           and cfg.stop_wasserstein_tol is None
           and kernels.pipeline_supported(be.model_d, be.ode_d, be.ode_model_d, be.integ_d, cfg.particles))
     return comm.all_min_int(1 if ok else 0) == 1
@@ -303,7 +312,8 @@ def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: N
 
     snap = be.empty((K + 1 if retain else 2, Ng + 1, P))
     fine = be.empty((Ng, P))
-    xi = be.empty((Ng, S, row_pitch(P)))
+    counter_mode = getattr(plan, "counter_based", False)
+    xi = be.empty((1, 1, 2) if counter_mode else (Ng, S, row_pitch(P)))
     macro = be.empty((K + 1, N + 1, nv))
     cache = be.empty((K + 1, N, nv))
     raw = be.empty((max(K, 1), N, nv))
@@ -332,22 +342,23 @@ def run_micro_macro_sharded(model, coarse, initial, cfg: PararealConfig, plan: N
     else:
         be.match(macro[0, a:a + 1], rho0, counts0, x0, sn(0)[0:1], 1, lift_first)
     be.restrict(sn(0), micro_local[0], micro_counts_local[0], scratch)
-    if not plan.fresh:
+    if not plan.fresh and not counter_mode:
         be.noise(plan.master_seed, a, Ng, S, P, 0, False, xi)
 
     timer = _StageTimer(record_timings and be.device.type == "cuda")
     stopped_at = None
     done = 0
     for k in range(K):
-        if plan.fresh:
+        if plan.fresh and not counter_mode:
             be.noise(plan.master_seed, a, Ng, S, P, k, True, xi)
+        xk = plan.counter_noise(k, a) if counter_mode else xi
         cur, nxt = sn(k), sn(k + 1)
         ev = timer.start()
         if I == 1:
-            be.fine_restrict(cur[:Ng], fine, times_d[a:a + Ng], S, dt, xi, bad_local[k], fine_local, fine_counts)
+            be.fine_restrict(cur[:Ng], fine, times_d[a:a + Ng], S, dt, xk, bad_local[k], fine_local, fine_counts)
             timer.stop("fine", ev)
         else:
-            be.fine(cur[:Ng], fine, times_d[a:a + Ng], S, dt, xi, bad_local[k])
+            be.fine(cur[:Ng], fine, times_d[a:a + Ng], S, dt, xk, bad_local[k])
             timer.stop("fine", ev)
             be.restrict(fine, fine_local, fine_counts, scratch)
         fine_all[k].copy_(comm.all_gather_rows(fine_local))

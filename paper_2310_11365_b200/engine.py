@@ -162,7 +162,8 @@ class _Workspace:
     I64 = ("micro_counts", "fine_counts", "counts0")
     I32 = ("bad", "coarse_status", "match_status")
 
-    def __init__(self, K: int, N: int, P: int, S: int, I: int, retain: bool, noise_slices: int | None = None):
+    def __init__(self, K: int, N: int, P: int, S: int, I: int, retain: bool, noise_slices: int | None = None,
+                 counter: bool = False):
         dev = device()
         nv = 3 * I
         Kc = max(K, 1)
@@ -188,6 +189,10 @@ class _Workspace:
         self.host = {dt: torch.empty(t.shape, dtype=dt, pin_memory=True) for dt, t in self.report.items()}
         # increments of a batch of slices: all N when they fit (frozen noise is
         # then generated once per run), else batches regenerated per iteration
+        if counter:  # increments generated in registers: no stream buffer
+            self.noise_slices = N
+            self.xi = torch.empty((1, 1, 2), dtype=torch.float64, device=dev)
+            return
         self.noise_slices = noise_slices if noise_slices else _noise_batch(N, S, P)
         self.xi = torch.empty((self.noise_slices, S, row_pitch(P)), dtype=torch.float64, device=dev)
 
@@ -239,7 +244,9 @@ class _RunPlan:
         self.N, self.K, self.P, self.S, self.I = N, K, P, S, I
         self.times = tuple(cfg.t_start + n * cfg.slice_length for n in range(N + 1))
         self.times_d = torch.tensor(self.times, dtype=torch.float64, device=device())
-        self.ws = _Workspace(K, N, P, S, I, cfg.retain_snapshots, noise_slices=N if injected else None)
+        self.counter = plan.counter_based and not injected
+        self.ws = _Workspace(K, N, P, S, I, cfg.retain_snapshots, noise_slices=N if injected else None,
+                             counter=self.counter)
         # single-region restriction of the fine outputs fused into the sweep
         self.fused_restrict = I == 1 and model_d.stat_kind == _lib.STAT_MEAN_OF_F
         # several regions: match and micro restriction in one cluster pass
@@ -283,7 +290,7 @@ class _RunPlan:
         N, P, S = self.N, self.P, self.S
         ws.reset_status()
         self.snap(0)[0].copy_(ws.x0[0])
-        noise_here = not injected and not self.plan.fresh and self.batch == N
+        noise_here = not injected and not self.counter and not self.plan.fresh and self.batch == N
         if noise_here and self.pipeline and not timer.enabled:
             main = torch.cuda.current_stream()
             if self.side_stream is None:
@@ -331,9 +338,12 @@ class _RunPlan:
     def issue_iteration(self, k, timer, injected=False):
         ws, part_d, N, S, B = self.ws, self.part_d, self.N, self.S, self.batch
         cur, nxt = self.snap(k), self.snap(k + 1)
+        counter = self.plan.counter_noise(k) if self.counter else None
         for a in range(0, N, B):
             nb = min(B, N - a)
-            if not injected and (self.plan.fresh or B < N):
+            if counter is not None:
+                counter.slice_offset = a
+            elif not injected and (self.plan.fresh or B < N):
                 ev = timer.start()
                 slice_noise(self.plan.master_seed, a, nb, S, self.P, k, self.plan.fresh, out=ws.xi[:nb])
                 timer.stop("noise", ev)
@@ -341,10 +351,11 @@ class _RunPlan:
             if self.fused_restrict:  # R(F_n) computed by the sweep from registers
                 kernels.fine_sweep(self.model_d, cur[a:a + nb], ws.fine[a:a + nb], self.times_d[a:a + nb], S,
                                    self.cfg.step.dt, ws.xi[:nb], ws.bad[k][a:a + nb],
-                                   stats=ws.fine_stats[k][a:a + nb], counts=ws.fine_counts[k][a:a + nb])
+                                   stats=ws.fine_stats[k][a:a + nb], counts=ws.fine_counts[k][a:a + nb],
+                                   counter=counter)
             else:
                 kernels.fine_sweep(self.model_d, cur[a:a + nb], ws.fine[a:a + nb], self.times_d[a:a + nb], S,
-                                   self.cfg.step.dt, ws.xi[:nb], ws.bad[k][a:a + nb])
+                                   self.cfg.step.dt, ws.xi[:nb], ws.bad[k][a:a + nb], counter=counter)
             timer.stop("fine", ev)
         if not self.fused_restrict:
             ev = timer.start()
@@ -383,7 +394,7 @@ class _RunPlan:
                                   self.cfg.step.dt, self.S, self.reuse, self.times_d, ws.x0, ws.rho0, ws.counts0,
                                   ws.xi, ws.snap, ws.fine, ws.macro, ws.micro, ws.micro_counts, ws.fine_stats,
                                   ws.fine_counts, ws.raw, ws.cache, ws.bad, ws.coarse_status, ws.match_status,
-                                  self.flags)
+                                  self.flags, counter=self.plan.counter_noise(0) if self.counter else None)
         timer.stop("iterations", ev)
 
     def stream_row(self, k):
@@ -674,10 +685,11 @@ def _fine_sweep(model, ensembles, times, cfg: PararealConfig, plan: NoisePlan, i
     x = torch.stack([e.device_positions for e in list(ensembles)[:N]])
     out = torch.empty_like(x)
     bad = torch.empty(N, dtype=torch.int32, device=device())
-    xi = slice_noise(plan.master_seed, 0, N, S, P, iteration, plan.fresh)
+    counter = plan.counter_noise(iteration) if plan.counter_based else None
+    xi = None if counter is not None else slice_noise(plan.master_seed, 0, N, S, P, iteration, plan.fresh)
     t0 = torch.tensor(list(times[:N]), dtype=torch.float64, device=device())
     start = time.perf_counter()
-    kernels.fine_sweep(desc, x, out, t0, S, cfg.step.dt, xi, bad)
+    kernels.fine_sweep(desc, x, out, t0, S, cfg.step.dt, xi, bad, counter=counter)
     b = bad.cpu().numpy()
     elapsed = time.perf_counter() - start
     for n in range(N):
@@ -698,6 +710,10 @@ def _serial_chains(desc, ens0, plans, cfg: PararealConfig, iteration: int):
     xs = torch.empty((R, N + 1, P), dtype=torch.float64, device=device())
     for r, e in enumerate(ens0):
         xs[r, 0].copy_(e.device_positions)
+    if any(pl.counter_based for pl in plans):
+        if not all(pl.counter_based for pl in plans):
+            raise ValueError("replica plans must all use counter-based noise or none")
+        return _serial_chains_counter(desc, ens0, plans, cfg, iteration, xs)
     B = max(1, min(N, _noise_batch(N * R, S, P) // R)) if N else 1
     xi = torch.empty((B, R, S, pitch), dtype=torch.float64, device=device())
     bad = torch.empty((max(N, 1), R), dtype=torch.int32, device=device())
@@ -711,6 +727,25 @@ def _serial_chains(desc, ens0, plans, cfg: PararealConfig, iteration: int):
             kernels.fine_sweep(desc, xs[:, n], xs[:, n + 1], t0[n], S, cfg.step.dt, xi[n - a], bad[n])
     b = bad.cpu().numpy()
     for r in range(R):  # chain by chain, as separate serial runs would raise
+        for n in range(N):
+            if b[n, r] != _lib.STAT_OK:
+                raise NumericalBlowup(f"non-finite particle position in slice {n}, step {int(b[n, r])}",
+                                      slice_index=n, step_index=int(b[n, r]))
+    return [[ens0[r]] + [ParticleEnsemble._wrap(xs[r, n]) for n in range(1, N + 1)] for r in range(R)]
+
+
+def _serial_chains_counter(desc, ens0, plans, cfg: PararealConfig, iteration: int, xs):
+    """_serial_chains with counter-based increments (no noise buffers): one
+    launch per (chain, slice)."""
+    R, N, S = len(plans), cfg.n_slices, cfg.step.steps_per_slice
+    bad = torch.empty((max(N, 1), R), dtype=torch.int32, device=device())
+    t0 = [torch.tensor([cfg.t_start + n * cfg.slice_length], dtype=torch.float64, device=device()) for n in range(N)]
+    for r, pl in enumerate(plans):
+        for n in range(N):
+            kernels.fine_sweep(desc, xs[r, n:n + 1], xs[r, n + 1:n + 2], t0[n], S, cfg.step.dt, None, bad[n, r:r + 1],
+                               counter=pl.counter_noise(iteration, n))
+    b = bad.cpu().numpy()
+    for r in range(R):
         for n in range(N):
             if b[n, r] != _lib.STAT_OK:
                 raise NumericalBlowup(f"non-finite particle position in slice {n}, step {int(b[n, r])}",

@@ -28,17 +28,32 @@ def _rows(t, name):
 
 
 def fine_sweep(model: _lib.Model, x_in, x_out, t0, steps: int, dt: float, xi, bad_step, final_mean=None,
-               stats=None, counts=None, stream=None) -> None:
+               stats=None, counts=None, stream=None, counter: _lib.CounterNoise | None = None) -> None:
     """EM over ``steps`` steps for every row of x_in (E, P) -> x_out (E, P).
     xi: (E, steps, pitch) increments; t0: (E,) float64; bad_step: (E,) int32.
     stats (E, 3) / counts (E, 1): single-region restriction of x_out fused
-    into the sweep (MEAN_OF_F models)."""
+    into the sweep (MEAN_OF_F models).  ``counter`` (NoiseMode.PHILOX*):
+    increments generated in registers by counter-based Philox; xi unused."""
     require_cuda()
     E, P = x_in.shape
     in_pitch = _rows(x_in, "x_in")
     out_pitch = _rows(x_out, "x_out")
     if x_out.shape != x_in.shape:
         raise ValueError("x_out must match x_in")
+    if counter is not None:
+        if model.stat_kind != _lib.STAT_MEAN_OF_F:
+            raise _lib.MmprError("counter-based noise runs the MEAN_OF_F fine kernels only")
+        if bad_step.dtype != torch.int32 or bad_step.numel() < E:
+            raise ValueError("bad_step must be int32 (E,)")
+        if stats is not None:
+            _f64(stats, "stats")
+            if stats.numel() < 3 * E or not stats.is_contiguous():
+                raise ValueError("stats must be contiguous float64 (E, 3)")
+        _lib.call("mmpr_fine_sweep_counter", ctypes.byref(model), int(E), int(P), int(steps), float(dt),
+                  float(math.sqrt(dt)), t0.data_ptr(), x_in.data_ptr(), int(in_pitch), x_out.data_ptr(),
+                  int(out_pitch), ctypes.byref(counter), bad_step.data_ptr(), _lib.ptr(stats), _lib.ptr(counts),
+                  _lib.stream_handle(stream))
+        return
     _f64(xi, "xi")
     if xi.dim() != 3 or xi.shape[0] != E or xi.shape[1] < steps or xi.stride(2) != 1:
         raise ValueError("xi must be (E, >=steps, pitch)")
@@ -229,7 +244,7 @@ def parareal_pipeline(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Mo
                       dt: float, steps: int,
                       reuse: bool, times, x0, rho0, counts0, xi, snap, fine, macro, micro, micro_counts,
                       fine_stats, fine_counts, raw, cache, bad, coarse_status, match_status, flags,
-                      stream=None) -> None:
+                      stream=None, counter: _lib.CounterNoise | None = None) -> None:
     """Iterations 1..K of run_micro_macro in one launch (after the prologue).
 
     snap: (K+1 or 2, N+1, P); fine: (2, N, P); macro/micro: (K+1, N+1, 3);
@@ -246,9 +261,10 @@ def parareal_pipeline(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Mo
     _f64(fine, "fine")
     if fine.shape != (2, N, P) or fine.stride(2) != 1 or fine.stride(0) != N * fine.stride(1):
         raise ValueError("fine must be (2, N, P) with uniform row pitch")
-    _f64(xi, "xi")
-    if xi.dim() != 3 or xi.shape[0] < N or xi.shape[1] < steps or xi.stride(2) != 1:
-        raise ValueError("xi must be (N, >=steps, pitch)")
+    if counter is None:
+        _f64(xi, "xi")
+        if xi.dim() != 3 or xi.shape[0] < N or xi.shape[1] < steps or xi.stride(2) != 1:
+            raise ValueError("xi must be (N, >=steps, pitch)")
     for t, shape, dtype, name in ((macro, (K + 1, N + 1, 3), torch.float64, "macro"),
                                   (micro, (K + 1, N + 1, 3), torch.float64, "micro"),
                                   (micro_counts, (K + 1, N + 1, 1), torch.int64, "micro_counts"),
@@ -264,13 +280,19 @@ def parareal_pipeline(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Mo
     if flags.dtype != torch.int32 or flags.numel() < pipeline_flags_size(N, K):
         raise ValueError("flags must be int32 of pipeline_flags_size(N, K)")
     io = _lib.PipelineIO(times=times.data_ptr(), x0=x0.data_ptr(), rho0=rho0.data_ptr(), counts0=counts0.data_ptr(),
-                         xi=xi.data_ptr(), xi_slice_pitch=xi.stride(0), xi_row_pitch=xi.stride(1),
+                         xi=xi.data_ptr() if counter is None else None,
+                         xi_slice_pitch=xi.stride(0) if counter is None else 0,
+                         xi_row_pitch=xi.stride(1) if counter is None else 0,
                          snap=snap.data_ptr(), snap_iter_stride=snap.stride(0), snap_slice_pitch=snap.stride(1),
                          snap_rows=snap.shape[0], fine=fine.data_ptr(), fine_pitch=fine.stride(1),
                          macro=macro.data_ptr(), micro=micro.data_ptr(), micro_counts=micro_counts.data_ptr(),
                          fine_stats=fine_stats.data_ptr(), fine_counts=fine_counts.data_ptr(), raw=raw.data_ptr(),
                          cache=cache.data_ptr(), bad=bad.data_ptr(), coarse_status=coarse_status.data_ptr(),
                          match_status=match_status.data_ptr(), flags=flags.data_ptr())
+    if counter is not None:
+        io.counter_noise = 1
+        io.counter_key[0], io.counter_key[1] = counter.key[0], counter.key[1]
+        io.counter_kfield = counter.kfield
     _lib.call("mmpr_parareal_pipeline", ctypes.byref(model), ctypes.byref(ode), ctypes.byref(ode_model),
               ctypes.byref(integ), int(N), int(K),
               int(P), int(steps), float(dt), float(math.sqrt(dt)), 1 if reuse else 0, ctypes.byref(io),

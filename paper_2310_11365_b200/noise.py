@@ -18,6 +18,7 @@ DOMAIN_INIT = 0
 DOMAIN_STEP_FROZEN = 1
 DOMAIN_STEP_FRESH = 2
 DOMAIN_DERIVED = 3
+DOMAIN_COUNTER = 4  # key of the counter-based Philox mode (NoiseMode.PHILOX*)
 
 
 def entropy_words(entropy) -> np.ndarray:
@@ -124,4 +125,35 @@ def log1p_libm(x):
     x = torch.as_tensor(x, dtype=torch.float64, device=device()).contiguous()
     out = torch.empty_like(x)
     _lib.call("mmpr_log1p_libm", x.data_ptr(), out.data_ptr(), int(x.numel()), _lib.stream_handle())
+    return out
+
+
+def counter_key(seed: int) -> tuple[int, int]:
+    """Philox4x32-10 key of the counter-based mode:
+    SeedSequence((seed, 4)).generate_state(2, uint32)."""
+    w = np.random.SeedSequence((int(seed), DOMAIN_COUNTER)).generate_state(2, np.uint32)
+    return int(w[0]), int(w[1])
+
+
+def counter_noise(seed: int, fresh: bool, iteration: int = 0, slice_offset: int = 0) -> _lib.CounterNoise:
+    """mmpr_counter_noise of a plan: frozen (kfield 0) or fresh (iteration + 1)."""
+    c = _lib.CounterNoise()
+    c.key[0], c.key[1] = counter_key(seed)
+    c.kfield = (int(iteration) + 1) if fresh else 0
+    if c.kfield >= 1 << 24:
+        raise ValueError("iteration index too large for the counter layout")
+    c.slice_offset = int(slice_offset)
+    return c
+
+
+def counter_normals(seed: int, fresh: bool, slice_index: int, step_index: int, count: int, iteration: int = 0,
+                    rows: int = 1, first_particle: int = 0, stream=None):
+    """Device (rows, count) increments of particles first_particle.. at steps
+    step_index.. of slice slice_index in the counter-based mode."""
+    require_cuda()
+    c = counter_noise(seed, fresh, iteration)
+    out = torch.empty((rows, count), dtype=torch.float64, device=device())
+    import ctypes
+    _lib.call("mmpr_counter_normals_fill", ctypes.byref(c), int(slice_index), int(step_index), int(rows),
+              int(first_particle), int(count), out.data_ptr(), int(count), _lib.stream_handle(stream))
     return out

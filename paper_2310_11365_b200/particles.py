@@ -27,8 +27,16 @@ _DOMAIN_DERIVED = noise.DOMAIN_DERIVED
 
 
 class NoiseMode(enum.Enum):
+    """FROZEN / FRESH: the reference's numpy streams (particles.py:22-71),
+    reproduced bit for bit and materialised in HBM.  PHILOX / PHILOX_FRESH:
+    the north star's counter-based mode -- numpy's ziggurat over
+    Philox4x32-10 addressed by (particle, step, slice[, iteration]),
+    generated in registers by the fine kernels (counter_noise.cuh);
+    statistically equivalent to the reference's streams, not bitwise."""
     FROZEN = "frozen"
     FRESH = "fresh"
+    PHILOX = "philox"
+    PHILOX_FRESH = "philox-fresh"
 
 
 @dataclass(frozen=True)
@@ -47,9 +55,20 @@ class NoisePlan:
 
     @property
     def fresh(self) -> bool:
-        return self.mode is NoiseMode.FRESH
+        return self.mode in (NoiseMode.FRESH, NoiseMode.PHILOX_FRESH)
+
+    @property
+    def counter_based(self) -> bool:
+        """Increments generated in registers (no materialised stream)."""
+        return self.mode in (NoiseMode.PHILOX, NoiseMode.PHILOX_FRESH)
+
+    def counter_noise(self, iteration: int = 0, slice_offset: int = 0):
+        return noise.counter_noise(self.master_seed, self.fresh, iteration, slice_offset)
 
     def device_normals(self, slice_index: int, step_index: int, count: int, iteration: int = 0):
+        if self.counter_based:
+            return noise.counter_normals(self.master_seed, self.fresh, slice_index, step_index, count,
+                                         iteration)[0]
         return noise.normals(self.master_seed, self.fresh, slice_index, step_index, count, iteration)
 
     def normals(self, slice_index: int, step_index: int, count: int, iteration: int = 0) -> np.ndarray:
@@ -58,6 +77,14 @@ class NoisePlan:
 
     def slice_noise(self, n_offset: int, n_slices: int, steps: int, count: int, iteration: int = 0, out=None):
         """Device (n_slices, steps, pitch) increments of consecutive slices."""
+        if self.counter_based:
+            pitch = noise.row_pitch(count)
+            if out is None:
+                out = torch.empty((n_slices, steps, pitch), dtype=torch.float64, device=device())
+            for a in range(n_slices):
+                out[a, :, :count] = noise.counter_normals(self.master_seed, self.fresh, n_offset + a, 0, count,
+                                                          iteration, rows=steps)
+            return out
         return noise.slice_noise(self.master_seed, n_offset, n_slices, steps, count, iteration, self.fresh, out)
 
     def init_rng(self) -> np.random.Generator:
@@ -173,6 +200,14 @@ def propagate_fine(model: McKeanVlasovModel, ens: ParticleEnsemble, slice_index:
     increments instead of drawing the plan's addressed stream."""
     desc = device_model(model)
     P, S = ens.size, cfg.steps_per_slice
+    if increments is None and plan.counter_based:
+        out = torch.empty((1, P), dtype=torch.float64, device=device())
+        bad = torch.empty(1, dtype=torch.int32, device=device())
+        t0d = torch.tensor([float(t0)], dtype=torch.float64, device=device())
+        kernels.fine_sweep(desc, ens.device_positions.reshape(1, P), out, t0d, S, cfg.dt, None, bad,
+                           counter=plan.counter_noise(iteration, slice_index))
+        _blowup_check(bad, slice_index)
+        return ParticleEnsemble._wrap(out[0])
     if increments is None:
         xi = plan.slice_noise(slice_index, 1, S, P, iteration)
     else:
