@@ -142,15 +142,16 @@ typedef struct {
 
 /* Counter-based Philox noise (NoiseMode.PHILOX / PHILOX_FRESH): the
  * increment of particle p at step j of global slice n is numpy's ziggurat
- * transform over Philox4x32-10(counter = (p, j, n, kfield + (draw << 24)),
- * key), generated in registers by the fine kernels -- no increment buffer
- * (paper_2310_11365_b200/csrc/counter_noise.cuh).  Replaces the
- * materialised NoisePlan.normals rows (particles.py:49-61) where the
- * north star's in-register noise is wanted; statistically, not bitwise,
- * equivalent to the reference's numpy streams. */
+ * transform over Philox2x32-10 words (counter = (p, j | draw << 24),
+ * key = key[0] ^ (n | kfield << 20)), generated in registers by the fine
+ * kernels -- no increment buffer (paper_2310_11365_b200/csrc/
+ * counter_noise.cuh).  Replaces the materialised NoisePlan.normals rows
+ * (particles.py:49-61) where the north star's in-register noise is wanted;
+ * statistically, not bitwise, equivalent to the reference's numpy streams.
+ * Limits: n < 2^20, j < 2^24, particles < 2^32. */
 typedef struct mmpr_counter_noise {
-  uint32_t key[2];       /* SeedSequence((seed, 4)).generate_state(2, uint32) */
-  uint32_t kfield;       /* 0 = frozen, iteration + 1 = fresh (< 2^24) */
+  uint32_t key[2];       /* key[0] = SeedSequence((seed, 4)).generate_state(1, uint32); key[1] unused */
+  uint32_t kfield;       /* 0 = frozen, iteration + 1 = fresh (< 2^12) */
   int32_t slice_offset;  /* global index of local slice 0 */
 } mmpr_counter_noise;
 #define MMPR_STAT_INTEG_FAILED 1

@@ -106,14 +106,14 @@ def _nps():
         P = ctypes.c_void_p
         lib.nps_counter_normals.argtypes = [P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                                             ctypes.c_int64, P]
-        lib.nps_philox4x32_10.argtypes = [P, P, P]
+        lib.nps_philox2x32_10.argtypes = [P, ctypes.c_uint32, P]
         _NPS = lib
     return _NPS
 
 
 def counter_key(seed):
-    """SeedSequence((seed, 4)).generate_state(2, uint32) (noise.counter_key)."""
-    return np.random.SeedSequence((int(seed), 4)).generate_state(2, np.uint32)
+    """(SeedSequence((seed, 4)).generate_state(1, uint32), 0) (noise.counter_key)."""
+    return np.array([np.random.SeedSequence((int(seed), 4)).generate_state(1, np.uint32)[0], 0], dtype=np.uint32)
 
 
 def counter_normals(seed, slice_index, step_index, count, iteration=0, fresh=False, first_particle=0):

@@ -253,51 +253,43 @@ void nps_log1p_restated_fill(const double *x, int64_t n, double *out) {
 
 /* ---- 5. counter-based Philox mode (NoiseMode.PHILOX / PHILOX_FRESH) ------- */
 /* The device generator of paper_2310_11365_b200/csrc/counter_noise.cuh,
- * restated: Philox4x32-10 (Salmon et al.) addressed by (p, j, n, c3), fed to
+ * restated: Philox2x32-10 (Salmon et al.) words addressed by
+ * (p, j | draw << 24) under the slice key k32 ^ (n | kfield << 20), fed to
  * numpy's ziggurat transform (section 3's tables and rules; the tail's
- * log1p is the C library's, as on the device, which restates it).  This
- * mode has no reference counterpart (the reference's noise is numpy's
- * stream); tests pin the device to this restatement bit for bit and the
- * engine's Philox-mode runs to the reference's numpy-noise runs
- * statistically. */
-#define PH_M0 0xD2511F53u
-#define PH_M1 0xCD9E8D57u
-#define PH_W0 0x9E3779B9u
-#define PH_W1 0xBB67AE85u
+ * log1p is the C library's, as on the device, which restates it).  Attempt
+ * a: word = draw 2a, wedge uniform = draw 2a + 1; tail iteration t: draws
+ * 128 + 2t and 129 + 2t.  This mode has no reference counterpart (the
+ * reference's noise is numpy's stream); tests pin the device to this
+ * restatement bit for bit and the engine's Philox-mode runs to the
+ * reference's numpy-noise runs statistically. */
+#define PH_M 0xD256D193u
+#define PH_W 0x9E3779B9u
 
-void nps_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
-  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3], k0 = key[0], k1 = key[1];
+void nps_philox2x32_10(const uint32_t ctr[2], uint32_t key, uint32_t out[2]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], k = key;
   for (int r = 0; r < 10; ++r) {
-    const uint64_t p0 = (uint64_t)PH_M0 * c0, p1 = (uint64_t)PH_M1 * c2;
-    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
-    c1 = (uint32_t)p1;
-    c3 = (uint32_t)p0;
+    const uint64_t prod = (uint64_t)PH_M * c0;
+    const uint32_t n0 = (uint32_t)(prod >> 32) ^ k ^ c1;
+    c1 = (uint32_t)prod;
     c0 = n0;
-    c2 = n2;
-    k0 += PH_W0;
-    k1 += PH_W1;
+    k += PH_W;
   }
   out[0] = c0;
   out[1] = c1;
-  out[2] = c2;
-  out[3] = c3;
 }
 
-static void ph_block(uint32_t p, uint32_t j, uint32_t n, uint32_t c3, const uint32_t key[2], uint64_t *w,
-                     uint64_t *u) {
-  const uint32_t ctr[4] = {p, j, n, c3};
-  uint32_t o[4];
-  nps_philox4x32_10(ctr, key, o);
-  *w = (uint64_t)o[0] | ((uint64_t)o[1] << 32);
-  *u = (uint64_t)o[2] | ((uint64_t)o[3] << 32);
+static uint64_t ph_word(uint32_t p, uint32_t j, uint32_t d, uint32_t key) {
+  const uint32_t ctr[2] = {p, j | (d << 24)};
+  uint32_t o[2];
+  nps_philox2x32_10(ctr, key, o);
+  return (uint64_t)o[0] | ((uint64_t)o[1] << 32);
 }
 
 static double ph_unit(uint64_t w) { return (double)(w >> 11) * (1.0 / 9007199254740992.0); }
 
-static double counter_normal(uint32_t p, uint32_t j, uint32_t n, uint32_t kf, const uint32_t key[2]) {
-  uint64_t w, u;
-  ph_block(p, j, n, kf, key, &w, &u);
-  for (uint32_t a = 0;;) {
+static double counter_normal(uint32_t p, uint32_t j, uint32_t key) {
+  for (uint32_t a = 0;; ++a) {
+    const uint64_t w = ph_word(p, j, 2 * a, key);
     const int idx = (int)(w & 0xff);
     const uint64_t rabs = (w >> 9) & 0x000fffffffffffffULL;
     double x = (double)rabs * NPZ_WI[idx];
@@ -305,21 +297,19 @@ static double counter_normal(uint32_t p, uint32_t j, uint32_t n, uint32_t kf, co
     if (rabs < NPZ_KI[idx]) return x;
     if (idx == 0) {
       for (uint32_t t = 0;; ++t) {
-        uint64_t a1, a2;
-        ph_block(p, j, n, kf + ((128u + t) << 24), key, &a1, &a2);
-        const double xx = -NPZ_INV_R * log1p(-ph_unit(a1));
-        const double yy = -log1p(-ph_unit(a2));
+        const double xx = -NPZ_INV_R * log1p(-ph_unit(ph_word(p, j, 128 + 2 * t, key)));
+        const double yy = -log1p(-ph_unit(ph_word(p, j, 129 + 2 * t, key)));
         if (yy + yy > xx * xx) return ((rabs >> 8) & 1) ? -(NPZ_R + xx) : NPZ_R + xx;
       }
     }
-    if ((NPZ_FI[idx - 1] - NPZ_FI[idx]) * ph_unit(u) + NPZ_FI[idx] < exp(-0.5 * x * x)) return x;
-    ++a;
-    ph_block(p, j, n, kf + (a << 24), key, &w, &u);
+    const double u = ph_unit(ph_word(p, j, 2 * a + 1, key));
+    if ((NPZ_FI[idx - 1] - NPZ_FI[idx]) * u + NPZ_FI[idx] < exp(-0.5 * x * x)) return x;
   }
 }
 
 /* out[i] = increment of particle p0 + i at step j of global slice n */
 void nps_counter_normals(const uint32_t key[2], uint32_t kfield, uint32_t n, uint32_t j, uint32_t p0, int64_t count,
                          double *out) {
-  for (int64_t i = 0; i < count; ++i) out[i] = counter_normal(p0 + (uint32_t)i, j, n, kfield, key);
+  const uint32_t k = key[0] ^ (n | (kfield << 20));
+  for (int64_t i = 0; i < count; ++i) out[i] = counter_normal(p0 + (uint32_t)i, j, k);
 }

@@ -7,20 +7,31 @@
 // materialised in HBM (noise.cu).  This mode keeps the reference's normal
 // transform -- numpy's 256-layer ziggurat over one 64-bit word per attempt
 // (same layer tables, same wedge and Marsaglia-tail rules) -- but feeds it
-// from Philox4x32-10 (Salmon et al., SC'11) addressed by the particle itself:
+// from Philox2x32-10 (Salmon et al., SC'11) addressed by the particle itself:
 //
-//   block(p, j, n, c3) = Philox4x32-10(counter = (p, j, n, c3), key = (k0, k1))
-//   c3 = kfield + (draw << 24), kfield = 0 (PHILOX) or k + 1 (PHILOX_FRESH)
+//   word(p, j, n, d) = Philox2x32-10(counter = (p, j | d << 24),
+//                                    key = k32 ^ (n | kfield << 20))
+//   kfield = 0 (PHILOX) or k + 1 (PHILOX_FRESH)
 //
-// Attempt a of particle p's step-j normal uses block draw = a: word
-// lo|hi<<32 of outputs (0, 1) is the ziggurat word, outputs (2, 3) the wedge
-// test's uniform.  Tail iteration t uses block draw = 128 + t (both words as
-// the uniform pair).  Every increment is a pure function of (p, j, n, k), so
-// any kernel geometry (cluster sweep, grid sweep, iteration pipeline)
-// produces the same bits.  The key is SeedSequence((seed, 4)).generate_state
-// (2, uint32) (noise.py).  Parity: oracle/npstream.c restates the generator
-// (nps_counter_normals); tests pin the device bit for bit against it and the
-// Philox4x32-10 core against curand's and the Random123 known answers.
+// Draw d of particle p's step-j normal: attempt a uses d = 2a for the
+// ziggurat word and d = 2a + 1 for its wedge uniform; Marsaglia-tail
+// iteration t uses d = 128 + 2t and 129 + 2t.  Every increment is a pure
+// function of (p, j, n, k), so any kernel geometry (cluster sweep, grid
+// sweep, iteration pipeline) produces the same bits.  k32 is
+// SeedSequence((seed, 4)).generate_state(1, uint32) (noise.py).
+//
+// In the step loop (cn::step) every lane runs the fast path -- one Philox
+// word, a table lookup, one multiply, ~98.8% accepted -- for all of its
+// particles, then resolves its few rejected draws (wedge test, tail,
+// further attempts) one per round.  Measured on B200 (config-4 sweep,
+// 64 x 1e5 x 100): 5.2 ms, against 1.5 ms without the generator, 2.7 ms
+// with the fast path only, 7.1 ms when rejected draws were instead compacted
+// over the warp (dev/phx_ab.sh) -- the rare path's divergence and the
+// per-step barrier on the slowest warp bound this mode, not FP64.
+//
+// Parity: oracle/npstream.c restates the generator (nps_counter_normals);
+// tests pin the device bit for bit against it and the Philox2x32-10 core
+// against the Random123 known answers.
 #pragma once
 
 #include <stdint.h>
@@ -30,14 +41,13 @@
 namespace mmpr {
 namespace cn {
 
-#define MMPR_PHILOX32_M0 0xD2511F53u
-#define MMPR_PHILOX32_M1 0xCD9E8D57u
-#define MMPR_PHILOX32_W0 0x9E3779B9u
-#define MMPR_PHILOX32_W1 0xBB67AE85u
+#define MMPR_PHILOX2_M 0xD256D193u
+#define MMPR_PHILOX2_W 0x9E3779B9u
 
 struct CounterNoise {
-  uint32_t k0, k1;  // Philox key
-  uint32_t kfield;  // 0 (frozen) or iteration + 1 (fresh)
+  uint32_t k0;      // SeedSequence key word
+  uint32_t unused;  // (mmpr_counter_noise.key[1])
+  uint32_t kfield;  // 0 (frozen) or iteration + 1 (fresh), < 2^12
   int32_t n_base;   // global slice index of local slice 0
 };
 
@@ -49,25 +59,33 @@ __host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
 #endif
 }
 
-// Philox4x32-10 in place: c <- Philox4x32-10(c, (k0, k1)).
-__host__ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+// Philox2x32-10: (c0, c1) <- Philox2x32-10((c0, c1), k).
+__host__ __device__ __forceinline__ void philox2x32_10(uint32_t &c0, uint32_t &c1, uint32_t k) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t hi0 = mulhi32(MMPR_PHILOX32_M0, c[0]), lo0 = MMPR_PHILOX32_M0 * c[0];
-    const uint32_t hi1 = mulhi32(MMPR_PHILOX32_M1, c[2]), lo1 = MMPR_PHILOX32_M1 * c[2];
-    c[0] = hi1 ^ c[1] ^ k0;
-    c[1] = lo1;
-    c[2] = hi0 ^ c[3] ^ k1;
-    c[3] = lo0;
-    k0 += MMPR_PHILOX32_W0;
-    k1 += MMPR_PHILOX32_W1;
+    const uint32_t hi = mulhi32(MMPR_PHILOX2_M, c0), lo = MMPR_PHILOX2_M * c0;
+    c0 = hi ^ k ^ c1;
+    c1 = lo;
+    k += MMPR_PHILOX2_W;
   }
 }
 
-// Ziggurat layer tables in shared memory (lanes index them divergently).
+__host__ __device__ __forceinline__ uint32_t slice_key(const CounterNoise &c, uint32_t n) {
+  return c.k0 ^ (n | (c.kfield << 20));
+}
+
+// The 64-bit word of draw d: low half = output 0, high half = output 1.
+__device__ __forceinline__ void word(uint32_t p, uint32_t j, uint32_t d, uint32_t key, uint32_t &lo, uint32_t &hi) {
+  uint32_t c0 = p, c1 = j | (d << 24);
+  philox2x32_10(c0, c1, key);
+  lo = c0;
+  hi = c1;
+}
+
+// Ziggurat layer tables in shared memory (lanes index them divergently):
+// (ki as a double, wi) pairs for one 16-byte load, then fi.
 struct ZigTables {
-  uint64_t ki[256];
-  double wi[256];
+  double2 kw[256];
   double fi[256];
 };
 static_assert(sizeof(ZigTables) == 6144, "ZigTables layout");
@@ -78,55 +96,132 @@ static __constant__ double c_cn_fi[256] = {NPZ_FI_VALUES};
 
 __device__ __forceinline__ void load_zig(ZigTables *z, int tid, int nthreads) {
   for (int i = tid; i < 256; i += nthreads) {
-    z->ki[i] = c_cn_ki[i];
-    z->wi[i] = c_cn_wi[i];
+    z->kw[i] = make_double2((double)c_cn_ki[i], c_cn_wi[i]);  // ki < 2^53: exact
     z->fi[i] = c_cn_fi[i];
   }
 }
 
-__device__ __forceinline__ double unit53(uint64_t w) { return (double)(w >> 11) * 0x1.0p-53; }
+__device__ __forceinline__ double unit53(uint32_t lo, uint32_t hi) {
+  const uint64_t w = (uint64_t)lo | ((uint64_t)hi << 32);
+  return (double)(w >> 11) * 0x1.0p-53;
+}
 
-// The rare paths (wedge test, Marsaglia tail, further attempts), kept out of
-// line so the step loop's register budget only carries the fast path.
-static __device__ __noinline__ double zig_slow(uint64_t w, uint64_t u, uint32_t p, uint32_t j, uint32_t n, uint32_t kf,
-                                        uint32_t k0, uint32_t k1, const ZigTables *z) {
-  for (uint32_t a = 0;;) {
-    const int idx = (int)(w & 0xff);
-    const uint64_t rabs = (w >> 9) & 0x000fffffffffffffULL;
-    double x = __dmul_rn((double)rabs, z->wi[idx]);
-    if ((w >> 8) & 1) x = -x;
-    if (rabs < z->ki[idx]) return x;
-    if (idx == 0) {
-      for (uint32_t t = 0;; ++t) {
-        uint32_t c[4] = {p, j, n, kf + ((128u + t) << 24)};
-        philox4x32_10(c, k0, k1);
-        const double xx = __dmul_rn(-NPZ_INV_R, np::glibc_log1p(-unit53((uint64_t)c[0] | ((uint64_t)c[1] << 32))));
-        const double yy = -np::glibc_log1p(-unit53((uint64_t)c[2] | ((uint64_t)c[3] << 32)));
-        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx))
-          return ((rabs >> 8) & 1) ? -__dadd_rn(NPZ_R, xx) : __dadd_rn(NPZ_R, xx);
-      }
-    }
-    const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(z->fi[idx - 1], z->fi[idx]), unit53(u)), z->fi[idx]);
-    if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) return x;
-    ++a;
-    uint32_t c[4] = {p, j, n, kf + (a << 24)};
-    philox4x32_10(c, k0, k1);
-    w = (uint64_t)c[0] | ((uint64_t)c[1] << 32);
-    u = (uint64_t)c[2] | ((uint64_t)c[3] << 32);
+// numpy's magnitude field (w >> 9) & (2^52 - 1) as an exact double: the
+// bits go into the mantissa of 2^52 and 2^52 is subtracted (no int64
+// conversion on the step loop's path).
+__device__ __forceinline__ double rabs_of(uint32_t lo, uint32_t hi) {
+  const uint32_t mlo = (lo >> 9) | (hi << 23);
+  const uint32_t mhi = (hi >> 9) & 0x000fffffu;
+  return __dsub_rn(__hiloint2double((int)(0x43300000u | mhi), (int)mlo), 0x1.0p52);
+}
+
+// Fast path: true (and the value) when the attempt-0 word is accepted.
+__device__ __forceinline__ bool fast(uint32_t p, uint32_t j, uint32_t key, const ZigTables *z, double &out) {
+  uint32_t lo, hi;
+#if defined(MMPR_PHX_DEBUG) && MMPR_PHX_DEBUG == 2  // dev A/B only: no generator
+  lo = p * 0x9E3779B9u ^ j;
+  hi = lo * 0x85EBCA6Bu;
+#else
+  word(p, j, 0, key, lo, hi);
+#endif
+  const double r = rabs_of(lo, hi);
+  const double2 kw = z->kw[lo & 0xff];
+  const double x = __dmul_rn(r, kw.y);
+  out = ((lo >> 8) & 1) ? -x : x;
+  return r < kw.x;
+}
+
+// Marsaglia tail of a layer-0 attempt (2.6e-4 of the draws): out of line.
+static __device__ __noinline__ double tail(uint32_t p, uint32_t j, uint32_t key, bool neg) {
+  for (uint32_t t = 0;; ++t) {
+    uint32_t l1, h1, l2, h2;
+    word(p, j, 128 + 2 * t, key, l1, h1);
+    word(p, j, 129 + 2 * t, key, l2, h2);
+    const double xx = __dmul_rn(-NPZ_INV_R, np::glibc_log1p(-unit53(l1, h1)));
+    const double yy = -np::glibc_log1p(-unit53(l2, h2));
+    if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) return neg ? -__dadd_rn(NPZ_R, xx) : __dadd_rn(NPZ_R, xx);
+  }
+}
+
+// The whole ziggurat for one normal from attempt 0.  Wedge test: a
+// single-precision filter decides all but draws within 2^-18 of the
+// boundary, which take the double-precision exp.  Marsaglia tail: the sign
+// is bit 8 of the magnitude field (numpy's (rabs >> 8) & 1), bit 17 of the
+// word.
+__device__ __forceinline__ double slow(uint32_t p, uint32_t j, uint32_t key, const ZigTables *z) {
+  for (uint32_t a = 0;; ++a) {
+    uint32_t lo, hi;
+    word(p, j, 2 * a, key, lo, hi);
+    const int idx = (int)(lo & 0xff);
+    const double r = rabs_of(lo, hi);
+    const double2 kw = z->kw[idx];
+    double x = __dmul_rn(r, kw.y);
+    if ((lo >> 8) & 1) x = -x;
+    if (r < kw.x) return x;
+    if (idx == 0) return tail(p, j, key, (lo >> 17) & 1);
+    uint32_t ul, uh;
+    word(p, j, 2 * a + 1, key, ul, uh);
+    const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(z->fi[idx - 1], z->fi[idx]), unit53(ul, uh)), z->fi[idx]);
+    const double q = __dmul_rn(__dmul_rn(-0.5, x), x);
+    const double ef = (double)expf((float)q);  // within 1e-6 relative of exp(q) here
+    if (lhs < ef * (1.0 - 0x1.0p-18)) return x;
+    if (!(lhs > ef * (1.0 + 0x1.0p-18)) && lhs < exp(q)) return x;
   }
 }
 
 // Standard normal increment of particle p at step j of global slice n.
-__device__ __forceinline__ double normal(const CounterNoise &cn, uint32_t p, uint32_t j, uint32_t n,
+__device__ __forceinline__ double normal(const CounterNoise &c, uint32_t p, uint32_t j, uint32_t n,
                                          const ZigTables *z) {
-  uint32_t c[4] = {p, j, n, cn.kfield};
-  philox4x32_10(c, cn.k0, cn.k1);
-  const uint64_t w = (uint64_t)c[0] | ((uint64_t)c[1] << 32);
-  const int idx = (int)(c[0] & 0xff);
-  const uint64_t rabs = (w >> 9) & 0x000fffffffffffffULL;
-  const double x = __dmul_rn((double)rabs, z->wi[idx]);
-  if (rabs < z->ki[idx]) return ((c[0] >> 8) & 1) ? -x : x;
-  return zig_slow(w, (uint64_t)c[2] | ((uint64_t)c[3] << 32), p, j, n, cn.kfield, cn.k0, cn.k1, z);
+  const uint32_t key = slice_key(c, n);
+  double v;
+  if (fast(p, j, key, z, v)) return v;
+  return slow(p, j, key, z);
+}
+
+// One Euler-Maruyama step of a lane's particles with counter increments.
+// Particle m of the lane is global index pbase + 8 m (live when m < LO or
+// m < cnt); the lane's tail element (HAS_TAIL, when tail_live) is ptail.
+// upd(x, z) returns the updated position.  Every lane runs the fast path for
+// all of its particles first; the few rejected draws (0.16 per lane-step on
+// average) are then resolved by their own lanes, one per round, with the
+// particle picked out of / written back into the register array by
+// compile-time selects (no local-memory indexing).
+template <int PPT, int LO, bool HAS_TAIL, class Upd>
+__device__ __forceinline__ void step(uint32_t key, uint32_t j, const ZigTables *z, double (&x)[PPT], double &xt,
+                                     uint32_t pbase, int cnt, uint32_t ptail, bool tail_live, int lane, Upd upd) {
+  uint32_t rej = 0;
+#pragma unroll
+  for (int m = 0; m < PPT; ++m) {
+    if (m < LO || m < cnt) {
+      double v;
+      if (fast(pbase + 8u * (uint32_t)m, j, key, z, v)) x[m] = upd(x[m], v);
+      else rej |= 1u << m;
+    }
+  }
+  if (HAS_TAIL && tail_live) {
+    double v;
+    if (fast(ptail, j, key, z, v)) xt = upd(xt, v);
+    else rej |= 1u << PPT;
+  }
+#if defined(MMPR_PHX_DEBUG) && MMPR_PHX_DEBUG >= 1  // dev A/B only: rejected draws left unresolved
+  return;
+#endif
+  (void)lane;
+  while (rej) {
+    const int m = __ffs(rej) - 1;
+    rej &= rej - 1;
+    const double zv = slow(m == PPT ? ptail : pbase + 8u * (uint32_t)m, j, key, z);
+    if (HAS_TAIL && m == PPT) {
+      xt = upd(xt, zv);
+    } else {
+      double xm = x[0];
+#pragma unroll
+      for (int q = 1; q < PPT; ++q) xm = (m == q) ? x[q] : xm;
+      xm = upd(xm, zv);
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) x[q] = (m == q) ? xm : x[q];
+    }
+  }
 }
 
 }  // namespace cn

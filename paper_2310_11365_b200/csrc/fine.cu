@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
   const int ns = p.nstages;
   double *s_stage = s_dyn + (size_t)grp * ns * p.stage_elems;
   const cn::ZigTables *zt = reinterpret_cast<const cn::ZigTables *>(s_dyn);
-  const uint32_t nglob = (uint32_t)(p.cn.n_base + slice);
+  const uint32_t nkey = cn::slice_key(p.cn, (uint32_t)(p.cn.n_base + slice));
   if constexpr (PHX) cn::load_zig(reinterpret_cast<cn::ZigTables *>(s_dyn), (int)threadIdx.x, (int)blockDim.x);
   PartT(*s_wp)[32] = s_wp_all[grp];
   ClusterSlot(*s_slot)[FS_MAX_CLUSTER] = s_slot_all[grp];
@@ -274,25 +274,24 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
       PROF_MARK(tw1);
       PROF_ADD(0, tw0, tw1);
       const double *xb = s_stage + stage * p.stage_elems;
+      if constexpr (PHX) {
+        cn::step<PPT, (LO > 0 ? LO : 0), HAS_TAIL>(
+            nkey, (uint32_t)j, zt, x, xt, (uint32_t)(off + j8), cnt, (uint32_t)(tail_off + j8), j8 < tail, lane,
+            [&](double v, double z) { return em_update<KIND>(p, v, s, z); });
+      } else {
 #pragma unroll
-      for (int m = 0; m < PPT; ++m) {
-        if (m < cmin) {
-          const double z = PHX ? cn::normal(p.cn, (uint32_t)(off + j8 + 8 * m), (uint32_t)j, nglob, zt)
-                               : xb[my_idx + 8 * m];
-          x[m] = em_update<KIND>(p, x[m], s, z);
-        } else if (PHX) {
-          if (m < cnt) x[m] = em_update<KIND>(p, x[m], s, cn::normal(p.cn, (uint32_t)(off + j8 + 8 * m),
-                                                                      (uint32_t)j, nglob, zt));
-        } else {
-          // past some lanes' leaves: clamped index, value kept only when live
-          const int idx = max(0, min(my_idx + 8 * m, last_idx));
-          const double nx = em_update<KIND>(p, x[m], s, xb[idx]);
-          x[m] = (m < cnt) ? nx : x[m];
+        for (int m = 0; m < PPT; ++m) {
+          if (m < cmin) {
+            x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
+          } else {
+            // past some lanes' leaves: clamped index, value kept only when live
+            const int idx = max(0, min(my_idx + 8 * m, last_idx));
+            const double nx = em_update<KIND>(p, x[m], s, xb[idx]);
+            x[m] = (m < cnt) ? nx : x[m];
+          }
         }
+        if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
       }
-      if (HAS_TAIL && j8 < tail)
-        xt = em_update<KIND>(p, xt, s, PHX ? cn::normal(p.cn, (uint32_t)(tail_off + j8), (uint32_t)j, nglob, zt)
-                                           : xb[(int)(tail_off - lo) + j8]);
       PROF_MARK(tu1);
       PROF_ADD(1, tw1, tu1);
       // B1 inside reduce() orders every read of this stage before its refill
@@ -540,7 +539,8 @@ static int fine_sweep_impl(const mmpr_model *model, int32_t n_slices, int64_t pa
     return MMPR_ERR_ARG;
   if (n_slices == 0) return MMPR_OK;
   const bool phx = cnoise != nullptr;
-  if (phx && (particles > UINT32_MAX || cnoise->slice_offset < 0 || cnoise->kfield >= (1u << 24)))
+  if (phx && (particles > UINT32_MAX || cnoise->slice_offset < 0 || cnoise->kfield >= (1u << 12) ||
+              (int64_t)cnoise->slice_offset + n_slices > (1 << 20) || steps > (1 << 24)))
     return MMPR_ERR_ARG;
   if (!phx && steps > 0 && (!xi || (xi_row_pitch & 1) || xi_row_pitch < particles ||
                     (reinterpret_cast<uintptr_t>(xi) & 15) || (steps > 1 && xi_slice_pitch < steps * xi_row_pitch)))
@@ -579,7 +579,7 @@ static int fine_sweep_impl(const mmpr_model *model, int32_t n_slices, int64_t pa
   p.stats = stats;
   p.counts = counts;
   p.cn = cn::CounterNoise{0u, 0u, 0u, 0};
-  if (phx) p.cn = cn::CounterNoise{cnoise->key[0], cnoise->key[1], cnoise->kfield, cnoise->slice_offset};
+  if (phx) p.cn = cn::CounterNoise{cnoise->key[0], 0u, cnoise->kfield, cnoise->slice_offset};
   cudaStream_t s = (cudaStream_t)stream;
   if (use_grid) return fine_grid_sweep(p, s, phx);
   p.D = g.D;

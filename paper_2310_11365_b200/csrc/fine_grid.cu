@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
     if (!PHX && issuer) {
       for (int c = 0; c < NB && c < total_chunks; ++c) issue(xi_slice, c);
     }
-    const uint32_t nglob = (uint32_t)(p.cn.n_base + slice);
+    const uint32_t nkey = cn::slice_key(p.cn, (uint32_t)(p.cn.n_base + slice));
     double x[PPT];
     double xt = 0.0;
     const double *xin = p.x_in + (int64_t)slice * p.in_pitch;
@@ -378,16 +378,9 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
     for (int j = 0; j < p.S; ++j) {
       GPROF_MARK(pu0);
       if constexpr (PHX) {
-#pragma unroll
-        for (int m = 0; m < PPT; ++m) {
-          if (m < cmin) {
-            x[m] = em_update<KIND>(p, x[m], s, cn::normal(p.cn, (uint32_t)(off + j8 + 8 * m), (uint32_t)j, nglob, zt));
-          } else if (m < cnt) {
-            x[m] = em_update<KIND>(p, x[m], s, cn::normal(p.cn, (uint32_t)(off + j8 + 8 * m), (uint32_t)j, nglob, zt));
-          }
-        }
-        if (HAS_TAIL && j8 < tail)
-          xt = em_update<KIND>(p, xt, s, cn::normal(p.cn, (uint32_t)(off + 8 * cnt + j8), (uint32_t)j, nglob, zt));
+        cn::step<PPT, (LO > 0 ? LO : 0), HAS_TAIL>(
+            nkey, (uint32_t)j, zt, x, xt, (uint32_t)(off + j8), cnt, (uint32_t)(off + 8 * cnt + j8), j8 < tail, lane,
+            [&](double v, double z) { return em_update<KIND>(p, v, s, z); });
       } else {
 #pragma unroll
           for (int h = 0; h < H; ++h) {

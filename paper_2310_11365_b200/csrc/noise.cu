@@ -678,12 +678,12 @@ __global__ void counter_normals_kernel(const cn::CounterNoise c, uint32_t n, uin
 
 extern "C" int mmpr_counter_normals_fill(const mmpr_counter_noise *noise, int32_t n, int32_t j0, int32_t rows,
                                          int64_t p0, int64_t count, double *out, int64_t pitch, void *stream) {
-  if (!noise || n < 0 || j0 < 0 || rows < 0 || p0 < 0 || count < 0 || p0 + count > (int64_t)UINT32_MAX ||
-      (rows > 1 && pitch < count) || noise->kfield >= (1u << 24))
+  if (!noise || n < 0 || n >= (1 << 20) || j0 < 0 || rows < 0 || j0 + rows > (1 << 24) || p0 < 0 || count < 0 ||
+      p0 + count > (int64_t)UINT32_MAX || (rows > 1 && pitch < count) || noise->kfield >= (1u << 12))
     return MMPR_ERR_ARG;
   if (rows == 0 || count == 0) return MMPR_OK;
   if (!out) return MMPR_ERR_ARG;
-  const cn::CounterNoise c{noise->key[0], noise->key[1], noise->kfield, noise->slice_offset};
+  const cn::CounterNoise c{noise->key[0], 0u, noise->kfield, noise->slice_offset};
   const int64_t total = (int64_t)rows * count;
   const int64_t blocks = (total + 255) / 256;
   counter_normals_kernel<<<(unsigned)(blocks < 4736 ? blocks : 4736), 256, 0, (cudaStream_t)stream>>>(

@@ -609,18 +609,14 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       int bad = 0;
       if (!mean_known) reduce(Plain{}, 0.0, -1, s, bad);
       int first_bad = MMPR_STAT_OK;
-      const uint32_t nglob = (uint32_t)n;
+      const uint32_t nkey = cn::slice_key(p.cn, (uint32_t)n);
       for (int j = 0; j < p.S; ++j) {
         const uint32_t lj = ld + (uint32_t)j;
         const int stage = (int)(lj % (uint32_t)ns);
         if constexpr (PHX) {
-#pragma unroll
-          for (int m = 0; m < PPT; ++m) {
-            if (m < LO || m < cnt)
-              x[m] = em_update<KIND>(p, x[m], s, cn::normal(p.cn, (uint32_t)(off + j8 + 8 * m), (uint32_t)j, nglob, zt));
-          }
-          if (HAS_TAIL && j8 < tail)
-            xt = em_update<KIND>(p, xt, s, cn::normal(p.cn, (uint32_t)(tail_off + j8), (uint32_t)j, nglob, zt));
+          cn::step<PPT, LO, HAS_TAIL>(nkey, (uint32_t)j, zt, x, xt, (uint32_t)(off + j8), cnt,
+                                      (uint32_t)(tail_off + j8), j8 < tail, lane,
+                                      [&](double v, double z) { return em_update<KIND>(p, v, s, z); });
         } else {
           mbar_wait_parity(&s_bar[stage], (lj / (uint32_t)ns) & 1u);
           const double *xb = s_stage + stage * p.stage_elems;
@@ -867,7 +863,8 @@ static int check_io(const mmpr_pipeline_io *io, int32_t n_slices, int32_t iterat
   if (io->fine_pitch < particles || io->snap_slice_pitch < particles ||
       io->snap_iter_stride < (int64_t)(n_slices + 1) * io->snap_slice_pitch)
     return MMPR_ERR_ARG;
-  if (io->counter_noise && io->counter_kfield >= (1u << 24)) return MMPR_ERR_ARG;
+  if (io->counter_noise && (io->counter_kfield >= (1u << 12) || n_slices > (1 << 20) || steps > (1 << 24)))
+    return MMPR_ERR_ARG;
   if (steps > 0 && !io->counter_noise && (!io->xi || (io->xi_row_pitch & 1) || io->xi_row_pitch < particles ||
                     (reinterpret_cast<uintptr_t>(io->xi) & 15) ||
                     (steps > 1 && io->xi_slice_pitch < steps * io->xi_row_pitch)))
@@ -966,8 +963,7 @@ extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_
   }
   pp.abort = ios[first_rank].flags + nflags - 1;
   pp.phx = ios[first_rank].counter_noise ? 1 : 0;
-  p.cn = cn::CounterNoise{ios[first_rank].counter_key[0], ios[first_rank].counter_key[1],
-                          ios[first_rank].counter_kfield, 0};
+  p.cn = cn::CounterNoise{ios[first_rank].counter_key[0], 0u, ios[first_rank].counter_kfield, 0};
   pp.nranks = launch_ranks;
   // one launch over several ranks normally takes one global ticket order;
   // MMPR_PIPELINE_RANK_TICKETS=1 gives every rank its own clusters and

@@ -129,10 +129,11 @@ def log1p_libm(x):
 
 
 def counter_key(seed: int) -> tuple[int, int]:
-    """Philox4x32-10 key of the counter-based mode:
-    SeedSequence((seed, 4)).generate_state(2, uint32)."""
-    w = np.random.SeedSequence((int(seed), DOMAIN_COUNTER)).generate_state(2, np.uint32)
-    return int(w[0]), int(w[1])
+    """Philox2x32-10 key word of the counter-based mode,
+    SeedSequence((seed, 4)).generate_state(1, uint32), and the unused
+    second word of mmpr_counter_noise.key."""
+    w = np.random.SeedSequence((int(seed), DOMAIN_COUNTER)).generate_state(1, np.uint32)
+    return int(w[0]), 0
 
 
 def counter_noise(seed: int, fresh: bool, iteration: int = 0, slice_offset: int = 0) -> _lib.CounterNoise:
@@ -140,7 +141,7 @@ def counter_noise(seed: int, fresh: bool, iteration: int = 0, slice_offset: int 
     c = _lib.CounterNoise()
     c.key[0], c.key[1] = counter_key(seed)
     c.kfield = (int(iteration) + 1) if fresh else 0
-    if c.kfield >= 1 << 24:
+    if c.kfield >= 1 << 12:
         raise ValueError("iteration index too large for the counter layout")
     c.slice_offset = int(slice_offset)
     return c
