@@ -181,6 +181,14 @@ int mmpr_fine_sweep_counter(const mmpr_model *model, int32_t n_slices, int64_t p
 int mmpr_counter_normals_fill(const mmpr_counter_noise *noise, int32_t n, int32_t j0, int32_t rows,
                               int64_t p0, int64_t count, double *out, int64_t pitch, void *stream);
 
+/* The interaction statistic of the ROTATOR_SUM / EMPIRICAL_CDF kinds
+ * (models.ensemble_statistic, models.py:61-83): stat[2n], stat[2n+1] =
+ * (np.mean(sin x_n), np.mean(cos x_n)) in numpy's pairwise order, or
+ * stat[n*P + i] = (rank_i + 0.5) / P with ranks from a stable argsort.
+ * workspace = NULL queries *workspace_bytes. */
+int mmpr_ensemble_statistic(const mmpr_model *model, int32_t n_slices, int64_t particles, const double *x,
+                            int64_t pitch, double *stat, void *workspace, uint64_t *workspace_bytes, void *stream);
+
 /* Max concurrently resident clusters of the fine-sweep kernel for P
  * particles per slice (cudaOccupancyMaxActiveClusters). */
 int mmpr_fine_sweep_occupancy(int64_t particles, int32_t *clusters_out, int32_t *ctas_per_slice_out);

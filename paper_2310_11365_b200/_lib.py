@@ -132,6 +132,7 @@ SIGNATURES = {
                                                  _P, _I64, _I64, _P, _P, _P, _P]),
     "mmpr_fine_sweep_stepwise": (ctypes.c_int, [_P, _I32, _I64, _I32, _D, _D, _P, _I64, _P, _I64, _P, _I64,
                                                  _I64, _P, _P, _P, _P]),
+    "mmpr_ensemble_statistic": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _P, _P, _P, _P]),
     "mmpr_sort_rows": (ctypes.c_int, [_I32, _I64, _P, _P, _I64, _P, _P, _P]),
     "mmpr_mean_abs_diff": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I64, _P, _P]),
     "mmpr_histogram_sorted": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I32, _P, _P]),

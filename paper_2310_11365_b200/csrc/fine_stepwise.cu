@@ -284,3 +284,68 @@ extern "C" int mmpr_fine_sweep_stepwise(const mmpr_model *model, int32_t n_slice
   }
   return MMPR_OK;
 }
+
+// The interaction statistic alone (models.ensemble_statistic,
+// /root/reference/pkg/src/mcparareal/models.py:61-83) for the ROTATOR_SUM
+// and EMPIRICAL_CDF kinds: stat[2n..2n+1] = (np.mean(sin x), np.mean(cos x))
+// per slice, or stat[n*P + i] = (rank_i + 0.5) / P with a stable argsort.
+// Same kernels as the stepwise sweep; workspace queried with workspace = NULL.
+extern "C" int mmpr_ensemble_statistic(const mmpr_model *model, int32_t n_slices, int64_t particles,
+                                       const double *x, int64_t pitch, double *stat, void *workspace,
+                                       uint64_t *workspace_bytes, void *stream) {
+  if (!model || n_slices < 0 || particles < 1 || !workspace_bytes || (n_slices > 1 && pitch < particles))
+    return MMPR_ERR_ARG;
+  const bool rotator = model->stat_kind == MMPR_STAT_ROTATOR_SUM;
+  const bool burgers = model->stat_kind == MMPR_STAT_EMPIRICAL_CDF;
+  if (!rotator && !burgers) return MMPR_ERR_UNSUPPORTED;
+  const int64_t P = particles;
+  const int64_t items = (int64_t)n_slices * P;
+  if (burgers && items > INT32_MAX) return MMPR_ERR_UNSUPPORTED;
+  if (rotator) {
+    const int D = pw_depth(P);
+    if (D > 7 && ((int64_t(1) << D) / 128) > SW_MAX_CHUNKS) return MMPR_ERR_UNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t key_bytes = burgers ? align256((size_t)items * 8) : 0;
+  const size_t idx_bytes = burgers ? align256((size_t)items * 4) : 0;
+  size_t cub_bytes = 0;
+  cub::CountingInputIterator<int64_t> rows(0);
+  cub::TransformInputIterator<int64_t, DenseOffset, cub::CountingInputIterator<int64_t>> seg_begin(rows,
+                                                                                                 DenseOffset{P, 0});
+  cub::TransformInputIterator<int64_t, DenseOffset, cub::CountingInputIterator<int64_t>> seg_end(rows,
+                                                                                               DenseOffset{P, P});
+  if (burgers) {
+    cudaError_t err = cub::DeviceSegmentedSort::StableSortPairs(
+        (void *)nullptr, cub_bytes, (const double *)nullptr, (double *)nullptr, (const int32_t *)nullptr,
+        (int32_t *)nullptr, (int)items, n_slices, seg_begin, seg_end, st);
+    if (err != cudaSuccess) return mmpr_check(err, "ensemble_statistic: sort size query");
+  }
+  const size_t need = 2 * key_bytes + 2 * idx_bytes + align256(cub_bytes) + 256;
+  if (!workspace) {
+    *workspace_bytes = (uint64_t)need;
+    return MMPR_OK;
+  }
+  if (*workspace_bytes < need || !x || !stat) return MMPR_ERR_ARG;
+  if (n_slices == 0) return MMPR_OK;
+  if (rotator) {
+    rotator_stat_kernel<<<n_slices, SW_THREADS, 0, st>>>(P, x, n_slices > 1 ? pitch : P, stat);
+    return mmpr_check_launch("rotator_stat_kernel");
+  }
+  char *w = (char *)workspace;
+  double *keys_in = (double *)w;
+  double *keys_out = (double *)(w + key_bytes);
+  int32_t *idx_in = (int32_t *)(w + 2 * key_bytes);
+  int32_t *idx_out = (int32_t *)(w + 2 * key_bytes + idx_bytes);
+  void *cub_temp = (void *)(w + 2 * key_bytes + 2 * idx_bytes);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int eblocks = (int)std::min<int64_t>((items + 255) / 256, (int64_t)sms * 8);
+  rank_prep_kernel<<<eblocks, 256, 0, st>>>(n_slices, P, x, n_slices > 1 ? pitch : P, keys_in, idx_in);
+  size_t bytes = cub_bytes;
+  cudaError_t err = cub::DeviceSegmentedSort::StableSortPairs(cub_temp, bytes, keys_in, keys_out, idx_in, idx_out,
+                                                              (int)items, n_slices, seg_begin, seg_end, st);
+  if (err != cudaSuccess) return mmpr_check(err, "ensemble_statistic: sort");
+  rank_scatter_kernel<<<eblocks, 256, 0, st>>>(n_slices, P, idx_out, stat);
+  return mmpr_check_launch("rank_scatter_kernel");
+}

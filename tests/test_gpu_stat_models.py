@@ -95,3 +95,20 @@ def test_rotator_taylor_singularity(mm):
     st = mm.integrate_macro(mm.burgers_rhs(0.4), mm.MacroState((0.0,), (-0.1,), (1.0,)), 0.0, 0.5,
                             mm.EulerConfig(0.1))
     assert st.means[0] == pytest.approx(0.25)
+
+
+@pytest.mark.parametrize("P", [1, 2, 7, 1000, 4099, 100_000])
+def test_ensemble_statistic_device_kinds(mm, P):
+    """models.ensemble_statistic for ROTATOR_SUM / EMPIRICAL_CDF on the
+    device (mmpr_ensemble_statistic) against the oracle's numpy statement
+    (models.py:61-83): CDF ranks bitwise (ties by index), rotator means to
+    libm-ulp tolerance."""
+    rng = np.random.default_rng(P)
+    x = rng.uniform(0.0, 2.0 * math.pi, P)
+    x[: P // 3] = np.round(x[: P // 3], 1)  # ties
+    rot = mm.make_plane_rotator(mm.PlaneRotatorSpec(K=0.7, kBT=0.1))
+    got = mm.ensemble_statistic(rot, x)
+    want = O.statistic(O.model_rotator(0.7, 0.1), x)
+    assert abs(got[0] - want[0]) <= 1e-14 and abs(got[1] - want[1]) <= 1e-14
+    bur = mm.make_burgers(mm.BurgersSpec())
+    assert np.array_equal(mm.ensemble_statistic(bur, x), O.statistic(O.model_burgers(0.5), x))
