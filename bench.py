@@ -431,12 +431,78 @@ def our_arm(args):
         line["drivers"] = {d: {"ms_per_step": r[0], "value": psteps / (r[0] / 1e3), "gpu_launches": r[1]}
                            for d, r in drivers.items()}
         line["drivers_bitwise_equal"] = len(drivers) == 2
+    if G == 1 and not args.no_configs:
+        line["other_configs"] = other_configs(mm, torch)
     if G == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def other_configs(mm, torch, reps: int = 3) -> dict:
+    """The other BASELINE workloads on this GPU, graph-replayed, measured in
+    the same run (CUDA events around each full run_micro_macro; mean of
+    `reps` after one warm-up): configs 1, 2, 3, config 5 at one GPU's share
+    of its 8-GPU run (N = 32 of 256 slices, full P = 2^20, S = 200, K = 10),
+    and config 4 in the counter-based Philox noise mode."""
+    import math as _m
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    ou = mm.make_perturbed_ou(mm.PerturbedOUSpec(a=-1.0, a_E=0.5, B=0.5))
+    init1 = mm.InitialDistribution.normal(1.0, 0.01)
+    cub = mm.CubicMeanFieldSpec(1.0, 1.0, 1.0, 0.4)
+    mc = mm.make_cubic_meanfield(cub)
+    dw = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.5)
+    mdw = mm.make_double_well(dw)
+    part = dw.default_partition()
+    dw5 = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.3 * _m.sqrt(1.8))
+    m5 = mm.make_double_well_multiplicative(dw5, 0.3)
+    part5 = dw5.default_partition()
+    bim = mm.bimodal_initial(-1.0, 1.0, 0.2)
+
+    def cfg(N, K, T0, P, dt, S, euler, partition=mm.SINGLE_REGION):
+        return mm.PararealConfig(n_slices=N, iterations=K, slice_length=T0, particles=P, step=mm.StepConfig(dt, S),
+                                 partition=partition, integrator=mm.EulerConfig(euler), retain_snapshots=False)
+
+    cases = [
+        ("config1", "linear mean-field OU, N=10, P=1e4, S=100, K=5", cfg(10, 5, 0.1, 10_000, 1e-3, 100, 1e-2),
+         ou, mm.unimodal_rhs(ou), init1, mm.NoisePlan(0)),
+        ("config2", "cubic mean field, Gaussian closure, N=32, P=1e5, S=64, K=8",
+         cfg(32, 8, 0.0625, 100_000, 2.0 ** -10, 64, 2.0 ** -6), mc, mm.gaussian_closure_rhs(cub),
+         mm.InitialDistribution.normal(0.5, 0.04), mm.NoisePlan(0)),
+        ("config3", "bimodal double well, two regions, N=32, P=1e5, S=64, K=10",
+         cfg(32, 10, 0.0625, 100_000, 2.0 ** -10, 64, 2.0 ** -6, part), mdw,
+         mm.multimodal_rhs(mdw, part, dw.potential, dw.sigma), bim, mm.NoisePlan(0)),
+        ("config5_one_gpu_share", "multiplicative-noise double well, N=32 of 256, P=2^20, S=200, K=10",
+         cfg(32, 10, 0.1, 1 << 20, 5e-4, 200, 1e-2, part5), m5,
+         mm.multimodal_rhs(m5, part5, dw5.potential, dw5.sigma), bim, mm.NoisePlan(0)),
+        ("config4_philox_noise", "config 4 with NoiseMode.PHILOX (increments in registers)",
+         cfg(64, 5, 0.1, 100_000, 1e-3, 100, 1e-2), ou, mm.unimodal_rhs(ou), init1,
+         mm.NoisePlan(0, mm.NoiseMode.PHILOX)),
+    ]
+    out = {}
+    for name, desc, c, model, ode, init, plan in cases:
+        ens = mm.sample_initial(init, mm.NoisePlan(0), c.particles)
+        ms = timed(lambda: mm.run_micro_macro(model, ode, ens, c, plan))
+        ps = c.iterations * c.n_slices * c.particles * c.step.steps_per_slice
+        out[name] = {"workload": desc, "ms_per_run": round(ms, 4), "value": ps / (ms / 1e3), "unit": UNIT,
+                     "pipeline": bool(mm.engine.last_run_info.get("pipeline"))}
+        mm.engine.clear_graph_cache()
+        torch.cuda.empty_cache()
+    return out
 
 
 def relaunch(args) -> int:
@@ -459,6 +525,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the timings of the other BASELINE configs (one GPU)")
     ap.add_argument("--no-reference-loop", action="store_true",
                     help="reference arm: skip the one-off timing of the reference's own run_micro_macro")
     args = ap.parse_args()
