@@ -446,7 +446,7 @@ def other_configs(mm, torch, reps: int = 3) -> dict:
     the same run (CUDA events around each full run_micro_macro; mean of
     `reps` after one warm-up): configs 1, 2, 3, config 5 at one GPU's share
     of its 8-GPU run (N = 32 of 256 slices, full P = 2^20, S = 200, K = 10),
-    and config 4 in the counter-based Philox noise mode."""
+    and configs 4 and 5 in the counter-based Philox noise mode."""
     import math as _m
 
     def timed(fn):
@@ -492,6 +492,9 @@ def other_configs(mm, torch, reps: int = 3) -> dict:
         ("config4_philox_noise", "config 4 with NoiseMode.PHILOX (increments in registers)",
          cfg(64, 5, 0.1, 100_000, 1e-3, 100, 1e-2), ou, mm.unimodal_rhs(ou), init1,
          mm.NoisePlan(0, mm.NoiseMode.PHILOX)),
+        ("config5_one_gpu_share_philox_noise", "config 5's one-GPU share with NoiseMode.PHILOX (increments in registers)",
+         cfg(32, 10, 0.1, 1 << 20, 5e-4, 200, 1e-2, part5), m5,
+         mm.multimodal_rhs(m5, part5, dw5.potential, dw5.sigma), bim, mm.NoisePlan(0, mm.NoiseMode.PHILOX)),
     ]
     out = {}
     for name, desc, c, model, ode, init, plan in cases:

@@ -16,6 +16,8 @@ declare -A CASES=(
   [fine_grid]="tests/test_gpu_fine.py::test_grid_variant_bitwise_ou[1048576-32-1-2]"
   [regions]="tests/test_gpu_regions.py::test_match_restrict_regions_equals_separate_passes[5000-0]"
   [noise]="tests/test_gpu_noise.py::test_slice_noise_matches_numpy[100000]"
+  [philox_fine]="tests/test_gpu_philox.py::test_propagate_fine_counter_equals_oracle[ou-100000]"
+  [philox_run]="tests/test_gpu_philox.py::test_run_philox_equals_oracle_with_counter_noise[True]"
 )
 : > $O/summary.txt
 for tool in ${TOOLS:-memcheck racecheck synccheck}; do

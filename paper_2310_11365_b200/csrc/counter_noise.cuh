@@ -41,6 +41,16 @@
 namespace mmpr {
 namespace cn {
 
+// CTAs of 512 threads per SM the generate-ahead kernels are compiled for
+// (the register budget: 2 -> 64 registers per thread, 1 -> 128)
+#ifndef MMPR_PHX_MINB
+#define MMPR_PHX_MINB 2
+#endif
+// unroll factor of cn::gen's fast path over a lane's particles
+#ifndef MMPR_PHX_GEN_UNROLL
+#define MMPR_PHX_GEN_UNROLL 16
+#endif
+
 #define MMPR_PHILOX2_M 0xD256D193u
 #define MMPR_PHILOX2_W 0x9E3779B9u
 
@@ -148,10 +158,12 @@ static __device__ __noinline__ double tail(uint32_t p, uint32_t j, uint32_t key,
 // boundary, which take the double-precision exp.  Marsaglia tail: the sign
 // is bit 8 of the magnitude field (numpy's (rabs >> 8) & 1), bit 17 of the
 // word.
-__device__ __forceinline__ double slow(uint32_t p, uint32_t j, uint32_t key, const ZigTables *z) {
+// slow_from: attempt 0's word (lo, hi) is already known (the fast path made
+// it); later attempts make their own.
+__device__ __forceinline__ double slow_from(uint32_t p, uint32_t j, uint32_t key, const ZigTables *z, uint32_t lo,
+                                            uint32_t hi) {
   for (uint32_t a = 0;; ++a) {
-    uint32_t lo, hi;
-    word(p, j, 2 * a, key, lo, hi);
+    if (a > 0) word(p, j, 2 * a, key, lo, hi);
     const int idx = (int)(lo & 0xff);
     const double r = rabs_of(lo, hi);
     const double2 kw = z->kw[idx];
@@ -167,6 +179,12 @@ __device__ __forceinline__ double slow(uint32_t p, uint32_t j, uint32_t key, con
     if (lhs < ef * (1.0 - 0x1.0p-18)) return x;
     if (!(lhs > ef * (1.0 + 0x1.0p-18)) && lhs < exp(q)) return x;
   }
+}
+
+__device__ __forceinline__ double slow(uint32_t p, uint32_t j, uint32_t key, const ZigTables *z) {
+  uint32_t lo, hi;
+  word(p, j, 0, key, lo, hi);
+  return slow_from(p, j, key, z, lo, hi);
 }
 
 // Standard normal increment of particle p at step j of global slice n.
@@ -222,6 +240,61 @@ __device__ __forceinline__ void step(uint32_t key, uint32_t j, const ZigTables *
       for (int q = 0; q < PPT; ++q) x[q] = (m == q) ? xm : x[q];
     }
   }
+}
+
+// Step j's increments of a lane's particles, written to the lane's column of
+// a shared-memory buffer (element m at zb[m * stride], the tail element at
+// zb[PPT * stride]) one step AHEAD of their use: the kernels call this while
+// the previous step's cluster-wide mean is in flight, so the generator's
+// issue work (and the divergent resolution of rejected draws) fills the
+// latency of the per-step reduction instead of lengthening the step's
+// critical path.  A rejected draw's slot first holds its attempt-0 word,
+// which the resolution reuses.  Only the generating lane reads its column
+// (program order; no barrier).  Same values as step()/normal().
+constexpr int kGenUnroll = MMPR_PHX_GEN_UNROLL;
+
+template <int PPT, int LO, bool HAS_TAIL>
+__device__ __forceinline__ void gen(uint32_t key, uint32_t j, const ZigTables *z, double *zb, int stride,
+                                    uint32_t pbase, int cnt, uint32_t ptail, bool tail_live) {
+  uint32_t rej = 0;
+#pragma unroll kGenUnroll
+  for (int m = 0; m < PPT; ++m) {
+    if (m < LO || m < cnt) {
+      const uint32_t pm = pbase + 8u * (uint32_t)m;
+      uint32_t lo, hi;
+      word(pm, j, 0, key, lo, hi);
+      const double r = rabs_of(lo, hi);
+      const double2 kw = z->kw[lo & 0xff];
+      const double xv = __dmul_rn(r, kw.y);
+      const bool acc = r < kw.x;
+      zb[m * stride] = acc ? (((lo >> 8) & 1) ? -xv : xv) : __hiloint2double((int)hi, (int)lo);
+      rej |= acc ? 0u : (1u << m);
+    }
+  }
+  if (HAS_TAIL && tail_live) {
+    uint32_t lo, hi;
+    word(ptail, j, 0, key, lo, hi);
+    const double r = rabs_of(lo, hi);
+    const double2 kw = z->kw[lo & 0xff];
+    const double xv = __dmul_rn(r, kw.y);
+    const bool acc = r < kw.x;
+    zb[PPT * stride] = acc ? (((lo >> 8) & 1) ? -xv : xv) : __hiloint2double((int)hi, (int)lo);
+    rej |= acc ? 0u : (1u << PPT);
+  }
+  while (rej) {
+    const int m = __ffs(rej) - 1;
+    rej &= rej - 1;
+    const double w = zb[m * stride];
+    const uint32_t pm = (HAS_TAIL && m == PPT) ? ptail : pbase + 8u * (uint32_t)m;
+    zb[m * stride] = slow_from(pm, j, key, z, (uint32_t)__double2loint(w), (uint32_t)__double2hiint(w));
+  }
+}
+
+// dynamic shared memory of a generate-ahead kernel with T threads and PPT
+// accumulator elements per lane: the ziggurat tables, then the increment
+// columns
+__host__ __device__ constexpr size_t gen_smem_bytes(int ppt, int threads) {
+  return sizeof(ZigTables) + (size_t)(ppt + 1) * (size_t)threads * sizeof(double);
 }
 
 }  // namespace cn

@@ -64,7 +64,7 @@ __device__ __forceinline__ void group_sync(int grp, int nthreads) {
 // (counter_noise.cuh) instead of read from HBM; the dynamic shared memory
 // then holds the ziggurat tables and no copy pipeline runs.
 template <int KIND, int PPT, bool HAS_TAIL, bool PADDED, int MAXT, int GROUPS, int LO = -1, bool PHX = false>
-__global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const FineParams p) {
+__global__ void __launch_bounds__(MAXT, PHX ? (MMPR_PHX_MINB * 512 / MAXT > 0 ? MMPR_PHX_MINB * 512 / MAXT : 1) : 1024 / MAXT) fine_sweep_kernel(const FineParams p) {
   using PartT = Part<PADDED>;
   extern __shared__ __align__(128) double s_dyn[];  // [GROUPS][nstages][stage_elems]
   __shared__ PartT s_wp_all[GROUPS][2][32];
@@ -89,6 +89,9 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
   const cn::ZigTables *zt = reinterpret_cast<const cn::ZigTables *>(s_dyn);
   const uint32_t nkey = cn::slice_key(p.cn, (uint32_t)(p.cn.n_base + slice));
   if constexpr (PHX) cn::load_zig(reinterpret_cast<cn::ZigTables *>(s_dyn), (int)threadIdx.x, (int)blockDim.x);
+  // PHX: this thread's increment column, generated one step ahead (cn::gen)
+  double *zb = reinterpret_cast<double *>(reinterpret_cast<char *>(s_dyn) + sizeof(cn::ZigTables)) + threadIdx.x;
+  const int zstride = (int)blockDim.x;
   PartT(*s_wp)[32] = s_wp_all[grp];
   ClusterSlot(*s_slot)[FS_MAX_CLUSTER] = s_slot_all[grp];
   int *s_bad = s_bad_all[grp];
@@ -157,7 +160,14 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
   // by thread 0 after B1 of call r+1 (before it reaches B1 of r+2, after
   // which the slot's next writers run).  `refill` (>= 0) is the step whose
   // increments go into the stage this step just consumed.
-  auto reduce = [&](int r, int refill, double &mean_out, int &bad_out) {
+  // PHX: `gen_step` >= 0 generates that step's increments while the
+  // partials are in flight.
+  auto gen = [&](int jg) {
+    if constexpr (PHX)
+      cn::gen<PPT, (LO > 0 ? LO : 0), HAS_TAIL>(nkey, (uint32_t)jg, zt, zb, zstride, (uint32_t)(off + j8), cnt,
+                                                 (uint32_t)(tail_off + j8), j8 < tail);
+  };
+  auto reduce = [&](int r, int refill, double &mean_out, int &bad_out, int gen_step) {
     PROF_MARK(tr0);
     const int par = r & 1;
     const int bslot = r % 3;
@@ -239,6 +249,7 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
       }
       PROF_MARK(tc0);
       PROF_ADD(7, tb1, tc0);
+      if (PHX && gen_step >= 0) gen(gen_step);
       mbar_wait_parity(&s_red_bar[par], (uint32_t)((r >> 1) & 1));
       PROF_MARK(tc1);
       PROF_ADD(3, tc0, tc1);
@@ -255,6 +266,7 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
       bad = __any_sync(MMPR_FULL_MASK, b);
     } else {
       total = __shfl_sync(MMPR_FULL_MASK, v.v, 0);  // lanes >= nwarps folded empty slots
+      if (PHX && gen_step >= 0) gen(gen_step);
     }
     mean_out = div(total, (double)p.P);
     bad_out = bad;
@@ -266,7 +278,7 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
   int bad = 0;
   int first_bad = MMPR_STAT_OK;
   if (active) {
-    reduce(0, -1, s, bad);
+    reduce(0, -1, s, bad, p.S > 0 ? 0 : -1);
     for (int j = 0; j < p.S; ++j) {
       const int stage = j % ns;
       PROF_MARK(tw0);
@@ -275,9 +287,11 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
       PROF_ADD(0, tw0, tw1);
       const double *xb = s_stage + stage * p.stage_elems;
       if constexpr (PHX) {
-        cn::step<PPT, (LO > 0 ? LO : 0), HAS_TAIL>(
-            nkey, (uint32_t)j, zt, x, xt, (uint32_t)(off + j8), cnt, (uint32_t)(tail_off + j8), j8 < tail, lane,
-            [&](double v, double z) { return em_update<KIND>(p, v, s, z); });
+        // this step's increments were generated during the previous reduction
+#pragma unroll
+        for (int m = 0; m < PPT; ++m)
+          if (m < (LO > 0 ? LO : 0) || m < cnt) x[m] = em_update<KIND>(p, x[m], s, zb[m * zstride]);
+        if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, zb[PPT * zstride]);
       } else {
 #pragma unroll
         for (int m = 0; m < PPT; ++m) {
@@ -295,7 +309,7 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
       PROF_MARK(tu1);
       PROF_ADD(1, tw1, tu1);
       // B1 inside reduce() orders every read of this stage before its refill
-      reduce(j + 1, (!PHX && j + ns < p.S) ? j + ns : -1, s, bad);
+      reduce(j + 1, (!PHX && j + ns < p.S) ? j + ns : -1, s, bad, j + 1 < p.S ? j + 1 : -1);
       if (bad) {
         first_bad = j;
         break;
@@ -332,7 +346,7 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) fine_sweep_kernel(const Fin
       xt = mul(d, d);
     }
     int bad2 = 0;
-    reduce(p.S + 1, -1, var, bad2);
+    reduce(p.S + 1, -1, var, bad2, -1);
   }
 
   if (p.ctas > 1) cluster_sync_all();  // no peer may still be writing into this CTA
@@ -591,7 +605,7 @@ static int fine_sweep_impl(const mmpr_model *model, int32_t n_slices, int64_t pa
   p.l2_ahead = 3;
   if (const char *env = getenv("MMPR_FINE_L2_AHEAD")) p.l2_ahead = max(0, min(16, atoi(env)));
   if (phx) {
-    g.smem_bytes = MMPR_PHX_SMEM;
+    g.smem_bytes = cn::gen_smem_bytes(g.ppt <= 8 ? 8 : (g.ppt <= 13 ? 13 : 16), g.threads);
     p.nstages = 2;
     p.l2_ahead = 0;
   }

@@ -149,6 +149,9 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
 
   const cn::ZigTables *zt = reinterpret_cast<const cn::ZigTables *>(s_buf);
   if constexpr (PHX) cn::load_zig(reinterpret_cast<cn::ZigTables *>(s_buf), tid, (int)blockDim.x);
+  // PHX: this thread's increment column, generated one step ahead (cn::gen)
+  double *zb = reinterpret_cast<double *>(reinterpret_cast<char *>(s_buf) + sizeof(cn::ZigTables)) + tid;
+  const int zstride = (int)blockDim.x;
   if (tid == 0) {
     for (int q = 0; q < NB; ++q) mbar_init(&s_bar[q], 1);
     mbar_init(&s_red_bar[0], 1);
@@ -213,7 +216,15 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
     if (HAS_TAIL && j8 < tail) xt = xin[off + 8 * cnt + j8];
 
     // sum(x) in numpy's pairwise order + blow-up flag over the team
-    auto reduce = [&](int refill_step, double &mean_out, int &bad_out) {
+    // PHX: `gen_step` >= 0 generates that step's increments during the team
+    // exchange (warps 1.. right after B1, warp 0 between publishing its
+    // partial and polling for the team's)
+    auto gen = [&](int jg) {
+      if constexpr (PHX)
+        cn::gen<PPT, (LO > 0 ? LO : 0), HAS_TAIL>(nkey, (uint32_t)jg, zt, zb, zstride, (uint32_t)(off + j8), cnt,
+                                                   (uint32_t)(off + 8 * cnt + j8), j8 < tail);
+    };
+    auto reduce = [&](int refill_step, double &mean_out, int &bad_out, int gen_step) {
       double acc = x[0];
 #pragma unroll
       for (int m = 1; m < PPT; ++m) {
@@ -258,6 +269,7 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
         }
       }
       GridPart *parts = (epoch & 1) ? parts1 : parts0;
+      if (PHX && warp != 0 && gen_step >= 0) gen(gen_step);
       if (warp == 0) {
         PartT v = (lane < nwarps) ? s_wp[lane] : PartT::make(0.0, false);
 #pragma unroll
@@ -297,7 +309,6 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
           publisher = crank == 0;
         }
         if (lane == 0) {
-          const unsigned long long t0 = globaltimer();
           if (publisher) {  // level 2: one partial per cluster (per CTA without clusters) through L2
             int4 w;
             w.x = __double2loint(v.v);
@@ -310,6 +321,13 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
             GPROF_MARK(pp1);
             GPROF_ADD(2, pp0, pp1);
           }
+        }
+        if (PHX && gen_step >= 0) {
+          __syncwarp();
+          gen(gen_step);
+        }
+        if (lane == 0) {
+          const unsigned long long t0 = globaltimer();
           const unsigned int target = (epoch + 1) * (unsigned int)Cn;
           while (ld_acquire_gpu(counter) < target) {
             // a team member that never arrives (not co-resident) would hang
@@ -374,13 +392,15 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
     int bad = 0;
     int first_bad = MMPR_STAT_OK;
     int issued = PHX ? 0 : min(NB, total_chunks);
-    reduce(-1, s, bad);
+    reduce(-1, s, bad, p.S > 0 ? 0 : -1);
     for (int j = 0; j < p.S; ++j) {
       GPROF_MARK(pu0);
       if constexpr (PHX) {
-        cn::step<PPT, (LO > 0 ? LO : 0), HAS_TAIL>(
-            nkey, (uint32_t)j, zt, x, xt, (uint32_t)(off + j8), cnt, (uint32_t)(off + 8 * cnt + j8), j8 < tail, lane,
-            [&](double v, double z) { return em_update<KIND>(p, v, s, z); });
+        // this step's increments were generated during the previous exchange
+#pragma unroll
+        for (int m = 0; m < PPT; ++m)
+          if (m < (LO > 0 ? LO : 0) || m < cnt) x[m] = em_update<KIND>(p, x[m], s, zb[m * zstride]);
+        if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, zb[PPT * zstride]);
       } else {
 #pragma unroll
           for (int h = 0; h < H; ++h) {
@@ -405,7 +425,7 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
       }
       GPROF_MARK(pu1);
       GPROF_ADD(0, pu0, pu1);
-      reduce(j, s, bad);  // refills the buffers step j consumed
+      reduce(j, s, bad, j + 1 < p.S ? j + 1 : -1);  // refills the buffers step j consumed
       GPROF_MARK(pu2);
       GPROF_ADD(6, pu1, pu2);
       if (!PHX) issued = min(total_chunks, NB + (j + 1) * H);
@@ -444,7 +464,7 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
         xt = mul(d, d);
       }
       int bad2 = 0;
-      reduce(-1, var, bad2);
+      reduce(-1, var, bad2, -1);
     }
     if (tid == 0 && rank == 0) {
       p.bad_step[slice] = first_bad;
@@ -668,7 +688,7 @@ int fine_grid_sweep(FineParams p, cudaStream_t stream, bool phx) {
   int st = grid_geometry(p.P, p.n_slices, &g);
   if (st != MMPR_OK) return st;
   if (phx) {
-    g.smem = MMPR_PHX_SMEM;
+    g.smem = cn::gen_smem_bytes(16, g.threads);
     g.H = 1;
   }
   p.D = g.D;

@@ -261,7 +261,7 @@ __device__ __forceinline__ void pl_advance_chain(const PipeParams &pp, int k, in
 // (counter_noise.cuh) -- the dynamic shared memory holds the ziggurat tables
 // and the increment copies, their mbarriers and the L2 prefetch disappear.
 template <int KIND, int PPT, bool HAS_TAIL, int OK, int MK, bool MULTI, bool PHX = false>
-__global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
+__global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(const PipeParams pp) {
   constexpr int LO = PPT - 1;  // every leaf has PPT-1 or PPT accumulator elements per lane
   using PartT = Part<false>;
   const FineParams &p = pp.f;
@@ -307,6 +307,8 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
   const int ns = p.nstages;
   const cn::ZigTables *zt = reinterpret_cast<const cn::ZigTables *>(s_stage);
   if constexpr (PHX) cn::load_zig(reinterpret_cast<cn::ZigTables *>(s_stage), tid, gthreads);
+  // PHX: this thread's increment column, generated one step ahead (cn::gen)
+  double *zb = reinterpret_cast<double *>(reinterpret_cast<char *>(s_stage) + sizeof(cn::ZigTables)) + tid;
 
   if (tid == 0) {
     for (int q = 0; q < ns; ++q) mbar_init(&s_bar[q], 1);
@@ -327,7 +329,10 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
   // as fine.cu's reduce (B1, warp fold, one st.async per peer CTA).
   // `refill` >= 0: the unit's step whose increments go into the stage freed
   // by the step just taken.
-  auto reduce = [&](auto centered, double c, int refill, double &mean_out, int &bad_out) {
+  // PHX: `gen_step` >= 0 generates that step's increments of slice `gen_n`
+  // while the partials are in flight (cn::gen).
+  auto reduce = [&](auto centered, double c, int refill, double &mean_out, int &bad_out, int gen_step = -1,
+                    uint32_t gen_key = 0) {
     constexpr bool CEN = decltype(centered)::value;
     auto f = [&](double v) {
       if constexpr (CEN) {
@@ -402,6 +407,9 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
         st_async_v2(remote, __double_as_longlong(v.v),
                     (unsigned long long)1u | ((unsigned long long)(uint32_t)bad << 32), rbar);
       }
+      if (PHX && gen_step >= 0)
+        cn::gen<PPT, LO, HAS_TAIL>(gen_key, (uint32_t)gen_step, zt, zb, gthreads, (uint32_t)(off + j8), cnt,
+                                   (uint32_t)(tail_off + j8), j8 < tail);
       mbar_wait_parity(&s_red_bar[par], (r >> 1) & 1u);
       PartT cc = PartT::make(0.0, false);
       int b = 0;
@@ -416,6 +424,9 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       bad = __any_sync(MMPR_FULL_MASK, b);
     } else {
       total = __shfl_sync(MMPR_FULL_MASK, v.v, 0);
+      if (PHX && gen_step >= 0)
+        cn::gen<PPT, LO, HAS_TAIL>(gen_key, (uint32_t)gen_step, zt, zb, gthreads, (uint32_t)(off + j8), cnt,
+                                   (uint32_t)(tail_off + j8), j8 < tail);
     }
     mean_out = div(total, (double)p.P);
     bad_out = bad;
@@ -566,7 +577,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
       double var;
       int b0;
       reduce(Plain{}, 0.0, -1, s, b0);
-      reduce(Centered{}, s, -1, var, b0);
+      reduce(Centered{}, s, -1, var, b0, (PHX && has_fine && p.S > 0) ? 0 : -1, cn::slice_key(p.cn, (uint32_t)n));
       mean_known = true;
       if (rank == 0 && tid == 0) {
         double *mo = io.micro + ((int64_t)k * (N + 1) + n) * 3;
@@ -607,16 +618,18 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
     if (has_fine) {
       // ---- F(u^k_n): S Euler-Maruyama steps, particles in registers ------------
       int bad = 0;
-      if (!mean_known) reduce(Plain{}, 0.0, -1, s, bad);
-      int first_bad = MMPR_STAT_OK;
       const uint32_t nkey = cn::slice_key(p.cn, (uint32_t)n);
+      if (!mean_known) reduce(Plain{}, 0.0, -1, s, bad, (PHX && p.S > 0) ? 0 : -1, nkey);
+      int first_bad = MMPR_STAT_OK;
       for (int j = 0; j < p.S; ++j) {
         const uint32_t lj = ld + (uint32_t)j;
         const int stage = (int)(lj % (uint32_t)ns);
         if constexpr (PHX) {
-          cn::step<PPT, LO, HAS_TAIL>(nkey, (uint32_t)j, zt, x, xt, (uint32_t)(off + j8), cnt,
-                                      (uint32_t)(tail_off + j8), j8 < tail, lane,
-                                      [&](double v, double z) { return em_update<KIND>(p, v, s, z); });
+          // this step's increments were generated during the previous reduction
+#pragma unroll
+          for (int m = 0; m < PPT; ++m)
+            if (m < LO || m < cnt) x[m] = em_update<KIND>(p, x[m], s, zb[m * gthreads]);
+          if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, zb[PPT * gthreads]);
         } else {
           mbar_wait_parity(&s_bar[stage], (lj / (uint32_t)ns) & 1u);
           const double *xb = s_stage + stage * p.stage_elems;
@@ -634,7 +647,7 @@ __global__ void __launch_bounds__(512, 2) pipeline_kernel(const PipeParams pp) {
           }
           if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
         }
-        reduce(Plain{}, 0.0, (!PHX && j + ns < p.S) ? j + ns : -1, s, bad);
+        reduce(Plain{}, 0.0, (!PHX && j + ns < p.S) ? j + ns : -1, s, bad, (PHX && j + 1 < p.S) ? j + 1 : -1, nkey);
         if (bad) {
           first_bad = j;
           break;
@@ -795,7 +808,7 @@ template <int KIND, int OK, int MK>
 static int dispatch_pipe_tail(const PipeParams &pp, const PipeGeometry &g, cudaStream_t s) {
   if (pp.phx) {
     PipeGeometry gp = g;
-    gp.smem = MMPR_PHX_SMEM;
+    gp.smem = cn::gen_smem_bytes(13, g.threads);
     if (pp.G > 1) {
       if (g.tail) return launch_pipe<pipeline_kernel<KIND, 13, true, OK, MK, true, true>>(pp, gp, s);
       return launch_pipe<pipeline_kernel<KIND, 13, false, OK, MK, true, true>>(pp, gp, s);
