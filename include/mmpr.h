@@ -389,8 +389,8 @@ int mmpr_integrate_macro(const mmpr_moment_ode *ode, const mmpr_model *model,
 typedef struct mmpr_pipeline_io {
   const double *times;        /* [N+1] slice boundaries */
   const double *x0;           /* [P] ens0 */
-  const double *rho0;         /* [3] R(ens0) */
-  const int64_t *counts0;     /* [1] */
+  const double *rho0;         /* [3I] R(ens0) */
+  const int64_t *counts0;     /* [I] */
   const double *xi;           /* increments, slice n step j at xi + n*xi_slice_pitch + j*xi_row_pitch */
   int64_t xi_slice_pitch, xi_row_pitch;
   double *snap;               /* snapshot row k slice n at snap + k'*snap_iter_stride + n*snap_slice_pitch */
@@ -398,13 +398,13 @@ typedef struct mmpr_pipeline_io {
   int32_t snap_rows;          /* K+1 (k' = k) or 2 (k' = k % 2, retain_snapshots=False) */
   double *fine;               /* [2][N] rows of fine_pitch: F^k_n in row (k%2)*N + n */
   int64_t fine_pitch;
-  double *macro;              /* [K+1][N+1][3] */
-  double *micro;              /* [K+1][N+1][3] */
-  int64_t *micro_counts;      /* [K+1][N+1] */
-  double *fine_stats;         /* [K][N][3] */
-  int64_t *fine_counts;       /* [K][N] */
-  double *raw;                /* [K][N][3] */
-  double *cache;              /* [K+1][N][3] (row 0 from the prologue) */
+  double *macro;              /* [K+1][N+1][3I] (I regions: means, variances, fractions) */
+  double *micro;              /* [K+1][N+1][3I] */
+  int64_t *micro_counts;      /* [K+1][N+1][I] */
+  double *fine_stats;         /* [K][N][3I] */
+  int64_t *fine_counts;       /* [K][N][I] */
+  double *raw;                /* [K][N][3I] */
+  double *cache;              /* [K+1][N][3I] (row 0 from the prologue) */
   int32_t *bad;               /* [K][N] */
   int32_t *coarse_status;     /* [K+1][N] */
   int32_t *match_status;      /* [K+1][N] */
@@ -413,14 +413,20 @@ typedef struct mmpr_pipeline_io {
                                  mmpr_counter_noise), 0: from xi */
   uint32_t counter_key[2];
   uint32_t counter_kfield;    /* 0: frozen (the pipeline runs frozen noise only) */
+  /* two-region runs (ode->n_regions == 2, one rank; particles.region_statistics
+   * and the per-region coupling.match inside the units): */
+  mmpr_partition partition;   /* the run's partition (n_regions == ode->n_regions) */
+  double *region_scratch;     /* [region_scratch_rows][n_regions][P] compacted region members */
+  int64_t region_scratch_rows; /* persistent clusters the launch may use (>= 1) */
 } mmpr_pipeline_io;
 
 /* int32 scratch words the pipeline needs for (n_slices, iterations). */
 int64_t mmpr_pipeline_flags_size(int32_t n_slices, int32_t iterations);
 
 /* MMPR_OK when (model, ode, ode_model, integrator, particles) has a pipeline
- * instantiation (single region, MEAN_OF_F, forward-Euler coarse, the
- * 16 x 512-thread cluster geometry of P ~ 1e5); else MMPR_ERR_UNSUPPORTED
+ * instantiation (MEAN_OF_F, forward-Euler coarse, the 16 x 512-thread
+ * cluster geometry of P ~ 1e5; one region, or two regions for the double
+ * well with the multimodal closure on one rank); else MMPR_ERR_UNSUPPORTED
  * and the caller runs the per-iteration kernels. */
 int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_moment_ode *ode,
                             const mmpr_model *ode_model, const mmpr_integrator *integ,

@@ -88,7 +88,9 @@ class PipelineIO(ctypes.Structure):
                 ("fine_counts", ctypes.c_void_p), ("raw", ctypes.c_void_p), ("cache", ctypes.c_void_p),
                 ("bad", ctypes.c_void_p), ("coarse_status", ctypes.c_void_p), ("match_status", ctypes.c_void_p),
                 ("flags", ctypes.c_void_p), ("counter_noise", ctypes.c_int32),
-                ("counter_key", ctypes.c_uint32 * 2), ("counter_kfield", ctypes.c_uint32)]
+                ("counter_key", ctypes.c_uint32 * 2), ("counter_kfield", ctypes.c_uint32),
+                ("partition", Partition), ("region_scratch", ctypes.c_void_p),
+                ("region_scratch_rows", ctypes.c_int64)]
 
 
 class CounterNoise(ctypes.Structure):

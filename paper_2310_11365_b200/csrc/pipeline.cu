@@ -39,8 +39,24 @@
 #include "coarse_device.cuh"
 #include "fine_common.cuh"
 #include "mmpr_device.cuh"
+#include "regions_device.cuh"
 
 namespace mmpr {
+
+#ifdef MMPR_PIPE_PROFILE
+// dev builds only: per-CTA cycle totals of a unit's phases (thread 0)
+__device__ unsigned long long g_pipe_prof[1024][8];
+#define PPROF_START long long pprof_t = clock64()
+#define PPROF(k)                                                        \
+  if (threadIdx.x == 0) {                                               \
+    const long long pprof_now = clock64();                              \
+    g_pipe_prof[blockIdx.x & 1023][k] += (unsigned long long)(pprof_now - pprof_t); \
+    pprof_t = pprof_now;                                                \
+  }
+#else
+#define PPROF_START
+#define PPROF(k)
+#endif
 
 #define PL_MAX_RANKS 8
 
@@ -70,6 +86,9 @@ struct PipeParams {
   long long watchdog;  // pl_wait limit in cycles (see pl_wait)
   int *abort;          // this launch's abort word (last flag word of rank r0)
   int phx;             // increments from counter-based Philox (f.cn) instead of io.xi
+  mmpr_partition part;  // NR > 1: the regions
+  double *rg_scratch;   // NR > 1: [clusters][NR][P] compacted members of the unit's restrictions
+  int rg_rows;          // NR > 1: clusters the scratch holds (the launch uses at most this many)
 };
 
 __device__ __forceinline__ int pl_ld_acquire(const int *p, bool sys) {
@@ -169,49 +188,60 @@ __device__ __forceinline__ int pl_owner(const PipeParams &pp, int m) {
 // STORE: write macro[k][m], cache[k][m-1], raw[k-1][m-1],
 // coarse_status[k][m-1] and publish chain_done(k, m); the corrected state
 // also goes to s_chain for the calling CTA.
-template <int OK, int MK, bool STORE = true>
+template <int OK, int MK, int NR, bool STORE = true>
 __device__ __forceinline__ void pl_chain_step(const PipeParams &pp, const mmpr_pipeline_io &io,
                                               const mmpr_pipeline_io &iop, const PlFlags &fl, int k, int m,
                                               bool remote, double *s_out = nullptr) {
+  constexpr int NV = 3 * NR;  // means, variances, fractions per region
   const int N = pp.N;
-  const double *fs = iop.fine_stats + ((int64_t)(k - 1) * N + (m - 1)) * 3;
-  const double *cin = io.cache + ((int64_t)(k - 1) * N + (m - 1)) * 3;
-  double cur[3], f[3], c[3], pred[3], raw[3];
+  const double *fs = iop.fine_stats + ((int64_t)(k - 1) * N + (m - 1)) * NV;
+  const double *cin = io.cache + ((int64_t)(k - 1) * N + (m - 1)) * NV;
+  double cur[NV], f[NV], c[NV], pred[NV], raw[NV];
 #pragma unroll
-  for (int v = 0; v < 3; ++v) {
-    cur[v] = (m - 1 == 0) ? io.rho0[v] : pl_ld(iop.macro + ((int64_t)k * (N + 1) + (m - 1)) * 3 + v, remote);
+  for (int v = 0; v < NV; ++v) {
+    cur[v] = (m - 1 == 0) ? io.rho0[v] : pl_ld(iop.macro + ((int64_t)k * (N + 1) + (m - 1)) * NV + v, remote);
     f[v] = pl_ld(fs + v, remote);
     c[v] = __ldcg(cin + v);
   }
   int st = MMPR_STAT_OK;
   if (pp.reuse && m - 1 < k) {
 #pragma unroll
-    for (int v = 0; v < 3; ++v) pred[v] = c[v];
+    for (int v = 0; v < NV; ++v) pred[v] = c[v];
   } else {
 #pragma unroll
-    for (int v = 0; v < 3; ++v) pred[v] = cur[v];
+    for (int v = 0; v < NV; ++v) pred[v] = cur[v];
     long long steps;
     double h;
     const double t0 = __ldg(io.times + m - 1);
     euler_grid(pp.integ.dt, t0, __ldg(io.times + m), &steps, &h);
-    st = integrate_euler_n<3, OK, MK>(pp.ode, pp.ode_model, steps, h, t0, pred);
+    st = integrate_euler_n<NV, OK, MK>(pp.ode, pp.ode_model, steps, h, t0, pred);
   }
 #pragma unroll
-  for (int v = 0; v < 3; ++v) raw[v] = add(f[v], sub(pred[v], c[v]));
-  const bool neg = raw[1] < 0.0;
-  const double nxt[3] = {raw[0], (neg && raw[1] < 0.0) ? 0.0 : raw[1], f[2]};
+  for (int v = 0; v < NV; ++v) raw[v] = add(f[v], sub(pred[v], c[v]));
+  // variance clamp when any region's corrected variance is negative; the
+  // fractions stay the fine restriction's (engine.py:218-231)
+  bool neg = false;
+#pragma unroll
+  for (int i = 0; i < NR; ++i) neg |= raw[NR + i] < 0.0;
+  double nxt[NV];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    nxt[i] = raw[i];
+    nxt[NR + i] = (neg && raw[NR + i] < 0.0) ? 0.0 : raw[NR + i];
+    nxt[2 * NR + i] = f[2 * NR + i];
+  }
   if (s_out) {
 #pragma unroll
-    for (int v = 0; v < 3; ++v) s_out[v] = nxt[v];
+    for (int v = 0; v < NV; ++v) s_out[v] = nxt[v];
   }
   if (STORE) {
     const int64_t e = (int64_t)(k - 1) * N + (m - 1);
     io.coarse_status[(int64_t)k * N + (m - 1)] = st;
 #pragma unroll
-    for (int v = 0; v < 3; ++v) {
-      io.cache[((int64_t)k * N + (m - 1)) * 3 + v] = pred[v];
-      io.raw[e * 3 + v] = raw[v];
-      io.macro[((int64_t)k * (N + 1) + m) * 3 + v] = nxt[v];
+    for (int v = 0; v < NV; ++v) {
+      io.cache[((int64_t)k * N + (m - 1)) * NV + v] = pred[v];
+      io.raw[e * NV + v] = raw[v];
+      io.macro[((int64_t)k * (N + 1) + m) * NV + v] = nxt[v];
     }
     pl_publish_value(fl.chain_done(k, m), pp.epoch, pp.sys != 0);
   }
@@ -225,7 +255,7 @@ __device__ __forceinline__ void pl_chain_step(const PipeParams &pp, const mmpr_p
 // row is done instead of only when its last unit of the row starts.
 // Steps evaluated twice (by two units racing) are identical and publish the
 // same value.
-template <int OK, int MK>
+template <int OK, int MK, int NR>
 __device__ __forceinline__ void pl_advance_chain(const PipeParams &pp, int k, int r, int n_must) {
   const int N = pp.N, K = pp.K, ep = pp.epoch, cdone = pp.epoch * pp.f.ctas;
   const bool sys = pp.sys != 0;
@@ -250,7 +280,7 @@ __device__ __forceinline__ void pl_advance_chain(const PipeParams &pp, int k, in
       if (m - 1 >= 1) pl_wait(flm.chain_done(k, m - 1), ep, msys, pp.watchdog, pp.abort);
       if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, m), ep, false, pp.watchdog, pp.abort);
     }
-    pl_chain_step<OK, MK>(pp, io, iom, fl, k, m, rem);
+    pl_chain_step<OK, MK, NR>(pp, io, iom, fl, k, m, rem);
     atomicMax(fl.chain_front(k), ep * (N + 2) + m + 1);
   }
 }
@@ -260,9 +290,14 @@ __device__ __forceinline__ void pl_advance_chain(const PipeParams &pp, int k, in
 // PHX: every unit's increments come from counter-based Philox in registers
 // (counter_noise.cuh) -- the dynamic shared memory holds the ziggurat tables
 // and the increment copies, their mbarriers and the L2 prefetch disappear.
-template <int KIND, int PPT, bool HAS_TAIL, int OK, int MK, bool MULTI, bool PHX = false>
+// NR: regions of the partition (bimodal configs: 2) -- the match is per
+// region with membership from the pre-transform positions, and R(u^k_n) /
+// R(F^k_n) are region restrictions over compacted members (rg_restrict,
+// regions_device.cuh) instead of the single-region tree passes.
+template <int KIND, int PPT, bool HAS_TAIL, int OK, int MK, bool MULTI, bool PHX = false, int NR = 1>
 __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(const PipeParams pp) {
   constexpr int LO = PPT - 1;  // every leaf has PPT-1 or PPT accumulator elements per lane
+  constexpr int NV = 3 * NR;   // macro state: means, variances, fractions per region
   using PartT = Part<false>;
   const FineParams &p = pp.f;
   extern __shared__ __align__(128) double s_stage[];  // [nstages][stage_elems]
@@ -272,9 +307,14 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
   __shared__ __align__(8) uint64_t s_bar[FS_MAX_STAGES];
   __shared__ __align__(8) uint64_t s_red_bar[2];
   __shared__ int s_ticket[2];
-  __shared__ double s_match[3];  // mu, scale, mc
-  __shared__ double s_chain[3];  // this CTA's evaluation of the corrected state (one rank)
-  __shared__ int s_mode;
+  __shared__ double s_mu[NR], s_scale[NR], s_mc[NR];  // per-region match maps
+  __shared__ double s_chain[NV];  // this CTA's evaluation of the corrected state (one rank)
+  __shared__ int s_mode[NR];
+  __shared__ std::conditional_t<(NR > 1), RgSmem, char> s_rg;  // region restriction (NR > 1 only)
+  // the partition in shared memory: the out-of-line restriction takes it by
+  // reference, and a reference into the kernel parameters would make the
+  // compiler copy the whole parameter block into the stack frame
+  __shared__ std::conditional_t<(NR > 1), mmpr_partition, char> s_part;
   __shared__ const double *s_xi_base;  // this CTA's increments of the unit's slice, step 0
   __shared__ uint32_t s_stage_bytes;
 
@@ -310,6 +350,9 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
   // PHX: this thread's increment column, generated one step ahead (cn::gen)
   double *zb = reinterpret_cast<double *>(reinterpret_cast<char *>(s_stage) + sizeof(cn::ZigTables)) + tid;
 
+  if constexpr (NR > 1) {
+    if (tid == 0) s_part = pp.part;
+  }
   if (tid == 0) {
     for (int q = 0; q < ns; ++q) mbar_init(&s_bar[q], 1);
     mbar_init(&s_red_bar[0], 1);
@@ -494,6 +537,7 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
 
     double s = 0.0;
     bool mean_known = false;
+    PPROF_START;
     if (has_match) {
       // F^{k-1}_{n-1}, its restriction and macro[k][n-1] belong to the owner
       // of slice n-1 (another rank for the first slice of a rank)
@@ -506,6 +550,7 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
       // evaluates the serial correction
       if (tid == 0) pl_wait(flp.fine_done(k - 1, n - 1), cdone, rsys, pp.watchdog, pp.abort);
       __syncthreads();
+      PPROF(0);
       const double *src = iop.fine + ((int64_t)((k - 1) & 1) * N + (n - 1)) * iop.fine_pitch;
 #pragma unroll
       for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? pl_ld(src + off + j8 + 8 * m, remote) : 0.0;
@@ -515,54 +560,63 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
         if constexpr (MULTI) {
           // the chain of row k advances independently of unit order
           // (pl_advance_chain); other CTAs only wait for boundary n
-          if (rank == 0) pl_advance_chain<OK, MK>(pp, k, r, n);
+          if (rank == 0) pl_advance_chain<OK, MK, NR>(pp, k, r, n);
           else pl_wait(fl.chain_done(k, n), ep, false, pp.watchdog, pp.abort);
         } else {
           // one rank: the chain follows the ticket order; every CTA evaluates
           // the step (identically) and the first CTA publishes it
           if (n - 1 >= 1) pl_wait(flp.chain_done(k, n - 1), ep, rsys, pp.watchdog, pp.abort);
           if (k - 1 >= 1) pl_wait(fl.chain_done(k - 1, n), ep, false, pp.watchdog, pp.abort);
-          if (rank == 0) pl_chain_step<OK, MK>(pp, io, iop, fl, k, n, remote, s_chain);
-          else pl_chain_step<OK, MK, false>(pp, io, iop, fl, k, n, remote, s_chain);
+          if (rank == 0) pl_chain_step<OK, MK, NR>(pp, io, iop, fl, k, n, remote, s_chain);
+          else pl_chain_step<OK, MK, NR, false>(pp, io, iop, fl, k, n, remote, s_chain);
         }
         // row 0's reader of this snapshot slot (units (0, n < N) read it)
         if (!pp.retain && k == 2 && n < N) pl_wait(fl.consumed(0, n), cdone, false, pp.watchdog, pp.abort);
-        double nxt[3], f[3];
+        double nxt[NV], f[NV];
 #pragma unroll
-        for (int v = 0; v < 3; ++v) {
-          nxt[v] = MULTI ? __ldcg(io.macro + ((int64_t)k * (N + 1) + n) * 3 + v) : s_chain[v];
-          f[v] = pl_ld(iop.fine_stats + ((int64_t)(k - 1) * N + (n - 1)) * 3 + v, remote);
+        for (int v = 0; v < NV; ++v) {
+          nxt[v] = MULTI ? __ldcg(io.macro + ((int64_t)k * (N + 1) + n) * NV + v) : s_chain[v];
+          f[v] = pl_ld(iop.fine_stats + ((int64_t)(k - 1) * N + (n - 1)) * NV + v, remote);
         }
-        // match(corrected, F^{k-1}_{n-1}), raise policy (coupling.py:32-95)
-        const int64_t cn = pl_ld64(iop.fine_counts + (int64_t)(k - 1) * N + (n - 1), remote);
-        int mode = PL_KEEP, status = MMPR_STAT_OK;
-        double scale = 1.0, mc = 0.0, mu = 0.0;
-        if (cn != 0) {
-          mu = nxt[0];
-          double var_t = nxt[1];
-          if (var_t < 0.0) var_t = 0.0;
-          mc = f[0];
-          const double cur_var = f[1];
-          if (cur_var == 0.0) {
-            if (var_t > 0.0) status = 0;
-            mode = PL_SET;
-          } else {
-            scale = __dsqrt_rn(div(var_t, cur_var));
-            if (!(scale == 1.0 && mu == mc)) mode = PL_AFFINE;
+        // match(corrected, F^{k-1}_{n-1}), raise policy (coupling.py:32-95):
+        // per region an affine map onto the corrected moments; an empty
+        // region is skipped, the first degenerate one is the status
+        int status = MMPR_STAT_OK;
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          const int64_t cn = pl_ld64(iop.fine_counts + ((int64_t)(k - 1) * N + (n - 1)) * NR + q, remote);
+          int mode = PL_KEEP;
+          double scale = 1.0, mc = 0.0, mu = 0.0;
+          if (cn != 0) {
+            mu = nxt[q];
+            double var_t = nxt[NR + q];
+            if (var_t < 0.0) var_t = 0.0;
+            mc = f[q];
+            const double cur_var = f[NR + q];
+            if (cur_var == 0.0) {
+              if (var_t > 0.0 && status == MMPR_STAT_OK) status = q;
+              mode = PL_SET;
+            } else {
+              scale = __dsqrt_rn(div(var_t, cur_var));
+              if (!(scale == 1.0 && mu == mc)) mode = PL_AFFINE;
+            }
           }
+          s_mu[q] = mu;
+          s_scale[q] = scale;
+          s_mc[q] = mc;
+          s_mode[q] = mode;
         }
         if (rank == 0)
           io.match_status[(int64_t)k * N + (n - 1)] = *(volatile int *)pp.abort ? MMPR_STAT_WATCHDOG : status;
-        s_match[0] = mu;
-        s_match[1] = scale;
-        s_match[2] = mc;
-        s_mode = mode;
       }
       __syncthreads();
-      const double mu = s_match[0], scale = s_match[1], mc = s_match[2];
-      const int mode = s_mode;
+      // membership from the pre-transform position (coupling.py:54)
       auto apply = [&](double v) {
-        return mode == PL_SET ? mu : (mode == PL_AFFINE ? add(mul(scale, sub(v, mc)), mu) : v);
+        int q = 0;
+        if constexpr (NR > 1) q = rg_region<NR>(s_part, v);
+        const int mode = s_mode[q];
+        const double mu = s_mu[q];
+        return mode == PL_SET ? mu : (mode == PL_AFFINE ? add(mul(s_scale[q], sub(v, s_mc[q])), mu) : v);
       };
 #pragma unroll
       for (int m = 0; m < PPT; ++m) x[m] = apply(x[m]);
@@ -573,18 +627,32 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
       for (int m = 0; m < PPT; ++m)
         if (m < cnt) snap_kn[off + j8 + 8 * m] = x[m];
       if (HAS_TAIL && j8 < tail) snap_kn[tail_off + j8] = xt;
+      PPROF(1);
       // micro restriction R(u^k_n) from registers (np.mean, two-pass np.var)
-      double var;
-      int b0;
-      reduce(Plain{}, 0.0, -1, s, b0);
-      reduce(Centered{}, s, -1, var, b0, (PHX && has_fine && p.S > 0) ? 0 : -1, cn::slice_key(p.cn, (uint32_t)n));
-      mean_known = true;
-      if (rank == 0 && tid == 0) {
-        double *mo = io.micro + ((int64_t)k * (N + 1) + n) * 3;
-        mo[0] = s;
-        mo[1] = var;
-        mo[2] = div((double)p.P, (double)p.P);
-        io.micro_counts[(int64_t)k * (N + 1) + n] = p.P;
+      if constexpr (NR == 1) {
+        double var;
+        int b0;
+        reduce(Plain{}, 0.0, -1, s, b0);
+        reduce(Centered{}, s, -1, var, b0, (PHX && has_fine && p.S > 0) ? 0 : -1, cn::slice_key(p.cn, (uint32_t)n));
+        mean_known = true;
+        if (rank == 0 && tid == 0) {
+          double *mo = io.micro + ((int64_t)k * (N + 1) + n) * 3;
+          mo[0] = s;
+          mo[1] = var;
+          mo[2] = div((double)p.P, (double)p.P);
+          io.micro_counts[(int64_t)k * (N + 1) + n] = p.P;
+        }
+      } else {
+        const int64_t e = (int64_t)k * (N + 1) + n;
+        rg_restrict_reload<PPT, HAS_TAIL, NR>(s_rg, snap_kn, off, cnt, tail, p.ctas, rank, s_part, p.P,
+                                          pp.rg_scratch + (int64_t)(blockIdx.x / p.ctas) * NR * p.P,
+                                          io.micro + e * NV, io.micro_counts + e * NR);
+        // the particles again from the snapshot this thread just wrote: no
+        // value of x stays live across the call (which would keep the whole
+        // array in the stack frame through the step loop)
+#pragma unroll
+        for (int m = 0; m < PPT; ++m) x[m] = (m < cnt) ? snap_kn[off + j8 + 8 * m] : 0.0;
+        xt = (HAS_TAIL && j8 < tail) ? snap_kn[tail_off + j8] : 0.0;
       }
     } else if (k >= 1) {
       // n == 0: u^k_0 = ens0 (engine.py:208); boundary-0 rows of the trace
@@ -598,11 +666,12 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
       if (rank == 0 && tid == 0) {
         const int64_t e = (int64_t)k * (N + 1);
 #pragma unroll
-        for (int v = 0; v < 3; ++v) {
-          io.macro[e * 3 + v] = io.rho0[v];
-          io.micro[e * 3 + v] = io.rho0[v];
+        for (int v = 0; v < NV; ++v) {
+          io.macro[e * NV + v] = io.rho0[v];
+          io.micro[e * NV + v] = io.rho0[v];
         }
-        io.micro_counts[e] = io.counts0[0];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) io.micro_counts[e * NR + q] = io.counts0[q];
       }
     } else if (has_fine) {
       // row 0: the lifted ensembles written by the prologue
@@ -617,6 +686,7 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
 
     if (has_fine) {
       // ---- F(u^k_n): S Euler-Maruyama steps, particles in registers ------------
+      PPROF(2);
       int bad = 0;
       const uint32_t nkey = cn::slice_key(p.cn, (uint32_t)n);
       if (!mean_known) reduce(Plain{}, 0.0, -1, s, bad, (PHX && p.S > 0) ? 0 : -1, nkey);
@@ -675,6 +745,7 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
       const mmpr_pipeline_io &io = pp.io[r];
       const PlFlags fl{io.flags, N, K};
 
+      PPROF(3);
       // ---- write F^k_n into the parity buffer, restriction, publish -------------
       if (k >= 2) {
         // the reader of F^{k-2}_n (unit (k-1, n+1), owner of slice n+1) is done
@@ -689,13 +760,20 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
       double var = 0.0;
       const bool ok = first_bad == MMPR_STAT_OK;
       if (ok) {
-        int b2;
-        reduce(Centered{}, s, -1, var, b2);
+        if constexpr (NR == 1) {
+          int b2;
+          reduce(Centered{}, s, -1, var, b2);
+        } else {
+          const int64_t e = (int64_t)k * N + n;
+          rg_restrict_reload<PPT, HAS_TAIL, NR>(s_rg, xo, off, cnt, tail, p.ctas, rank, s_part, p.P,
+                                            pp.rg_scratch + (int64_t)(blockIdx.x / p.ctas) * NR * p.P,
+                                            io.fine_stats + e * NV, io.fine_counts + e * NR);
+        }
       }
       if (rank == 0 && tid == 0) {
         const int64_t e = (int64_t)k * N + n;
         io.bad[e] = *(volatile int *)pp.abort ? MMPR_STAT_WATCHDOG : first_bad;
-        if (ok) {
+        if (ok && NR == 1) {
           io.fine_stats[e * 3 + 0] = s;
           io.fine_stats[e * 3 + 1] = var;
           io.fine_stats[e * 3 + 2] = div((double)p.P, (double)p.P);
@@ -704,6 +782,12 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
       }
       __syncthreads();
       if (tid == 0) pl_publish(fl.fine_done(k, n), 1, sys);
+      PPROF(4);
+      if (threadIdx.x == 0) {
+#ifdef MMPR_PIPE_PROFILE
+        g_pipe_prof[blockIdx.x & 1023][5] += 1;
+#endif
+      }
     }
   }
 }
@@ -799,9 +883,18 @@ static int launch_pipe(const PipeParams &pp, const PipeGeometry &g, cudaStream_t
     if (v >= 1 && v < clusters) clusters = v;
   }
   if (clusters > pp.units) clusters = pp.units;
+  if (pp.rg_rows > 0 && clusters > pp.rg_rows) clusters = pp.rg_rows;
   cfg.gridDim = dim3((unsigned)(clusters * g.ctas), 1, 1);
   err = cudaLaunchKernelEx(&cfg, KERN, pp);
   return mmpr_check(err, "pipeline_kernel launch");
+}
+
+// two regions: one rank, numpy-stream or injected increments
+template <int KIND, int OK, int MK>
+static int dispatch_pipe_regions(const PipeParams &pp, const PipeGeometry &g, cudaStream_t s) {
+  if (pp.phx || pp.G > 1) return MMPR_ERR_UNSUPPORTED;
+  if (g.tail) return launch_pipe<pipeline_kernel<KIND, 13, true, OK, MK, false, false, 2>>(pp, g, s);
+  return launch_pipe<pipeline_kernel<KIND, 13, false, OK, MK, false, false, 2>>(pp, g, s);
 }
 
 template <int KIND, int OK, int MK>
@@ -825,11 +918,19 @@ static int dispatch_pipe_tail(const PipeParams &pp, const PipeGeometry &g, cudaS
 }
 
 // (fine model kind, ODE kind, ODE model kind) combinations with a pipeline
-// instantiation: the BASELINE unimodal configs and their close relatives.
+// instantiation: the BASELINE unimodal configs and their close relatives,
+// and config 3's bimodal double well with the two-region closure.
 static int dispatch_pipe(const mmpr_model &model, const mmpr_moment_ode &ode, const mmpr_model &ode_model,
                          const PipeParams *pp, const PipeGeometry &g, cudaStream_t s) {
   const int fk = model.kind, ok = ode.kind, mk = ode_model.kind;
   const bool run = pp != nullptr;
+  if (ode.n_regions == 2) {
+    if (fk == MMPR_MODEL_DOUBLE_WELL && ok == MMPR_ODE_MULTIMODAL && mk == MMPR_MODEL_DOUBLE_WELL)
+      return run ? dispatch_pipe_regions<MMPR_MODEL_DOUBLE_WELL, MMPR_ODE_MULTIMODAL, MMPR_MODEL_DOUBLE_WELL>(*pp, g, s)
+                 : MMPR_OK;
+    return MMPR_ERR_UNSUPPORTED;
+  }
+  if (ode.n_regions != 1) return MMPR_ERR_UNSUPPORTED;
   if (fk == MMPR_MODEL_OU && ok == MMPR_ODE_UNIMODAL && mk == MMPR_MODEL_OU)
     return run ? dispatch_pipe_tail<MMPR_MODEL_OU, MMPR_ODE_UNIMODAL, MMPR_MODEL_OU>(*pp, g, s) : MMPR_OK;
   if (fk == MMPR_MODEL_OU && ok == MMPR_ODE_PERTURBED_OU)
@@ -848,6 +949,28 @@ static int dispatch_pipe(const mmpr_model &model, const mmpr_moment_ode &ode, co
 
 using namespace mmpr;
 
+#ifdef MMPR_PIPE_PROFILE
+extern "C" int mmpr_dev_rg_prof(unsigned long long *host_out, int reset) {
+  cudaDeviceSynchronize();
+  if (host_out) cudaMemcpyFromSymbol(host_out, mmpr::g_rg_prof, sizeof(mmpr::g_rg_prof));
+  if (reset) {
+    static unsigned long long zeros[1024][8];
+    cudaMemcpyToSymbol(mmpr::g_rg_prof, zeros, sizeof(zeros));
+  }
+  return (int)cudaGetLastError();
+}
+
+extern "C" int mmpr_dev_pipe_prof(unsigned long long *host_out, int reset) {
+  cudaDeviceSynchronize();
+  if (host_out) cudaMemcpyFromSymbol(host_out, mmpr::g_pipe_prof, sizeof(mmpr::g_pipe_prof));
+  if (reset) {
+    static unsigned long long zeros[1024][8];
+    cudaMemcpyToSymbol(mmpr::g_pipe_prof, zeros, sizeof(zeros));
+  }
+  return (int)cudaGetLastError();
+}
+#endif
+
 extern "C" int64_t mmpr_pipeline_flags_size(int32_t n_slices, int32_t iterations) {
   if (n_slices < 1 || iterations < 0) return 0;
   const int64_t N = n_slices, K = iterations;
@@ -858,7 +981,7 @@ extern "C" int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_momen
                                        const mmpr_model *ode_model, const mmpr_integrator *integ,
                                        int64_t particles) {
   if (!model || !ode || !ode_model || !integ) return MMPR_ERR_ARG;
-  if (model->stat_kind != MMPR_STAT_MEAN_OF_F || ode->n_regions != 1) return MMPR_ERR_UNSUPPORTED;
+  if (model->stat_kind != MMPR_STAT_MEAN_OF_F || ode->n_regions < 1 || ode->n_regions > 2) return MMPR_ERR_UNSUPPORTED;
   if (integ->kind != MMPR_INTEG_EULER || !(integ->dt > 0.0)) return MMPR_ERR_UNSUPPORTED;
   PipeGeometry g;
   const int st = pipe_geometry(particles, &g);
@@ -934,6 +1057,7 @@ extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_
   p.bsd = 0.0;
   switch (model->kind) {
     case MMPR_MODEL_OU: p.bsd = model->p[2] * sqrt_dt; break;
+    case MMPR_MODEL_DOUBLE_WELL: p.bsd = model->p[4] * sqrt_dt; break;
     case MMPR_MODEL_CUBIC_MF: p.bsd = model->p[3] * sqrt_dt; break;
     default: break;
   }
@@ -978,6 +1102,16 @@ extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_
   pp.phx = ios[first_rank].counter_noise ? 1 : 0;
   p.cn = cn::CounterNoise{ios[first_rank].counter_key[0], 0u, ios[first_rank].counter_kfield, 0};
   pp.nranks = launch_ranks;
+  if (ode->n_regions > 1) {
+    // bimodal units restrict over compacted members in per-cluster scratch
+    const mmpr_pipeline_io &io = ios[first_rank];
+    if (n_ranks != 1 || io.partition.n_regions != ode->n_regions || !io.region_scratch ||
+        io.region_scratch_rows < 1)
+      return MMPR_ERR_ARG;
+    pp.part = io.partition;
+    pp.rg_scratch = io.region_scratch;
+    pp.rg_rows = (int)(io.region_scratch_rows < INT_MAX ? io.region_scratch_rows : INT_MAX);
+  }
   // one launch over several ranks normally takes one global ticket order;
   // MMPR_PIPELINE_RANK_TICKETS=1 gives every rank its own clusters and
   // ticket counter instead, the scheduling of one launch per GPU (the

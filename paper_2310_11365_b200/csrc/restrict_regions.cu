@@ -37,47 +37,25 @@
 #include "fine_common.cuh"
 #include "mmpr_device.cuh"
 #include "regions.cuh"
+#include "regions_device.cuh"
 
 namespace mmpr {
 
 enum { RG_KEEP = 0, RG_SET = 1, RG_AFFINE = 2 };
 
-__device__ __forceinline__ int rg_region(const mmpr_partition &part, double v) {
-  // searchsorted(seps, v, side="right"); NaN sorts last (state.py:73-78)
-  if (isnan(v)) return part.n_regions - 1;
-  int r = 0;
-#pragma unroll
-  for (int i = 0; i < MMPR_MAX_REGIONS - 1; ++i)
-    if (i < part.n_regions - 1 && part.seps[i] <= v) r = i + 1;
-  return r;
-}
-
-struct __align__(16) RgSlot {
-  double v;
-  int ok;
-  int pad;
-};
-
 template <int PPT, bool HAS_TAIL, bool MATCH>
 __global__ void __launch_bounds__(1024, 1) restrict_regions_kernel(const RegionsParams p) {
-  __shared__ PwVal s_wp[32];
-  __shared__ PwVal s_chunk[32];  // per-chunk CTA partials of a member tree deeper than the ensemble's
-  __shared__ __align__(16) RgSlot s_slot[FS_MAX_CLUSTER];
-  __shared__ long long s_ccnt[FS_MAX_CLUSTER][MMPR_MAX_REGIONS];  // CTA member counts, written by peers
-  __shared__ int s_wcnt[MMPR_MAX_REGIONS][32];                  // warp member counts -> exclusive offsets
-  __shared__ int64_t s_off[MMPR_MAX_REGIONS], s_n[MMPR_MAX_REGIONS];
-  __shared__ double s_mean;
+  __shared__ RgSmem s_rg;
   __shared__ int s_mode[MMPR_MAX_REGIONS];
   __shared__ double s_scale[MMPR_MAX_REGIONS], s_m[MMPR_MAX_REGIONS], s_mu[MMPR_MAX_REGIONS];
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = (int)blockDim.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = p.ctas > 1 ? (int)cluster_ctarank() : 0;
   const int e = (int)blockIdx.x / p.ctas;
   const int I = p.part.n_regions;
   const int64_t nslots = int64_t(1) << p.D;
   const int64_t slot = (int64_t)rank * p.slots_per_cta + warp * 4 + (lane >> 3);
   const int j8 = lane & 7;
-  const int gbase = lane & 24;  // first lane of my leaf's 8-lane group
   int64_t off = 0, len = 0;
   if (slot < nslots) pw_leaf(p.P, p.D, slot, &off, &len);
   const int cnt = (int)(len >> 3);
@@ -141,192 +119,8 @@ __global__ void __launch_bounds__(1024, 1) restrict_regions_kernel(const Regions
     if (HAS_TAIL && j8 < tail) xo[off + 8 * cnt + j8] = xt;
   }
 
-  // ---- compaction: index-order ranks of every region's members ---------------
-  // leaf element (m, j8) has index off + 8m + j8, the trailing ones follow
-  auto slot_bits = [&](bool pred) { return (__ballot_sync(MMPR_FULL_MASK, pred) >> gbase) & 0xffu; };
-  int slot_cnt[MMPR_MAX_REGIONS] = {0, 0, 0, 0};
-#pragma unroll
-  for (int q = 0; q < MMPR_MAX_REGIONS; ++q) {
-    if (q < I) {
-      int c = 0;
-#pragma unroll
-      for (int m = 0; m < PPT; ++m) c += __popc(slot_bits(m < cnt && rg_region(p.part, x[m]) == q));
-      if (HAS_TAIL) c += __popc(slot_bits(j8 < tail && rg_region(p.part, xt) == q));
-      slot_cnt[q] = c;
-    }
-  }
-  // exclusive prefix over the warp's four leaf groups, then over warps
-  int pre_slot[MMPR_MAX_REGIONS] = {0, 0, 0, 0};
-#pragma unroll
-  for (int q = 0; q < MMPR_MAX_REGIONS; ++q) {
-    if (q < I) {
-      const int c = slot_cnt[q];
-      const int c0 = __shfl_sync(MMPR_FULL_MASK, c, 0), c1 = __shfl_sync(MMPR_FULL_MASK, c, 8),
-                c2 = __shfl_sync(MMPR_FULL_MASK, c, 16), c3 = __shfl_sync(MMPR_FULL_MASK, c, 24);
-      const int g = lane >> 3;
-      pre_slot[q] = (g > 0 ? c0 : 0) + (g > 1 ? c1 : 0) + (g > 2 ? c2 : 0);
-      if (lane == 0) s_wcnt[q][warp] = c0 + c1 + c2 + c3;
-    }
-  }
-  __syncthreads();
-  if (warp == 0) {
-    for (int q = 0; q < I; ++q) {
-      const int v = lane < nwarps ? s_wcnt[q][lane] : 0;
-      int incl = v;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int u = __shfl_up_sync(MMPR_FULL_MASK, incl, d);
-        if (lane >= d) incl += u;
-      }
-      const int total = __shfl_sync(MMPR_FULL_MASK, incl, 31);
-      if (lane < nwarps) s_wcnt[q][lane] = incl - v;  // exclusive
-      // this CTA's total to every CTA of the cluster
-      if (p.ctas > 1) {
-        if (lane < p.ctas)
-          asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(mapa_shared(smem_addr(&s_ccnt[rank][q]), (uint32_t)lane)),
-                       "l"((long long)total)
-                       : "memory");
-      } else if (lane == 0) {
-        s_ccnt[0][q] = total;
-      }
-    }
-  }
-  if (p.ctas > 1) cluster_sync_all();
-  else __syncthreads();
-  if (tid < I) {
-    int64_t before = 0, all = 0;
-    for (int c = 0; c < p.ctas; ++c) {
-      const int64_t v = s_ccnt[c][tid];
-      if (c < rank) before += v;
-      all += v;
-    }
-    s_off[tid] = before;
-    s_n[tid] = all;
-  }
-  __syncthreads();
-  // scatter in index order
-  double *scr = p.scratch + (int64_t)e * I * p.P;
-#pragma unroll
-  for (int q = 0; q < MMPR_MAX_REGIONS; ++q) {
-    if (q < I) {
-      int64_t pos = s_off[q] + s_wcnt[q][warp] + pre_slot[q];
-      double *dst = scr + (int64_t)q * p.P;
-#pragma unroll
-      for (int m = 0; m < PPT; ++m) {
-        const bool mine = m < cnt && rg_region(p.part, x[m]) == q;
-        const unsigned bits = slot_bits(mine);
-        if (mine) dst[pos + __popc(bits & ((1u << j8) - 1u))] = x[m];
-        pos += __popc(bits);
-      }
-      if (HAS_TAIL) {
-        const bool mine = j8 < tail && rg_region(p.part, xt) == q;
-        const unsigned bits = slot_bits(mine);
-        if (mine) dst[pos + __popc(bits & ((1u << j8) - 1u))] = xt;
-      }
-    }
-  }
-  // every CTA's members visible to the cluster (global memory, cluster scope)
-  if (p.ctas > 1) cluster_sync_all();
-  else __syncthreads();
-
-  // ---- per region: pairwise tree over the n members, mean then variance -------
-  double *st = p.stats + (int64_t)e * 3 * I;
-  for (int q = 0; q < I; ++q) {
-    const int64_t n = s_n[q];
-    const double *a = scr + (int64_t)q * p.P;
-    double mean = 0.0, var = 0.0;
-    if (n >= 2) {
-      // The member tree can be deeper than the ensemble's (an unaligned n
-      // grows the right spine), so a CTA may own more slots than it has
-      // 8-lane groups: it walks them in power-of-two chunks of `cap` slots
-      // (consecutive subtrees) and folds the chunk partials as one more
-      // tree level.
-      const int Dq = pw_depth(n);
-      const int64_t nsq = int64_t(1) << Dq;
-      const int64_t spq = nsq >= p.ctas ? nsq / p.ctas : 1;
-      const int64_t cap = (int64_t)nwarps * 4;
-      const int64_t per = spq < cap ? spq : cap;
-      const int nchunks = (int)(spq / per);
-      const int64_t ls = warp * 4 + (lane >> 3);
-#pragma unroll 1
-      for (int pass = 0; pass < 2; ++pass) {
-        auto f = [&](double v) { return pass ? mul(sub(v, mean), sub(v, mean)) : v; };
-#pragma unroll 1
-        for (int ch = 0; ch < nchunks; ++ch) {
-          const bool valid = ls < per && (nsq >= p.ctas || rank < nsq);
-          const int64_t sq = nsq >= p.ctas ? rank * spq + (int64_t)ch * per + ls : rank;
-          int64_t qoff = 0, qlen = 0;
-          if (valid) pw_leaf(n, Dq, sq, &qoff, &qlen);
-          const int64_t qcnt = qlen >> 3;
-          double acc = 0.0;
-          if (qcnt > 0) {
-            acc = f(a[qoff + j8]);
-            for (int64_t k = 1; k < qcnt; ++k) acc = add(acc, f(a[qoff + j8 + 8 * k]));
-          }
-          acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 1));
-          acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 2));
-          acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 4));
-          if (qcnt == 0) acc = 0.0;
-          for (int64_t i = qcnt * 8; i < qlen; ++i) acc = add(acc, f(a[qoff + i]));
-          PwVal leaf;
-          leaf.v = acc;
-          leaf.ok = qlen > 0;
-          leaf = pw_xor_level(leaf, lane, 8);
-          leaf = pw_xor_level(leaf, lane, 16);
-          if (lane == 0) s_wp[warp] = leaf;
-          __syncthreads();
-          if (warp == 0) {
-            PwVal v = lane < nwarps ? s_wp[lane] : PwVal{0.0, 0};
-#pragma unroll
-            for (int k = 1; k < 32; k <<= 1)
-              if (k < nwarps) v = pw_xor_level(v, lane, k);
-            if (lane == 0) s_chunk[ch] = v;
-          }
-          __syncthreads();  // s_wp is rewritten by the next chunk
-        }
-        if (warp == 0) {
-          PwVal v = lane < nchunks ? s_chunk[lane] : PwVal{0.0, 0};
-#pragma unroll
-          for (int k = 1; k < 32; k <<= 1)
-            if (k < nchunks) v = pw_xor_level(v, lane, k);
-          v.v = __shfl_sync(MMPR_FULL_MASK, v.v, 0);  // every sending lane holds the CTA partial
-          v.ok = __shfl_sync(MMPR_FULL_MASK, v.ok, 0);
-          if (p.ctas > 1) {
-            if (lane < p.ctas)
-              st_cluster_v2(mapa_shared(smem_addr(&s_slot[rank]), (uint32_t)lane),
-                            (unsigned long long)__double_as_longlong(v.v), (unsigned long long)(uint32_t)v.ok);
-          } else if (lane == 0) {
-            s_slot[0].v = v.v;
-            s_slot[0].ok = v.ok;
-          }
-        }
-        if (p.ctas > 1) cluster_sync_all();
-        else __syncthreads();
-        if (warp == 0) {
-          PwVal c = lane < p.ctas ? PwVal{s_slot[lane].v, s_slot[lane].ok} : PwVal{0.0, 0};
-#pragma unroll
-          for (int k = 1; k < FS_MAX_CLUSTER; k <<= 1)
-            if (k < p.ctas) c = pw_xor_level(c, lane, k);
-          if (lane == 0) s_mean = div(c.v, (double)n);
-        }
-        // s_slot is rewritten by the next pass's peers only after they pass
-        // this barrier, which needs every CTA's fold above to be done
-        if (p.ctas > 1) cluster_sync_all();
-        else __syncthreads();
-        if (pass == 0) mean = s_mean;
-        else var = s_mean;
-      }
-    } else {  // empty: the region's center, 0; one member: x, 0 (particles.py:192-199)
-      mean = n == 0 ? p.part.centers[q] : a[0];
-      var = 0.0;
-    }
-    if (rank == 0 && tid == 0) {
-      st[q] = mean;
-      st[I + q] = var;
-      st[2 * I + q] = div((double)n, (double)p.P);
-      if (p.counts) p.counts[(int64_t)e * I + q] = n;
-    }
-  }
+  rg_restrict<PPT, HAS_TAIL>(s_rg, x, xt, cnt, tail, p.ctas, rank, p.part, p.P, p.scratch + (int64_t)e * I * p.P,
+                             p.stats + (int64_t)e * 3 * I, p.counts ? p.counts + (int64_t)e * I : nullptr, true);
 }
 
 // ---------------------------------------------------------------------------

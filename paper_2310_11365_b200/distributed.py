@@ -151,8 +151,9 @@ last_run_info: dict = {"pipeline": False}
 
 def _pipeline_sharded_ok(be, cfg: PararealConfig, plan: NoisePlan, comm) -> bool:
     """Every rank agrees to run the multi-GPU iteration pipeline: GPU
-    backend, an instantiated configuration, FROZEN noise, no Wasserstein
-    stop, N divisible by the world size, at most 8 ranks."""
+    backend, an instantiated single-region configuration (the two-region
+    units run on one rank only), FROZEN noise, no Wasserstein stop, N
+    divisible by the world size, at most 8 ranks."""
     if (not isinstance(be, GpuBackend) or os.environ.get("MMPR_PIPELINE", "1") == "0"
             or not hasattr(comm, "all_min_int")):
         return False
@@ -162,7 +163,7 @@ def _pipeline_sharded_ok(be, cfg: PararealConfig, plan: NoisePlan, comm) -> bool
         return False
     G = comm.world
     ok = (G <= 8 and cfg.n_slices % G == 0 and cfg.iterations >= 1 and not plan.fresh and not plan.counter_based
-          and cfg.stop_wasserstein_tol is None
+          and cfg.stop_wasserstein_tol is None and cfg.partition.n_regions == 1
           and kernels.pipeline_supported(be.model_d, be.ode_d, be.ode_model_d, be.integ_d, cfg.particles))
     return comm.all_min_int(1 if ok else 0) == 1
 

@@ -271,12 +271,18 @@ class _RunPlan:
         # Wasserstein stop criterion (a host decision after every iteration)
         # or per-iteration increment callables (allow_pipeline=False).
         self.prev_trace = None  # weakref to the last trace built on this plan's buffers
-        self.pipeline = (allow_pipeline and K >= 1 and self.fused_restrict and not plan.fresh and self.batch == N
+        # (two regions: the units restrict over compacted members themselves)
+        pipe_restrict = self.fused_restrict or (I == 2 and model_d.stat_kind == _lib.STAT_MEAN_OF_F)
+        self.pipeline = (allow_pipeline and K >= 1 and pipe_restrict and not plan.fresh and self.batch == N
                          and not host_snapshots and os.environ.get("MMPR_PIPELINE", "1") != "0"
                          and kernels.pipeline_supported(model_d, ode_d, ode_model_d, integ_d, P))
+        self.rg_scratch = None
         if self.pipeline:
             self.ws.fine = torch.empty((2, N, P), dtype=torch.float64, device=device())
             self.flags = torch.empty((kernels.pipeline_flags_size(N, K),), dtype=torch.int32, device=device())
+            if I > 1:
+                self.rg_scratch = torch.empty((kernels.PIPELINE_SCRATCH_ROWS, I, P), dtype=torch.float64,
+                                              device=device())
 
     def snap(self, k):
         return self.ws.snap[k if self.cfg.retain_snapshots else k % 2]
@@ -394,7 +400,8 @@ class _RunPlan:
                                   self.cfg.step.dt, self.S, self.reuse, self.times_d, ws.x0, ws.rho0, ws.counts0,
                                   ws.xi, ws.snap, ws.fine, ws.macro, ws.micro, ws.micro_counts, ws.fine_stats,
                                   ws.fine_counts, ws.raw, ws.cache, ws.bad, ws.coarse_status, ws.match_status,
-                                  self.flags, counter=self.plan.counter_noise(0) if self.counter else None)
+                                  self.flags, counter=self.plan.counter_noise(0) if self.counter else None,
+                                  partition=self.part_d if self.I > 1 else None, region_scratch=self.rg_scratch)
         timer.stop("iterations", ev)
 
     def stream_row(self, k):

@@ -236,6 +236,11 @@ def pipeline_supported(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.M
                                                ctypes.byref(integ), int(particles)) == 0
 
 
+# persistent clusters a multi-region pipeline launch may use (its scratch
+# rows): at least the co-resident 16-CTA clusters of a B200 (148 SMs x 2 / 16)
+PIPELINE_SCRATCH_ROWS = 24
+
+
 def pipeline_flags_size(n_slices: int, iterations: int) -> int:
     return int(_lib.load().mmpr_pipeline_flags_size(int(n_slices), int(iterations)))
 
@@ -244,16 +249,21 @@ def parareal_pipeline(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Mo
                       dt: float, steps: int,
                       reuse: bool, times, x0, rho0, counts0, xi, snap, fine, macro, micro, micro_counts,
                       fine_stats, fine_counts, raw, cache, bad, coarse_status, match_status, flags,
-                      stream=None, counter: _lib.CounterNoise | None = None) -> None:
+                      stream=None, counter: _lib.CounterNoise | None = None,
+                      partition: _lib.Partition | None = None, region_scratch=None) -> None:
     """Iterations 1..K of run_micro_macro in one launch (after the prologue).
 
-    snap: (K+1 or 2, N+1, P); fine: (2, N, P); macro/micro: (K+1, N+1, 3);
-    micro_counts (K+1, N+1, 1); fine_stats/raw: (K, N, 3); fine_counts
-    (K, N, 1); cache (K+1, N, 3); bad (K, N); coarse_status/match_status
-    (K+1, N) int32; flags: int32 scratch of pipeline_flags_size(N, K)."""
+    With I regions: snap: (K+1 or 2, N+1, P); fine: (2, N, P); macro/micro:
+    (K+1, N+1, 3I); micro_counts (K+1, N+1, I); fine_stats/raw: (K, N, 3I);
+    fine_counts (K, N, I); cache (K+1, N, 3I); bad (K, N);
+    coarse_status/match_status (K+1, N) int32; flags: int32 scratch of
+    pipeline_flags_size(N, K).  I > 1 also takes the partition and a float64
+    region_scratch of shape (rows, I, P), rows >= 1 (one per persistent
+    cluster the launch may use; pipeline_scratch_rows())."""
     require_cuda()
-    K1, N1, _ = macro.shape
+    K1, N1, NV = macro.shape
     K, N = K1 - 1, N1 - 1
+    I = NV // 3
     P = x0.shape[-1]
     _f64(snap, "snap")
     if snap.dim() != 3 or snap.shape[1:] != (N + 1, P) or snap.shape[0] not in (K + 1, 2) or snap.stride(2) != 1:
@@ -265,13 +275,13 @@ def parareal_pipeline(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Mo
         _f64(xi, "xi")
         if xi.dim() != 3 or xi.shape[0] < N or xi.shape[1] < steps or xi.stride(2) != 1:
             raise ValueError("xi must be (N, >=steps, pitch)")
-    for t, shape, dtype, name in ((macro, (K + 1, N + 1, 3), torch.float64, "macro"),
-                                  (micro, (K + 1, N + 1, 3), torch.float64, "micro"),
-                                  (micro_counts, (K + 1, N + 1, 1), torch.int64, "micro_counts"),
-                                  (fine_stats, (K, N, 3), torch.float64, "fine_stats"),
-                                  (fine_counts, (K, N, 1), torch.int64, "fine_counts"),
-                                  (raw, (K, N, 3), torch.float64, "raw"),
-                                  (cache, (K + 1, N, 3), torch.float64, "cache"),
+    for t, shape, dtype, name in ((macro, (K + 1, N + 1, 3 * I), torch.float64, "macro"),
+                                  (micro, (K + 1, N + 1, 3 * I), torch.float64, "micro"),
+                                  (micro_counts, (K + 1, N + 1, I), torch.int64, "micro_counts"),
+                                  (fine_stats, (K, N, 3 * I), torch.float64, "fine_stats"),
+                                  (fine_counts, (K, N, I), torch.int64, "fine_counts"),
+                                  (raw, (K, N, 3 * I), torch.float64, "raw"),
+                                  (cache, (K + 1, N, 3 * I), torch.float64, "cache"),
                                   (bad, (K, N), torch.int32, "bad"),
                                   (coarse_status, (K + 1, N), torch.int32, "coarse_status"),
                                   (match_status, (K + 1, N), torch.int32, "match_status")):
@@ -293,6 +303,15 @@ def parareal_pipeline(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Mo
         io.counter_noise = 1
         io.counter_key[0], io.counter_key[1] = counter.key[0], counter.key[1]
         io.counter_kfield = counter.kfield
+    if I > 1:
+        if partition is None or region_scratch is None:
+            raise ValueError("a multi-region pipeline needs the partition and region_scratch")
+        _f64(region_scratch, "region_scratch")
+        if region_scratch.dim() != 3 or region_scratch.shape[1:] != (I, P) or not region_scratch.is_contiguous():
+            raise ValueError("region_scratch must be contiguous (rows, I, P)")
+        io.partition = partition
+        io.region_scratch = region_scratch.data_ptr()
+        io.region_scratch_rows = region_scratch.shape[0]
     _lib.call("mmpr_parareal_pipeline", ctypes.byref(model), ctypes.byref(ode), ctypes.byref(ode_model),
               ctypes.byref(integ), int(N), int(K),
               int(P), int(steps), float(dt), float(math.sqrt(dt)), 1 if reuse else 0, ctypes.byref(io),

@@ -101,6 +101,70 @@ def test_pipeline_cubic_gaussian_closure(mm, monkeypatch):
     _same(a, b)
 
 
+def _bimodal_case(mm, N, K, S, P=100_000, retain=True, init=None):
+    """BASELINE config 3's model, partition and closure at reduced N / K / S."""
+    dw = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.5)
+    model = mm.make_double_well(dw)
+    part = dw.default_partition()
+    dt = 2.0 ** -10
+    cfg = mm.PararealConfig(n_slices=N, iterations=K, slice_length=S * dt, particles=P, step=mm.StepConfig(dt, S),
+                            partition=part, integrator=mm.EulerConfig(2.0 ** -6), retain_snapshots=retain)
+    ode = mm.multimodal_rhs(model, part, dw.potential, dw.sigma)
+    return model, ode, init or mm.bimodal_initial(-1.0, 1.0, 0.2), cfg
+
+
+@pytest.mark.parametrize("N,K,S,P,retain", [(8, 4, 16, 100_000, True), (20, 3, 8, 100_000, False),
+                                            (5, 5, 8, 98_307, True), (3, 1, 4, 106_496, True)])
+def test_pipeline_bimodal_equals_per_iteration_kernels(mm, monkeypatch, N, K, S, P, retain):
+    """Two regions (config 3): per-region match with pre-transform
+    membership and region restrictions over compacted members inside the
+    units -- every trace field bit for bit against the per-iteration
+    kernels (separate match + multi-kernel restriction)."""
+    model, ode, init, cfg = _bimodal_case(mm, N, K, S, P, retain)
+    plan = mm.NoisePlan(0)
+    a = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
+    b = _run(mm, monkeypatch, False, model, ode, init, cfg, plan)
+    _same(a, b)
+
+
+def test_pipeline_bimodal_degenerate_match_like_reference(mm, monkeypatch):
+    """An ensemble started right of the separatrix: the reference (the
+    oracle) raises DegenerateMatch for region 0 in this run; the pipeline's
+    per-region match raises the same error as the per-iteration kernels."""
+    model, ode, _, cfg = _bimodal_case(mm, 6, 3, 8)
+    init = mm.InitialDistribution.normal(1.0, 0.05)
+    plan = mm.NoisePlan(0)
+    with pytest.raises(mm.DegenerateMatch) as ea:
+        _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
+    with pytest.raises(mm.DegenerateMatch) as eb:
+        _run(mm, monkeypatch, False, model, ode, init, cfg, plan)
+    assert ea.value.region == eb.value.region == 0
+    assert str(ea.value) == str(eb.value)
+
+
+def test_pipeline_bimodal_matches_oracle(mm, monkeypatch):
+    """Against the numpy restatement: trajectories within 1e-12, moments
+    within 1e-10 (the double well's x**3 is numpy's vectorised pow)."""
+    N, K, S, P = 4, 3, 16, 100_000
+    model, ode, init, cfg = _bimodal_case(mm, N, K, S, P)
+    plan = mm.NoisePlan(0)
+    a = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
+    ens0 = mm.sample_initial(init, plan, P).positions.copy()
+    om = O.model_double_well(0.25, 0.4, 0.2, 0.0, 0.5)
+    dw = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.5)
+    part = dw.default_partition()
+    opart = O.Partition(tuple(part.separatrices), tuple(part.peaks))
+    oode = O.ode_multimodal(om, opart, dw.potential, dw.sigma)
+    ref = O.run_micro_macro(om, oode, ens0, N, K, S * 2.0 ** -10, 2.0 ** -10, S, 0, integ=O.Euler(2.0 ** -6),
+                            part=opart)
+    ref_snap = np.array([[e for e in row] for row in ref.snapshots])
+    dx = np.max(np.abs(a["snap"] - ref_snap)) / max(1.0, np.max(np.abs(ref_snap)))
+    dm = np.max(np.abs(a["macro"] - np.asarray(ref.macro))) / max(1.0, np.max(np.abs(ref.macro)))
+    du = np.max(np.abs(a["micro"] - np.asarray(ref.micro))) / max(1.0, np.max(np.abs(ref.micro)))
+    assert dx <= 1e-12, dx
+    assert dm <= 1e-10 and du <= 1e-10, (dm, du)
+
+
 def test_pipeline_without_converged_reuse_and_injected(mm, monkeypatch):
     model, ode, init, cfg = _ou_case(mm, 5, 3, 12)
     plan = mm.NoisePlan(0)

@@ -38,8 +38,9 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.Partition) == 8 + 8 * (_lib.MAX_REGIONS - 1) + 8 * _lib.MAX_REGIONS
     assert ctypes.sizeof(_lib.MomentOde) == 8 + 8 * _lib.MAX_ODE_PARAMS
     assert ctypes.sizeof(_lib.Integrator) == 8 + 4 * 8
-    # 21 pointers / int64 + snap_rows padded to 8, then counter_noise, counter_key[2], counter_kfield
-    assert ctypes.sizeof(_lib.PipelineIO) == 24 * 8 + 16
+    # 21 pointers / int64 + snap_rows padded to 8, then counter_noise, counter_key[2], counter_kfield,
+    # the partition, region_scratch, region_scratch_rows
+    assert ctypes.sizeof(_lib.PipelineIO) == 24 * 8 + 16 + ctypes.sizeof(_lib.Partition) + 16
     assert ctypes.sizeof(_lib.CounterNoise) == 16
 
 
@@ -62,7 +63,11 @@ def test_pipeline_support_query_without_a_gpu():
     dw = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.5)
     dwm = mm.make_double_well(dw)
     ode_m, odm_m = moments.device_ode(mm.multimodal_rhs(dwm, dw.default_partition(), dw.potential, dw.sigma))
-    assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 100_000)  # two regions
+    assert kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 100_000)  # two regions (config 3)
+    assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, dp54, 100_000)
+    three = mm.RegionPartition(separatrices=(-0.5, 0.5), peaks=(-1.0, 0.0, 1.0))
+    ode_3, odm_3 = moments.device_ode(mm.multimodal_rhs(dwm, three, dw.potential, dw.sigma))
+    assert not kernels.pipeline_supported(dwm.descriptor, ode_3, odm_3, euler, 100_000)  # three regions
     assert kernels.pipeline_flags_size(64, 5) == 1 + 5 * 64 + 2 * 6 * 65 + 6 + 1  # ..., abort word
     lib = _lib.load()
     assert lib.mmpr_pipeline_supported(None, None, None, None, 100_000) == 1
