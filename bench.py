@@ -369,7 +369,7 @@ def our_arm(args):
     stage_ms = {}
     for _ in range(2):
         tr_t = run(ens0_dev, timings=True)
-        for key, vals in tr_t.timings.items():
+        for key, vals in tr_t.stage_timings.items():
             if isinstance(vals, list):
                 stage_ms.setdefault(key, []).extend(1e3 * v for v in vals)
     fine_ms = stage_ms.get("fine", [])

@@ -15,6 +15,6 @@ init = mm.bimodal_initial(-1.0, 1.0, 0.2)
 plan = mm.NoisePlan(0)
 for _ in range(2):
     tr = mm.run_micro_macro(model, ode, init, cfg, plan, record_timings=True)
-t = {k: round(1e3 * sum(v), 3) for k, v in tr.timings.items() if isinstance(v, list) and v}
-n = {k: len(v) for k, v in tr.timings.items() if isinstance(v, list) and v}
+t = {k: round(1e3 * sum(v), 3) for k, v in tr.stage_timings.items() if isinstance(v, list) and v}
+n = {k: len(v) for k, v in tr.stage_timings.items() if isinstance(v, list) and v}
 print(t, n, round(sum(t.values()), 3))

@@ -24,4 +24,4 @@ print(f"config3 {os.environ.get('TAG', '')}: {e0.elapsed_time(e1) / 5:.3f} ms pe
 if os.environ.get("STAGES"):
     mm.engine.clear_graph_cache()
     tr = mm.run_micro_macro(mdw, ode, ens, c, mm.NoisePlan(0), record_timings=True)
-    print({k: round(sum(v) * 1e3, 3) for k, v in tr.timings.items()})
+    print({k: round(sum(v) * 1e3, 3) for k, v in tr.stage_timings.items()})

@@ -418,10 +418,20 @@ typedef struct mmpr_pipeline_io {
   mmpr_partition partition;   /* the run's partition (n_regions == ode->n_regions) */
   double *region_scratch;     /* [region_scratch_rows][n_regions][P] compacted region members */
   int64_t region_scratch_rows; /* persistent clusters the launch may use (>= 1) */
+  int64_t *fine_times;        /* optional [K][N][2]: globaltimer ns at the start and end of each
+                                 unit's fine propagation (NULL: not recorded) */
 } mmpr_pipeline_io;
 
 /* int32 scratch words the pipeline needs for (n_slices, iterations). */
 int64_t mmpr_pipeline_flags_size(int32_t n_slices, int32_t iterations);
+
+/* Per-slice timestamps of the next fine sweeps (mmpr_fine_sweep,
+ * mmpr_fine_sweep_restrict, mmpr_fine_sweep_counter) launched from the
+ * calling host thread: globaltimer ns at the start and the end of slice s's
+ * propagation go to slice_times[2s], slice_times[2s+1] (the reference's
+ * per-slice fine timings, engine.py:110-124 / :204).  NULL stops recording.
+ * The pointer is bound when a launch is issued (a captured graph keeps it). */
+int mmpr_set_fine_times(int64_t *slice_times);
 
 /* MMPR_OK when (model, ode, ode_model, integrator, particles) has a pipeline
  * instantiation (MEAN_OF_F, forward-Euler coarse, the 16 x 512-thread

@@ -90,7 +90,7 @@ class PipelineIO(ctypes.Structure):
                 ("flags", ctypes.c_void_p), ("counter_noise", ctypes.c_int32),
                 ("counter_key", ctypes.c_uint32 * 2), ("counter_kfield", ctypes.c_uint32),
                 ("partition", Partition), ("region_scratch", ctypes.c_void_p),
-                ("region_scratch_rows", ctypes.c_int64)]
+                ("region_scratch_rows", ctypes.c_int64), ("fine_times", ctypes.c_void_p)]
 
 
 class CounterNoise(ctypes.Structure):
@@ -109,6 +109,7 @@ SIGNATURES = {
     "mmpr_version": (ctypes.c_char_p, []),
     "mmpr_last_error": (ctypes.c_char_p, []),
     "mmpr_fine_sweep_occupancy": (ctypes.c_int, [_I64, _P, _P]),
+    "mmpr_set_fine_times": (ctypes.c_int, [_P]),
     "mmpr_noise_keys": (ctypes.c_int, [_U64, _I32, _I32, _I32, _I32, _I32, _P, _P]),
     "mmpr_entropy_key": (ctypes.c_int, [_P, _I32, _P, _P]),
     "mmpr_normals_fill": (ctypes.c_int, [_P, _I32, _I64, _P, _I64, _I32, _D, _D, _P]),

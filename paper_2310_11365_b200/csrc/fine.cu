@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(MAXT, PHX ? (MMPR_PHX_MINB * 512 / MAXT > 0 ? 
   double s = 0.0;
   int bad = 0;
   int first_bad = MMPR_STAT_OK;
+  if (p.t_slice && active && tid == 0 && rank == 0) p.t_slice[2 * slice] = globaltimer_ns();
   if (active) {
     reduce(0, -1, s, bad, p.S > 0 ? 0 : -1);
     for (int j = 0; j < p.S; ++j) {
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(MAXT, PHX ? (MMPR_PHX_MINB * 512 / MAXT > 0 ? 
     }
   }
 
+  if (p.t_slice && active && tid == 0 && rank == 0) p.t_slice[2 * slice + 1] = globaltimer_ns();
   if (active) {
     double *xo = p.x_out + (int64_t)slice * p.out_pitch;
 #pragma unroll
@@ -544,6 +546,16 @@ static int dispatch_tail(const FineParams &p, const FineGeometry &g, cudaStream_
 
 using namespace mmpr;
 
+// per-slice timestamp sink of the next fine sweeps of this host thread
+// (mmpr_set_fine_times); read when a launch is configured, so a captured
+// graph keeps the pointer it was captured with
+static thread_local int64_t *g_fine_times = nullptr;
+
+extern "C" int mmpr_set_fine_times(int64_t *slice_times) {
+  g_fine_times = slice_times;
+  return MMPR_OK;
+}
+
 static int fine_sweep_impl(const mmpr_model *model, int32_t n_slices, int64_t particles, int32_t steps,
                            double dt, double sqrt_dt, const double *t0, const double *x_in, int64_t in_pitch,
                            double *x_out, int64_t out_pitch, const double *xi, int64_t xi_slice_pitch,
@@ -593,6 +605,7 @@ static int fine_sweep_impl(const mmpr_model *model, int32_t n_slices, int64_t pa
   p.stats = stats;
   p.counts = counts;
   p.cn = cn::CounterNoise{0u, 0u, 0u, 0};
+  p.t_slice = reinterpret_cast<long long *>(g_fine_times);
   if (phx) p.cn = cn::CounterNoise{cnoise->key[0], 0u, cnoise->kfield, cnoise->slice_offset};
   cudaStream_t s = (cudaStream_t)stream;
   if (use_grid) return fine_grid_sweep(p, s, phx);

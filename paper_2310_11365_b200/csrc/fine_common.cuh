@@ -38,6 +38,7 @@ struct FineParams {
   int cnt_min;        // min elements per lane over populated slots
   int l2_ahead;       // steps of increments prefetched into L2 beyond the smem stages
   cn::CounterNoise cn;  // PHX kernels: increments from counter-based Philox (xi unused)
+  long long *t_slice;   // optional [n_slices][2] globaltimer stamps (ns): slice start, slice end
 };
 
 // dynamic shared memory of a PHX kernel: the ziggurat tables

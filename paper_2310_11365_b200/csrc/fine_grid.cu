@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
     int bad = 0;
     int first_bad = MMPR_STAT_OK;
     int issued = PHX ? 0 : min(NB, total_chunks);
+    if (p.t_slice && tid == 0 && rank == 0) p.t_slice[2 * slice] = globaltimer_ns();
     reduce(-1, s, bad, p.S > 0 ? 0 : -1);
     for (int j = 0; j < p.S; ++j) {
       GPROF_MARK(pu0);
@@ -443,6 +444,7 @@ __global__ void __launch_bounds__(1024, 1) fine_grid_kernel(const FineParams p, 
       }
     }
     qbase += (uint32_t)issued;
+    if (p.t_slice && tid == 0 && rank == 0) p.t_slice[2 * slice + 1] = globaltimer_ns();
     __syncthreads();  // buffers free before the next slice's prologue
     double *xo = p.x_out + (int64_t)slice * p.out_pitch;
 #pragma unroll

@@ -243,6 +243,13 @@ __device__ __forceinline__ void st_cluster_v2(uint32_t addr, unsigned long long 
 }
 
 // Bulk prefetch of global memory into L2 (no shared-memory destination).
+// %globaltimer (ns): per-slice timestamps of the fine sweeps
+__device__ __forceinline__ long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (long long)t;
+}
+
 __device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }

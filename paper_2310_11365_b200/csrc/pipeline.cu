@@ -689,6 +689,7 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
       PPROF(2);
       int bad = 0;
       const uint32_t nkey = cn::slice_key(p.cn, (uint32_t)n);
+      if (io.fine_times && rank == 0 && tid == 0) io.fine_times[((int64_t)k * N + n) * 2] = globaltimer_ns();
       if (!mean_known) reduce(Plain{}, 0.0, -1, s, bad, (PHX && p.S > 0) ? 0 : -1, nkey);
       int first_bad = MMPR_STAT_OK;
       for (int j = 0; j < p.S; ++j) {
@@ -744,6 +745,7 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
       const int r = owner(n);
       const mmpr_pipeline_io &io = pp.io[r];
       const PlFlags fl{io.flags, N, K};
+      if (io.fine_times && rank == 0 && tid == 0) io.fine_times[((int64_t)k * N + n) * 2 + 1] = globaltimer_ns();
 
       PPROF(3);
       // ---- write F^k_n into the parity buffer, restriction, publish -------------

@@ -81,7 +81,11 @@ class PararealTrace:
     """Macro and micro iterates plus diagnostics of one run (engine.py:79-107).
 
     ``snapshots[k][n]`` are device-resident ensembles (views into the run's
-    snapshot buffer).  ``timings`` holds per-stage device times in seconds.
+    snapshot buffer).  ``timings`` has the reference's keys: "fine" holds
+    one device time per slice propagation (iteration-major, seconds);
+    "coarse" / "restrict" / "match" hold CUDA-event stage times when the run
+    recorded timings.  ``stage_timings``: every recorded stage (also
+    "noise" and "iterations", the pipeline launch).
     """
 
     times: tuple[float, ...]
@@ -94,6 +98,7 @@ class PararealTrace:
     fraction_gaps: list = field(default_factory=list)
     lift_collapses: list = field(default_factory=list)
     timings: dict = field(default_factory=dict)
+    stage_timings: dict = field(default_factory=dict)
     stopped_at: int | None = None
     d2h_bytes: int = 0
     snapshot_positions: np.ndarray | None = None  # host copy streamed during the run (snapshots_to_host)
@@ -159,7 +164,7 @@ class _Workspace:
     the end-of-run transfer is three copies."""
 
     F64 = ("macro", "micro", "fine_stats", "raw", "rho0")
-    I64 = ("micro_counts", "fine_counts", "counts0")
+    I64 = ("micro_counts", "fine_counts", "counts0", "fine_times")
     I32 = ("bad", "coarse_status", "match_status")
 
     def __init__(self, K: int, N: int, P: int, S: int, I: int, retain: bool, noise_slices: int | None = None,
@@ -169,7 +174,8 @@ class _Workspace:
         Kc = max(K, 1)
         shapes = {"macro": (K + 1, N + 1, nv), "micro": (K + 1, N + 1, nv), "fine_stats": (Kc, N, nv),
                   "raw": (Kc, N, nv), "rho0": (1, nv), "micro_counts": (K + 1, N + 1, I),
-                  "fine_counts": (Kc, N, I), "counts0": (1, I), "bad": (Kc, N), "coarse_status": (K + 1, N),
+                  "fine_counts": (Kc, N, I), "counts0": (1, I), "fine_times": (Kc, N, 2), "bad": (Kc, N),
+                  "coarse_status": (K + 1, N),
                   "match_status": (K + 1, N)}
         self.report = {}
         for names, dtype in ((self.F64, torch.float64), (self.I64, torch.int64), (self.I32, torch.int32)):
@@ -358,10 +364,11 @@ class _RunPlan:
                 kernels.fine_sweep(self.model_d, cur[a:a + nb], ws.fine[a:a + nb], self.times_d[a:a + nb], S,
                                    self.cfg.step.dt, ws.xi[:nb], ws.bad[k][a:a + nb],
                                    stats=ws.fine_stats[k][a:a + nb], counts=ws.fine_counts[k][a:a + nb],
-                                   counter=counter)
+                                   counter=counter, times=ws.fine_times[k][a:a + nb])
             else:
                 kernels.fine_sweep(self.model_d, cur[a:a + nb], ws.fine[a:a + nb], self.times_d[a:a + nb], S,
-                                   self.cfg.step.dt, ws.xi[:nb], ws.bad[k][a:a + nb], counter=counter)
+                                   self.cfg.step.dt, ws.xi[:nb], ws.bad[k][a:a + nb], counter=counter,
+                                   times=ws.fine_times[k][a:a + nb])
             timer.stop("fine", ev)
         if not self.fused_restrict:
             ev = timer.start()
@@ -401,7 +408,8 @@ class _RunPlan:
                                   ws.xi, ws.snap, ws.fine, ws.macro, ws.micro, ws.micro_counts, ws.fine_stats,
                                   ws.fine_counts, ws.raw, ws.cache, ws.bad, ws.coarse_status, ws.match_status,
                                   self.flags, counter=self.plan.counter_noise(0) if self.counter else None,
-                                  partition=self.part_d if self.I > 1 else None, region_scratch=self.rg_scratch)
+                                  partition=self.part_d if self.I > 1 else None, region_scratch=self.rg_scratch,
+                                  fine_times=ws.fine_times)
         timer.stop("iterations", ev)
 
     def stream_row(self, k):
@@ -680,7 +688,22 @@ def _build_trace(h, ws, cfg, plan, times, K, I, timer, stopped_at) -> PararealTr
         neg = raw[:, :, I:2 * I]
         trace.clamp_events = [(int(k) + 1, int(n) + 1, int(i), float(neg[k, n, i]))
                               for k, n, i in np.argwhere(neg < 0.0)]
-    trace.timings = timer.resolve()
+    # the reference's timings (engine.py:149-233): per-slice fine propagation
+    # times, here device time between each slice's first and last step
+    # (globaltimer, so per-slice times overlap as the slices run
+    # concurrently); the other stages as recorded CUDA-event times
+    # (record_timings=True), every stage including the noise and the
+    # iteration pipeline in stage_timings
+    stages = timer.resolve()
+    ft = h.get("fine_times")
+    if ft is not None:
+        ft = ft[:K].astype(np.int64)
+        fine = np.where((ft[..., 0] > 0) & (ft[..., 1] >= ft[..., 0]), (ft[..., 1] - ft[..., 0]) * 1e-9, 0.0)
+    else:  # multi-rank drivers: not gathered
+        fine = np.zeros((0,))
+    trace.timings = {"coarse": list(stages.get("coarse", [])), "fine": fine.reshape(-1).tolist(),
+                     "restrict": list(stages.get("restrict", [])), "match": list(stages.get("match", []))}
+    trace.stage_timings = stages
     return trace
 
 

@@ -28,13 +28,23 @@ def _rows(t, name):
 
 
 def fine_sweep(model: _lib.Model, x_in, x_out, t0, steps: int, dt: float, xi, bad_step, final_mean=None,
-               stats=None, counts=None, stream=None, counter: _lib.CounterNoise | None = None) -> None:
+               stats=None, counts=None, stream=None, counter: _lib.CounterNoise | None = None, times=None) -> None:
     """EM over ``steps`` steps for every row of x_in (E, P) -> x_out (E, P).
     xi: (E, steps, pitch) increments; t0: (E,) float64; bad_step: (E,) int32.
     stats (E, 3) / counts (E, 1): single-region restriction of x_out fused
     into the sweep (MEAN_OF_F models).  ``counter`` (NoiseMode.PHILOX*):
-    increments generated in registers by counter-based Philox; xi unused."""
+    increments generated in registers by counter-based Philox; xi unused.
+    ``times`` (E, 2) int64: globaltimer ns at each slice's start and end."""
     require_cuda()
+    if times is not None:
+        if times.dtype != torch.int64 or tuple(times.shape) != (x_in.shape[0], 2) or not times.is_contiguous():
+            raise ValueError("times must be contiguous int64 (E, 2)")
+        _lib.call("mmpr_set_fine_times", times.data_ptr())
+        try:
+            fine_sweep(model, x_in, x_out, t0, steps, dt, xi, bad_step, final_mean, stats, counts, stream, counter)
+        finally:
+            _lib.call("mmpr_set_fine_times", None)
+        return
     E, P = x_in.shape
     in_pitch = _rows(x_in, "x_in")
     out_pitch = _rows(x_out, "x_out")
@@ -250,7 +260,7 @@ def parareal_pipeline(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Mo
                       reuse: bool, times, x0, rho0, counts0, xi, snap, fine, macro, micro, micro_counts,
                       fine_stats, fine_counts, raw, cache, bad, coarse_status, match_status, flags,
                       stream=None, counter: _lib.CounterNoise | None = None,
-                      partition: _lib.Partition | None = None, region_scratch=None) -> None:
+                      partition: _lib.Partition | None = None, region_scratch=None, fine_times=None) -> None:
     """Iterations 1..K of run_micro_macro in one launch (after the prologue).
 
     With I regions: snap: (K+1 or 2, N+1, P); fine: (2, N, P); macro/micro:
@@ -303,6 +313,10 @@ def parareal_pipeline(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Mo
         io.counter_noise = 1
         io.counter_key[0], io.counter_key[1] = counter.key[0], counter.key[1]
         io.counter_kfield = counter.kfield
+    if fine_times is not None:
+        if fine_times.dtype != torch.int64 or tuple(fine_times.shape) != (K, N, 2) or not fine_times.is_contiguous():
+            raise ValueError("fine_times must be contiguous int64 (K, N, 2)")
+        io.fine_times = fine_times.data_ptr()
     if I > 1:
         if partition is None or region_scratch is None:
             raise ValueError("a multi-region pipeline needs the partition and region_scratch")

@@ -184,7 +184,9 @@ def test_pipeline_eager_timings(mm, monkeypatch):
     monkeypatch.setenv("MMPR_PIPELINE", "1")
     tr = mm.run_micro_macro(model, ode, init, cfg, mm.NoisePlan(0), record_timings=True)
     assert mm.engine.last_run_info["pipeline"]
-    assert sum(tr.timings["iterations"]) > 0.0
+    assert sum(tr.stage_timings["iterations"]) > 0.0
+    assert len(tr.timings["fine"]) == 4 * 2 and all(v > 0.0 for v in tr.timings["fine"])
+    assert set(tr.timings) == {"coarse", "fine", "restrict", "match"}
 
 
 def test_pipeline_blowup_is_reported_like_the_sweep(mm, monkeypatch):

@@ -39,8 +39,8 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.MomentOde) == 8 + 8 * _lib.MAX_ODE_PARAMS
     assert ctypes.sizeof(_lib.Integrator) == 8 + 4 * 8
     # 21 pointers / int64 + snap_rows padded to 8, then counter_noise, counter_key[2], counter_kfield,
-    # the partition, region_scratch, region_scratch_rows
-    assert ctypes.sizeof(_lib.PipelineIO) == 24 * 8 + 16 + ctypes.sizeof(_lib.Partition) + 16
+    # the partition, region_scratch, region_scratch_rows, fine_times
+    assert ctypes.sizeof(_lib.PipelineIO) == 24 * 8 + 16 + ctypes.sizeof(_lib.Partition) + 24
     assert ctypes.sizeof(_lib.CounterNoise) == 16
 
 
