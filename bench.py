@@ -446,7 +446,9 @@ def other_configs(mm, torch, reps: int = 3) -> dict:
     the same run (CUDA events around each full run_micro_macro; mean of
     `reps` after one warm-up): configs 1, 2, 3, config 5 at one GPU's share
     of its 8-GPU run (N = 32 of 256 slices, full P = 2^20, S = 200, K = 10),
-    and configs 4 and 5 in the counter-based Philox noise mode."""
+    configs 4 and 5 in the counter-based Philox noise mode, and config 4
+    with FRESH noise (numpy-exact streams regenerated every iteration vs
+    counter-based increments in registers)."""
     import math as _m
 
     def timed(fn):
@@ -492,6 +494,13 @@ def other_configs(mm, torch, reps: int = 3) -> dict:
         ("config4_philox_noise", "config 4 with NoiseMode.PHILOX (increments in registers)",
          cfg(64, 5, 0.1, 100_000, 1e-3, 100, 1e-2), ou, mm.unimodal_rhs(ou), init1,
          mm.NoisePlan(0, mm.NoiseMode.PHILOX)),
+        ("config4_fresh_numpy_noise", "config 4 with NoiseMode.FRESH (new numpy-exact streams every iteration)",
+         cfg(64, 5, 0.1, 100_000, 1e-3, 100, 1e-2), ou, mm.unimodal_rhs(ou), init1,
+         mm.NoisePlan(0, mm.NoiseMode.FRESH)),
+        ("config4_philox_fresh_noise", "config 4 with NoiseMode.PHILOX_FRESH (new counter-based increments every "
+                                       "iteration, in registers)",
+         cfg(64, 5, 0.1, 100_000, 1e-3, 100, 1e-2), ou, mm.unimodal_rhs(ou), init1,
+         mm.NoisePlan(0, mm.NoiseMode.PHILOX_FRESH)),
         ("config5_one_gpu_share_philox_noise", "config 5's one-GPU share with NoiseMode.PHILOX (increments in registers)",
          cfg(32, 10, 0.1, 1 << 20, 5e-4, 200, 1e-2, part5), m5,
          mm.multimodal_rhs(m5, part5, dw5.potential, dw5.sigma), bim, mm.NoisePlan(0, mm.NoiseMode.PHILOX)),

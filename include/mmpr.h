@@ -386,6 +386,8 @@ int mmpr_integrate_macro(const mmpr_moment_ode *ode, const mmpr_model *model,
  * increments) must already be on the stream; the pipeline writes every
  * row k >= 1 of macro/micro/micro_counts/cache/coarse_status/match_status,
  * all rows of fine_stats/fine_counts/raw/bad, and snapshot rows 1..K. */
+#define MMPR_COUNTER_FRESH 0xFFFFFFFFu
+
 typedef struct mmpr_pipeline_io {
   const double *times;        /* [N+1] slice boundaries */
   const double *x0;           /* [P] ens0 */
@@ -412,7 +414,8 @@ typedef struct mmpr_pipeline_io {
   int32_t counter_noise;      /* 1: increments from counter-based Philox (xi unused; see
                                  mmpr_counter_noise), 0: from xi */
   uint32_t counter_key[2];
-  uint32_t counter_kfield;    /* 0: frozen (the pipeline runs frozen noise only) */
+  uint32_t counter_kfield;    /* 0: frozen; MMPR_COUNTER_FRESH: fresh, iteration k's fine parts
+                                 draw with kfield k + 1 (as mmpr_counter_noise of iteration k) */
   /* two-region runs (ode->n_regions == 2, one rank; particles.region_statistics
    * and the per-region coupling.match inside the units): */
   mmpr_partition partition;   /* the run's partition (n_regions == ode->n_regions) */

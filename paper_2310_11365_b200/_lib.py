@@ -77,6 +77,9 @@ class Integrator(ctypes.Structure):
                 ("abs_tol", ctypes.c_double), ("first_step", ctypes.c_double)]
 
 
+COUNTER_FRESH = 0xFFFFFFFF  # mmpr_pipeline_io.counter_kfield: fresh counter noise
+
+
 class PipelineIO(ctypes.Structure):
     """mmpr_pipeline_io: device buffers of one run of the iteration pipeline."""
     _fields_ = [("times", ctypes.c_void_p), ("x0", ctypes.c_void_p), ("rho0", ctypes.c_void_p),

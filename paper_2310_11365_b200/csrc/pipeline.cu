@@ -86,6 +86,7 @@ struct PipeParams {
   long long watchdog;  // pl_wait limit in cycles (see pl_wait)
   int *abort;          // this launch's abort word (last flag word of rank r0)
   int phx;             // increments from counter-based Philox (f.cn) instead of io.xi
+  int phx_fresh;       // PHILOX_FRESH: unit (k, n)'s fine part draws iteration k's increments
   mmpr_partition part;  // NR > 1: the regions
   double *rg_scratch;   // NR > 1: [clusters][NR][P] compacted members of the unit's restrictions
   int rg_rows;          // NR > 1: clusters the scratch holds (the launch uses at most this many)
@@ -633,7 +634,8 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
         double var;
         int b0;
         reduce(Plain{}, 0.0, -1, s, b0);
-        reduce(Centered{}, s, -1, var, b0, (PHX && has_fine && p.S > 0) ? 0 : -1, cn::slice_key(p.cn, (uint32_t)n));
+        reduce(Centered{}, s, -1, var, b0, (PHX && has_fine && p.S > 0) ? 0 : -1,
+               pp.phx_fresh ? p.cn.k0 ^ ((uint32_t)n | ((uint32_t)(k + 1) << 20)) : cn::slice_key(p.cn, (uint32_t)n));
         mean_known = true;
         if (rank == 0 && tid == 0) {
           double *mo = io.micro + ((int64_t)k * (N + 1) + n) * 3;
@@ -688,7 +690,10 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
       // ---- F(u^k_n): S Euler-Maruyama steps, particles in registers ------------
       PPROF(2);
       int bad = 0;
-      const uint32_t nkey = cn::slice_key(p.cn, (uint32_t)n);
+      // (fresh counter noise: iteration k's field, as the per-iteration sweep's
+      // plan.counter_noise(k))
+      const uint32_t nkey = pp.phx_fresh ? p.cn.k0 ^ ((uint32_t)n | ((uint32_t)(k + 1) << 20))
+                                         : cn::slice_key(p.cn, (uint32_t)n);
       if (io.fine_times && rank == 0 && tid == 0) io.fine_times[((int64_t)k * N + n) * 2] = globaltimer_ns();
       if (!mean_known) reduce(Plain{}, 0.0, -1, s, bad, (PHX && p.S > 0) ? 0 : -1, nkey);
       int first_bad = MMPR_STAT_OK;
@@ -1001,7 +1006,9 @@ static int check_io(const mmpr_pipeline_io *io, int32_t n_slices, int32_t iterat
   if (io->fine_pitch < particles || io->snap_slice_pitch < particles ||
       io->snap_iter_stride < (int64_t)(n_slices + 1) * io->snap_slice_pitch)
     return MMPR_ERR_ARG;
-  if (io->counter_noise && (io->counter_kfield >= (1u << 12) || n_slices > (1 << 20) || steps > (1 << 24)))
+  if (io->counter_noise && ((io->counter_kfield >= (1u << 12) && io->counter_kfield != MMPR_COUNTER_FRESH) ||
+                            n_slices > (1 << 20) || steps > (1 << 24) || (io->counter_kfield == MMPR_COUNTER_FRESH &&
+                                                                          iterations >= (1 << 12))))
     return MMPR_ERR_ARG;
   if (steps > 0 && !io->counter_noise && (!io->xi || (io->xi_row_pitch & 1) || io->xi_row_pitch < particles ||
                     (reinterpret_cast<uintptr_t>(io->xi) & 15) ||
@@ -1102,7 +1109,8 @@ extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_
   }
   pp.abort = ios[first_rank].flags + nflags - 1;
   pp.phx = ios[first_rank].counter_noise ? 1 : 0;
-  p.cn = cn::CounterNoise{ios[first_rank].counter_key[0], 0u, ios[first_rank].counter_kfield, 0};
+  pp.phx_fresh = pp.phx && ios[first_rank].counter_kfield == MMPR_COUNTER_FRESH;
+  p.cn = cn::CounterNoise{ios[first_rank].counter_key[0], 0u, pp.phx_fresh ? 0u : ios[first_rank].counter_kfield, 0};
   pp.nranks = launch_ranks;
   if (ode->n_regions > 1) {
     // bimodal units restrict over compacted members in per-cluster scratch

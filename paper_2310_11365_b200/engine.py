@@ -279,7 +279,11 @@ class _RunPlan:
         self.prev_trace = None  # weakref to the last trace built on this plan's buffers
         # (two regions: the units restrict over compacted members themselves)
         pipe_restrict = self.fused_restrict or (I == 2 and model_d.stat_kind == _lib.STAT_MEAN_OF_F)
-        self.pipeline = (allow_pipeline and K >= 1 and pipe_restrict and not plan.fresh and self.batch == N
+        # (FRESH noise: in the counter-based mode only -- each unit draws its
+        # iteration's increments in registers; the numpy streams of a FRESH
+        # run are materialised per iteration)
+        self.pipeline = (allow_pipeline and K >= 1 and pipe_restrict and (not plan.fresh or self.counter)
+                         and self.batch == N
                          and not host_snapshots and os.environ.get("MMPR_PIPELINE", "1") != "0"
                          and kernels.pipeline_supported(model_d, ode_d, ode_model_d, integ_d, P))
         self.rg_scratch = None
@@ -407,10 +411,18 @@ class _RunPlan:
                                   self.cfg.step.dt, self.S, self.reuse, self.times_d, ws.x0, ws.rho0, ws.counts0,
                                   ws.xi, ws.snap, ws.fine, ws.macro, ws.micro, ws.micro_counts, ws.fine_stats,
                                   ws.fine_counts, ws.raw, ws.cache, ws.bad, ws.coarse_status, ws.match_status,
-                                  self.flags, counter=self.plan.counter_noise(0) if self.counter else None,
+                                  self.flags, counter=self._pipeline_counter(),
                                   partition=self.part_d if self.I > 1 else None, region_scratch=self.rg_scratch,
                                   fine_times=ws.fine_times)
         timer.stop("iterations", ev)
+
+    def _pipeline_counter(self):
+        if not self.counter:
+            return None
+        c = self.plan.counter_noise(0)
+        if self.plan.fresh:
+            c.kfield = _lib.COUNTER_FRESH  # iteration k's units draw with field k + 1
+        return c
 
     def stream_row(self, k):
         """Copy snapshot row k to pinned host memory on the side stream."""

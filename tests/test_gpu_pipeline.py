@@ -165,6 +165,18 @@ def test_pipeline_bimodal_matches_oracle(mm, monkeypatch):
     assert dm <= 1e-10 and du <= 1e-10, (dm, du)
 
 
+@pytest.mark.parametrize("mode", ["PHILOX", "PHILOX_FRESH"])
+def test_pipeline_counter_noise_equals_per_iteration_kernels(mm, monkeypatch, mode):
+    """Counter-based noise generated in registers by the pipeline's units
+    (FRESH: unit (k, n) draws iteration k's field) -- bitwise the
+    per-iteration sweeps with the same counter noise."""
+    model, ode, init, cfg = _ou_case(mm, 6, 3, 12)
+    plan = mm.NoisePlan(0, getattr(mm.NoiseMode, mode))
+    a = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
+    b = _run(mm, monkeypatch, False, model, ode, init, cfg, plan)
+    _same(a, b)
+
+
 def test_pipeline_without_converged_reuse_and_injected(mm, monkeypatch):
     model, ode, init, cfg = _ou_case(mm, 5, 3, 12)
     plan = mm.NoisePlan(0)
