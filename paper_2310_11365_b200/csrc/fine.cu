@@ -383,7 +383,18 @@ struct FineGeometry {
   size_t smem_bytes;
 };
 
-static int fine_geometry(int64_t P, FineGeometry *g) {
+static int fine_sm_count() {
+  static int sms_dev[MMPR_MAX_DEVICES] = {};
+  const int dev = mmpr_current_device();
+  if (sms_dev[dev] == 0) {
+    int v = 0;
+    sms_dev[dev] = (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) ? v : 148;
+  }
+  return sms_dev[dev];
+}
+
+// n_slices > 0: the launch's slice count, for the small-launch rule below.
+static int fine_geometry(int64_t P, FineGeometry *g, int n_slices = 0) {
   if (P < 1) return MMPR_ERR_ARG;
   g->D = pw_depth(P);
   const int64_t nslots = int64_t(1) << g->D;
@@ -414,6 +425,13 @@ static int fine_geometry(int64_t P, FineGeometry *g) {
   // FP64 update overlaps the other's reduction latency (measured 8% faster
   // than one 1024-thread CTA per SM at config 4).
   int spc = g->groups == 2 ? 64 : ((nslots >= 1024 && nslots / 64 <= FS_MAX_CLUSTER) ? 64 : 128);
+  // Few small ensembles (BASELINE config 1: 10 slices of 1e4 particles): one
+  // 1024-thread CTA per slice pulls the whole step's increments through one
+  // SM (80 KB per 2.6 us step, measured); 32 slots per CTA spread a slice
+  // over a 4-CTA cluster while every CTA of the launch still has its own SM
+  // (1.6 us per step; 16 and 8 slots per CTA measured no better).
+  if (spc == 128 && g->groups == 1 && n_slices > 0 && nslots >= 64 && n_slices * (nslots / 32) <= fine_sm_count())
+    spc = 32;
   if (const char *env = getenv("MMPR_FINE_SLOTS_PER_CTA")) {  // tuning override (one group)
     const int v = atoi(env);
     if (g->groups == 1 && v >= 4 && v <= 128 && (v & (v - 1)) == 0) spc = v;
@@ -573,7 +591,7 @@ static int fine_sweep_impl(const mmpr_model *model, int32_t n_slices, int64_t pa
     return MMPR_ERR_ARG;
   if (model->stat_kind != 0) return MMPR_ERR_UNSUPPORTED;
   FineGeometry g;
-  int st = fine_geometry(particles, &g);
+  int st = fine_geometry(particles, &g, n_slices);
   // beyond one cluster (or on request, for testing) the grid variant runs
   const char *force = getenv("MMPR_FINE_FORCE_GRID");
   const bool use_grid = (st == MMPR_ERR_UNSUPPORTED && g.ctas > FS_MAX_CLUSTER) || (force && atoi(force) == 1);
