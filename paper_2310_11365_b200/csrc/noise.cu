@@ -464,6 +464,7 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
   __shared__ double s_fi[256];
   __shared__ double s_tval[32 * NW_WORDS];  // tail starts (lane-private slots): value, length in words
   __shared__ uint16_t s_tlen[32 * NW_WORDS];
+  __shared__ __align__(16) unsigned long long s_w[32 * NW_WORDS + 1];  // the sub-chunk's words + the next one's first
   const int lane = threadIdx.x;
 #pragma unroll
   for (int i = lane; i < 256; i += 32) {
@@ -481,7 +482,6 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
     uint64_t w[NW_WORDS];
     np::philox_block(word0 / 4, k0, k1, w);
     np::philox_block(word0 / 4 + 1, k0, k1, w + 4);
-    const uint64_t succ = __shfl_down_sync(MMPR_FULL_MASK, w[0], 1);
     // fast path for every word, branch-free
     double x[NW_WORDS];
     uint32_t nf = 0;
@@ -500,71 +500,94 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
     // words in order, all lanes together, so the wedge test's arithmetic runs
     // once per round for the warp (one round in ~2/3 of the sub-chunks, two
     // in most of the rest); tail values and lengths go to lane-private slots.
+    // The words are staged in shared memory first, so the loop indexes them
+    // instead of selecting among 16 registers and they leave the registers.
     uint32_t pr = ~nf & 0xffu, tt = 0;
-    for (uint32_t rem = nf; __any_sync(MMPR_FULL_MASK, rem != 0);) {
-      if (rem) {
-        const int i = __ffs(rem) - 1;
-        rem &= rem - 1;
-        uint64_t rw = w[0], nx = w[1];
-#pragma unroll
-        for (int k = 1; k < NW_WORDS; ++k)
-          if (i == k) {
-            rw = w[k];
-            nx = k + 1 < NW_WORDS ? w[k + 1] : succ;
+    if (__any_sync(MMPR_FULL_MASK, nf != 0)) {
+      ulonglong2 *row = reinterpret_cast<ulonglong2 *>(&s_w[lane * NW_WORDS]);
+      row[0] = make_ulonglong2(w[0], w[1]);
+      row[1] = make_ulonglong2(w[2], w[3]);
+      row[2] = make_ulonglong2(w[4], w[5]);
+      row[3] = make_ulonglong2(w[6], w[7]);
+      // the last lane's last word: its successor opens the next sub-chunk
+      if (lane == 31 && (nf & 0x80u)) s_w[32 * NW_WORDS] = successor_word(word0 + NW_WORDS, k0, k1);
+      __syncwarp();
+      for (uint32_t rem = nf; __any_sync(MMPR_FULL_MASK, rem != 0);) {
+        if (rem) {
+          const int i = __ffs(rem) - 1;
+          rem &= rem - 1;
+          const uint64_t rw = s_w[lane * NW_WORDS + i];
+          const int layer = (int)(rw & 0xff);
+          const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
+          if (layer != 0) {
+            const uint64_t nx = s_w[lane * NW_WORDS + i + 1];
+            const double wi = __longlong_as_double((long long)zig[layer].y);
+            double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
+            if ((rw >> 8) & 1) v = -v;
+            pr |= (wedge_accepts(layer, v, nx, s_fi) ? 1u : 0u) << i;
+          } else {  // tail start: always produces
+            int L;
+            s_tval[lane * NW_WORDS + i] = tail_token(word0 + i, mant, k0, k1, &L);
+            s_tlen[lane * NW_WORDS + i] = (uint16_t)L;
+            pr |= 1u << i;
+            tt |= 1u << i;
           }
-        const int layer = (int)(rw & 0xff);
-        const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
-        if (layer != 0) {
-          // the last lane's last word: its successor opens the next sub-chunk
-          if (i == NW_WORDS - 1 && lane == 31) nx = successor_word(word0 + NW_WORDS, k0, k1);
-          const double wi = __longlong_as_double((long long)zig[layer].y);
-          double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
-          if ((rw >> 8) & 1) v = -v;
-          pr |= (wedge_accepts(layer, v, nx, s_fi) ? 1u : 0u) << i;
-        } else {  // tail start: always produces
-          int L;
-          s_tval[lane * NW_WORDS + i] = tail_token(word0 + i, mant, k0, k1, &L);
-          s_tlen[lane * NW_WORDS + i] = (uint16_t)L;
-          pr |= 1u << i;
-          tt |= 1u << i;
         }
       }
+      __syncwarp();  // the next sub-chunk overwrites the staged words
     }
-    // lane parse from entry 0, then stitch entries lane to lane until stable
+    // lane parse from entry 0, then the entries lane to lane.  Exits are 0 or
+    // 1 unless a tail token is involved, and an entry of 1 onto a word that
+    // starts an attempt in the entry-0 parse only drops word 0 (same
+    // boundaries after it, same exit): then one ballot resolves every entry.
+    // Anything else (entry onto a consumed word, tails, a long carry) takes
+    // the exact stitch loop.
     uint32_t S;
-    int ex, ecur = 0;
+    int ex;
     if (tt == 0) wedge_parse8(nf, 0, S, ex);
     else general_parse8(nf, tt, 0, &s_tlen[lane * NW_WORDS], &S, &ex);
-    for (;;) {
-      int e = __shfl_up_sync(MMPR_FULL_MASK, ex, 1);
-      if (lane == 0) e = carry;
-      bool changed = false;
-      if (e != ecur) {
-        changed = true;
-        if (e >= NW_WORDS) {
-          S = 0;
-          ex = e - NW_WORDS;
-        } else if (ecur == 0 && ((S >> e) & 1u)) {
-          S &= ~((1u << e) - 1u);  // same attempt boundaries from e on: same exit
-        } else if (tt == 0) {
-          wedge_parse8(nf, e, S, ex);
-        } else {
-          general_parse8(nf, tt, e, &s_tlen[lane * NW_WORDS], &S, &ex);
+    const uint32_t X = __ballot_sync(MMPR_FULL_MASK, ex != 0);
+    const int e1 = lane == 0 ? carry : (int)((X >> ((lane + 31) & 31)) & 1u);
+    const bool hard = ex > 1 || e1 > 1 || (e1 == 1 && !((S >> 1) & 1u));
+    if (!__any_sync(MMPR_FULL_MASK, hard)) {
+      S &= ~(uint32_t)e1;
+      carry = (int)(X >> 31);
+    } else {
+      int ecur = 0;
+      for (;;) {
+        int e = __shfl_up_sync(MMPR_FULL_MASK, ex, 1);
+        if (lane == 0) e = carry;
+        bool changed = false;
+        if (e != ecur) {
+          changed = true;
+          if (e >= NW_WORDS) {
+            S = 0;
+            ex = e - NW_WORDS;
+          } else if (ecur == 0 && ((S >> e) & 1u)) {
+            S &= ~((1u << e) - 1u);  // same attempt boundaries from e on: same exit
+          } else if (tt == 0) {
+            wedge_parse8(nf, e, S, ex);
+          } else {
+            general_parse8(nf, tt, e, &s_tlen[lane * NW_WORDS], &S, &ex);
+          }
+          ecur = e;
         }
-        ecur = e;
+        if (!__any_sync(MMPR_FULL_MASK, changed)) break;
       }
-      if (!__any_sync(MMPR_FULL_MASK, changed)) break;
+      carry = __shfl_sync(MMPR_FULL_MASK, ex, 31);
     }
+    // output offsets: words dropped before this lane, from four ballots of
+    // the per-lane dropped count (0..8) instead of a five-step shuffle scan
     const uint32_t O = S & pr;
     const int cnt = __popc(O);
-    int incl = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int v = __shfl_up_sync(MMPR_FULL_MASK, incl, d);
-      if (lane >= d) incl += v;
-    }
+    const uint32_t dr = (uint32_t)(NW_WORDS - cnt);
+    const uint32_t lt = (1u << lane) - 1u;
+    const int dropped_before = __popc(__ballot_sync(MMPR_FULL_MASK, dr & 1u) & lt) +
+                               2 * __popc(__ballot_sync(MMPR_FULL_MASK, dr & 2u) & lt) +
+                               4 * __popc(__ballot_sync(MMPR_FULL_MASK, dr & 4u) & lt) +
+                               8 * __popc(__ballot_sync(MMPR_FULL_MASK, dr & 8u) & lt);
+    const int incl = NW_WORDS * lane - dropped_before + cnt;
     const int total = __shfl_sync(MMPR_FULL_MASK, incl, 31);
-    carry = __shfl_sync(MMPR_FULL_MASK, ex, 31);
     const int64_t base = produced + incl - cnt;
     if (produced + 32 * NW_WORDS <= count) {  // warp-uniform: no bound checks in this sub-chunk
       double *dst = o + base;  // produced values are consecutive from base
