@@ -410,7 +410,10 @@ normals_fill_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__
 // entries are then stitched lane to lane with shuffles until stable (an
 // entry of 1 usually just truncates the speculative parse), the produced
 // normals are counted with a warp scan and written at their exact positions.
-#define NW_WORDS 8
+#ifndef NW_WORDS
+#define NW_WORDS 8  // words per lane and sub-chunk (8; 16 measured slower: 4.2 vs 3.3 ms)
+#endif
+#define NW_ALL ((1u << NW_WORDS) - 1u)
 
 // Lane parse of 8 words from entry e (< 8) when all non-fast words are wedges.
 __device__ __forceinline__ void wedge_parse8(uint32_t nf, int e, uint32_t &S, int &exit) {
@@ -445,25 +448,19 @@ __device__ __noinline__ uint64_t successor_word(uint64_t i, uint64_t k0, uint64_
   return np::philox_word(i, k0, k1);
 }
 
-template <typename T>
-__device__ __forceinline__ T pick8(const T (&v)[NW_WORDS], int i) {
-  T r = v[0];
-#pragma unroll
-  for (int k = 1; k < NW_WORDS; ++k) r = (i == k) ? v[k] : r;
-  return r;
-}
-
 // One single-warp CTA per stream: the Philox key is CTA-uniform (uniform
 // datapath for the key schedule), there is no block barrier in the loop,
 // and up to 32 streams run per SM.
+#ifndef NW_MINB
+#define NW_MINB 16
+#endif
 template <bool AFFINE>
-__global__ void __launch_bounds__(32, 16)
+__global__ void __launch_bounds__(32, NW_MINB)
 normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__restrict__ out, int64_t pitch,
                          double loc, double scale) {
   __shared__ ulonglong2 zig[256];
   __shared__ double s_fi[256];
-  __shared__ double s_tval[32 * NW_WORDS];  // tail starts (lane-private slots): value, length in words
-  __shared__ uint16_t s_tlen[32 * NW_WORDS];
+  __shared__ uint16_t s_tlen[32 * NW_WORDS];  // tail starts (lane-private slots): length in words
   __shared__ __align__(16) unsigned long long s_w[32 * NW_WORDS + 1];  // the sub-chunk's words + the next one's first
   const int lane = threadIdx.x;
 #pragma unroll
@@ -479,38 +476,43 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
   int64_t produced = 0;
   for (uint64_t sub = 0; produced < count; ++sub) {
     const uint64_t word0 = (sub * 32 + lane) * NW_WORDS;
-    uint64_t w[NW_WORDS];
-    np::philox_block(word0 / 4, k0, k1, w);
-    np::philox_block(word0 / 4 + 1, k0, k1, w + 4);
-    // fast path for every word, branch-free
+    // fast path for every word, branch-free, eight words (two Philox blocks)
+    // at a time; the words go to shared memory for the rare-word loop below
+    // (which indexes them instead of selecting among registers) and leave
+    // the registers
     double x[NW_WORDS];
     uint32_t nf = 0;
 #pragma unroll
-    for (int i = 0; i < NW_WORDS; ++i) {
-      const uint64_t rw = w[i];
-      const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
-      const ulonglong2 z = zig[rw & 0xff];
-      const double wi = __longlong_as_double((long long)z.y);
-      const double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
-      // sign bit 8 of the word -> sign of the double (one LOP3 on the high half)
-      x[i] = __hiloint2double(__double2hiint(v) ^ (int)(((uint32_t)rw << 23) & 0x80000000u), __double2loint(v));
-      nf |= (mant >= z.x ? 1u : 0u) << i;
-    }
-    // Rare words (~2.2%, ~0.2 per lane): each lane tests its own non-fast
-    // words in order, all lanes together, so the wedge test's arithmetic runs
-    // once per round for the warp (one round in ~2/3 of the sub-chunks, two
-    // in most of the rest); tail values and lengths go to lane-private slots.
-    // The words are staged in shared memory first, so the loop indexes them
-    // instead of selecting among 16 registers and they leave the registers.
-    uint32_t pr = ~nf & 0xffu, tt = 0;
-    if (__any_sync(MMPR_FULL_MASK, nf != 0)) {
-      ulonglong2 *row = reinterpret_cast<ulonglong2 *>(&s_w[lane * NW_WORDS]);
+    for (int g = 0; g < NW_WORDS; g += 8) {
+      uint64_t w[8];
+      np::philox_block(word0 / 4 + g / 4, k0, k1, w);
+      np::philox_block(word0 / 4 + g / 4 + 1, k0, k1, w + 4);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint64_t rw = w[i];
+        const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
+        const ulonglong2 z = zig[rw & 0xff];
+        const double wi = __longlong_as_double((long long)z.y);
+        const double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
+        // sign bit 8 of the word -> sign of the double (one LOP3 on the high half)
+        x[g + i] = __hiloint2double(__double2hiint(v) ^ (int)(((uint32_t)rw << 23) & 0x80000000u), __double2loint(v));
+        nf |= (mant >= z.x ? 1u : 0u) << (g + i);
+      }
+      ulonglong2 *row = reinterpret_cast<ulonglong2 *>(&s_w[lane * NW_WORDS + g]);
       row[0] = make_ulonglong2(w[0], w[1]);
       row[1] = make_ulonglong2(w[2], w[3]);
       row[2] = make_ulonglong2(w[4], w[5]);
       row[3] = make_ulonglong2(w[6], w[7]);
+    }
+    // Rare words (~2.2%, ~0.2 per lane): each lane tests its own non-fast
+    // words in order, all lanes together, so the wedge test's arithmetic runs
+    // once per round for the warp; a tail token's value replaces the
+    // fast-path value in the lane's registers, its length goes to a
+    // lane-private slot.
+    uint32_t pr = ~nf & NW_ALL, tt = 0;
+    if (__any_sync(MMPR_FULL_MASK, nf != 0)) {
       // the last lane's last word: its successor opens the next sub-chunk
-      if (lane == 31 && (nf & 0x80u)) s_w[32 * NW_WORDS] = successor_word(word0 + NW_WORDS, k0, k1);
+      if (lane == 31 && (nf >> (NW_WORDS - 1))) s_w[32 * NW_WORDS] = successor_word(word0 + NW_WORDS, k0, k1);
       __syncwarp();
       for (uint32_t rem = nf; __any_sync(MMPR_FULL_MASK, rem != 0);) {
         if (rem) {
@@ -527,15 +529,17 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
             pr |= (wedge_accepts(layer, v, nx, s_fi) ? 1u : 0u) << i;
           } else {  // tail start: always produces
             int L;
-            s_tval[lane * NW_WORDS + i] = tail_token(word0 + i, mant, k0, k1, &L);
+            const double v = tail_token(word0 + i, mant, k0, k1, &L);
+#pragma unroll
+            for (int k = 0; k < NW_WORDS; ++k) x[k] = (i == k) ? v : x[k];
             s_tlen[lane * NW_WORDS + i] = (uint16_t)L;
             pr |= 1u << i;
             tt |= 1u << i;
           }
         }
       }
-      __syncwarp();  // the next sub-chunk overwrites the staged words
     }
+    __syncwarp();  // the next sub-chunk overwrites the staged words
     // lane parse from entry 0, then the entries lane to lane.  Exits are 0 or
     // 1 unless a tail token is involved, and an entry of 1 onto a word that
     // starts an attempt in the entry-0 parse only drops word 0 (same
@@ -576,16 +580,16 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
       }
       carry = __shfl_sync(MMPR_FULL_MASK, ex, 31);
     }
-    // output offsets: words dropped before this lane, from four ballots of
-    // the per-lane dropped count (0..8) instead of a five-step shuffle scan
+    // output offsets: words dropped before this lane, from ballots of the bits of
+    // the per-lane dropped count (0..NW_WORDS) instead of a five-step shuffle scan
     const uint32_t O = S & pr;
     const int cnt = __popc(O);
     const uint32_t dr = (uint32_t)(NW_WORDS - cnt);
     const uint32_t lt = (1u << lane) - 1u;
-    const int dropped_before = __popc(__ballot_sync(MMPR_FULL_MASK, dr & 1u) & lt) +
-                               2 * __popc(__ballot_sync(MMPR_FULL_MASK, dr & 2u) & lt) +
-                               4 * __popc(__ballot_sync(MMPR_FULL_MASK, dr & 4u) & lt) +
-                               8 * __popc(__ballot_sync(MMPR_FULL_MASK, dr & 8u) & lt);
+    int dropped_before = 0;
+#pragma unroll
+    for (int b = 0; (1 << b) <= NW_WORDS; ++b)
+      dropped_before += __popc(__ballot_sync(MMPR_FULL_MASK, (dr >> b) & 1u) & lt) << b;
     const int incl = NW_WORDS * lane - dropped_before + cnt;
     const int total = __shfl_sync(MMPR_FULL_MASK, incl, 31);
     const int64_t base = produced + incl - cnt;
@@ -602,14 +606,6 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
       for (int i = 0; i < NW_WORDS; ++i) {
         const int64_t idx = base + __popc(O & ((1u << i) - 1u));
         if (((O >> i) & 1u) && idx < count) o[idx] = AFFINE ? add(loc, mul(scale, x[i])) : x[i];
-      }
-    }
-    for (uint32_t rem = O & tt; rem; rem &= rem - 1) {  // rare: tail values overwrite
-      const int i = __ffs(rem) - 1;
-      const int64_t idx = base + __popc(O & ((1u << i) - 1u));
-      if (idx < count) {
-        const double v = s_tval[lane * NW_WORDS + i];
-        o[idx] = AFFINE ? add(loc, mul(scale, v)) : v;
       }
     }
     produced += total;
