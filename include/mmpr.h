@@ -437,13 +437,25 @@ int64_t mmpr_pipeline_flags_size(int32_t n_slices, int32_t iterations);
 int mmpr_set_fine_times(int64_t *slice_times);
 
 /* MMPR_OK when (model, ode, ode_model, integrator, particles) has a pipeline
- * instantiation (MEAN_OF_F, forward-Euler coarse, the 16 x 512-thread
- * cluster geometry of P ~ 1e5; one region, or two regions for the double
- * well with the multimodal closure on one rank); else MMPR_ERR_UNSUPPORTED
+ * instantiation (MEAN_OF_F, forward-Euler coarse, a cluster geometry with
+ * 13 or 10 accumulator elements per lane: P = 1e5 / 1e4 and their binary
+ * fractions / multiples within one cluster; one region, or two regions for
+ * the double well with the multimodal closure on one rank); else
+ * MMPR_ERR_UNSUPPORTED
  * and the caller runs the per-iteration kernels. */
 int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_moment_ode *ode,
                             const mmpr_model *ode_model, const mmpr_integrator *integ,
                             int64_t particles);
+
+/* The same for a given noise supply and rank count: the two-region units and
+ * the small-ensemble geometries (P = 1e4 .. 8e4 in binary steps) exist for
+ * one rank with numpy-stream or injected increments only (counter_noise = 0,
+ * n_ranks = 1).  Replaces nothing in the reference (engine.py:127-259 has no
+ * such switch); the host uses it to choose between the pipeline and the
+ * per-iteration kernels. */
+int mmpr_pipeline_supported_ex(const mmpr_model *model, const mmpr_moment_ode *ode,
+                               const mmpr_model *ode_model, const mmpr_integrator *integ,
+                               int64_t particles, int32_t counter_noise, int32_t n_ranks);
 
 /* Runs iterations 1..iterations (raise policy for the matches, predictions
  * of converged slices reused when reuse_converged != 0, as mmpr_coarse_row's

@@ -144,6 +144,7 @@ SIGNATURES = {
     "mmpr_histogram_sorted": (ctypes.c_int, [_I32, _I64, _P, _I64, _P, _I32, _P, _P]),
     "mmpr_pipeline_flags_size": (ctypes.c_int64, [_I32, _I32]),
     "mmpr_pipeline_supported": (ctypes.c_int, [_P, _P, _P, _P, _I64]),
+    "mmpr_pipeline_supported_ex": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _I32]),
     "mmpr_parareal_pipeline": (ctypes.c_int, [_P, _P, _P, _P, _I32, _I32, _I64, _I32, _D, _D, _I32, _P, _P]),
     "mmpr_parareal_pipeline_ranks": (ctypes.c_int, [_P, _P, _P, _P, _I32, _I32, _I64, _I32, _D, _D, _I32, _I32, _P,
                                                      _I32, _I32, _I32, _I32, _I32, _P]),

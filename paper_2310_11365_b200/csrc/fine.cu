@@ -430,11 +430,15 @@ static int fine_geometry(int64_t P, FineGeometry *g, int n_slices = 0) {
   // SM (80 KB per 2.6 us step, measured); 32 slots per CTA spread a slice
   // over a 4-CTA cluster while every CTA of the launch still has its own SM
   // (1.6 us per step; 16 and 8 slots per CTA measured no better).
-  if (spc == 128 && g->groups == 1 && n_slices > 0 && nslots >= 64 && n_slices * (nslots / 32) <= fine_sm_count())
+  // (the cluster fold sends lane c's copy of the CTA total to CTA c, and the
+  // warp butterfly leaves the total in the first `warps` lanes only: a
+  // cluster must not have more CTAs than a CTA has warps -- 8 at 32 slots)
+  if (spc == 128 && g->groups == 1 && n_slices > 0 && nslots >= 64 && nslots / 32 <= 8 &&
+      n_slices * (nslots / 32) <= fine_sm_count())
     spc = 32;
   if (const char *env = getenv("MMPR_FINE_SLOTS_PER_CTA")) {  // tuning override (one group)
     const int v = atoi(env);
-    if (g->groups == 1 && v >= 4 && v <= 128 && (v & (v - 1)) == 0) spc = v;
+    if (g->groups == 1 && v >= 4 && v <= 128 && (v & (v - 1)) == 0 && nslots / v <= v / 4) spc = v;  // CTAs <= warps
   }
   while (spc > 4 && (size_t)spc * max_leaf * 8 * 2 * g->groups > smem_budget) spc >>= 1;
   if (nslots <= spc) {

@@ -806,20 +806,24 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
 // host side
 // ---------------------------------------------------------------------------
 struct PipeGeometry {
-  int D, spc, ctas, threads, stage_elems, nstages;
+  int D, spc, ctas, threads, stage_elems, nstages, ppt;
   size_t smem;
   bool tail;
 };
 
-// The pipeline covers the fine-sweep geometry of the BASELINE ensembles
-// (P ~ 1e5: 1024 leaf slots of 96..104 particles, 16 CTAs x 512 threads,
-// 13 accumulator elements per lane); other sizes keep the per-iteration
-// kernels.
+// The pipeline covers the cluster geometries of the fine sweep whose leaves
+// hold PPT-1 or PPT accumulator elements per lane for an instantiated PPT:
+// 13 (P = 1e5 and its binary fractions down to 1.25e4: 96..104-particle
+// leaves; BASELINE configs 2-4) and 10 (P = 1e4, 2e4, 4e4, 8e4: 72..80;
+// BASELINE config 1), one cluster of up to 16 CTAs per unit -- 64 leaf
+// slots (512 threads) per CTA from 512 slots on, 32 (256 threads) below,
+// where a launch has too few units to fill the SMs otherwise.  Other sizes
+// keep the per-iteration kernels.
 static int pipe_geometry(int64_t P, PipeGeometry *g) {
   if (P < 1) return MMPR_ERR_ARG;
   const int D = pw_depth(P);
   const int64_t nslots = int64_t(1) << D;
-  if (nslots != 1024) return MMPR_ERR_UNSUPPORTED;
+  if (nslots < 64 || nslots > 1024) return MMPR_ERR_UNSUPPORTED;
   int64_t max_leaf = 0, min_leaf = INT64_MAX;
   for (int64_t s = 0; s < nslots; ++s) {
     int64_t o, l;
@@ -827,11 +831,12 @@ static int pipe_geometry(int64_t P, PipeGeometry *g) {
     if (l > max_leaf) max_leaf = l;
     if (l < min_leaf) min_leaf = l;
   }
-  if ((max_leaf + 7) / 8 != 13 || (min_leaf >> 3) < 12) return MMPR_ERR_UNSUPPORTED;
+  g->ppt = (int)((max_leaf + 7) / 8);
+  if ((g->ppt != 13 && g->ppt != 10) || (min_leaf >> 3) < g->ppt - 1) return MMPR_ERR_UNSUPPORTED;
   g->D = D;
-  g->spc = 64;
-  g->ctas = 16;
-  g->threads = 512;
+  g->spc = nslots >= 512 ? 64 : 32;
+  g->ctas = (int)(nslots / g->spc);
+  g->threads = g->spc * 8;
   int64_t max_range = 0;
   for (int c = 0; c < g->ctas; ++c) {
     int64_t lo, hi, l;
@@ -906,6 +911,11 @@ static int dispatch_pipe_regions(const PipeParams &pp, const PipeGeometry &g, cu
 
 template <int KIND, int OK, int MK>
 static int dispatch_pipe_tail(const PipeParams &pp, const PipeGeometry &g, cudaStream_t s) {
+  if (g.ppt == 10) {  // the small geometry: one rank, numpy-stream or injected increments
+    if (pp.phx || pp.G > 1) return MMPR_ERR_UNSUPPORTED;
+    if (g.tail) return launch_pipe<pipeline_kernel<KIND, 10, true, OK, MK, false>>(pp, g, s);
+    return launch_pipe<pipeline_kernel<KIND, 10, false, OK, MK, false>>(pp, g, s);
+  }
   if (pp.phx) {
     PipeGeometry gp = g;
     gp.smem = cn::gen_smem_bytes(13, g.threads);
@@ -928,10 +938,14 @@ static int dispatch_pipe_tail(const PipeParams &pp, const PipeGeometry &g, cudaS
 // instantiation: the BASELINE unimodal configs and their close relatives,
 // and config 3's bimodal double well with the two-region closure.
 static int dispatch_pipe(const mmpr_model &model, const mmpr_moment_ode &ode, const mmpr_model &ode_model,
-                         const PipeParams *pp, const PipeGeometry &g, cudaStream_t s) {
+                         const PipeParams *pp, const PipeGeometry &g, cudaStream_t s, bool probe_phx = false,
+                         int probe_ranks = 1) {
   const int fk = model.kind, ok = ode.kind, mk = ode_model.kind;
   const bool run = pp != nullptr;
+  // instantiations that exist on one rank with numpy-stream / injected increments only
+  if (!run && (probe_phx || probe_ranks > 1) && (ode.n_regions == 2 || g.ppt != 13)) return MMPR_ERR_UNSUPPORTED;
   if (ode.n_regions == 2) {
+    if (g.ppt != 13) return MMPR_ERR_UNSUPPORTED;
     if (fk == MMPR_MODEL_DOUBLE_WELL && ok == MMPR_ODE_MULTIMODAL && mk == MMPR_MODEL_DOUBLE_WELL)
       return run ? dispatch_pipe_regions<MMPR_MODEL_DOUBLE_WELL, MMPR_ODE_MULTIMODAL, MMPR_MODEL_DOUBLE_WELL>(*pp, g, s)
                  : MMPR_OK;
@@ -984,16 +998,22 @@ extern "C" int64_t mmpr_pipeline_flags_size(int32_t n_slices, int32_t iterations
   return 1 + K * N + 2 * (K + 1) * (N + 1) + (K + 1) + 1;  // ..., abort word
 }
 
-extern "C" int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_moment_ode *ode,
-                                       const mmpr_model *ode_model, const mmpr_integrator *integ,
-                                       int64_t particles) {
-  if (!model || !ode || !ode_model || !integ) return MMPR_ERR_ARG;
+extern "C" int mmpr_pipeline_supported_ex(const mmpr_model *model, const mmpr_moment_ode *ode,
+                                          const mmpr_model *ode_model, const mmpr_integrator *integ,
+                                          int64_t particles, int32_t counter_noise, int32_t n_ranks) {
+  if (!model || !ode || !ode_model || !integ || n_ranks < 1) return MMPR_ERR_ARG;
   if (model->stat_kind != MMPR_STAT_MEAN_OF_F || ode->n_regions < 1 || ode->n_regions > 2) return MMPR_ERR_UNSUPPORTED;
   if (integ->kind != MMPR_INTEG_EULER || !(integ->dt > 0.0)) return MMPR_ERR_UNSUPPORTED;
   PipeGeometry g;
   const int st = pipe_geometry(particles, &g);
   if (st != MMPR_OK) return st;
-  return dispatch_pipe(*model, *ode, *ode_model, nullptr, g, nullptr);
+  return dispatch_pipe(*model, *ode, *ode_model, nullptr, g, nullptr, counter_noise != 0, n_ranks);
+}
+
+extern "C" int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_moment_ode *ode,
+                                       const mmpr_model *ode_model, const mmpr_integrator *integ,
+                                       int64_t particles) {
+  return mmpr_pipeline_supported_ex(model, ode, ode_model, integ, particles, 0, 1);
 }
 
 static int check_io(const mmpr_pipeline_io *io, int32_t n_slices, int32_t iterations, int64_t particles,
@@ -1024,7 +1044,8 @@ extern "C" int mmpr_parareal_pipeline_ranks(const mmpr_model *model, const mmpr_
                                             int32_t n_ranks, const mmpr_pipeline_io *ios, int32_t first_rank,
                                             int32_t launch_ranks, int32_t epoch, int32_t reset_flags,
                                             int32_t multi_gpu, void *stream) {
-  int st = mmpr_pipeline_supported(model, ode, ode_model, integ, particles);
+  int st = mmpr_pipeline_supported_ex(model, ode, ode_model, integ, particles,
+                                      (ios && n_ranks >= 1 && ios[0].counter_noise) ? 1 : 0, n_ranks >= 1 ? n_ranks : 1);
   if (st != MMPR_OK) return st;
   if (!ios || n_slices < 1 || iterations < 1 || steps < 0 || n_ranks < 1 || n_ranks > PL_MAX_RANKS ||
       n_slices % n_ranks != 0 || first_rank < 0 || launch_ranks < 1 || first_rank + launch_ranks > n_ranks ||

@@ -164,7 +164,8 @@ def _pipeline_sharded_ok(be, cfg: PararealConfig, plan: NoisePlan, comm) -> bool
     G = comm.world
     ok = (G <= 8 and cfg.n_slices % G == 0 and cfg.iterations >= 1 and not plan.fresh and not plan.counter_based
           and cfg.stop_wasserstein_tol is None and cfg.partition.n_regions == 1
-          and kernels.pipeline_supported(be.model_d, be.ode_d, be.ode_model_d, be.integ_d, cfg.particles))
+          and kernels.pipeline_supported(be.model_d, be.ode_d, be.ode_model_d, be.integ_d, cfg.particles,
+                                            n_ranks=G))
     return comm.all_min_int(1 if ok else 0) == 1
 
 

@@ -285,7 +285,8 @@ class _RunPlan:
         self.pipeline = (allow_pipeline and K >= 1 and pipe_restrict and (not plan.fresh or self.counter)
                          and self.batch == N
                          and not host_snapshots and os.environ.get("MMPR_PIPELINE", "1") != "0"
-                         and kernels.pipeline_supported(model_d, ode_d, ode_model_d, integ_d, P))
+                         and kernels.pipeline_supported(model_d, ode_d, ode_model_d, integ_d, P,
+                                                        counter_noise=bool(self.counter)))
         self.rg_scratch = None
         if self.pipeline:
             self.ws.fine = torch.empty((2, N, P), dtype=torch.float64, device=device())

@@ -239,11 +239,13 @@ def coarse_row(ode: _lib.MomentOde, model: _lib.Model, integ: _lib.Integrator, t
 
 
 def pipeline_supported(model: _lib.Model, ode: _lib.MomentOde, ode_model: _lib.Model, integ: _lib.Integrator,
-                       particles: int) -> bool:
+                       particles: int, counter_noise: bool = False, n_ranks: int = 1) -> bool:
     """True when iterations 1..K of this configuration run as one persistent
-    kernel (mmpr_parareal_pipeline).  Host-only query."""
-    return _lib.load().mmpr_pipeline_supported(ctypes.byref(model), ctypes.byref(ode), ctypes.byref(ode_model),
-                                               ctypes.byref(integ), int(particles)) == 0
+    kernel (mmpr_parareal_pipeline) with this noise supply on this many
+    ranks.  Host-only query."""
+    return _lib.load().mmpr_pipeline_supported_ex(ctypes.byref(model), ctypes.byref(ode), ctypes.byref(ode_model),
+                                                  ctypes.byref(integ), int(particles), int(bool(counter_noise)),
+                                                  int(n_ranks)) == 0
 
 
 # persistent clusters a multi-region pipeline launch may use (its scratch

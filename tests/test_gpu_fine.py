@@ -62,7 +62,9 @@ def test_propagate_fine_matches_reference_golden(mm, golden, name, P):
             assert np.array_equal(out.positions, ref)
 
 
-@pytest.mark.parametrize("P", [8, 100, 10_000, 12_345, 100_000, 131_072, 200_003])
+# (20_000 .. 50_000: one-slice launches spread a slice over 8 x 256-thread CTAs; 40_000 / 50_000 must not --
+# 512 leaf slots at 32 per CTA would be 16 CTAs of 8 warps, more CTAs than the cluster fold has lanes with the total)
+@pytest.mark.parametrize("P", [8, 100, 10_000, 12_345, 20_000, 25_000, 40_000, 50_000, 100_000, 131_072, 200_003])
 def test_injected_mode_bitwise_ou(mm, P):
     """Same seeded increments on both sides: trajectories bit-identical."""
     rng = np.random.default_rng(P)

@@ -53,7 +53,13 @@ def _ou_case(mm, N, K, S, P=100_000, retain=True, dt=1e-3):
 
 
 @pytest.mark.parametrize("N,K,S,P", [(6, 4, 20, 100_000), (3, 1, 10, 100_000), (4, 4, 10, 98_307),
-                                     (40, 3, 6, 100_000), (20, 6, 4, 106_496)])
+                                     (40, 3, 6, 100_000), (20, 6, 4, 106_496),
+                                     # smaller clusters of the 13-element geometry (8 x 512, 8 x 256 threads; tail)
+                                     (4, 3, 8, 50_000), (4, 3, 8, 25_000), (3, 2, 6, 49_157),
+                                     # the 10-element geometry (config 1: 4 x 256; 8 x 256, 8 x 512, 16 x 512,
+                                     # 2 x 256 threads; tail; more slices than iterations, as many)
+                                     (5, 3, 10, 10_000), (4, 3, 8, 20_000), (4, 2, 6, 40_000), (3, 2, 6, 80_000),
+                                     (4, 3, 8, 5_000), (4, 3, 8, 9_221), (12, 5, 10, 10_000), (6, 6, 5, 10_000)])
 def test_pipeline_equals_per_iteration_kernels_ou(mm, monkeypatch, N, K, S, P):
     model, ode, init, cfg = _ou_case(mm, N, K, S, P)
     plan = mm.NoisePlan(0)
@@ -114,7 +120,8 @@ def _bimodal_case(mm, N, K, S, P=100_000, retain=True, init=None):
 
 
 @pytest.mark.parametrize("N,K,S,P,retain", [(8, 4, 16, 100_000, True), (20, 3, 8, 100_000, False),
-                                            (5, 5, 8, 98_307, True), (3, 1, 4, 106_496, True)])
+                                            (5, 5, 8, 98_307, True), (3, 1, 4, 106_496, True),
+                                            (6, 3, 8, 50_000, True), (4, 2, 8, 25_000, False)])
 def test_pipeline_bimodal_equals_per_iteration_kernels(mm, monkeypatch, N, K, S, P, retain):
     """Two regions (config 3): per-region match with pre-transform
     membership and region restrictions over compacted members inside the
@@ -174,6 +181,42 @@ def test_pipeline_counter_noise_equals_per_iteration_kernels(mm, monkeypatch, mo
     plan = mm.NoisePlan(0, getattr(mm.NoiseMode, mode))
     a = _run(mm, monkeypatch, True, model, ode, init, cfg, plan)
     b = _run(mm, monkeypatch, False, model, ode, init, cfg, plan)
+    _same(a, b)
+
+
+def test_small_geometry_is_one_rank_numpy_noise_only(mm, monkeypatch):
+    """The 10-element geometry and the two-region units exist for one rank
+    and numpy-stream / injected increments: with counter noise the engine
+    keeps the per-iteration kernels (and still matches the pipeline-free
+    run bit for bit, trivially), and the support query says so."""
+    from paper_2310_11365_b200 import kernels
+    from paper_2310_11365_b200.models import device_model
+    from paper_2310_11365_b200.moments import device_ode
+    from paper_2310_11365_b200.rk54 import integrator_descriptor
+    model, ode, init, cfg = _ou_case(mm, 4, 2, 6, 10_000)
+    ode_d, ode_model_d = device_ode(ode)
+    args = (device_model(model), ode_d, ode_model_d, integrator_descriptor(cfg.integrator))
+    assert kernels.pipeline_supported(*args, 10_000)
+    assert not kernels.pipeline_supported(*args, 10_000, counter_noise=True)
+    assert not kernels.pipeline_supported(*args, 10_000, n_ranks=2)
+    assert kernels.pipeline_supported(*args, 100_000, counter_noise=True, n_ranks=2)
+    assert not kernels.pipeline_supported(*args, 9_999)
+    monkeypatch.setenv("MMPR_PIPELINE", "1")
+    mm.engine.clear_graph_cache()
+    mm.run_micro_macro(model, ode, init, cfg, mm.NoisePlan(0, mm.NoiseMode.PHILOX))
+    assert mm.engine.last_run_info["pipeline"] is False
+    mm.engine.clear_graph_cache()
+
+
+def test_pipeline_cubic_small_geometry(mm, monkeypatch):
+    """The cubic mean-field model with its Gaussian closure at P = 2e4 (10 elements per lane, 8 x 256 threads)."""
+    spec = mm.CubicMeanFieldSpec(1.0, 1.0, 1.0, 0.4)
+    model = mm.make_cubic_meanfield(spec)
+    cfg = mm.PararealConfig(n_slices=6, iterations=3, slice_length=0.03125, particles=20_000,
+                            step=mm.StepConfig(2.0 ** -10, 32), integrator=mm.EulerConfig(2.0 ** -6))
+    args = (model, mm.gaussian_closure_rhs(spec), mm.InitialDistribution.normal(0.5, 0.04), cfg, mm.NoisePlan(0))
+    a = _run(mm, monkeypatch, True, *args)
+    b = _run(mm, monkeypatch, False, *args)
     _same(a, b)
 
 

@@ -52,7 +52,13 @@ def test_pipeline_support_query_without_a_gpu():
     euler = engine.integrator_descriptor(mm.EulerConfig(1e-2))
     assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 100_000)
     assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 98_307)
-    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 10_000)  # other geometry
+    assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 10_000)  # 10 elements per lane (config 1)
+    assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 50_000)  # 13 per lane, 8-CTA cluster
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 10_000, counter_noise=True)
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 10_000, n_ranks=2)
+    assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 100_000, counter_noise=True, n_ranks=2)
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 9_999)  # other geometry
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 30_000)
     assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 20)
     dp54 = engine.integrator_descriptor(mm.IntegratorConfig())
     assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, dp54, 100_000)
@@ -64,6 +70,8 @@ def test_pipeline_support_query_without_a_gpu():
     dwm = mm.make_double_well(dw)
     ode_m, odm_m = moments.device_ode(mm.multimodal_rhs(dwm, dw.default_partition(), dw.potential, dw.sigma))
     assert kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 100_000)  # two regions (config 3)
+    assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 100_000, counter_noise=True)
+    assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 10_000)
     assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, dp54, 100_000)
     three = mm.RegionPartition(separatrices=(-0.5, 0.5), peaks=(-1.0, 0.0, 1.0))
     ode_3, odm_3 = moments.device_ode(mm.multimodal_rhs(dwm, three, dw.potential, dw.sigma))
