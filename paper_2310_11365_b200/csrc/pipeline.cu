@@ -813,12 +813,13 @@ struct PipeGeometry {
 
 // The pipeline covers the cluster geometries of the fine sweep whose leaves
 // hold PPT-1 or PPT accumulator elements per lane for an instantiated PPT:
-// 13 (P = 1e5 and its binary fractions down to 1.25e4: 96..104-particle
-// leaves; BASELINE configs 2-4) and 10 (P = 1e4, 2e4, 4e4, 8e4: 72..80;
-// BASELINE config 1), one cluster of up to 16 CTAs per unit -- 64 leaf
-// slots (512 threads) per CTA from 512 slots on, 32 (256 threads) below,
-// where a launch has too few units to fill the SMs otherwise.  Other sizes
-// keep the per-iteration kernels.
+// 13 (96..104-particle leaves: P = 1e5 and its binary fractions down to
+// 6.25e3 -- BASELINE configs 2-4), 10 (72..80: P = 1e4, 2e4, 4e4, 8e4 --
+// BASELINE config 1) and 16 (120..128: the powers of two from 2^13 to 2^17
+// and sizes just below them), one cluster of up to 16 CTAs per unit -- 64
+// leaf slots (512 threads) per CTA from 512 slots on, 32 (256 threads)
+// below, where a launch has too few units to fill the SMs otherwise.  Other
+// sizes keep the per-iteration kernels.
 static int pipe_geometry(int64_t P, PipeGeometry *g) {
   if (P < 1) return MMPR_ERR_ARG;
   const int D = pw_depth(P);
@@ -832,7 +833,7 @@ static int pipe_geometry(int64_t P, PipeGeometry *g) {
     if (l < min_leaf) min_leaf = l;
   }
   g->ppt = (int)((max_leaf + 7) / 8);
-  if ((g->ppt != 13 && g->ppt != 10) || (min_leaf >> 3) < g->ppt - 1) return MMPR_ERR_UNSUPPORTED;
+  if ((g->ppt != 13 && g->ppt != 10 && g->ppt != 16) || (min_leaf >> 3) < g->ppt - 1) return MMPR_ERR_UNSUPPORTED;
   g->D = D;
   g->spc = nslots >= 512 ? 64 : 32;
   g->ctas = (int)(nslots / g->spc);
@@ -848,7 +849,8 @@ static int pipe_geometry(int64_t P, PipeGeometry *g) {
   g->stage_elems = (int)((max_range + 1) & ~int64_t(1));
   g->nstages = 2;
   g->smem = (size_t)g->stage_elems * 8 * g->nstages + 64;  // + pad for the unclamped last element
-  if (g->smem > 112 * 1024) return MMPR_ERR_UNSUPPORTED;  // two CTAs per SM
+  // two CTAs per SM where the stages allow it (P ~ 2^16 and 2^17 keep one: 64 KB per stage)
+  if (g->smem > 226 * 1024) return MMPR_ERR_UNSUPPORTED;
   g->tail = (P % 8) != 0;
   return MMPR_OK;
 }
@@ -911,8 +913,12 @@ static int dispatch_pipe_regions(const PipeParams &pp, const PipeGeometry &g, cu
 
 template <int KIND, int OK, int MK>
 static int dispatch_pipe_tail(const PipeParams &pp, const PipeGeometry &g, cudaStream_t s) {
-  if (g.ppt == 10) {  // the small geometry: one rank, numpy-stream or injected increments
+  if (g.ppt != 13) {  // the other geometries: one rank, numpy-stream or injected increments
     if (pp.phx || pp.G > 1) return MMPR_ERR_UNSUPPORTED;
+    if (g.ppt == 16) {
+      if (g.tail) return launch_pipe<pipeline_kernel<KIND, 16, true, OK, MK, false>>(pp, g, s);
+      return launch_pipe<pipeline_kernel<KIND, 16, false, OK, MK, false>>(pp, g, s);
+    }
     if (g.tail) return launch_pipe<pipeline_kernel<KIND, 10, true, OK, MK, false>>(pp, g, s);
     return launch_pipe<pipeline_kernel<KIND, 10, false, OK, MK, false>>(pp, g, s);
   }

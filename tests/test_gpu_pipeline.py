@@ -59,7 +59,12 @@ def _ou_case(mm, N, K, S, P=100_000, retain=True, dt=1e-3):
                                      # the 10-element geometry (config 1: 4 x 256; 8 x 256, 8 x 512, 16 x 512,
                                      # 2 x 256 threads; tail; more slices than iterations, as many)
                                      (5, 3, 10, 10_000), (4, 3, 8, 20_000), (4, 2, 6, 40_000), (3, 2, 6, 80_000),
-                                     (4, 3, 8, 5_000), (4, 3, 8, 9_221), (12, 5, 10, 10_000), (6, 6, 5, 10_000)])
+                                     (4, 3, 8, 5_000), (4, 3, 8, 9_221), (12, 5, 10, 10_000), (6, 6, 5, 10_000),
+                                     # the 16-element geometry (powers of two and sizes just below: 4 x 256,
+                                     # 2 x 256, 8 x 256, 8 x 512 and 16 x 512 threads -- the last two with one
+                                     # CTA per SM, 64 KB per increment stage; tail)
+                                     (5, 3, 8, 16_384), (4, 2, 6, 8_192), (4, 3, 6, 32_768), (4, 2, 6, 65_536),
+                                     (20, 3, 4, 131_072), (4, 3, 8, 7_685), (3, 2, 6, 122_885)])
 def test_pipeline_equals_per_iteration_kernels_ou(mm, monkeypatch, N, K, S, P):
     model, ode, init, cfg = _ou_case(mm, N, K, S, P)
     plan = mm.NoisePlan(0)

@@ -57,6 +57,9 @@ def test_pipeline_support_query_without_a_gpu():
     assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 10_000, counter_noise=True)
     assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 10_000, n_ranks=2)
     assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 100_000, counter_noise=True, n_ranks=2)
+    assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 17)  # 16 per lane, 16-CTA cluster
+    assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 13)
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 17, counter_noise=True)
     assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 9_999)  # other geometry
     assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 30_000)
     assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 20)
