@@ -437,10 +437,11 @@ int64_t mmpr_pipeline_flags_size(int32_t n_slices, int32_t iterations);
 int mmpr_set_fine_times(int64_t *slice_times);
 
 /* MMPR_OK when (model, ode, ode_model, integrator, particles) has a pipeline
- * instantiation (MEAN_OF_F, forward-Euler coarse, a cluster geometry with
+ * instantiation (MEAN_OF_F, forward-Euler coarse, an ensemble of one
+ * cluster: 4096 < P <= 2^17 with a balanced pairwise tree -- specialised for
  * 13, 10 or 16 accumulator elements per lane: P = 1e5 / 1e4 and their binary
- * fractions / multiples within one cluster, powers of two from 2^13 to 2^17;
- * one region, or two regions for
+ * fractions / multiples, powers of two from 2^13 to 2^17 -- and an any-size
+ * form otherwise; one region, or two regions for
  * the double well with the multimodal closure on one rank); else
  * MMPR_ERR_UNSUPPORTED
  * and the caller runs the per-iteration kernels. */
@@ -449,7 +450,7 @@ int mmpr_pipeline_supported(const mmpr_model *model, const mmpr_moment_ode *ode,
                             int64_t particles);
 
 /* The same for a given noise supply and rank count: the two-region units and
- * the 10- and 16-element geometries exist for
+ * every geometry but the 13-element one exist for
  * one rank with numpy-stream or injected increments only (counter_noise = 0,
  * n_ranks = 1).  Replaces nothing in the reference (engine.py:127-259 has no
  * such switch); the host uses it to choose between the pipeline and the

@@ -295,9 +295,12 @@ __device__ __forceinline__ void pl_advance_chain(const PipeParams &pp, int k, in
 // region with membership from the pre-transform positions, and R(u^k_n) /
 // R(F^k_n) are region restrictions over compacted members (rg_restrict,
 // regions_device.cuh) instead of the single-region tree passes.
-template <int KIND, int PPT, bool HAS_TAIL, int OK, int MK, bool MULTI, bool PHX = false, int NR = 1>
+// LOW >= 0 (the any-size form, PPT = 16): every leaf has at least LOW
+// accumulator elements per lane (numpy's leaves hold 64..128 particles once
+// an ensemble has more than one, so 8), the rest carry a predicate.
+template <int KIND, int PPT, bool HAS_TAIL, int OK, int MK, bool MULTI, bool PHX = false, int NR = 1, int LOW = -1>
 __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(const PipeParams pp) {
-  constexpr int LO = PPT - 1;  // every leaf has PPT-1 or PPT accumulator elements per lane
+  constexpr int LO = LOW >= 0 ? LOW : PPT - 1;  // LOW < 0: every leaf has PPT-1 or PPT elements per lane
   constexpr int NV = 3 * NR;   // macro state: means, variances, fractions per region
   using PartT = Part<false>;
   const FineParams &p = pp.f;
@@ -714,9 +717,9 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
             if (m < LO) {
               x[m] = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
             } else {
-              // past a 12-element leaf this reads up to 8 doubles beyond the
-              // CTA's range (into the next stage or the 64-byte pad after the
-              // last): the value is discarded, so no clamp is needed
+              // past a shorter leaf this reads up to 8 (PPT - LO) doubles
+              // beyond the CTA's range (into the next stage or the pad after
+              // the last): the value is discarded, so no clamp is needed
               const double nx = em_update<KIND>(p, x[m], s, xb[my_idx + 8 * m]);
               x[m] = (m < cnt) ? nx : x[m];
             }
@@ -807,6 +810,7 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
 // ---------------------------------------------------------------------------
 struct PipeGeometry {
   int D, spc, ctas, threads, stage_elems, nstages, ppt;
+  bool exact;  // every leaf has ppt-1 or ppt elements per lane and ppt is instantiated (else the any-size form)
   size_t smem;
   bool tail;
 };
@@ -818,8 +822,10 @@ struct PipeGeometry {
 // BASELINE config 1) and 16 (120..128: the powers of two from 2^13 to 2^17
 // and sizes just below them), one cluster of up to 16 CTAs per unit -- 64
 // leaf slots (512 threads) per CTA from 512 slots on, 32 (256 threads)
-// below, where a launch has too few units to fill the SMs otherwise.  Other
-// sizes keep the per-iteration kernels.
+// below, where a launch has too few units to fill the SMs otherwise.  Any
+// other size within one cluster (more than 4096 particles, at most 2^17)
+// takes the any-size form: 16 elements per lane, the first 8 unconditional
+// (numpy's leaves hold 64..128 particles), the rest predicated.
 static int pipe_geometry(int64_t P, PipeGeometry *g) {
   if (P < 1) return MMPR_ERR_ARG;
   const int D = pw_depth(P);
@@ -833,7 +839,8 @@ static int pipe_geometry(int64_t P, PipeGeometry *g) {
     if (l < min_leaf) min_leaf = l;
   }
   g->ppt = (int)((max_leaf + 7) / 8);
-  if ((g->ppt != 13 && g->ppt != 10 && g->ppt != 16) || (min_leaf >> 3) < g->ppt - 1) return MMPR_ERR_UNSUPPORTED;
+  g->exact = (g->ppt == 13 || g->ppt == 10 || g->ppt == 16) && (min_leaf >> 3) >= g->ppt - 1;
+  if (!g->exact && (g->ppt > 16 || (min_leaf >> 3) < 8)) return MMPR_ERR_UNSUPPORTED;
   g->D = D;
   g->spc = nslots >= 512 ? 64 : 32;
   g->ctas = (int)(nslots / g->spc);
@@ -848,7 +855,8 @@ static int pipe_geometry(int64_t P, PipeGeometry *g) {
   }
   g->stage_elems = (int)((max_range + 1) & ~int64_t(1));
   g->nstages = 2;
-  g->smem = (size_t)g->stage_elems * 8 * g->nstages + 64;  // + pad for the unclamped last element
+  // + pad for the unclamped elements past a short leaf (8 doubles per missing element)
+  g->smem = (size_t)g->stage_elems * 8 * g->nstages + (g->exact ? 64 : 8 * 8 * 8);
   // two CTAs per SM where the stages allow it (P ~ 2^16 and 2^17 keep one: 64 KB per stage)
   if (g->smem > 226 * 1024) return MMPR_ERR_UNSUPPORTED;
   g->tail = (P % 8) != 0;
@@ -913,8 +921,12 @@ static int dispatch_pipe_regions(const PipeParams &pp, const PipeGeometry &g, cu
 
 template <int KIND, int OK, int MK>
 static int dispatch_pipe_tail(const PipeParams &pp, const PipeGeometry &g, cudaStream_t s) {
-  if (g.ppt != 13) {  // the other geometries: one rank, numpy-stream or injected increments
+  if (g.ppt != 13 || !g.exact) {  // the other geometries: one rank, numpy-stream or injected increments
     if (pp.phx || pp.G > 1) return MMPR_ERR_UNSUPPORTED;
+    if (!g.exact) {  // any size within one cluster: 16 elements per lane, at least 8 of them populated
+      if (g.tail) return launch_pipe<pipeline_kernel<KIND, 16, true, OK, MK, false, false, 1, 8>>(pp, g, s);
+      return launch_pipe<pipeline_kernel<KIND, 16, false, OK, MK, false, false, 1, 8>>(pp, g, s);
+    }
     if (g.ppt == 16) {
       if (g.tail) return launch_pipe<pipeline_kernel<KIND, 16, true, OK, MK, false>>(pp, g, s);
       return launch_pipe<pipeline_kernel<KIND, 16, false, OK, MK, false>>(pp, g, s);
@@ -949,9 +961,9 @@ static int dispatch_pipe(const mmpr_model &model, const mmpr_moment_ode &ode, co
   const int fk = model.kind, ok = ode.kind, mk = ode_model.kind;
   const bool run = pp != nullptr;
   // instantiations that exist on one rank with numpy-stream / injected increments only
-  if (!run && (probe_phx || probe_ranks > 1) && (ode.n_regions == 2 || g.ppt != 13)) return MMPR_ERR_UNSUPPORTED;
+  if (!run && (probe_phx || probe_ranks > 1) && (ode.n_regions == 2 || g.ppt != 13 || !g.exact)) return MMPR_ERR_UNSUPPORTED;
   if (ode.n_regions == 2) {
-    if (g.ppt != 13) return MMPR_ERR_UNSUPPORTED;
+    if (g.ppt != 13 || !g.exact) return MMPR_ERR_UNSUPPORTED;
     if (fk == MMPR_MODEL_DOUBLE_WELL && ok == MMPR_ODE_MULTIMODAL && mk == MMPR_MODEL_DOUBLE_WELL)
       return run ? dispatch_pipe_regions<MMPR_MODEL_DOUBLE_WELL, MMPR_ODE_MULTIMODAL, MMPR_MODEL_DOUBLE_WELL>(*pp, g, s)
                  : MMPR_OK;

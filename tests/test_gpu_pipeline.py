@@ -64,7 +64,11 @@ def _ou_case(mm, N, K, S, P=100_000, retain=True, dt=1e-3):
                                      # 2 x 256, 8 x 256, 8 x 512 and 16 x 512 threads -- the last two with one
                                      # CTA per SM, 64 KB per increment stage; tail)
                                      (5, 3, 8, 16_384), (4, 2, 6, 8_192), (4, 3, 6, 32_768), (4, 2, 6, 65_536),
-                                     (20, 3, 4, 131_072), (4, 3, 8, 7_685), (3, 2, 6, 122_885)])
+                                     (20, 3, 4, 131_072), (4, 3, 8, 7_685), (3, 2, 6, 122_885),
+                                     # the any-size form (16 per lane, at least 8 populated): 9..15 elements,
+                                     # ragged leaves, tails, the smallest and largest ensembles of one cluster
+                                     (4, 3, 8, 9_999), (4, 3, 8, 30_000), (3, 2, 6, 70_000), (3, 2, 6, 120_001),
+                                     (4, 2, 6, 4_608), (4, 3, 8, 12_345), (6, 4, 10, 60_000), (3, 3, 6, 90_000)])
 def test_pipeline_equals_per_iteration_kernels_ou(mm, monkeypatch, N, K, S, P):
     model, ode, init, cfg = _ou_case(mm, N, K, S, P)
     plan = mm.NoisePlan(0)
@@ -205,7 +209,8 @@ def test_small_geometry_is_one_rank_numpy_noise_only(mm, monkeypatch):
     assert not kernels.pipeline_supported(*args, 10_000, counter_noise=True)
     assert not kernels.pipeline_supported(*args, 10_000, n_ranks=2)
     assert kernels.pipeline_supported(*args, 100_000, counter_noise=True, n_ranks=2)
-    assert not kernels.pipeline_supported(*args, 9_999)
+    assert kernels.pipeline_supported(*args, 9_999) and not kernels.pipeline_supported(*args, 9_999, counter_noise=True)
+    assert not kernels.pipeline_supported(*args, 4_096)
     monkeypatch.setenv("MMPR_PIPELINE", "1")
     mm.engine.clear_graph_cache()
     mm.run_micro_macro(model, ode, init, cfg, mm.NoisePlan(0, mm.NoiseMode.PHILOX))

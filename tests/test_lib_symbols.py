@@ -60,8 +60,11 @@ def test_pipeline_support_query_without_a_gpu():
     assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 17)  # 16 per lane, 16-CTA cluster
     assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 13)
     assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 17, counter_noise=True)
-    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 9_999)  # other geometry
-    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 30_000)
+    assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 9_999)  # any-size form (16 per lane, >= 8)
+    assert kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 30_000)
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 30_000, counter_noise=True)
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 4_096)  # fewer than 64 leaf slots
+    assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 17 + 8)  # beyond one cluster
     assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, euler, 2 ** 20)
     dp54 = engine.integrator_descriptor(mm.IntegratorConfig())
     assert not kernels.pipeline_supported(m.descriptor, ode, ode_model, dp54, 100_000)
@@ -75,6 +78,7 @@ def test_pipeline_support_query_without_a_gpu():
     assert kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 100_000)  # two regions (config 3)
     assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 100_000, counter_noise=True)
     assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 10_000)
+    assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 99_999)  # two regions: 13 per lane only
     assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, dp54, 100_000)
     three = mm.RegionPartition(separatrices=(-0.5, 0.5), peaks=(-1.0, 0.0, 1.0))
     ode_3, odm_3 = moments.device_ode(mm.multimodal_rhs(dwm, three, dw.potential, dw.sigma))
