@@ -7,7 +7,7 @@ import torch
 import paper_2310_11365_b200 as mm
 from paper_2310_11365_b200 import kernels
 
-N, S, P = int(os.environ.get("NG", "32")), 200, 1 << 20
+N, S, P = int(os.environ.get("NG", "32")), 200, int(os.environ.get("PG", str(1 << 20)))
 xi = kernels.noise_buffer(N, S, P)
 xi.normal_()
 dw5 = mm.DoubleWellSpec(alpha=0.25, gamma=0.4, beta=0.2, J=0.0, sigma=0.3 * math.sqrt(1.8))
