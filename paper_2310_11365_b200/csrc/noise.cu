@@ -465,7 +465,9 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
   const int lane = threadIdx.x;
 #pragma unroll
   for (int i = lane; i < 256; i += 32) {
-    zig[i] = make_ulonglong2(c_zig_ki[i], (unsigned long long)__double_as_longlong(c_zig_wi[i]));
+    // ki as the double 2^52 + ki (exact: ki < 2^52), so the fast-accept test
+    // is one FP64 compare against the 2^52 + mant the transform builds anyway
+    zig[i] = make_ulonglong2(0x4330000000000000ULL | c_zig_ki[i], (unsigned long long)__double_as_longlong(c_zig_wi[i]));
     s_fi[i] = c_zig_fi[i];
   }
   __syncwarp();
@@ -474,6 +476,9 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
 
   int carry = 0;
   int64_t produced = 0;
+  uint32_t m20, e52;  // opaque to the compiler, so they stay in registers (see the transform)
+  asm volatile("mov.b32 %0, 0x000FFFFF;" : "=r"(m20));
+  asm volatile("mov.b32 %0, 0x43300000;" : "=r"(e52));
   for (uint64_t sub = 0; produced < count; ++sub) {
     const uint64_t word0 = (sub * 32 + lane) * NW_WORDS;
     // fast path for every word, branch-free, eight words (two Philox blocks)
@@ -490,13 +495,17 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const uint64_t rw = w[i];
-        const uint64_t mant = (rw >> 9) & 0x000fffffffffffffULL;
         const ulonglong2 z = zig[rw & 0xff];
         const double wi = __longlong_as_double((long long)z.y);
-        const double v = __fma_rn(__longlong_as_double((long long)(0x4330000000000000ULL | mant)), wi, -0x1.0p52 * wi);
+        // 2^52 + mant, mant = (rw >> 9) & (2^52 - 1): the high half's mask and
+        // exponent in one LOP3 (both constants in registers)
+        uint32_t dhi;
+        asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(dhi) : "r"((uint32_t)(rw >> 41)), "r"(m20), "r"(e52));
+        const double d = __hiloint2double((int)dhi, (int)(uint32_t)(rw >> 9));
+        const double v = __fma_rn(d, wi, -0x1.0p52 * wi);
         // sign bit 8 of the word -> sign of the double (one LOP3 on the high half)
         x[g + i] = __hiloint2double(__double2hiint(v) ^ (int)(((uint32_t)rw << 23) & 0x80000000u), __double2loint(v));
-        nf |= (mant >= z.x ? 1u : 0u) << (g + i);
+        nf |= (d >= __longlong_as_double((long long)z.x) ? 1u : 0u) << (g + i);
       }
       ulonglong2 *row = reinterpret_cast<ulonglong2 *>(&s_w[lane * NW_WORDS + g]);
       row[0] = make_ulonglong2(w[0], w[1]);
