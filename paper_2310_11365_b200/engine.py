@@ -605,6 +605,12 @@ def _raise_first_error(h, N: int, K: int, I: int) -> None:
     if (h["bad"] == _lib.STAT_WATCHDOG).any() or (h["match_status"] == _lib.STAT_WATCHDOG).any():
         raise _lib.MmprError("iteration pipeline watchdog expired: a dependency between (k, n) units never "
                              "arrived; the run's results were discarded")
+    # nothing to report (the usual case): three array comparisons instead of
+    # the ordered scan below (which costs ~0.3 ms of host time for 64 x 5
+    # units, with the GPU idle behind it)
+    if (not (h["coarse_status"][:K + 1, :N] != _lib.STAT_OK).any() and not (h["bad"][:K, :N] != _lib.STAT_OK).any()
+            and not (h["match_status"][1:K + 1, :N] >= 0).any()):
+        return
     for n in range(N):
         if h["coarse_status"][0, n] != _lib.STAT_OK:
             raise _coarse_error(int(h["coarse_status"][0, n]), n, 0)
