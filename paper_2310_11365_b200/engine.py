@@ -120,6 +120,17 @@ class PararealTrace:
     def iterations(self) -> int:
         return len(self.macro) - 1
 
+    def __getattr__(self, name):
+        # diagnostics of an engine-built trace (clamp_events, fraction_gaps,
+        # lift_collapses, timings) are lists of Python tuples built on first
+        # access: building them eagerly is host time the GPU idles behind
+        lazy = self.__dict__.get("_lazy")
+        if lazy is not None and name in lazy:
+            value = lazy.pop(name)()
+            self.__dict__[name] = value
+            return value
+        raise AttributeError(name)
+
 
 class _StageTimer:
     """CUDA-event timing of engine stages, resolved after the run."""
@@ -178,13 +189,16 @@ class _Workspace:
                   "coarse_status": (K + 1, N),
                   "match_status": (K + 1, N)}
         self.report = {}
+        self.layout = {}  # dtype -> [(name, offset, size, shape)] of the packed report buffer
         for names, dtype in ((self.F64, torch.float64), (self.I64, torch.int64), (self.I32, torch.int32)):
             sizes = [int(np.prod(shapes[n])) for n in names]
             flat = torch.zeros(sum(sizes), dtype=dtype, device=dev)
             self.report[dtype] = flat
             off = 0
+            self.layout[dtype] = []
             for n, size in zip(names, sizes):
                 setattr(self, n, flat[off:off + size].view(shapes[n]))
+                self.layout[dtype].append((n, off, size, shapes[n]))
                 off += size
         self.snap = torch.empty((K + 1 if retain else 2, N + 1, P), dtype=torch.float64, device=dev)
         self.fine = torch.empty((N, P), dtype=torch.float64, device=dev)
@@ -210,15 +224,14 @@ class _Workspace:
         for dt, t in self.report.items():
             self.host[dt].copy_(t, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        # (host time from here to the next run's first launch is GPU idle
+        # time: one copy per packed buffer -- the pinned buffers are reused by
+        # the next run -- and views into it)
         h = {}
-        for names, dt in ((self.F64, torch.float64), (self.I64, torch.int64), (self.I32, torch.int32)):
-            flat = self.host[dt].numpy()
-            off = 0
-            for n in names:
-                shape = getattr(self, n).shape
-                size = int(np.prod(shape))
-                h[n] = flat[off:off + size].reshape(shape).copy()
-                off += size
+        for dt, entries in self.layout.items():
+            flat = self.host[dt].numpy().copy()
+            for n, off, size, shape in entries:
+                h[n] = flat[off:off + size].reshape(shape)
         return h
 
     def report_bytes(self) -> int:
@@ -694,19 +707,29 @@ def _build_trace(h, ws, cfg, plan, times, K, I, timer, stopped_at) -> PararealTr
     trace = PararealTrace(times=times, macro=_LazyRows(K + 1, macro_row), micro_stats=_LazyRows(K + 1, micro_row),
                           snapshots=snapshots, noise_mode=plan.mode.value, master_seed=plan.master_seed,
                           stopped_at=stopped_at)
-    # diagnostics (engine.py:178-181, 218-228), vectorised: abs/sub/max are exact
+    # diagnostics (engine.py:178-181, 218-228), vectorised (abs/sub/max are
+    # exact) and built on first access (PararealTrace.__getattr__)
     rho0 = h["rho0"][0]
-    lift = (rho0[I:2 * I] == 0.0) & (macro[0, 1:, I:2 * I] > 0.0) & (rho0[2 * I:] > 0.0)
-    trace.lift_collapses = [(0, int(n) + 1, int(i)) for n, i in np.argwhere(lift)]
-    gaps0 = np.max(np.abs(macro[0, 1:, 2 * I:] - micro[0, 1:, 2 * I:]), axis=1).tolist()
-    trace.fraction_gaps = [(0, n + 1, g) for n, g in enumerate(gaps0)]
-    if K > 0:
-        raw, fine = h["raw"][:K], h["fine_stats"][:K]
-        gaps = np.max(np.abs(raw[:, :, 2 * I:] - fine[:, :, 2 * I:]), axis=2).tolist()
-        trace.fraction_gaps += [(k + 1, n + 1, gaps[k][n]) for k in range(K) for n in range(N)]
-        neg = raw[:, :, I:2 * I]
-        trace.clamp_events = [(int(k) + 1, int(n) + 1, int(i), float(neg[k, n, i]))
-                              for k, n, i in np.argwhere(neg < 0.0)]
+
+    def lift_collapses():
+        lift = (rho0[I:2 * I] == 0.0) & (macro[0, 1:, I:2 * I] > 0.0) & (rho0[2 * I:] > 0.0)
+        return [(0, int(n) + 1, int(i)) for n, i in np.argwhere(lift)]
+
+    def fraction_gaps():
+        gaps0 = np.max(np.abs(macro[0, 1:, 2 * I:] - micro[0, 1:, 2 * I:]), axis=1).tolist()
+        out = [(0, n + 1, g) for n, g in enumerate(gaps0)]
+        if K > 0:
+            raw, fine = h["raw"][:K], h["fine_stats"][:K]
+            gaps = np.max(np.abs(raw[:, :, 2 * I:] - fine[:, :, 2 * I:]), axis=2).tolist()
+            out += [(k + 1, n + 1, gaps[k][n]) for k in range(K) for n in range(N)]
+        return out
+
+    def clamp_events():
+        if K == 0:
+            return []
+        neg = h["raw"][:K][:, :, I:2 * I]
+        return [(int(k) + 1, int(n) + 1, int(i), float(neg[k, n, i])) for k, n, i in np.argwhere(neg < 0.0)]
+
     # the reference's timings (engine.py:149-233): per-slice fine propagation
     # times, here device time between each slice's first and last step
     # (globaltimer, so per-slice times overlap as the slices run
@@ -714,14 +737,22 @@ def _build_trace(h, ws, cfg, plan, times, K, I, timer, stopped_at) -> PararealTr
     # (record_timings=True), every stage including the noise and the
     # iteration pipeline in stage_timings
     stages = timer.resolve()
-    ft = h.get("fine_times")
-    if ft is not None:
-        ft = ft[:K].astype(np.int64)
-        fine = np.where((ft[..., 0] > 0) & (ft[..., 1] >= ft[..., 0]), (ft[..., 1] - ft[..., 0]) * 1e-9, 0.0)
-    else:  # multi-rank drivers: not gathered
-        fine = np.zeros((0,))
-    trace.timings = {"coarse": list(stages.get("coarse", [])), "fine": fine.reshape(-1).tolist(),
-                     "restrict": list(stages.get("restrict", [])), "match": list(stages.get("match", []))}
+
+    def timings():
+        ft = h.get("fine_times")
+        if ft is not None:
+            ft = ft[:K].astype(np.int64)
+            fine = np.where((ft[..., 0] > 0) & (ft[..., 1] >= ft[..., 0]), (ft[..., 1] - ft[..., 0]) * 1e-9, 0.0)
+        else:  # multi-rank drivers: not gathered
+            fine = np.zeros((0,))
+        return {"coarse": list(stages.get("coarse", [])), "fine": fine.reshape(-1).tolist(),
+                "restrict": list(stages.get("restrict", [])), "match": list(stages.get("match", []))}
+
+    lazy = {"lift_collapses": lift_collapses, "fraction_gaps": fraction_gaps, "clamp_events": clamp_events,
+            "timings": timings}
+    for name in lazy:
+        del trace.__dict__[name]
+    trace.__dict__["_lazy"] = lazy
     trace.stage_timings = stages
     return trace
 
