@@ -167,6 +167,11 @@ const char *mmpr_version(void);
 /* Last CUDA error string recorded by a failing call on this thread. */
 const char *mmpr_last_error(void);
 
+/* Kernels this library has launched in this process so far (every launch
+ * site counts; a call may launch several).  Host-side bookkeeping for the
+ * benchmark's launch claim; nothing in the reference corresponds to it. */
+uint64_t mmpr_kernel_launches(void);
+
 /* mmpr_fine_sweep / mmpr_fine_sweep_restrict with counter-based Philox
  * increments generated in registers (no xi buffer).  stats/counts may be
  * NULL (no fused restriction). */

@@ -111,6 +111,7 @@ _D = ctypes.c_double
 SIGNATURES = {
     "mmpr_version": (ctypes.c_char_p, []),
     "mmpr_last_error": (ctypes.c_char_p, []),
+    "mmpr_kernel_launches": (ctypes.c_uint64, []),
     "mmpr_fine_sweep_occupancy": (ctypes.c_int, [_I64, _P, _P]),
     "mmpr_set_fine_times": (ctypes.c_int, [_P]),
     "mmpr_noise_keys": (ctypes.c_int, [_U64, _I32, _I32, _I32, _I32, _I32, _P, _P]),
@@ -195,9 +196,12 @@ launch_count = {"total": 0}
 def call(name: str, *args) -> None:
     """Invoke a status-returning entry point; raise MmprError on failure."""
     lib = load()
-    if name in LAUNCHING:
-        launch_count["total"] += 1
-    status = getattr(lib, name)(*args)
+    if name in LAUNCHING:  # kernels the call launched (libmmpr's own counter: a call may launch several)
+        before = lib.mmpr_kernel_launches()
+        status = getattr(lib, name)(*args)
+        launch_count["total"] += int(lib.mmpr_kernel_launches() - before)
+    else:
+        status = getattr(lib, name)(*args)
     if status != 0:
         detail = lib.mmpr_last_error().decode(errors="replace")
         raise MmprError(f"{name} failed: {STATUS_TEXT.get(status, status)}"

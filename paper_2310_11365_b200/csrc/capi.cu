@@ -9,6 +9,7 @@
 #endif
 
 static thread_local char g_last_error[512] = "";
+unsigned long long g_mmpr_kernel_launches = 0;
 
 void mmpr_set_error(const char *what, cudaError_t err) {
   snprintf(g_last_error, sizeof g_last_error, "%s: %s", what, cudaGetErrorString(err));
@@ -17,3 +18,5 @@ void mmpr_set_error(const char *what, cudaError_t err) {
 extern "C" const char *mmpr_version(void) { return "mmpr " MMPR_GIT_VERSION " sm_100a"; }
 
 extern "C" const char *mmpr_last_error(void) { return g_last_error; }
+
+extern "C" uint64_t mmpr_kernel_launches(void) { return (uint64_t)g_mmpr_kernel_launches; }

@@ -8,6 +8,11 @@
 // Records `what: cudaGetErrorString(err)` for mmpr_last_error().
 void mmpr_set_error(const char *what, cudaError_t err);
 
+// Kernel launches issued by this library in this process (mmpr_kernel_launches):
+// every launch site bumps it, so the host's launch claim counts kernels, not calls.
+extern unsigned long long g_mmpr_kernel_launches;
+static inline void mmpr_launched(int n = 1) { g_mmpr_kernel_launches += (unsigned long long)n; }
+
 // Checks the last launch; returns MMPR_OK or MMPR_ERR_CUDA.
 static inline int mmpr_check_launch(const char *what) {
   cudaError_t err = cudaGetLastError();

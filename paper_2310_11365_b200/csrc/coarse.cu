@@ -334,7 +334,7 @@ template <int NV, int OK, int MK>
 struct RowLaunch {
   using Args = RowArgs;
   static int run(const Args &a) {
-    coarse_row_kernel<NV, OK, MK><<<1, 32, 0, a.stream>>>(a.p);
+    coarse_row_kernel<NV, OK, MK><<<1, 32, 0, a.stream>>>(a.p); mmpr_launched();
     return mmpr_check_launch("coarse_row_kernel");
   }
 };
@@ -357,7 +357,7 @@ struct MacroLaunch {
     const int threads = 64;
     const int blocks = (a.n_states + threads - 1) / threads;
     integrate_macro_kernel<NV, OK, MK><<<blocks, threads, 0, a.stream>>>(a.ode, a.model, a.integ, a.n_states, a.t0,
-                                                                         a.t1, a.in, a.out, a.status);
+                                                                         a.t1, a.in, a.out, a.status); mmpr_launched();
     return mmpr_check_launch("integrate_macro_kernel");
   }
 };

@@ -403,13 +403,13 @@ static int restrict_multi(const mmpr_partition &part, int32_t n_ens, int64_t P, 
   int64_t *cnt = counts;  // the finisher needs the totals even when the caller passes none
   if (!cnt) return MMPR_ERR_ARG;
   const dim3 g1((unsigned)L.B, (unsigned)n_ens);
-  rm_count_kernel<<<g1, RM_THREADS, 0, st>>>(part, P, x, pitch, L);
-  rm_scatter_kernel<<<g1, RM_THREADS, 0, st>>>(part, P, x, pitch, L, cnt);
+  rm_count_kernel<<<g1, RM_THREADS, 0, st>>>(part, P, x, pitch, L); mmpr_launched();
+  rm_scatter_kernel<<<g1, RM_THREADS, 0, st>>>(part, P, x, pitch, L, cnt); mmpr_launched();
   const dim3 g3((unsigned)L.maxsub, (unsigned)I, (unsigned)n_ens);
   const int fin_blocks = (int)((n_ens * I + 127) / 128);
   for (int squares = 0; squares < 2; ++squares) {
-    rm_partial_kernel<<<g3, 1024, 0, st>>>(I, P, cnt, L, squares);
-    rm_finish_kernel<<<fin_blocks, 128, 0, st>>>(part, n_ens, P, cnt, L, stats, squares);
+    rm_partial_kernel<<<g3, 1024, 0, st>>>(I, P, cnt, L, squares); mmpr_launched();
+    rm_finish_kernel<<<fin_blocks, 128, 0, st>>>(part, n_ens, P, cnt, L, stats, squares); mmpr_launched();
   }
   return mmpr_check_launch("restrict_multi");
 }
@@ -542,7 +542,7 @@ extern "C" int mmpr_restrict(const mmpr_partition *part, int32_t n_ens, int64_t 
   p.stats = stats;
   p.counts = counts;
   p.scratch = scratch;
-  restrict_kernel<<<n_ens, RS_THREADS, 0, (cudaStream_t)stream>>>(p);
+  restrict_kernel<<<n_ens, RS_THREADS, 0, (cudaStream_t)stream>>>(p); mmpr_launched();
   return mmpr_check_launch("restrict_kernel");
 }
 
@@ -577,7 +577,7 @@ extern "C" int mmpr_match(const mmpr_partition *part, int32_t n_ens, int64_t par
   p.chunks_per_ens = (int)((particles + per_cta - 1) / per_cta);
   const int64_t grid = (int64_t)n_ens * p.chunks_per_ens;
   if (grid > 0x7fffffff) return MMPR_ERR_UNSUPPORTED;
-  match_kernel<<<(unsigned)grid, MT_THREADS, 0, (cudaStream_t)stream>>>(p);
+  match_kernel<<<(unsigned)grid, MT_THREADS, 0, (cudaStream_t)stream>>>(p); mmpr_launched();
   return mmpr_check_launch("match_kernel");
 }
 

@@ -543,6 +543,7 @@ static int launch_fine_t(const FineParams &p, const FineGeometry &g, cudaStream_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   err = cudaLaunchKernelEx(&cfg, kern, p);
+  if (err == cudaSuccess) mmpr_launched();
   return mmpr_check(err, "fine_sweep_kernel launch");
 }
 

@@ -642,6 +642,7 @@ static int launch_grid_t(const FineParams &p, const GridGeometry &g, cudaStream_
   e.chunk_elems = g.chunk_elems;
   cfg.gridDim = dim3((unsigned)(teams * g.C), 1, 1);
   err = cudaLaunchKernelEx(&cfg, KERN, p, e);
+  if (err == cudaSuccess) mmpr_launched();
   return mmpr_check(err, "fine_grid_kernel launch");
 }
 

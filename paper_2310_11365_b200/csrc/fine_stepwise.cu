@@ -236,7 +236,7 @@ extern "C" int mmpr_fine_sweep_stepwise(const mmpr_model *model, int32_t n_slice
   int32_t *idx_out = (int32_t *)(w + stat_bytes + 2 * key_bytes + idx_bytes);
   void *cub_temp = (void *)(w + stat_bytes + 2 * key_bytes + 2 * idx_bytes);
 
-  fill_status_kernel<<<(n_slices + 255) / 256, 256, 0, st>>>(n_slices, bad_step);
+  fill_status_kernel<<<(n_slices + 255) / 256, 256, 0, st>>>(n_slices, bad_step); mmpr_launched();
   int rc = mmpr_check_launch("fill_status_kernel");
   if (rc != MMPR_OK) return rc;
   if (steps == 0) {
@@ -263,15 +263,15 @@ extern "C" int mmpr_fine_sweep_stepwise(const mmpr_model *model, int32_t n_slice
     const double *src = j == 0 ? x_in : x_out;
     const int64_t src_pitch = j == 0 ? in_pitch : out_pitch;
     if (rotator) {
-      rotator_stat_kernel<<<n_slices, SW_THREADS, 0, st>>>(P, src, src_pitch, stat);
+      rotator_stat_kernel<<<n_slices, SW_THREADS, 0, st>>>(P, src, src_pitch, stat); mmpr_launched();
     } else {
-      rank_prep_kernel<<<eblocks, 256, 0, st>>>(n_slices, P, src, src_pitch, keys_in, idx_in);
+      rank_prep_kernel<<<eblocks, 256, 0, st>>>(n_slices, P, src, src_pitch, keys_in, idx_in); mmpr_launched();
       size_t bytes = cub_bytes;
       cudaError_t err = cub::DeviceSegmentedSort::StableSortPairs(cub_temp, bytes, keys_in, keys_out, idx_in,
                                                                   idx_out, (int)items, n_slices, seg_begin,
                                                                   seg_end, st);
       if (err != cudaSuccess) return mmpr_check(err, "fine_sweep_stepwise: sort");
-      rank_scatter_kernel<<<eblocks, 256, 0, st>>>(n_slices, P, idx_out, stat);
+      rank_scatter_kernel<<<eblocks, 256, 0, st>>>(n_slices, P, idx_out, stat); mmpr_launched();
     }
     u.step = j;
     u.x_in = src;
@@ -279,6 +279,7 @@ extern "C" int mmpr_fine_sweep_stepwise(const mmpr_model *model, int32_t n_slice
     u.xi = xi + (int64_t)j * xi_row_pitch;
     if (rotator) stepwise_update_kernel<MMPR_MODEL_ROTATOR><<<eblocks, 256, 0, st>>>(u);
     else stepwise_update_kernel<MMPR_MODEL_BURGERS><<<eblocks, 256, 0, st>>>(u);
+    mmpr_launched();
     rc = mmpr_check_launch("stepwise_update_kernel");
     if (rc != MMPR_OK) return rc;
   }
@@ -328,7 +329,7 @@ extern "C" int mmpr_ensemble_statistic(const mmpr_model *model, int32_t n_slices
   if (*workspace_bytes < need || !x || !stat) return MMPR_ERR_ARG;
   if (n_slices == 0) return MMPR_OK;
   if (rotator) {
-    rotator_stat_kernel<<<n_slices, SW_THREADS, 0, st>>>(P, x, n_slices > 1 ? pitch : P, stat);
+    rotator_stat_kernel<<<n_slices, SW_THREADS, 0, st>>>(P, x, n_slices > 1 ? pitch : P, stat); mmpr_launched();
     return mmpr_check_launch("rotator_stat_kernel");
   }
   char *w = (char *)workspace;
@@ -341,11 +342,11 @@ extern "C" int mmpr_ensemble_statistic(const mmpr_model *model, int32_t n_slices
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int eblocks = (int)std::min<int64_t>((items + 255) / 256, (int64_t)sms * 8);
-  rank_prep_kernel<<<eblocks, 256, 0, st>>>(n_slices, P, x, n_slices > 1 ? pitch : P, keys_in, idx_in);
+  rank_prep_kernel<<<eblocks, 256, 0, st>>>(n_slices, P, x, n_slices > 1 ? pitch : P, keys_in, idx_in); mmpr_launched();
   size_t bytes = cub_bytes;
   cudaError_t err = cub::DeviceSegmentedSort::StableSortPairs(cub_temp, bytes, keys_in, keys_out, idx_in, idx_out,
                                                               (int)items, n_slices, seg_begin, seg_end, st);
   if (err != cudaSuccess) return mmpr_check(err, "ensemble_statistic: sort");
-  rank_scatter_kernel<<<eblocks, 256, 0, st>>>(n_slices, P, idx_out, stat);
+  rank_scatter_kernel<<<eblocks, 256, 0, st>>>(n_slices, P, idx_out, stat); mmpr_launched();
   return mmpr_check_launch("rank_scatter_kernel");
 }

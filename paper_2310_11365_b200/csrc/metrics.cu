@@ -120,7 +120,7 @@ extern "C" int mmpr_histogram_sorted(int32_t n_rows, int64_t count, const double
   // differences it (n_edges - 1 bins per row)
   const int64_t total = (int64_t)n_rows * n_edges;
   hist_cum_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_rows, count, sorted, pitch,
-                                                                                    edges, n_edges, counts);
+                                                                                    edges, n_edges, counts); mmpr_launched();
   return mmpr_check_launch("hist_cum_kernel");
 }
 
@@ -155,6 +155,6 @@ extern "C" int mmpr_mean_abs_diff(int32_t n_rows, int64_t count, const double *a
   if (n_rows == 0) return MMPR_OK;
   const int D = pw_depth(count);
   if (D > 7 && ((int64_t(1) << D) / 128) > MA_MAX_CHUNKS) return MMPR_ERR_UNSUPPORTED;
-  mean_absdiff_kernel<<<n_rows, MA_THREADS, 0, (cudaStream_t)stream>>>(count, a, pitch_a, b, pitch_b, out);
+  mean_absdiff_kernel<<<n_rows, MA_THREADS, 0, (cudaStream_t)stream>>>(count, a, pitch_a, b, pitch_b, out); mmpr_launched();
   return mmpr_check_launch("mean_absdiff_kernel");
 }

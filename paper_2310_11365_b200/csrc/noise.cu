@@ -22,6 +22,7 @@
 //   4. every produced normal is written at its exact stream position.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "mmpr_device.cuh"
 #include "npstream.cuh"
@@ -454,10 +455,43 @@ __device__ __noinline__ uint64_t successor_word(uint64_t i, uint64_t k0, uint64_
 #ifndef NW_MINB
 #define NW_MINB 16
 #endif
+// Segments (more streams than resident warps): a stream's sub-chunks are cut
+// into `nseg` runs of `seg_subs`, one single-warp CTA per (stream, segment),
+// CTAs laid out segment-major (grid y = segment).  A segment starts from the (produced, carry)
+// state its predecessor leaves in the stream's LAST output slot -- a
+// mailbox only the final segment writes a normal to: the host sizes the
+// segments so that the earlier ones cannot produce `count` values (outputs
+// <= words), and a clear kernel zeroes the mailboxes ahead of the launch.
+// The CTAs of a 1-D grid are dispatched in index order (CUB's decoupled
+// look-back relies on the same), so a predecessor is resident or finished
+// before its successor starts; with more streams than resident warps it
+// finished long before and the wait is one load.  The launch then ends in
+// a full last wave instead of a ragged one (config 4: 2.7 waves of 2368
+// warps; measured ~5%).  A bounded spin turns a broken assumption into a
+// trap, not a hang.
+#define NW_TAG_SHIFT 56
+#define NW_CARRY_SHIFT 40
+
+__device__ __noinline__ unsigned long long mailbox_wait(const double *mail, int seg) {
+  const long long t0 = clock64();
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(mail) : "memory");
+    if ((int)(v >> NW_TAG_SHIFT) == seg) return v;
+    __nanosleep(100);
+    if (clock64() - t0 > (1LL << 33)) __trap();  // in-order dispatch assumption broken
+  }
+}
+
+__global__ void noise_mailbox_clear_kernel(double *__restrict__ out, int64_t pitch, int64_t count, int n_streams) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_streams) reinterpret_cast<unsigned long long *>(out + (int64_t)i * pitch)[count - 1] = 0ULL;
+}
+
 template <bool AFFINE>
 __global__ void __launch_bounds__(32, NW_MINB)
 normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, double *__restrict__ out, int64_t pitch,
-                         double loc, double scale) {
+                         double loc, double scale, int nseg, int seg_subs) {
   __shared__ ulonglong2 zig[256];
   __shared__ double s_fi[256];
   __shared__ uint16_t s_tlen[32 * NW_WORDS];  // tail starts (lane-private slots): length in words
@@ -471,15 +505,29 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
     s_fi[i] = c_zig_fi[i];
   }
   __syncwarp();
-  const uint64_t k0 = keys[2 * blockIdx.x], k1 = keys[2 * blockIdx.x + 1];
+  // (stream, segment) = (blockIdx.x, blockIdx.y): both CTA-uniform special
+  // registers, so the Philox key stays on the uniform datapath (an index
+  // division would move the key schedule to the vector registers); CTAs are
+  // dispatched x-fastest, i.e. segment-major
+  const int seg = (int)blockIdx.y;
   double *o = out + (int64_t)blockIdx.x * pitch;
-
   int carry = 0;
   int64_t produced = 0;
+  if (seg > 0) {  // the predecessor's state
+    // (every lane polls: one lane polling and a shuffle made the compiler
+    // precompute the ten round keys into 40 vector registers and spill them)
+    const unsigned long long v = mailbox_wait(o + count - 1, seg);
+    produced = (int64_t)(v & ((1ULL << NW_CARRY_SHIFT) - 1ULL));
+    carry = (int)((v >> NW_CARRY_SHIFT) & 0xffffULL);
+  }
+  const uint64_t k0 = keys[2 * blockIdx.x], k1 = keys[2 * blockIdx.x + 1];
+  // sub-chunks this segment may take (the last one runs to the end of the stream)
+  int left = seg == nseg - 1 ? 0x7fffffff : seg_subs;
+  const int next_tag = seg == nseg - 1 ? 0 : seg + 1;
   uint32_t m20, e52;  // opaque to the compiler, so they stay in registers (see the transform)
   asm volatile("mov.b32 %0, 0x000FFFFF;" : "=r"(m20));
   asm volatile("mov.b32 %0, 0x43300000;" : "=r"(e52));
-  for (uint64_t sub = 0; produced < count; ++sub) {
+  for (uint64_t sub = (uint64_t)seg * (uint64_t)seg_subs; left > 0 && produced < count; ++sub, --left) {
     const uint64_t word0 = (sub * 32 + lane) * NW_WORDS;
     // fast path for every word, branch-free, eight words (two Philox blocks)
     // at a time; the words go to shared memory for the rare-word loop below
@@ -619,6 +667,12 @@ normals_fill_warp_kernel(const uint64_t *__restrict__ keys, int64_t count, doubl
     }
     produced += total;
   }
+  if (next_tag != 0 && lane == 0) {  // hand the stream's state to the next segment
+    const unsigned long long v = ((unsigned long long)next_tag << NW_TAG_SHIFT) |
+                                 ((unsigned long long)(carry < 0xffff ? carry : 0xffff) << NW_CARRY_SHIFT) |
+                                 (unsigned long long)produced;
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(o + count - 1), "l"(v) : "memory");
+  }
 }
 
 }  // namespace mmpr
@@ -633,7 +687,7 @@ extern "C" int mmpr_noise_keys(uint64_t master_seed, int32_t fresh, int32_t iter
   const int threads = 128;
   const int64_t blocks = (total + threads - 1) / threads;
   noise_keys_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(master_seed, fresh, iteration,
-                                                                           n_offset, n_slices, steps, keys);
+                                                                           n_offset, n_slices, steps, keys); mmpr_launched();
   return mmpr_check_launch("noise_keys_kernel");
 }
 
@@ -641,7 +695,7 @@ extern "C" int mmpr_entropy_key(const uint32_t *words, int32_t n_words, uint64_t
   if (!words || n_words < 1 || n_words > 16 || !key_dev) return MMPR_ERR_ARG;
   EntropyWords e;
   for (int i = 0; i < 16; ++i) e.w[i] = i < n_words ? words[i] : 0u;
-  entropy_key_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(e, n_words, key_dev);
+  entropy_key_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(e, n_words, key_dev); mmpr_launched();
   return mmpr_check_launch("entropy_key_kernel");
 }
 
@@ -649,15 +703,45 @@ extern "C" int mmpr_normals_fill(const uint64_t *keys, int32_t n_streams, int64_
                                  int64_t pitch, int32_t affine, double loc, double scale, void *stream) {
   if (n_streams < 0 || count < 0 || !keys || !out || (n_streams > 1 && pitch < count)) return MMPR_ERR_ARG;
   if (n_streams == 0 || count == 0) return MMPR_OK;
-  if (n_streams >= MMPR_WARP_STREAMS_MIN) {  // one single-warp CTA per stream
-    if (affine)
-      normals_fill_warp_kernel<true><<<n_streams, 32, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, loc, scale);
-    else
-      normals_fill_warp_kernel<false><<<n_streams, 32, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, loc, scale);
+  if (n_streams >= MMPR_WARP_STREAMS_MIN) {  // one single-warp CTA per (stream, segment)
+    static int slots_dev[MMPR_MAX_DEVICES] = {};
+    const int dev = mmpr_current_device();
+    if (slots_dev[dev] == 0) {
+      int sms = 0;
+      if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
+      slots_dev[dev] = NW_MINB * sms;
+    }
+    // more streams than resident warps, and not so many that the waves are
+    // nearly full anyway: eight segments per stream; the segments before the
+    // last must not be able to reach the stream's last output slot
+    const char *segs_env = getenv("MMPR_NOISE_SEGS");  // A/B and tests: 1 = unsegmented, N = force N segments
+    int nseg = segs_env ? atoi(segs_env) : ((n_streams > slots_dev[dev] && n_streams < 8 * slots_dev[dev]) ? 8 : 1);
+    if (nseg < 1 || nseg > 64) nseg = 1;
+    int seg_subs = 0;
+    for (; nseg > 1; --nseg) {
+      seg_subs = (int)((count + count / 48) / ((int64_t)(32 * NW_WORDS) * nseg));
+      if (seg_subs >= 4 && (int64_t)(nseg - 1) * seg_subs * (32 * NW_WORDS) < count - 1 &&
+          (int64_t)nseg * n_streams < (int64_t)INT32_MAX && count < (1LL << NW_CARRY_SHIFT))
+        break;
+    }
+    if (nseg > 1) {
+      noise_mailbox_clear_kernel<<<(n_streams + 255) / 256, 256, 0, (cudaStream_t)stream>>>(out, pitch, count,
+                                                                                             n_streams); mmpr_launched();
+      const int st = mmpr_check_launch("noise_mailbox_clear_kernel");
+      if (st != MMPR_OK) return st;
+    }
+    const dim3 grid((unsigned)n_streams, (unsigned)nseg, 1);
+    if (affine) {
+      normals_fill_warp_kernel<true><<<grid, 32, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, loc, scale, nseg,
+                                                                           seg_subs); mmpr_launched();
+    } else {
+      normals_fill_warp_kernel<false><<<grid, 32, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, loc, scale, nseg,
+                                                                            seg_subs); mmpr_launched();
+    }
     return mmpr_check_launch("normals_fill_warp_kernel");
   }
   normals_fill_kernel<<<n_streams, NF_THREADS, 0, (cudaStream_t)stream>>>(keys, count, out, pitch, affine, loc,
-                                                                          scale);
+                                                                          scale); mmpr_launched();
   return mmpr_check_launch("normals_fill_kernel");
 }
 
@@ -685,7 +769,7 @@ extern "C" int mmpr_log1p_libm(const double *x, double *out, int64_t n, void *st
   if (n < 0 || (n > 0 && (!x || !out))) return MMPR_ERR_ARG;
   if (n == 0) return MMPR_OK;
   const int64_t blocks = (n + 255) / 256;
-  log1p_kernel<<<(unsigned)(blocks < 4736 ? blocks : 4736), 256, 0, (cudaStream_t)stream>>>(x, out, n);
+  log1p_kernel<<<(unsigned)(blocks < 4736 ? blocks : 4736), 256, 0, (cudaStream_t)stream>>>(x, out, n); mmpr_launched();
   return mmpr_check_launch("log1p_kernel");
 }
 
@@ -715,6 +799,6 @@ extern "C" int mmpr_counter_normals_fill(const mmpr_counter_noise *noise, int32_
   const int64_t total = (int64_t)rows * count;
   const int64_t blocks = (total + 255) / 256;
   counter_normals_kernel<<<(unsigned)(blocks < 4736 ? blocks : 4736), 256, 0, (cudaStream_t)stream>>>(
-      c, (uint32_t)n, (uint32_t)j0, rows, p0, count, out, pitch);
+      c, (uint32_t)n, (uint32_t)j0, rows, p0, count, out, pitch); mmpr_launched();
   return mmpr_check_launch("counter_normals_kernel");
 }

@@ -908,6 +908,7 @@ static int launch_pipe(const PipeParams &pp, const PipeGeometry &g, cudaStream_t
   if (pp.rg_rows > 0 && clusters > pp.rg_rows) clusters = pp.rg_rows;
   cfg.gridDim = dim3((unsigned)(clusters * g.ctas), 1, 1);
   err = cudaLaunchKernelEx(&cfg, KERN, pp);
+  if (err == cudaSuccess) mmpr_launched();
   return mmpr_check(err, "pipeline_kernel launch");
 }
 

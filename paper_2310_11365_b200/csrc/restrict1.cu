@@ -264,6 +264,7 @@ static int launch_r1(const Restrict1Params &p, int n_ens, int threads, cudaStrea
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   err = cudaLaunchKernelEx(&cfg, KERN, p);
+  if (err == cudaSuccess) mmpr_launched();
   return mmpr_check(err, "restrict1_kernel launch");
 }
 

@@ -192,6 +192,7 @@ static int launch_rg(const RegionsParams &p, int n_ens, int threads, cudaStream_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   err = cudaLaunchKernelEx(&cfg, KERN, p);
+  if (err == cudaSuccess) mmpr_launched();
   return mmpr_check(err, "restrict_regions_kernel launch");
 }
 

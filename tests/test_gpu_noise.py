@@ -141,3 +141,34 @@ def test_tail_heavy_streams_bitwise(dev):
             _assert_stream_equal(xi[n, j, :P], ref)
             tails += int((np.abs(ref) > TAIL).sum())
     assert tails > 2000
+
+
+@pytest.mark.parametrize("segs", ["2", "3", "8", "13"])
+def test_segmented_streams_equal_unsegmented_and_numpy(dev, monkeypatch, segs):
+    """Streams cut into segments chained through the mailbox in their last
+    output slot (the many-streams launch shape, forced here for 320 streams):
+    bit for bit the unsegmented fill, and numpy's streams -- ragged counts,
+    so carries, tails and the final partial sub-chunk cross segment ends."""
+    from paper_2310_11365_b200 import noise
+    for P in (20_000, 33_333):
+        N, S = 16, 20  # 320 streams: the warp-per-stream kernel
+        monkeypatch.setenv("MMPR_NOISE_SEGS", "1")
+        base = noise.slice_noise(5, 3, N, S, P).cpu().numpy()[:, :, :P]
+        monkeypatch.setenv("MMPR_NOISE_SEGS", segs)
+        got = noise.slice_noise(5, 3, N, S, P).cpu().numpy()[:, :, :P]
+        assert np.array_equal(got, base)
+        for n, j in ((0, 0), (7, 13), (15, 19)):
+            _assert_stream_equal(got[n, j], _np_stream((5, 1, 3 + n, j), P))
+
+
+def test_segmented_launch_shape_is_the_default_above_the_resident_warps(dev, monkeypatch):
+    """More streams than resident warps (2368 on a B200) take the segmented
+    shape without a switch; the result is the unsegmented one."""
+    from paper_2310_11365_b200 import noise
+    N, S, P = 30, 100, 12_000  # 3000 streams
+    monkeypatch.delenv("MMPR_NOISE_SEGS", raising=False)
+    got = noise.slice_noise(1, 0, N, S, P).cpu().numpy()[:, :, :P]
+    monkeypatch.setenv("MMPR_NOISE_SEGS", "1")
+    base = noise.slice_noise(1, 0, N, S, P).cpu().numpy()[:, :, :P]
+    assert np.array_equal(got, base)
+    _assert_stream_equal(got[29, 99], _np_stream((1, 1, 29, 99), P))
