@@ -408,7 +408,10 @@ static int fine_geometry(int64_t P, FineGeometry *g, int n_slices = 0) {
     empty |= l == 0;
   }
   g->cnt_min = (int)(min_leaf >> 3);
-  g->ppt = (int)((max_leaf + 7) / 8);
+  // accumulator elements per lane: a leaf of 8 c + r particles holds c per lane and its r < 8 trailing
+  // ones (only the last leaf of an ensemble whose size is not a multiple of 8 has any) in the tail element
+  g->ppt = (int)((P % 8) ? (max_leaf >> 3) : (max_leaf + 7) / 8);
+  if (g->ppt < 1) g->ppt = 1;
   // increment stages of the CTA's particle range(s) must fit next to the
   // ~2 KB of static shared memory (227 KB opt-in per CTA)
   const size_t smem_budget = 224 * 1024;
@@ -481,7 +484,7 @@ template <int KIND, int PPT, bool HAS_TAIL>
 static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t stream, bool phx) {
   if (phx) {
     if (g.groups != 1) return MMPR_ERR_UNSUPPORTED;
-    if (!g.padded && g.ppt == PPT && g.cnt_min >= PPT - 1) {
+    if (!g.padded && g.ppt <= PPT && g.cnt_min >= PPT - 1) {
       if (g.threads <= 512)
         return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 512, 1, PPT - 1, true>>(p, g, stream);
       return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 1024, 1, PPT - 1, true>>(p, g, stream);
@@ -500,7 +503,7 @@ static int launch_fine(const FineParams &p, const FineGeometry &g, cudaStream_t 
   // Every slot populated and every leaf within 8 elements of the longest
   // (P = 1e5: leaves of 96 and 104): only the last accumulator element is
   // predicated.  512-thread CTAs run two per SM (64 registers each).
-  if (!g.padded && g.ppt == PPT && g.cnt_min >= PPT - 1) {
+  if (!g.padded && g.ppt <= PPT && g.cnt_min >= PPT - 1) {
     if (g.threads <= 512)
       return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 512, 1, PPT - 1>>(p, g, stream);
     return launch_fine_t<fine_sweep_kernel<KIND, PPT, HAS_TAIL, false, 1024, 1, PPT - 1>>(p, g, stream);

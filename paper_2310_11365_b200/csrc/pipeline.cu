@@ -838,9 +838,21 @@ static int pipe_geometry(int64_t P, PipeGeometry *g) {
     if (l > max_leaf) max_leaf = l;
     if (l < min_leaf) min_leaf = l;
   }
-  g->ppt = (int)((max_leaf + 7) / 8);
-  g->exact = (g->ppt == 13 || g->ppt == 10 || g->ppt == 16) && (min_leaf >> 3) >= g->ppt - 1;
-  if (!g->exact && (g->ppt > 16 || (min_leaf >> 3) < 8)) return MMPR_ERR_UNSUPPORTED;
+  // accumulator elements per lane: a leaf of 8 c + r particles holds c per lane and its r < 8 trailing
+  // ones (only the last leaf of an ensemble whose size is not a multiple of 8 has any) in the tail element
+  int max_cnt = (int)((P % 8) ? (max_leaf >> 3) : (max_leaf + 7) / 8);
+  if (max_cnt < 1) max_cnt = 1;
+  const int min_cnt = (int)(min_leaf >> 3);
+  // the smallest specialised element count every leaf fits (PPT-1 or PPT elements per lane), else the
+  // any-size form
+  g->exact = false;
+  g->ppt = 16;
+  for (int ppt : {10, 13, 16})
+    if (!g->exact && max_cnt <= ppt && min_cnt >= ppt - 1) {
+      g->exact = true;
+      g->ppt = ppt;
+    }
+  if (!g->exact && (max_cnt > 16 || min_cnt < 8)) return MMPR_ERR_UNSUPPORTED;
   g->D = D;
   g->spc = nslots >= 512 ? 64 : 32;
   g->ctas = (int)(nslots / g->spc);
