@@ -68,7 +68,9 @@ def _ou_case(mm, N, K, S, P=100_000, retain=True, dt=1e-3):
                                      # the any-size form (16 per lane, at least 8 populated): 9..15 elements,
                                      # ragged leaves, tails, the smallest and largest ensembles of one cluster
                                      (4, 3, 8, 9_999), (4, 3, 8, 30_000), (3, 2, 6, 70_000), (3, 2, 6, 120_001),
-                                     (4, 2, 6, 4_608), (4, 3, 8, 12_345), (6, 4, 10, 60_000), (3, 3, 6, 90_000)])
+                                     (4, 2, 6, 4_608), (4, 3, 8, 12_345), (6, 4, 10, 60_000), (3, 3, 6, 90_000),
+                                     # ragged sizes on the specialised forms (13 / 10 per lane + a tail element)
+                                     (4, 3, 8, 99_999), (4, 3, 8, 100_003), (4, 3, 8, 10_001)])
 def test_pipeline_equals_per_iteration_kernels_ou(mm, monkeypatch, N, K, S, P):
     model, ode, init, cfg = _ou_case(mm, N, K, S, P)
     plan = mm.NoisePlan(0)
@@ -130,7 +132,8 @@ def _bimodal_case(mm, N, K, S, P=100_000, retain=True, init=None):
 
 @pytest.mark.parametrize("N,K,S,P,retain", [(8, 4, 16, 100_000, True), (20, 3, 8, 100_000, False),
                                             (5, 5, 8, 98_307, True), (3, 1, 4, 106_496, True),
-                                            (6, 3, 8, 50_000, True), (4, 2, 8, 25_000, False)])
+                                            (6, 3, 8, 50_000, True), (4, 2, 8, 25_000, False),
+                                            (4, 3, 8, 99_999, True)])
 def test_pipeline_bimodal_equals_per_iteration_kernels(mm, monkeypatch, N, K, S, P, retain):
     """Two regions (config 3): per-region match with pre-transform
     membership and region restrictions over compacted members inside the

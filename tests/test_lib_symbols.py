@@ -78,7 +78,8 @@ def test_pipeline_support_query_without_a_gpu():
     assert kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 100_000)  # two regions (config 3)
     assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 100_000, counter_noise=True)
     assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 10_000)
-    assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 99_999)  # two regions: 13 per lane only
+    assert kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 99_999)  # 12-13 per lane + a tail element
+    assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, euler, 90_000)  # two regions: 13 per lane only
     assert not kernels.pipeline_supported(dwm.descriptor, ode_m, odm_m, dp54, 100_000)
     three = mm.RegionPartition(separatrices=(-0.5, 0.5), peaks=(-1.0, 0.0, 1.0))
     ode_3, odm_3 = moments.device_ode(mm.multimodal_rhs(dwm, three, dw.potential, dw.sigma))
