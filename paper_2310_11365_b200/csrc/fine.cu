@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(MAXT, PHX ? (MMPR_PHX_MINB * 512 / MAXT > 0 ? 
   if (slot < nslots) pw_leaf(p.P, p.D, slot, &off, &len);
   const int cnt = (int)(len >> 3);       // elements per lane in the 8-way part
   const int tail = (int)(len & 7);       // trailing elements added one by one
+  // (trailing particles exist in the ensemble's last leaf only: the other warps skip their fold)
+  const bool warp_tail = HAS_TAIL && __any_sync(MMPR_FULL_MASK, tail != 0);
   const int64_t tail_off = off + (len & ~int64_t(7));
   const bool slot_ok = len > 0;
   const int cmin = LO >= 0 ? LO : p.cnt_min;  // min cnt over the slice's populated slots
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(MAXT, PHX ? (MMPR_PHX_MINB * 512 / MAXT > 0 ? 
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 2));
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 4));
     if (cnt == 0) acc = 0.0;  // a leaf shorter than 8 (P < 8) is summed from 0.0
-    if (HAS_TAIL) {
+    if (HAS_TAIL && warp_tail) {  // (warp-uniform: only the warp holding the ensemble's last leaf)
 #pragma unroll
       for (int i = 0; i < 7; ++i) {
         const double v = __shfl_sync(MMPR_FULL_MASK, xt, (lane & ~7) | i);

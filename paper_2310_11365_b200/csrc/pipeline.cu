@@ -348,6 +348,8 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
     if (tid == 0) s_stage_bytes = (uint32_t)((((hi64 - lo64) * 8) + 15) & ~int64_t(15));
   }
   const int my_idx = off - lo + j8;
+  // trailing particles exist in the ensemble's last leaf only: the other warps skip their fold
+  const bool warp_tail = HAS_TAIL && __any_sync(MMPR_FULL_MASK, tail != 0);
   const int ns = p.nstages;
   const cn::ZigTables *zt = reinterpret_cast<const cn::ZigTables *>(s_stage);
   if constexpr (PHX) cn::load_zig(reinterpret_cast<cn::ZigTables *>(s_stage), tid, gthreads);
@@ -404,7 +406,7 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 1));
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 2));
     acc = add(acc, __shfl_xor_sync(MMPR_FULL_MASK, acc, 4));
-    if (HAS_TAIL) {
+    if (HAS_TAIL && warp_tail) {  // (warp-uniform: only the warp holding the ensemble's last leaf)
       const double ft = f(xt);
 #pragma unroll
       for (int i = 0; i < 7; ++i) {
