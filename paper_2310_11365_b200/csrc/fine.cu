@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(MAXT, PHX ? (MMPR_PHX_MINB * 512 / MAXT > 0 ? 
             x[m] = (m < cnt) ? nx : x[m];
           }
         }
-        if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
+        if (HAS_TAIL && warp_tail && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
       }
       PROF_MARK(tu1);
       PROF_ADD(1, tw1, tu1);

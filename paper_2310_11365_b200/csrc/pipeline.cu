@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(512, PHX ? MMPR_PHX_MINB : 2) pipeline_kernel(
               x[m] = (m < cnt) ? nx : x[m];
             }
           }
-          if (HAS_TAIL && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
+          if (HAS_TAIL && warp_tail && j8 < tail) xt = em_update<KIND>(p, xt, s, xb[(int)(tail_off - lo) + j8]);
         }
         reduce(Plain{}, 0.0, (!PHX && j + ns < p.S) ? j + ns : -1, s, bad, (PHX && j + 1 < p.S) ? j + 1 : -1, nkey);
         if (bad) {
